@@ -1,0 +1,270 @@
+/* shardplan_gpu — C-ABI of the B200-native RecShard hot paths.
+ *
+ * The drop-in boundary: plain pointers, sizes and opaque handles, no torch or
+ * C++ types.  Every entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj/core/).  The C++ shim
+ * include/shardplan_gpu.hpp rebuilds the reference's `shardplan::` value API
+ * (profile / build_icdf / hash_utilization / hash_value / build_remap /
+ * translate / simulate) on top of it and rethrows the reference's exception
+ * types.
+ *
+ * Conventions
+ *  - Return value: RS_OK (0) or a negative RS_ERR_* status; the message of the
+ *    last failure on this thread is rs_last_error().
+ *  - `location` arguments say where a buffer lives: RS_MEM_HOST (pageable or
+ *    pinned host memory; staged over PCIe inside the call) or RS_MEM_DEVICE
+ *    (device memory of the context's GPU).
+ *  - Calls are ordered on the context's stream.  Calls that return host
+ *    results synchronise that stream before returning; rs_emb_* calls on
+ *    device buffers are asynchronous.
+ *  - One context per stream/thread; concurrent calls must use distinct
+ *    contexts (the reference functions are pure and re-entrant).
+ */
+#ifndef SHARDPLAN_GPU_H
+#define SHARDPLAN_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_ABI_VERSION 1
+
+/* Status codes — mirror include/shardplan/error.hpp:38-72. */
+#define RS_OK 0
+#define RS_ERR_INVALID_ARGUMENT (-1) /* shardplan::InvalidArgument          */
+#define RS_ERR_PARSE (-2)            /* shardplan::ParseError               */
+#define RS_ERR_INFEASIBLE (-3)       /* shardplan::InfeasibleError          */
+#define RS_ERR_IO (-4)               /* shardplan::IoError                  */
+#define RS_ERR_OUT_OF_RANGE (-5)     /* std::out_of_range (profiler.cpp:103) */
+#define RS_ERR_CUDA (-8)             /* CUDA runtime failure                */
+#define RS_ERR_INTERNAL (-9)
+
+#define RS_MEM_HOST 0
+#define RS_MEM_DEVICE 1
+
+#define RS_OPT_SGD 0               /* row-wise SGD                          */
+#define RS_OPT_ROWWISE_ADAGRAD 1   /* FBGEMM exact row-wise Adagrad         */
+
+int rs_abi_version(void);
+const char* rs_last_error(void);
+
+/* ------------------------------------------------------------- context */
+typedef struct rs_context rs_context;
+/* stream == NULL creates a private non-blocking stream. */
+int rs_context_create(int device, void* stream, rs_context** out);
+int rs_context_destroy(rs_context* ctx);
+int rs_context_synchronize(rs_context* ctx);
+
+/* ------------------------------------------------------------- types  */
+/* include/shardplan/types.hpp:26-34 (TableSpec) */
+typedef struct rs_table_spec {
+  uint32_t table_id;
+  uint64_t cardinality;
+  uint64_t hash_size;
+  uint32_t dim;
+  uint32_t elem_bytes;
+} rs_table_spec;
+
+/* include/shardplan/workload.hpp:41-58 (Trace) in structure-of-arrays form.
+ * Exactly one of `ids` (hashed rows) and `raw_ids` (pre-hash values, hashed
+ * on the GPU with hash_value's mix64 % hash_size) is non-NULL. */
+typedef struct rs_trace {
+  uint32_t num_tables;
+  const rs_table_spec* tables; /* host */
+  uint64_t num_samples;
+  uint64_t num_records;
+  const uint64_t* rec_sample;
+  const uint32_t* rec_table; /* table_id, not index */
+  const uint64_t* rec_offset;
+  const uint32_t* rec_len;
+  uint64_t num_ids;
+  const uint32_t* ids;
+  const uint64_t* raw_ids;
+  int location; /* of the record and id arrays */
+} rs_trace;
+
+/* ------------------------------------------------------------- hashing */
+/* include/shardplan/workload.hpp:28-31  hash_value(raw, hash_size) */
+int rs_hash_value(uint64_t raw_id, uint64_t hash_size, uint32_t* out);
+/* Batched hash_value on the GPU (K0).  raw/out: `location` buffers. */
+int rs_hash_ids(rs_context* ctx, const uint64_t* raw, uint64_t n,
+                uint64_t hash_size, uint32_t* out, int location);
+
+/* ------------------------------------------------------------- profiler */
+typedef struct rs_profile rs_profile;
+
+/* core/src/profiler.cpp:60-161  profile(trace, sample_rate, seed).
+ * K1 (select + hash + histogram) and K2 (rank, CDF, ICDF) run on the GPU.
+ * Errors as the reference: empty trace / rate outside (0,1] / zero samples
+ * selected -> RS_ERR_INVALID_ARGUMENT; a selected record of an unknown
+ * table -> RS_ERR_OUT_OF_RANGE. */
+int rs_profile_run(rs_context* ctx, const rs_trace* trace, double sample_rate,
+                   uint64_t seed, rs_profile** out);
+
+/* include/shardplan/profiler.hpp:31-45 (FeatureStats) view. Pointers stay
+ * valid until rs_profile_destroy. */
+typedef struct rs_feature_stats {
+  uint32_t table_id;
+  double coverage;
+  double avg_pooling;
+  uint64_t distinct_rows_accessed;
+  uint64_t total_accesses;
+  const uint64_t* icdf_steps;      /* 101 entries, host */
+  const double* access_cdf;        /* distinct entries, host */
+  const uint32_t* rows_by_rank;    /* distinct entries, host */
+  const uint32_t* d_rows_by_rank;  /* same, device (feeds rs_build_remap) */
+} rs_feature_stats;
+
+int rs_profile_num_tables(const rs_profile* p, uint32_t* out);
+int rs_profile_get(const rs_profile* p, uint32_t j, rs_feature_stats* out);
+/* Number of selected samples (the coverage denominator, profiler.cpp:68-76). */
+int rs_profile_selected(const rs_profile* p, uint64_t* out);
+int rs_profile_destroy(rs_profile* p);
+
+/* core/src/profiler.cpp:49-58  build_icdf(counts) on the GPU (sort + scan).
+ * counts: `location` buffer of n u64; out: host u64[101]. */
+int rs_build_icdf(rs_context* ctx, const uint64_t* counts, uint64_t n,
+                  int location, uint64_t* out101);
+
+/* core/src/profiler.cpp:163-174  hash_utilization(stats, spec, distinct_raw) */
+int rs_hash_utilization(uint64_t distinct_rows_accessed, uint64_t hash_size,
+                        uint64_t distinct_raw_ids_seen, double* sparsity,
+                        double* collisions);
+
+/* ------------------------------------------------------------- remap   */
+/* core/src/remap.cpp:40-105  build_remap(entry, stats, spec, opts) (K3).
+ * rows_by_rank: `rows_location` buffer of `distinct` u32 (e.g. the device
+ * view of rs_feature_stats); entries: `out_location` buffer of hash_size
+ * int32 (sign-bit tier encoding, include/shardplan/remap.hpp:27-29). */
+int rs_build_remap(rs_context* ctx, uint32_t table_id, uint64_t hash_size,
+                   uint64_t hbm_rows, const uint32_t* rows_by_rank,
+                   uint64_t distinct, int rows_location, int omit_unaccessed,
+                   int32_t* entries, int out_location,
+                   uint64_t* slow_rows_allocated);
+
+/* ------------------------------------------------------------- simulate */
+/* include/shardplan/plan.hpp:27-34 (PlanEntry) */
+typedef struct rs_plan_entry {
+  uint32_t table_id;
+  uint32_t gpu;
+  uint32_t step;
+  uint64_t hbm_rows;
+  double pct;
+  uint64_t mem_bytes;
+} rs_plan_entry;
+
+/* include/shardplan/types.hpp:82-89 (SystemSpec) */
+typedef struct rs_system_spec {
+  uint32_t num_gpus;
+  uint64_t batch_size;
+  uint64_t cap_hbm_bytes;
+  uint64_t cap_dram_bytes;
+  double bw_hbm;
+  double bw_uvm;
+} rs_system_spec;
+
+/* include/shardplan/remap.hpp:27-39 (RemapTable) */
+typedef struct rs_remap_view {
+  uint32_t table_id;
+  uint64_t hash_size;
+  uint64_t hbm_rows;
+  const int32_t* entries;
+  int location;
+} rs_remap_view;
+
+/* include/shardplan/simulator.hpp:24-39 (SimReport); caller-owned arrays:
+ * gpu_* hold num_gpus entries, table_fast_fraction num_tables. */
+typedef struct rs_sim_report {
+  double* gpu_hbm_accesses;
+  double* gpu_uvm_accesses;
+  double* gpu_est_iter_cost;
+  uint64_t batches;
+  uint64_t total_accesses;
+  double min_cost, max_cost, mean_cost, stddev_cost;
+  double uvm_access_fraction;
+  double* table_fast_fraction;
+} rs_sim_report;
+
+/* core/src/simulator.cpp:26-139  simulate(trace, plan, remaps, system, B).
+ * The per-GPU / per-table tier counts are exact u64 from the GPU; the
+ * report formulas are applied on the host exactly as the reference does. */
+int rs_simulate(rs_context* ctx, const rs_trace* trace, uint32_t num_entries,
+                const rs_plan_entry* entries, uint32_t num_remaps,
+                const rs_remap_view* remaps, const rs_system_spec* system,
+                uint64_t batch_size, rs_sim_report* out);
+
+/* ------------------------------------------------------------- EmbeddingBag
+ * The tiered operator that serves a plan (no reference implementation: the
+ * paper used FBGEMM; semantics PAPER.md:275 and :605-607).
+ * Each table's rows live in the fast tier (HBM) or the slow tier (pinned
+ * host memory read zero-copy over PCIe) as its remap says.  Weights are fp32.
+ *
+ * Batch format (table-major CSR, the reference Trace regrouped per table):
+ *   offsets: u32[T*B + 1]; bag (t, b) = indices[offsets[t*B+b] .. offsets[t*B+b+1])
+ *   indices: u32 ORIGINAL row ids (< hash_size); remap is applied in-kernel.
+ *   pooled:  f32[B, sum_t dim_t], table t at column sum_{u<t} dim_u.      */
+typedef struct rs_emb rs_emb;
+
+typedef struct rs_emb_table {
+  uint32_t table_id;
+  uint64_t hash_size;
+  uint32_t dim;                 /* multiple of 4, <= 1024 */
+  const int32_t* remap;         /* hash_size entries, host or device */
+  int remap_location;
+  uint64_t hbm_rows;            /* fast-tier rows (remap >= 0) */
+  uint64_t slow_rows;           /* slow-tier rows to back (remap < 0) */
+} rs_emb_table;
+
+int rs_emb_create(rs_context* ctx, uint32_t num_tables, const rs_emb_table* tables,
+                  uint64_t max_batch, uint64_t max_lookups, int optimizer, float eps,
+                  rs_emb** out);
+int rs_emb_destroy(rs_emb* e);
+/* Deterministic init on ORIGINAL rows (oracle/oracle.h or_init_weight). */
+int rs_emb_init_weights(rs_emb* e, uint64_t seed, float scale);
+/* K4: sum-pooled forward.  hit_counts (device u64[2*T], may be NULL) receives
+ * += per-table fast / slow lookup counts (the simulate() accounting). */
+int rs_emb_forward(rs_emb* e, uint64_t batch, const uint32_t* offsets,
+                   const uint32_t* indices, float* pooled, uint64_t* hit_counts);
+/* K5: backward + optimizer update, deterministic (sorted-segment reduction). */
+int rs_emb_backward(rs_emb* e, uint64_t batch, const uint32_t* offsets,
+                    const uint32_t* indices, const float* grad_pooled, float lr);
+/* Reads rows by ORIGINAL id into host memory (parity checks). */
+int rs_emb_read_rows(rs_emb* e, uint32_t t, const uint32_t* rows, uint64_t n,
+                     float* out, float* momentum_out);
+/* Bytes of HBM / pinned host memory held by the tiers. */
+int rs_emb_memory(const rs_emb* e, uint64_t* hbm_bytes, uint64_t* host_bytes);
+
+/* ------------------------------------------------------------- synthetic workload
+ * Bench/test INPUT generation — not part of the reference boundary.  Mirrors
+ * core/src/workload.cpp:198-217 (per (sample, table) substream, coverage
+ * Bernoulli, pooling law, bounded Zipf raw values, hash_value) on the GPU;
+ * not bit-identical to the reference generator (GPU libm). */
+typedef struct rs_gen_table {
+  uint32_t table_id;
+  uint64_t cardinality;
+  uint64_t hash_size;
+  double zipf_exponent;
+  double mean_pooling;
+  double coverage;
+  int pooling_law; /* 0 constant, 1 poisson, 2 lognormal (types.hpp:57) */
+} rs_gen_table;
+
+/* Writes a table-major CSR batch (device offsets[T*B+1], indices) for samples
+ * [sample_base, sample_base + B).  *total = lookups; fails without writing
+ * indices if total > capacity. */
+int rs_gen_batch(rs_context* ctx, uint32_t T, const rs_gen_table* tables, uint64_t B,
+                 uint64_t sample_base, uint64_t seed, uint32_t* offsets, uint32_t* indices,
+                 uint64_t capacity, uint64_t* total);
+/* Device view of a CSR batch as reference Trace records (present bags only). */
+int rs_kjt_to_records(rs_context* ctx, uint32_t T, const uint32_t* table_ids, uint64_t B,
+                      uint64_t sample_base, const uint32_t* offsets, uint64_t* rec_sample,
+                      uint32_t* rec_table, uint64_t* rec_offset, uint32_t* rec_len,
+                      uint64_t* num_records);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

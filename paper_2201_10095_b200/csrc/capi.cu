@@ -1,0 +1,261 @@
+// The extern "C" boundary (include/shardplan_gpu.h): validation, error
+// mapping and dispatch into the host orchestration of each hot path.
+#include <cmath>
+#include <string>
+
+#include "../../include/shardplan_gpu.h"
+#include "context.cuh"
+
+struct rs_profile;
+struct rs_emb;
+
+namespace rs {
+rs_profile* profile_run(rs_context*, const rs_trace*, double, uint64_t);
+void hash_ids(rs_context*, const uint64_t*, uint64_t, uint64_t, uint32_t*, int);
+void build_icdf(rs_context*, const uint64_t*, uint64_t, int, uint64_t*);
+void build_remap(rs_context*, uint32_t, uint64_t, uint64_t, const uint32_t*, uint64_t, int, int,
+                 int32_t*, int, uint64_t*);
+void simulate(rs_context*, const rs_trace*, uint32_t, const rs_plan_entry*, uint32_t,
+              const rs_remap_view*, const rs_system_spec*, uint64_t, rs_sim_report*);
+rs_emb* emb_create(rs_context*, uint32_t, const rs_emb_table*, uint64_t, uint64_t, int, float);
+void emb_init_weights(rs_emb*, uint64_t, float);
+void emb_forward(rs_emb*, uint64_t, const uint32_t*, const uint32_t*, float*, uint64_t*);
+void emb_backward(rs_emb*, uint64_t, const uint32_t*, const uint32_t*, const float*, float);
+void emb_read_rows(rs_emb*, uint32_t, const uint32_t*, uint64_t, float*, float*);
+void emb_memory(const rs_emb*, uint64_t*, uint64_t*);
+void profile_view(const rs_profile*, uint32_t, rs_feature_stats*);
+uint32_t profile_tables(const rs_profile*);
+uint64_t profile_selected(const rs_profile*);
+void profile_free(rs_profile*);
+void emb_free(rs_emb*);
+}  // namespace rs
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return RS_OK;
+  } catch (const rs::Error& e) {
+    g_err = e.what();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return RS_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return RS_ERR_INTERNAL;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw rs::InvalidArgument(std::string(what) + " is null");
+}
+}  // namespace
+
+namespace rs {
+void set_error(const std::string& m) { g_err = m; }
+}  // namespace rs
+
+extern "C" {
+
+int rs_abi_version(void) { return RS_ABI_VERSION; }
+const char* rs_last_error(void) { return g_err.c_str(); }
+
+int rs_context_create(int device, void* stream, rs_context** out) {
+  return guarded([&] {
+    need(out, "out");
+    RS_CUDA(cudaSetDevice(device));
+    auto* c = new rs_context;
+    c->device = device;
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+      if (e != cudaSuccess) {
+        delete c;
+        throw rs::CudaError(std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+      }
+      c->own_stream = true;
+    }
+    *out = c;
+  });
+}
+
+int rs_context_destroy(rs_context* c) {
+  return guarded([&] {
+    if (!c) return;
+    cudaStreamSynchronize(c->stream);
+    if (c->arena) cudaFree(c->arena);
+    if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+  });
+}
+
+int rs_context_synchronize(rs_context* c) {
+  return guarded([&] {
+    need(c, "ctx");
+    c->sync();
+  });
+}
+
+int rs_hash_value(uint64_t raw, uint64_t hash_size, uint32_t* out) {
+  return guarded([&] {
+    need(out, "out");
+    if (hash_size == 0) throw rs::InvalidArgument("hash_value: hash_size must be >= 1");
+    *out = static_cast<uint32_t>(rs::mix64(raw) % hash_size);  // inc/workload.hpp:28-31
+  });
+}
+
+int rs_hash_ids(rs_context* c, const uint64_t* raw, uint64_t n, uint64_t H, uint32_t* out, int loc) {
+  return guarded([&] {
+    need(c, "ctx");
+    if (n) {
+      need(raw, "raw");
+      need(out, "out");
+    }
+    rs::hash_ids(c, raw, n, H, out, loc);
+  });
+}
+
+int rs_profile_run(rs_context* c, const rs_trace* tr, double rate, uint64_t seed, rs_profile** out) {
+  return guarded([&] {
+    need(c, "ctx");
+    need(out, "out");
+    *out = rs::profile_run(c, tr, rate, seed);
+  });
+}
+
+int rs_profile_num_tables(const rs_profile* p, uint32_t* out) {
+  return guarded([&] {
+    need(p, "profile");
+    *out = rs::profile_tables(p);
+  });
+}
+
+int rs_profile_get(const rs_profile* p, uint32_t j, rs_feature_stats* out) {
+  return guarded([&] {
+    need(p, "profile");
+    need(out, "out");
+    rs::profile_view(p, j, out);
+  });
+}
+
+int rs_profile_selected(const rs_profile* p, uint64_t* out) {
+  return guarded([&] {
+    need(p, "profile");
+    *out = rs::profile_selected(p);
+  });
+}
+
+int rs_profile_destroy(rs_profile* p) {
+  return guarded([&] { rs::profile_free(p); });
+}
+
+int rs_build_icdf(rs_context* c, const uint64_t* counts, uint64_t n, int loc, uint64_t* out101) {
+  return guarded([&] {
+    need(c, "ctx");
+    need(out101, "out");
+    if (n) need(counts, "counts");
+    rs::build_icdf(c, counts, n, loc, out101);
+  });
+}
+
+int rs_hash_utilization(uint64_t distinct, uint64_t hash_size, uint64_t distinct_raw, double* sp,
+                        double* col) {
+  return guarded([&] {
+    need(sp, "sparsity");
+    need(col, "collisions");
+    // core/src/profiler.cpp:163-174
+    const double h = static_cast<double>(hash_size);
+    *sp = static_cast<double>(hash_size - distinct) / h;
+    *col = (static_cast<double>(distinct_raw) - static_cast<double>(distinct)) / h;
+  });
+}
+
+int rs_build_remap(rs_context* c, uint32_t table_id, uint64_t H, uint64_t hbm_rows,
+                   const uint32_t* rows_by_rank, uint64_t distinct, int rows_loc, int omit,
+                   int32_t* entries, int out_loc, uint64_t* slow_alloc) {
+  return guarded([&] {
+    need(c, "ctx");
+    if (H) need(entries, "entries");
+    rs::build_remap(c, table_id, H, hbm_rows, rows_by_rank, distinct, rows_loc, omit, entries, out_loc,
+                    slow_alloc);
+  });
+}
+
+int rs_simulate(rs_context* c, const rs_trace* tr, uint32_t ne, const rs_plan_entry* entries,
+                uint32_t nr, const rs_remap_view* remaps, const rs_system_spec* sys, uint64_t B,
+                rs_sim_report* out) {
+  return guarded([&] {
+    need(c, "ctx");
+    need(tr, "trace");
+    need(sys, "system");
+    need(out, "out");
+    rs::simulate(c, tr, ne, entries, nr, remaps, sys, B, out);
+  });
+}
+
+int rs_emb_create(rs_context* c, uint32_t T, const rs_emb_table* tabs, uint64_t max_batch,
+                  uint64_t max_lookups, int opt, float eps, rs_emb** out) {
+  return guarded([&] {
+    need(c, "ctx");
+    need(tabs, "tables");
+    need(out, "out");
+    *out = rs::emb_create(c, T, tabs, max_batch, max_lookups, opt, eps);
+  });
+}
+
+int rs_emb_destroy(rs_emb* e) {
+  return guarded([&] { rs::emb_free(e); });
+}
+
+int rs_emb_init_weights(rs_emb* e, uint64_t seed, float scale) {
+  return guarded([&] {
+    need(e, "emb");
+    rs::emb_init_weights(e, seed, scale);
+  });
+}
+
+int rs_emb_forward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx, float* pooled,
+                   uint64_t* hits) {
+  return guarded([&] {
+    need(e, "emb");
+    need(off, "offsets");
+    need(pooled, "pooled");
+    rs::emb_forward(e, B, off, idx, pooled, hits);
+  });
+}
+
+int rs_emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx,
+                    const float* grad, float lr) {
+  return guarded([&] {
+    need(e, "emb");
+    need(off, "offsets");
+    need(grad, "grad");
+    rs::emb_backward(e, B, off, idx, grad, lr);
+  });
+}
+
+int rs_emb_read_rows(rs_emb* e, uint32_t t, const uint32_t* rows, uint64_t n, float* out, float* mom) {
+  return guarded([&] {
+    need(e, "emb");
+    if (n) {
+      need(rows, "rows");
+      need(out, "out");
+    }
+    rs::emb_read_rows(e, t, rows, n, out, mom);
+  });
+}
+
+int rs_emb_memory(const rs_emb* e, uint64_t* hbm, uint64_t* host) {
+  return guarded([&] {
+    need(e, "emb");
+    rs::emb_memory(e, hbm, host);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,772 @@
+// HP2 — the tiered EmbeddingBag operator that serves a RecShard plan.
+//
+// No reference implementation exists (the paper ran FBGEMM); the
+// semantics follow the paper: sum-pool with an empty bag pooling to 0
+// (PAPER.md:275), fast and slow tier rows read inside the same kernel
+// (PAPER.md:605-607), the remap applied as part of the lookup (
+// encoding include/shardplan/remap.hpp:27-29).  The forward's fast/slow hit
+// counters equal simulate()'s accounting (core/src/simulator.cpp:86).
+//
+// HBM layout: per table a fast-tier block [hbm_rows, dim] fp32 in one device
+// pool, a slow-tier block [slow_rows, dim] fp32 in one pinned, mapped host
+// pool read zero-copy over PCIe, the int32 remap [hash_size] in HBM, and for
+// row-wise Adagrad one fp32 momentum per row in the row's tier.
+//
+// K4 forward: a G-lane group per bag (G = lanes to cover dim/4 float4s, <=32),
+//   32/G bags per warp, one table per warp.  Lanes load G indices and their
+//   remap entries in parallel, then the group issues 8 row gathers
+//   (128-bit ld.global.nc) before accumulating them in lookup order.
+// K5 backward: keys (row id) / values (sample) -> stable LSD radix sort ->
+//   fixed 64-position chunks: a warp reduces each row-segment piece in its
+//   chunk in sorted order; pieces crossing a chunk edge are combined by the
+//   owning chunk in chunk order.  Fully deterministic, no float atomics.
+#include <algorithm>
+#include <numeric>
+
+#include "../../include/shardplan_gpu.h"
+#include "context.cuh"
+
+namespace rs {
+namespace emb {
+
+struct TableDev {
+  const int32_t* remap;
+  float* fast;
+  float* slow;       // device view of pinned host memory
+  float* mom_fast;
+  float* mom_slow;
+  uint64_t hash_size;
+  uint64_t col;      // column offset in pooled rows
+  uint32_t dim;
+  uint32_t key_base; // backward key space offset
+  uint64_t hbm_rows;
+  uint64_t slow_rows;
+};
+
+__host__ __device__ inline int lanes_for(uint32_t dim) {
+  uint32_t v = dim / 4, L = 1;
+  while (L < v && L < 32) L <<= 1;
+  return int(L);
+}
+
+__device__ __forceinline__ float* row_ptr(const TableDev& td, int32_t e) {
+  return e >= 0 ? td.fast + uint64_t(e) * td.dim : td.slow + uint64_t(-int64_t(e) - 1) * td.dim;
+}
+__device__ __forceinline__ float* mom_ptr(const TableDev& td, int32_t e) {
+  return e >= 0 ? td.mom_fast + uint64_t(e) : td.mom_slow + uint64_t(-int64_t(e) - 1);
+}
+
+constexpr int kFwdThreads = 256;
+constexpr int kFwdUnroll = 8;
+
+template <int G, int VPL>
+__global__ void __launch_bounds__(kFwdThreads)
+forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__ cls_tables,
+               uint32_t ntab, uint64_t B, const uint32_t* __restrict__ offsets,
+               const uint32_t* __restrict__ indices, float* __restrict__ out, uint64_t stride,
+               unsigned long long* __restrict__ hits) {
+  constexpr int BPW = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / G, lg = lane % G;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
+  const uint64_t wpt = (B + BPW - 1) / BPW;
+  const uint64_t total_w = wpt * ntab;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < total_w; w += nwarps) {
+    const uint32_t t = cls_tables[w / wpt];
+    const TableDev td = tables[t];
+    const uint32_t V = td.dim >> 2;
+    const uint64_t b = (w % wpt) * BPW + grp;
+    const bool valid = b < B;
+    uint32_t s = 0, e = 0;
+    if (valid) {
+      s = offsets[uint64_t(t) * B + b];
+      e = offsets[uint64_t(t) * B + b + 1];
+    }
+    float4 acc[VPL];
+#pragma unroll
+    for (int vv = 0; vv < VPL; ++vv) acc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t fast = 0;
+    for (uint32_t base = s; base < e; base += G) {
+      const uint32_t n = min(uint32_t(G), e - base);
+      int32_t ent = 0;
+      if (uint32_t(lg) < n) {
+        const uint32_t idx = ld_stream_u32(indices + base + lg);
+        ent = td.remap[idx];
+        fast += ent >= 0;
+      }
+      for (uint32_t j = 0; j < n; j += kFwdUnroll) {
+        float4 v[kFwdUnroll][VPL];
+#pragma unroll
+        for (int u = 0; u < kFwdUnroll; ++u) {
+          const int32_t eu = __shfl_sync(gmask, ent, int(j) + u, G);
+          const float4* row = reinterpret_cast<const float4*>(row_ptr(td, eu));
+#pragma unroll
+          for (int vv = 0; vv < VPL; ++vv) {
+            const uint32_t vec = lg + vv * G;
+            v[u][vv] = (j + u < n && vec < V) ? ld_nc_f4(row + vec) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kFwdUnroll; ++u) {
+          if (j + u < n) {
+#pragma unroll
+            for (int vv = 0; vv < VPL; ++vv) {
+              acc[vv].x = __fadd_rn(acc[vv].x, v[u][vv].x);
+              acc[vv].y = __fadd_rn(acc[vv].y, v[u][vv].y);
+              acc[vv].z = __fadd_rn(acc[vv].z, v[u][vv].z);
+              acc[vv].w = __fadd_rn(acc[vv].w, v[u][vv].w);
+            }
+          }
+        }
+      }
+    }
+    if (valid) {
+      float4* o = reinterpret_cast<float4*>(out + b * stride + td.col);
+#pragma unroll
+      for (int vv = 0; vv < VPL; ++vv) {
+        const uint32_t vec = lg + vv * G;
+        if (vec < V) o[vec] = acc[vv];
+      }
+    }
+    if (hits) {
+      uint32_t tot = (valid && lg == 0) ? e - s : 0u;
+#pragma unroll
+      for (int o2 = 16; o2; o2 >>= 1) {
+        fast += __shfl_xor_sync(0xffffffffu, fast, o2);
+        tot += __shfl_xor_sync(0xffffffffu, tot, o2);
+      }
+      if (lane == 0 && tot) {
+        atomicAdd(&hits[2 * uint64_t(t)], (unsigned long long)fast);
+        atomicAdd(&hits[2 * uint64_t(t) + 1], (unsigned long long)(tot - fast));
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ backward
+// keys[l] = key_base[t] + index, vals[l] = sample b, for every lookup l of
+// bag (t, b); warps flatten 32 bags' lookups so stores stay coalesced.
+__global__ void __launch_bounds__(256)
+keygen_kernel(const TableDev* __restrict__ tables, uint32_t T, uint64_t B,
+              const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ indices,
+              uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, unsigned* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nbags = uint64_t(T) * B;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t c = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; c * 32 < nbags; c += nwarps) {
+    const uint64_t g = c * 32 + lane;
+    uint32_t s = 0, len = 0, kb = 0, t = 0;
+    uint64_t H = 0;
+    if (g < nbags) {
+      s = offsets[g];
+      len = offsets[g + 1] - s;
+      t = uint32_t(g / B);
+      kb = tables[t].key_base;
+      H = tables[t].hash_size;
+    }
+    const uint32_t incl = warp_incl_scan(len);
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t excl = incl - len;
+    const uint32_t s0 = __shfl_sync(0xffffffffu, s, 0);
+    for (uint32_t p = 0; p < total; p += 32) {
+      const uint32_t q = p + lane;
+      int k = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        uint32_t ex = __shfl_sync(0xffffffffu, excl, k + step);
+        if (ex <= q) k += step;
+      }
+      const uint32_t kbk = __shfl_sync(0xffffffffu, kb, k);
+      const uint64_t Hk = __shfl_sync(0xffffffffu, H, k);
+      const uint64_t gk = c * 32 + k;
+      if (q < total) {
+        const uint32_t l = s0 + q;  // bags are contiguous in table-major CSR
+        const uint32_t idx = indices[l];
+        if (idx >= Hk) atomicOr(err, 1u);
+        keys[l] = kb + (idx < Hk ? idx : 0u);
+        vals[l] = uint32_t(gk % B);
+      }
+    }
+  }
+}
+
+constexpr int kChunk = 64;
+
+struct BwdArgs {
+  const TableDev* tables;
+  const uint32_t* key_base_sorted;  // key_base per table, ascending (T entries)
+  uint32_t T;
+  const uint32_t* keys;
+  const uint32_t* vals;
+  uint64_t L;
+  const float* grad;
+  uint64_t stride;
+  float* part;       // [nchunks][2][dmax]
+  uint32_t dmax;
+  float lr, eps;
+  int opt;
+};
+
+__device__ __forceinline__ uint32_t table_of_key(const BwdArgs& a, uint32_t key) {
+  uint32_t lo = 0, hi = a.T;
+  while (lo + 1 < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (a.key_base_sorted[mid] <= key) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Apply the optimizer to one row with its full gradient g (VPL float4 per lane,
+// vec = lane + vv*32).  Arithmetic order matches or_emb_backward.
+template <int VPL>
+__device__ __forceinline__ void apply_update(const BwdArgs& a, const TableDev& td, uint32_t row,
+                                             const float4 (&g)[VPL]) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t V = td.dim >> 2;
+  const int32_t e = td.remap[row];
+  float4* w = reinterpret_cast<float4*>(row_ptr(td, e));
+  float mult = a.lr;
+  if (a.opt == RS_OPT_ROWWISE_ADAGRAD) {
+    float s = 0.f;
+#pragma unroll
+    for (int vv = 0; vv < VPL; ++vv) {
+      if (uint32_t(lane + vv * 32) < V) {
+        s = __fadd_rn(s, __fmul_rn(g[vv].x, g[vv].x));
+        s = __fadd_rn(s, __fmul_rn(g[vv].y, g[vv].y));
+        s = __fadd_rn(s, __fmul_rn(g[vv].z, g[vv].z));
+        s = __fadd_rn(s, __fmul_rn(g[vv].w, g[vv].w));
+      }
+    }
+    const int L = lanes_for(td.dim);
+    for (int o = L >> 1; o >= 1; o >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+    float* mp = mom_ptr(td, e);
+    const float m = __fadd_rn(*mp, __fdiv_rn(s, float(td.dim)));
+    __syncwarp();
+    if (lane == 0) *mp = m;
+    mult = __fdiv_rn(a.lr, __fadd_rn(__fsqrt_rn(m), a.eps));
+  }
+#pragma unroll
+  for (int vv = 0; vv < VPL; ++vv) {
+    const uint32_t vec = lane + vv * 32;
+    if (vec < V) {
+      float4 x = w[vec];
+      x.x = __fsub_rn(x.x, __fmul_rn(mult, g[vv].x));
+      x.y = __fsub_rn(x.y, __fmul_rn(mult, g[vv].y));
+      x.z = __fsub_rn(x.z, __fmul_rn(mult, g[vv].z));
+      x.w = __fsub_rn(x.w, __fmul_rn(mult, g[vv].w));
+      w[vec] = x;
+    }
+  }
+}
+
+template <int VPL>
+__device__ __forceinline__ void store_part(const BwdArgs& a, uint64_t chunk, int slot, uint32_t V,
+                                           const float4 (&g)[VPL]) {
+  const int lane = threadIdx.x & 31;
+  float4* p = reinterpret_cast<float4*>(a.part + (chunk * 2 + slot) * a.dmax);
+#pragma unroll
+  for (int vv = 0; vv < VPL; ++vv)
+    if (uint32_t(lane + vv * 32) < V) p[lane + vv * 32] = g[vv];
+}
+
+// One warp per chunk of kChunk sorted positions.
+template <int VPL>
+__global__ void __launch_bounds__(256) bwd_chunk_kernel(BwdArgs a) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nchunks = (a.L + kChunk - 1) / kChunk;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t c = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; c < nchunks; c += nwarps) {
+    const uint64_t c0 = c * kChunk;
+    const uint64_t c1 = min(c0 + kChunk, a.L);
+    uint32_t kr[kChunk / 32], vr[kChunk / 32];
+#pragma unroll
+    for (int h = 0; h < kChunk / 32; ++h) {
+      const uint64_t i = c0 + h * 32 + lane;
+      kr[h] = i < c1 ? a.keys[i] : 0xFFFFFFFFu;
+      vr[h] = i < c1 ? a.vals[i] : 0u;
+    }
+    const uint32_t key_before = c0 > 0 ? a.keys[c0 - 1] : 0xFFFFFFFFu;
+    const uint32_t key_after = c1 < a.L ? a.keys[c1] : 0xFFFFFFFFu;
+    uint32_t cur = __shfl_sync(0xffffffffu, kr[0], 0);
+    uint32_t t = table_of_key(a, cur);
+    TableDev td = a.tables[t];
+    uint32_t tend = t + 1 < a.T ? a.key_base_sorted[t + 1] : 0xFFFFFFFFu;
+    uint64_t piece_start = c0;
+    float4 acc[VPL];
+#pragma unroll
+    for (int vv = 0; vv < VPL; ++vv) acc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const uint32_t n = uint32_t(c1 - c0);
+    auto flush = [&](uint64_t pend) {
+      const bool before = piece_start == c0 && cur == key_before;
+      const bool after = pend == c1 && cur == key_after;
+      const uint32_t V = td.dim >> 2;
+      if (!before && !after) apply_update<VPL>(a, td, cur - td.key_base, acc);
+      else store_part<VPL>(a, c, before ? 0 : 1, V, acc);
+    };
+    for (uint32_t j = 0; j < n; j += 8) {
+      float4 v[8][VPL];
+      uint32_t ku[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t pos = j + u;
+        const uint32_t src = pos & 31;
+        uint32_t kk = 0, bb = 0;
+#pragma unroll
+        for (int h = 0; h < kChunk / 32; ++h) {
+          const uint32_t k2 = __shfl_sync(0xffffffffu, kr[h], src);
+          const uint32_t b2 = __shfl_sync(0xffffffffu, vr[h], src);
+          if (pos / 32 == uint32_t(h)) {
+            kk = k2;
+            bb = b2;
+          }
+        }
+        ku[u] = kk;
+        // table of this key (sorted keys: tables only advance)
+        uint32_t tt = t;
+        if (pos < n) {
+          while (kk >= (tt + 1 < a.T ? a.key_base_sorted[tt + 1] : 0xFFFFFFFFu)) ++tt;
+        }
+        const TableDev& tdu = a.tables[tt];
+        const float4* gr = reinterpret_cast<const float4*>(a.grad + uint64_t(bb) * a.stride + tdu.col);
+        const uint32_t Vu = tdu.dim >> 2;
+#pragma unroll
+        for (int vv = 0; vv < VPL; ++vv) {
+          const uint32_t vec = lane + vv * 32;
+          v[u][vv] = (pos < n && vec < Vu) ? ld_nc_f4(gr + vec) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t pos = j + u;
+        if (pos >= n) break;
+        if (ku[u] != cur) {
+          flush(c0 + pos);
+          cur = ku[u];
+          piece_start = c0 + pos;
+#pragma unroll
+          for (int vv = 0; vv < VPL; ++vv) acc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (cur >= tend) {
+            t = table_of_key(a, cur);
+            td = a.tables[t];
+            tend = t + 1 < a.T ? a.key_base_sorted[t + 1] : 0xFFFFFFFFu;
+          }
+        }
+#pragma unroll
+        for (int vv = 0; vv < VPL; ++vv) {
+          acc[vv].x = __fadd_rn(acc[vv].x, v[u][vv].x);
+          acc[vv].y = __fadd_rn(acc[vv].y, v[u][vv].y);
+          acc[vv].z = __fadd_rn(acc[vv].z, v[u][vv].z);
+          acc[vv].w = __fadd_rn(acc[vv].w, v[u][vv].w);
+        }
+      }
+    }
+    flush(c1);
+  }
+}
+
+// Segments that cross chunk edges: the chunk holding the segment's first
+// position sums its tail piece and the following chunks' head pieces in order.
+template <int VPL>
+__global__ void __launch_bounds__(256) bwd_finalize_kernel(BwdArgs a) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nchunks = (a.L + kChunk - 1) / kChunk;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t c = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; c < nchunks; c += nwarps) {
+    const uint64_t c0 = c * kChunk;
+    const uint64_t c1 = min(c0 + kChunk, a.L);
+    if (c1 >= a.L) continue;
+    const uint32_t kl = a.keys[c1 - 1];
+    if (a.keys[c1] != kl) continue;  // last segment ends inside this chunk
+    // does the segment start inside this chunk?
+    const bool starts_before = (a.keys[c0] == kl) && c0 > 0 && a.keys[c0 - 1] == kl;
+    if (starts_before) continue;
+    const uint32_t t = table_of_key(a, kl);
+    const TableDev td = a.tables[t];
+    const uint32_t V = td.dim >> 2;
+    float4 acc[VPL];
+    const float4* p = reinterpret_cast<const float4*>(a.part + (c * 2 + 1) * a.dmax);
+#pragma unroll
+    for (int vv = 0; vv < VPL; ++vv) {
+      const uint32_t vec = lane + vv * 32;
+      acc[vv] = vec < V ? p[vec] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (uint64_t c2 = c + 1; c2 < nchunks; ++c2) {
+      const float4* q = reinterpret_cast<const float4*>(a.part + (c2 * 2) * a.dmax);
+#pragma unroll
+      for (int vv = 0; vv < VPL; ++vv) {
+        const uint32_t vec = lane + vv * 32;
+        if (vec < V) {
+          const float4 x = q[vec];
+          acc[vv].x = __fadd_rn(acc[vv].x, x.x);
+          acc[vv].y = __fadd_rn(acc[vv].y, x.y);
+          acc[vv].z = __fadd_rn(acc[vv].z, x.z);
+          acc[vv].w = __fadd_rn(acc[vv].w, x.w);
+        }
+      }
+      const uint64_t e2 = min((c2 + 1) * kChunk, a.L);
+      if (e2 >= a.L || a.keys[e2] != kl || a.keys[e2 - 1] != kl) break;
+    }
+    apply_update<VPL>(a, td, kl - td.key_base, acc);
+  }
+}
+
+// ------------------------------------------------------------------ init / read
+__global__ void init_kernel(TableDev td, uint32_t table_id, uint64_t seed, float scale) {
+  const uint32_t V = td.dim >> 2;
+  const uint64_t n = td.hash_size * V;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t row = i / V;
+    const uint32_t vec = uint32_t(i % V);
+    const uint64_t ds = derive_stream(seed, table_id, row);
+    float x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t u = mix64(ds + vec * 4 + k) >> 40;
+      x[k] = __fmul_rn(__fsub_rn(__fmul_rn(float(u), 0x1.0p-24f), 0.5f), scale);
+    }
+    const int32_t e = td.remap[row];
+    float4* w = reinterpret_cast<float4*>(row_ptr(td, e));
+    w[vec] = make_float4(x[0], x[1], x[2], x[3]);
+    if (vec == 0 && td.mom_fast) *mom_ptr(td, e) = 0.f;
+  }
+}
+
+__global__ void read_rows_kernel(TableDev td, const uint32_t* __restrict__ rows, uint64_t n,
+                                 float* __restrict__ out, float* __restrict__ mom_out) {
+  const uint32_t V = td.dim >> 2;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n * V;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / V;
+    const uint32_t vec = uint32_t(i % V);
+    const int32_t e = td.remap[rows[r]];
+    reinterpret_cast<float4*>(out + r * td.dim)[vec] =
+        reinterpret_cast<const float4*>(row_ptr(td, e))[vec];
+    if (mom_out && vec == 0) mom_out[r] = td.mom_fast ? *mom_ptr(td, e) : 0.f;
+  }
+}
+
+__global__ void check_remap_kernel(const int32_t* __restrict__ remap, uint64_t H, uint64_t hbm_rows,
+                                   uint64_t slow_rows, unsigned* __restrict__ err) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < H;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const int32_t e = remap[i];
+    if (e >= 0 ? uint64_t(e) >= hbm_rows : uint64_t(-int64_t(e) - 1) >= slow_rows) atomicOr(err, 1u);
+  }
+}
+
+}  // namespace emb
+}  // namespace rs
+
+using rs::emb::TableDev;
+
+struct rs_emb {
+  rs_context* ctx = nullptr;
+  uint32_t T = 0;
+  uint64_t max_batch = 0, max_lookups = 0;
+  int opt = RS_OPT_SGD;
+  float eps = 1e-8f;
+  std::vector<TableDev> h_tables;
+  std::vector<uint32_t> table_ids;
+  TableDev* d_tables = nullptr;
+  uint64_t total_dim = 0;
+  uint32_t dmax = 0;
+  char* fast_pool = nullptr;
+  size_t fast_bytes = 0;
+  char* host_pool = nullptr;
+  char* host_pool_dev = nullptr;
+  size_t host_bytes = 0;
+  int32_t* remap_pool = nullptr;
+  size_t remap_bytes = 0;
+  // forward classes: (G, VPL) -> table list
+  struct Class {
+    int G, VPL;
+    std::vector<uint32_t> tables;
+    uint32_t* d_list = nullptr;
+  };
+  std::vector<Class> classes;
+  uint32_t* d_key_base_sorted = nullptr;
+  uint32_t key_bits = 0;
+  int bwd_vpl = 1;
+  // backward buffers
+  uint32_t* keys = nullptr;
+  uint32_t* vals = nullptr;
+  float* part = nullptr;
+  unsigned* d_err = nullptr;
+  char* sort_scratch = nullptr;
+  size_t sort_scratch_bytes = 0;
+
+  ~rs_emb() {
+    if (d_tables) cudaFree(d_tables);
+    if (fast_pool) cudaFree(fast_pool);
+    if (host_pool) cudaFreeHost(host_pool);
+    if (remap_pool) cudaFree(remap_pool);
+    for (auto& c : classes)
+      if (c.d_list) cudaFree(c.d_list);
+    if (d_key_base_sorted) cudaFree(d_key_base_sorted);
+    if (keys) cudaFree(keys);
+    if (vals) cudaFree(vals);
+    if (part) cudaFree(part);
+    if (d_err) cudaFree(d_err);
+    if (sort_scratch) cudaFree(sort_scratch);
+  }
+};
+
+namespace rs {
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64_t max_batch,
+                   uint64_t max_lookups, int opt, float eps) {
+  using namespace emb;
+  if (T == 0) throw InvalidArgument("emb: no tables");
+  if (opt != RS_OPT_SGD && opt != RS_OPT_ROWWISE_ADAGRAD) throw InvalidArgument("emb: unknown optimizer");
+  if (max_batch == 0) throw InvalidArgument("emb: max_batch must be >= 1");
+  if (max_lookups >= (uint64_t(1) << 32)) throw InvalidArgument("emb: max_lookups must be < 2^32");
+  auto* e = new rs_emb;
+  e->ctx = ctx;
+  e->T = T;
+  e->max_batch = max_batch;
+  e->max_lookups = max_lookups;
+  e->opt = opt;
+  e->eps = eps;
+  try {
+    cudaStream_t st = ctx->stream;
+    size_t fb = 0, hb = 0, rb = 0;
+    uint64_t key_acc = 0;
+    std::vector<size_t> foff(T), hoff(T), roff(T), mfoff(T), mhoff(T);
+    for (uint32_t t = 0; t < T; ++t) {
+      const rs_emb_table& x = tabs[t];
+      if (x.dim == 0 || x.dim % 4 || x.dim > 1024)
+        throw InvalidArgument("emb: table " + std::to_string(x.table_id) + ": dim must be a multiple of 4 in [4, 1024]");
+      if (x.hash_size == 0 || x.hash_size > 0x7FFFFFFFULL)
+        throw InvalidArgument("emb: table " + std::to_string(x.table_id) + ": hash_size out of range");
+      if (x.hbm_rows > x.hash_size) throw InvalidArgument("emb: hbm_rows exceeds hash_size");
+      if (!x.remap) throw InvalidArgument("emb: table " + std::to_string(x.table_id) + " has no remap");
+      foff[t] = fb;
+      fb += align256(x.hbm_rows * x.dim * 4);
+      hoff[t] = hb;
+      hb += align256(x.slow_rows * x.dim * 4);
+      roff[t] = rb;
+      rb += align256(x.hash_size * 4);
+      e->total_dim += x.dim;
+      e->dmax = std::max(e->dmax, x.dim);
+      e->table_ids.push_back(x.table_id);
+      if (key_acc + x.hash_size > 0x7FFFFFFFULL)
+        throw InvalidArgument("emb: sum of hash sizes must be < 2^31 per operator (split the tables)");
+      key_acc += x.hash_size;
+    }
+    if (opt == RS_OPT_ROWWISE_ADAGRAD) {
+      for (uint32_t t = 0; t < T; ++t) {
+        mfoff[t] = fb;
+        fb += align256(tabs[t].hbm_rows * 4);
+        mhoff[t] = hb;
+        hb += align256(tabs[t].slow_rows * 4);
+      }
+    }
+    e->fast_bytes = std::max<size_t>(fb, 256);
+    e->host_bytes = std::max<size_t>(hb, 256);
+    e->remap_bytes = rb;
+    RS_CUDA(cudaMalloc(&e->fast_pool, e->fast_bytes));
+    RS_CUDA(cudaHostAlloc(&e->host_pool, e->host_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    RS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->host_pool_dev), e->host_pool, 0));
+    RS_CUDA(cudaMalloc(&e->remap_pool, std::max<size_t>(rb, 256)));
+    RS_CUDA(cudaMalloc(&e->d_err, 16));
+    uint64_t col = 0;
+    uint32_t kb = 0;
+    e->h_tables.resize(T);
+    for (uint32_t t = 0; t < T; ++t) {
+      const rs_emb_table& x = tabs[t];
+      TableDev& d = e->h_tables[t];
+      d.remap = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(e->remap_pool) + roff[t]);
+      RS_CUDA(cudaMemcpyAsync(const_cast<int32_t*>(d.remap), x.remap, x.hash_size * 4,
+                              x.remap_location == RS_MEM_DEVICE ? cudaMemcpyDeviceToDevice
+                                                                : cudaMemcpyHostToDevice,
+                              st));
+      d.fast = reinterpret_cast<float*>(e->fast_pool + foff[t]);
+      d.slow = reinterpret_cast<float*>(e->host_pool_dev + hoff[t]);
+      d.mom_fast = opt == RS_OPT_ROWWISE_ADAGRAD ? reinterpret_cast<float*>(e->fast_pool + mfoff[t]) : nullptr;
+      d.mom_slow = opt == RS_OPT_ROWWISE_ADAGRAD ? reinterpret_cast<float*>(e->host_pool_dev + mhoff[t]) : nullptr;
+      d.hash_size = x.hash_size;
+      d.col = col;
+      d.dim = x.dim;
+      d.key_base = kb;
+      d.hbm_rows = x.hbm_rows;
+      d.slow_rows = x.slow_rows;
+      col += x.dim;
+      kb += uint32_t(x.hash_size);
+      // every remap entry must land inside its tier's allocation
+      RS_CUDA(cudaMemsetAsync(e->d_err, 0, 4, st));
+      unsigned g = unsigned(std::min<uint64_t>((x.hash_size + 255) / 256, uint64_t(sm_count()) * 8));
+      check_remap_kernel<<<std::max(1u, g), 256, 0, st>>>(d.remap, x.hash_size, x.hbm_rows, x.slow_rows, e->d_err);
+      unsigned herr = 0;
+      RS_CUDA(cudaMemcpyAsync(&herr, e->d_err, 4, cudaMemcpyDeviceToHost, st));
+      RS_CUDA(cudaStreamSynchronize(st));
+      if (herr)
+        throw InvalidArgument("emb: table " + std::to_string(x.table_id) +
+                              ": remap entry outside the fast/slow tier sizes");
+    }
+    e->key_bits = 1;
+    while (e->key_bits < 32 && (uint64_t(1) << e->key_bits) < uint64_t(kb)) ++e->key_bits;
+    RS_CUDA(cudaMalloc(&e->d_tables, sizeof(TableDev) * T));
+    RS_CUDA(cudaMemcpyAsync(e->d_tables, e->h_tables.data(), sizeof(TableDev) * T, cudaMemcpyHostToDevice, st));
+    std::vector<uint32_t> kbs(T);
+    for (uint32_t t = 0; t < T; ++t) kbs[t] = e->h_tables[t].key_base;
+    RS_CUDA(cudaMalloc(&e->d_key_base_sorted, 4 * T));
+    RS_CUDA(cudaMemcpyAsync(e->d_key_base_sorted, kbs.data(), 4 * T, cudaMemcpyHostToDevice, st));
+    // forward classes
+    for (uint32_t t = 0; t < T; ++t) {
+      const int G = lanes_for(tabs[t].dim);
+      const int VPL = int((tabs[t].dim / 4 + G - 1) / G);
+      int vp2 = 1;
+      while (vp2 < VPL) vp2 <<= 1;
+      auto it = std::find_if(e->classes.begin(), e->classes.end(),
+                             [&](const rs_emb::Class& c) { return c.G == G && c.VPL == vp2; });
+      if (it == e->classes.end()) {
+        e->classes.push_back({G, vp2, {}, nullptr});
+        it = e->classes.end() - 1;
+      }
+      it->tables.push_back(t);
+    }
+    for (auto& c : e->classes) {
+      RS_CUDA(cudaMalloc(&c.d_list, 4 * c.tables.size()));
+      RS_CUDA(cudaMemcpyAsync(c.d_list, c.tables.data(), 4 * c.tables.size(), cudaMemcpyHostToDevice, st));
+    }
+    {
+      int v = 1;
+      while (v * 32 * 4 < int(e->dmax)) v <<= 1;
+      e->bwd_vpl = v;
+    }
+    // backward buffers
+    const size_t L = std::max<uint64_t>(max_lookups, 1);
+    RS_CUDA(cudaMalloc(&e->keys, L * 4));
+    RS_CUDA(cudaMalloc(&e->vals, L * 4));
+    const size_t nch = (L + emb::kChunk - 1) / emb::kChunk;
+    RS_CUDA(cudaMalloc(&e->part, nch * 2 * e->dmax * 4));
+    e->sort_scratch_bytes = radix_sort_scratch_bytes(L) + (4 << 20);
+    RS_CUDA(cudaMalloc(&e->sort_scratch, e->sort_scratch_bytes));
+    RS_CUDA(cudaStreamSynchronize(st));
+  } catch (...) {
+    delete e;
+    throw;
+  }
+  return e;
+}
+
+void emb_init_weights(rs_emb* e, uint64_t seed, float scale) {
+  cudaStream_t st = e->ctx->stream;
+  for (uint32_t t = 0; t < e->T; ++t) {
+    const TableDev& d = e->h_tables[t];
+    const uint64_t n = d.hash_size * (d.dim / 4);
+    unsigned g = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(sm_count()) * 16));
+    emb::init_kernel<<<std::max(1u, g), 256, 0, st>>>(d, e->table_ids[t], seed, scale);
+  }
+  RS_LAUNCH_CHECK();
+}
+
+template <int G, int VPL>
+static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint32_t* off,
+                       const uint32_t* idx, float* out, unsigned long long* hits) {
+  constexpr int BPW = 32 / G;
+  const uint64_t warps = (B + BPW - 1) / BPW * c.tables.size();
+  const uint64_t blocks = (warps * 32 + emb::kFwdThreads - 1) / emb::kFwdThreads;
+  const unsigned grid = unsigned(std::min<uint64_t>(blocks, uint64_t(sm_count()) * 64));
+  emb::forward_kernel<G, VPL><<<std::max(1u, grid), emb::kFwdThreads, 0, e->ctx->stream>>>(
+      e->d_tables, c.d_list, uint32_t(c.tables.size()), B, off, idx, out, e->total_dim, hits);
+}
+
+void emb_forward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx, float* out,
+                 uint64_t* hits) {
+  if (B == 0 || B > e->max_batch) throw InvalidArgument("emb_forward: batch outside [1, max_batch]");
+  auto* h = reinterpret_cast<unsigned long long*>(hits);
+  for (const auto& c : e->classes) {
+    switch (c.G * 100 + c.VPL) {
+      case 101: launch_fwd<1, 1>(e, c, B, off, idx, out, h); break;
+      case 201: launch_fwd<2, 1>(e, c, B, off, idx, out, h); break;
+      case 401: launch_fwd<4, 1>(e, c, B, off, idx, out, h); break;
+      case 801: launch_fwd<8, 1>(e, c, B, off, idx, out, h); break;
+      case 1601: launch_fwd<16, 1>(e, c, B, off, idx, out, h); break;
+      case 3201: launch_fwd<32, 1>(e, c, B, off, idx, out, h); break;
+      case 3202: launch_fwd<32, 2>(e, c, B, off, idx, out, h); break;
+      case 3204: launch_fwd<32, 4>(e, c, B, off, idx, out, h); break;
+      case 3208: launch_fwd<32, 8>(e, c, B, off, idx, out, h); break;
+      default: throw Error(-9, "emb_forward: unsupported lane class");
+    }
+  }
+  RS_LAUNCH_CHECK();
+}
+
+template <int VPL>
+static void launch_bwd(rs_emb* e, const emb::BwdArgs& a) {
+  const uint64_t nch = (a.L + emb::kChunk - 1) / emb::kChunk;
+  const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((nch + 7) / 8, uint64_t(sm_count()) * 32)));
+  emb::bwd_chunk_kernel<VPL><<<grid, 256, 0, e->ctx->stream>>>(a);
+  emb::bwd_finalize_kernel<VPL><<<grid, 256, 0, e->ctx->stream>>>(a);
+}
+
+void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx, const float* grad,
+                  float lr) {
+  if (B == 0 || B > e->max_batch) throw InvalidArgument("emb_backward: batch outside [1, max_batch]");
+  cudaStream_t st = e->ctx->stream;
+  uint32_t L = 0;
+  RS_CUDA(cudaMemcpyAsync(&L, off + uint64_t(e->T) * B, 4, cudaMemcpyDeviceToHost, st));
+  uint32_t L0 = 0;
+  RS_CUDA(cudaMemcpyAsync(&L0, off, 4, cudaMemcpyDeviceToHost, st));
+  RS_CUDA(cudaStreamSynchronize(st));
+  if (L0 != 0) throw InvalidArgument("emb_backward: offsets must start at 0");
+  if (L > e->max_lookups) throw InvalidArgument("emb_backward: more lookups than max_lookups");
+  if (L == 0) return;
+  RS_CUDA(cudaMemsetAsync(e->d_err, 0, 4, st));
+  {
+    const uint64_t nb = uint64_t(e->T) * B;
+    unsigned g = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((nb / 32 + 7) / 8, uint64_t(sm_count()) * 16)));
+    emb::keygen_kernel<<<g, 256, 0, st>>>(e->d_tables, e->T, B, off, idx, e->keys, e->vals, e->d_err);
+  }
+  Scratch scr;
+  scr.base = e->sort_scratch;
+  scr.cap = e->sort_scratch_bytes;
+  radix_sort_pairs(e->keys, e->vals, L, int(e->key_bits), scr, st);
+  emb::BwdArgs a{e->d_tables, e->d_key_base_sorted, e->T, e->keys, e->vals, L, grad,
+                 e->total_dim, e->part, e->dmax, lr, e->eps, e->opt};
+  switch (e->bwd_vpl) {
+    case 1: launch_bwd<1>(e, a); break;
+    case 2: launch_bwd<2>(e, a); break;
+    case 4: launch_bwd<4>(e, a); break;
+    case 8: launch_bwd<8>(e, a); break;
+    default: throw Error(-9, "emb_backward: unsupported dim");
+  }
+  RS_LAUNCH_CHECK();
+}
+
+void emb_read_rows(rs_emb* e, uint32_t t, const uint32_t* rows, uint64_t n, float* out, float* mom) {
+  if (t >= e->T) throw InvalidArgument("emb_read_rows: table index out of range");
+  cudaStream_t st = e->ctx->stream;
+  const TableDev& d = e->h_tables[t];
+  for (uint64_t i = 0; i < n; ++i)
+    if (rows[i] >= d.hash_size) throw InvalidArgument("emb_read_rows: row out of range");
+  if (n == 0) return;
+  Scratch scr = e->ctx->scratch(n * (4 + 4 + size_t(d.dim) * 4) + (1 << 20));
+  uint32_t* d_rows = stage(rows, n, false, scr, st);
+  float* d_out = scr.take<float>(n * d.dim);
+  float* d_mom = scr.take<float>(n);
+  unsigned g = unsigned(std::min<uint64_t>((n * d.dim / 4 + 255) / 256, uint64_t(sm_count()) * 8));
+  emb::read_rows_kernel<<<std::max(1u, g), 256, 0, st>>>(d, d_rows, n, d_out, d_mom);
+  RS_LAUNCH_CHECK();
+  RS_CUDA(cudaMemcpyAsync(out, d_out, n * d.dim * 4, cudaMemcpyDeviceToHost, st));
+  if (mom) RS_CUDA(cudaMemcpyAsync(mom, d_mom, n * 4, cudaMemcpyDeviceToHost, st));
+  RS_CUDA(cudaStreamSynchronize(st));
+}
+
+void emb_free(rs_emb* e) {
+  if (e) cudaStreamSynchronize(e->ctx->stream);
+  delete e;
+}
+
+void emb_memory(const rs_emb* e, uint64_t* hbm, uint64_t* host) {
+  if (hbm) *hbm = e->fast_bytes + e->remap_bytes;
+  if (host) *host = e->host_bytes;
+}
+
+}  // namespace rs

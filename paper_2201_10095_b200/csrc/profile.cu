@@ -1,0 +1,648 @@
+// HP1 — the training-data profiler on the GPU.
+//
+//   K0 hash_ids      raw u64 -> mix64(raw) % H           inc/workload.hpp:28-31
+//   K1 hash_hist     per-sample selection + per-row histogram
+//                                                        core/src/profiler.cpp:68-112
+//   K2 rank          compact accessed rows -> stable radix sort on (table,
+//                    count desc) over row-ascending input -> u64 prefix ->
+//                    access_cdf + 101-step ICDF          core/src/profiler.cpp:114-159
+//
+// Bit-exactness: every count is an exact integer; access_cdf is the IEEE
+// division double(cum)/double(total) of exact u64s (correctly rounded on both
+// CPU and GPU); the ICDF uses the reference's integer test
+// 100*prefix(k) >= i*total (core/src/profiler.cpp:38).
+#include <algorithm>
+#include <numeric>
+
+#include "../../include/shardplan_gpu.h"
+#include "context.cuh"
+
+struct rs_profile {
+  uint32_t J = 0;
+  uint64_t selected = 0;
+  std::vector<uint32_t> table_ids;
+  std::vector<double> coverage, avg_pooling;
+  std::vector<uint64_t> distinct, total, present;
+  std::vector<uint64_t> icdf;   // J * 101
+  std::vector<uint64_t> start;  // J + 1 offsets into rows / cdf
+  std::vector<uint32_t> rows;
+  std::vector<double> cdf;
+  uint32_t* d_rows = nullptr;
+  ~rs_profile() {
+    if (d_rows) cudaFree(d_rows);
+  }
+};
+
+namespace rs {
+namespace prof {
+
+constexpr uint64_t kProfileStream = 0x70726f66ULL;  // "prof", profiler.cpp:29
+constexpr int kHistThreads = 256;
+constexpr uint32_t kMaxSmemTables = 4096;
+constexpr unsigned kErrUnknownTable = 1u;
+constexpr unsigned kErrRowRange = 2u;
+
+__device__ __forceinline__ int lookup_table(const uint32_t* __restrict__ sorted_ids,
+                                            const uint32_t* __restrict__ sorted_idx,
+                                            uint32_t J, uint32_t id) {
+  uint32_t lo = 0, hi = J;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (sorted_ids[mid] < id) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < J && sorted_ids[lo] == id) ? int(sorted_idx[lo]) : -1;
+}
+
+__device__ __forceinline__ bool sample_selected(uint64_t s, double rate, uint64_t seed) {
+  return rate >= 1.0 || first_double(derive_stream(seed, s, kProfileStream)) < rate;
+}
+
+// |{s < S : selected(s)}| — the coverage denominator (profiler.cpp:68-74).
+__global__ void count_selected(uint64_t S, double rate, uint64_t seed,
+                               unsigned long long* out) {
+  uint64_t c = 0;
+  for (uint64_t s = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; s < S;
+       s += uint64_t(gridDim.x) * blockDim.x)
+    c += sample_selected(s, rate, seed);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
+
+struct Tables {
+  const uint32_t* sorted_ids;
+  const uint32_t* sorted_idx;
+  const uint64_t* base;   // counter offset of table index t (group-local)
+  const uint64_t* hsize;
+  const uint64_t* magic;
+  uint32_t J;
+  uint32_t t_lo, t_hi;    // table-index range counted by this launch
+};
+
+// K1.  Each warp takes 32 records, scans their (selected) lengths, then walks
+// the flattened id stream 32 ids at a time so every lane has work and the id
+// loads are coalesced whenever records are contiguous (the generator's
+// layout).  AGG: warp-aggregate same-row increments with match.any before the
+// global atomic, which takes the Zipf head off the L2 atomic unit.
+template <bool RAW, bool AGG>
+__global__ void __launch_bounds__(kHistThreads)
+hash_hist(const uint64_t* __restrict__ rec_sample, const uint32_t* __restrict__ rec_table,
+          const uint64_t* __restrict__ rec_offset, const uint32_t* __restrict__ rec_len,
+          uint64_t R, const uint32_t* __restrict__ ids, const uint64_t* __restrict__ raw,
+          Tables tp, double rate, uint64_t seed, bool count_records,
+          uint32_t* __restrict__ counters, unsigned long long* __restrict__ present,
+          unsigned long long* __restrict__ accesses, unsigned* __restrict__ err) {
+  extern __shared__ uint32_t sm[];
+  const bool use_sm = count_records && tp.J <= kMaxSmemTables;
+  uint32_t* pres_s = sm;
+  uint32_t* acc_s = sm + (use_sm ? tp.J : 0);
+  if (use_sm)
+    for (uint32_t i = threadIdx.x; i < 2 * tp.J; i += blockDim.x) sm[i] = 0;
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t c = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; c * 32 < R;
+       c += nwarps) {
+    const uint64_t r = c * 32 + lane;
+    uint32_t len = 0;
+    uint64_t off = 0;
+    int t = 0;
+    if (r < R && sample_selected(rec_sample[r], rate, seed)) {
+      t = lookup_table(tp.sorted_ids, tp.sorted_idx, tp.J, rec_table[r]);
+      if (t < 0) {
+        atomicOr(err, kErrUnknownTable);
+        t = 0;
+      } else {
+        len = rec_len[r];
+        off = rec_offset[r];
+        if (count_records) {
+          if (use_sm) {
+            atomicAdd(&pres_s[t], 1u);
+            atomicAdd(&acc_s[t], len);
+          } else {
+            atomicAdd(&present[t], 1ull);
+            atomicAdd(&accesses[t], (unsigned long long)len);
+          }
+        }
+        if (uint32_t(t) < tp.t_lo || uint32_t(t) >= tp.t_hi) len = 0;
+      }
+    }
+    const uint32_t incl = warp_incl_scan(len);
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t excl = incl - len;
+    for (uint32_t p = 0; p < total; p += 32) {
+      const uint32_t q = p + lane;
+      int k = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        uint32_t e = __shfl_sync(0xffffffffu, excl, k + step);
+        if (e <= q) k += step;
+      }
+      const uint64_t offk = __shfl_sync(0xffffffffu, off, k);
+      const uint32_t exk = __shfl_sync(0xffffffffu, excl, k);
+      const int tk = __shfl_sync(0xffffffffu, t, k);
+      bool ok = q < total;
+      uint64_t addr = 0;
+      if (ok) {
+        const uint64_t idx = offk + (q - exk);
+        const uint64_t H = tp.hsize[tk];
+        uint64_t row;
+        if (RAW) row = fast_mod(mix64(raw[idx]), H, tp.magic[tk]);
+        else row = ld_stream_u32(ids + idx);
+        if (row >= H) {
+          atomicOr(err, kErrRowRange);
+          ok = false;
+        } else {
+          addr = tp.base[tk] + row;
+        }
+      }
+      if (AGG) {
+        const unsigned am = __ballot_sync(0xffffffffu, ok);
+        if (ok) {
+          const unsigned peers = __match_any_sync(am, addr);
+          if ((peers & lanemask_lt()) == 0) atomicAdd(&counters[addr], uint32_t(__popc(peers)));
+        }
+      } else if (ok) {
+        atomicAdd(&counters[addr], 1u);
+      }
+    }
+  }
+  if (use_sm) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < tp.J; i += blockDim.x) {
+      if (pres_s[i]) atomicAdd(&present[i], (unsigned long long)pres_s[i]);
+      if (acc_s[i]) atomicAdd(&accesses[i], (unsigned long long)acc_s[i]);
+    }
+  }
+}
+
+// K0 — batched hash_value.
+__global__ void hash_ids_kernel(const uint64_t* __restrict__ raw, uint64_t n, uint64_t H,
+                                uint64_t magic, uint32_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    out[i] = uint32_t(fast_mod(mix64(raw[i]), H, magic));
+}
+
+// ------------------------------------------------------------------ K2
+// Compaction of accessed rows.  Pass 1: per-tile nonzero counts + global max.
+__global__ void __launch_bounds__(kScanThreads)
+nz_tile_sums(const uint32_t* __restrict__ c, size_t n, uint32_t* __restrict__ sums,
+             unsigned* __restrict__ maxc) {
+  const size_t base = size_t(blockIdx.x) * kScanTile + size_t(threadIdx.x) * kScanItems;
+  uint32_t s = 0, m = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    size_t k = base + i;
+    uint32_t v = k < n ? c[k] : 0u;
+    s += v != 0;
+    m = max(m, v);
+  }
+  uint32_t tot;
+  block_excl_scan<uint32_t, kScanThreads>(s, tot);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(maxc, m);
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+// Pass 2: scatter (key = table << cbits | (maxc - count), value = row) in row
+// order, so a stable ascending sort yields (table asc, count desc, row asc).
+__global__ void __launch_bounds__(kScanThreads)
+nz_scatter(const uint32_t* __restrict__ c, size_t n, const uint32_t* __restrict__ tile_pre,
+           const uint64_t* __restrict__ base, uint32_t J, int cbits, uint32_t maxc,
+           uint32_t* __restrict__ keys, uint32_t* __restrict__ rows) {
+  const size_t k0 = size_t(blockIdx.x) * kScanTile + size_t(threadIdx.x) * kScanItems;
+  uint32_t v[kScanItems];
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    size_t k = k0 + i;
+    v[i] = k < n ? c[k] : 0u;
+    s += v[i] != 0;
+  }
+  uint32_t tot;
+  uint32_t pos = block_excl_scan<uint32_t, kScanThreads>(s, tot) + tile_pre[blockIdx.x];
+  if (s == 0) return;
+  // table of k0 (binary search once, then walk forward)
+  uint32_t lo = 0, hi = J;
+  while (lo + 1 < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (base[mid] <= k0) lo = mid;
+    else hi = mid;
+  }
+  uint32_t t = lo;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    size_t k = k0 + i;
+    if (v[i]) {
+      while (t + 1 < J && base[t + 1] <= k) ++t;
+      keys[pos] = (cbits >= 32 ? 0u : (uint32_t(t) << cbits)) | (maxc - v[i]);
+      rows[pos] = uint32_t(k - base[t]);
+      ++pos;
+    }
+  }
+}
+
+struct CountOfKey {
+  const uint32_t* keys;
+  uint32_t cmask, maxc;
+  __device__ __forceinline__ uint64_t operator()(size_t i) const {
+    return uint64_t(maxc - (keys[i] & cmask));
+  }
+};
+
+__device__ __forceinline__ uint32_t key_table(uint32_t key, int cbits) {
+  return cbits >= 32 ? 0u : key >> cbits;
+}
+
+// tstart[t] = first compacted index of table t (tstart[J] = n).
+__global__ void table_starts(const uint32_t* __restrict__ keys, size_t n, int cbits, uint32_t J,
+                             uint64_t* __restrict__ tstart) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i <= n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const int prev = i == 0 ? -1 : int(key_table(keys[i - 1], cbits));
+    const int cur = i == n ? int(J) : int(key_table(keys[i], cbits));
+    for (int t = prev + 1; t <= cur; ++t) tstart[t] = i;
+  }
+}
+
+// access_cdf[i] = double(cum_t(i)) / double(total_t), cum inclusive within table.
+__global__ void cdf_kernel(const uint32_t* __restrict__ keys, size_t n, int cbits, uint32_t maxc,
+                           const uint64_t* __restrict__ cum_excl, const uint64_t* __restrict__ tstart,
+                           const unsigned long long* __restrict__ totals, double* __restrict__ cdf) {
+  const uint32_t cmask = cbits >= 32 ? ~0u : ((1u << cbits) - 1u);
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    uint32_t key = keys[i];
+    uint32_t t = key_table(key, cbits);
+    uint64_t cnt = maxc - (key & cmask);
+    uint64_t cum = cum_excl[i] + cnt - cum_excl[tstart[t]];
+    cdf[i] = double(cum) / double(totals[t]);
+  }
+}
+
+// icdf[t][p] = min k : 100 * prefix(k) >= p * total  (profiler.cpp:31-45),
+// found by binary search over the inclusive prefix; icdf[t][0] = 0.
+__global__ void icdf_kernel(const uint64_t* __restrict__ cum_excl, const uint64_t* __restrict__ tstart,
+                            const unsigned long long* __restrict__ totals, uint32_t J,
+                            uint64_t* __restrict__ icdf) {
+  const uint32_t t = blockIdx.x;
+  const int p = threadIdx.x;
+  if (t >= J || p > 100) return;
+  const uint64_t total = totals[t];
+  if (p == 0 || total == 0) {
+    icdf[size_t(t) * 101 + p] = 0;
+    return;
+  }
+  const uint64_t s = tstart[t], e = tstart[t + 1], c0 = cum_excl[s];
+  const uint64_t need = uint64_t(p) * total;
+  // smallest k in [1, e-s] with 100 * (cum_excl[s+k] - c0) >= need
+  uint64_t lo = 1, hi = e - s;
+  while (lo < hi) {
+    uint64_t mid = (lo + hi) >> 1;
+    if ((cum_excl[s + mid] - c0) * 100 >= need) hi = mid;
+    else lo = mid + 1;
+  }
+  icdf[size_t(t) * 101 + p] = lo;
+}
+
+struct RankDevice {
+  uint32_t* rows;     // n
+  double* cdf;        // n
+  uint64_t* icdf;     // J * 101
+  uint64_t* tstart;   // J + 1
+  size_t n;
+};
+
+inline int bits_for(uint64_t v) {  // bits needed to represent values 0..v
+  int b = 0;
+  while (b < 64 && (v >> b)) ++b;
+  return b;
+}
+
+// K2 over one table group's u32 counters (table-major, h_base[J] offsets).
+// totals: device per-table totals (the reference's st.total_accesses).
+inline RankDevice rank_group(rs_context* ctx, Scratch& scr, const uint32_t* d_counters,
+                             const std::vector<uint64_t>& h_base, uint32_t J,
+                             const unsigned long long* d_totals) {
+  cudaStream_t st = ctx->stream;
+  const size_t n = h_base[J];
+  const size_t tiles = (n + kScanTile - 1) / kScanTile;
+  uint64_t* d_base = stage(h_base.data(), h_base.size(), false, scr, st);
+  uint32_t* sums = scr.take<uint32_t>(tiles + 1);
+  unsigned* d_max = scr.take<unsigned>(2);
+  uint32_t* d_total = reinterpret_cast<uint32_t*>(d_max + 1);
+  RS_CUDA(cudaMemsetAsync(d_max, 0, 2 * sizeof(unsigned), st));
+  if (tiles) {
+    nz_tile_sums<<<unsigned(tiles), kScanThreads, 0, st>>>(d_counters, n, sums, d_max);
+    scan_sums_inplace<uint32_t>(sums, tiles, d_total, scr, st);
+  }
+  unsigned* h2 = ctx->pinned_buf<unsigned>(2);
+  RS_CUDA(cudaMemcpyAsync(h2, d_max, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  ctx->sync();
+  const uint32_t maxc = h2[0];
+  const size_t nd = h2[1];
+  const int cbits = std::max(1, bits_for(maxc));
+  const int tbits = bits_for(J > 0 ? J - 1 : 0);
+  if (cbits + tbits > 32)
+    throw Error(-9, "rank: table/count key exceeds 32 bits; split the table group");
+
+  RankDevice out{};
+  out.n = nd;
+  out.rows = scr.take<uint32_t>(nd + 1);
+  out.cdf = scr.take<double>(nd + 1);
+  out.icdf = scr.take<uint64_t>(size_t(J) * 101);
+  out.tstart = scr.take<uint64_t>(J + 1);
+  uint32_t* keys = scr.take<uint32_t>(nd + 1);
+  if (tiles && nd)
+    nz_scatter<<<unsigned(tiles), kScanThreads, 0, st>>>(d_counters, n, sums, d_base, J, cbits,
+                                                         maxc, keys, out.rows);
+  radix_sort_pairs(keys, out.rows, nd, cbits + tbits, scr, st);
+  uint64_t* cum = scr.take<uint64_t>(nd + 1);
+  exclusive_scan<uint64_t>(CountOfKey{keys, cbits >= 32 ? ~0u : ((1u << cbits) - 1u), maxc}, nd,
+                           cum, cum + nd, scr, st);
+  const int g = std::max(1, int(std::min<size_t>((nd + 255) / 256, size_t(sm_count()) * 8)));
+  table_starts<<<g, 256, 0, st>>>(keys, nd, cbits, J, out.tstart);
+  if (nd) cdf_kernel<<<g, 256, 0, st>>>(keys, nd, cbits, maxc, cum, out.tstart, d_totals, out.cdf);
+  if (J) icdf_kernel<<<J, 128, 0, st>>>(cum, out.tstart, d_totals, J, out.icdf);
+  RS_LAUNCH_CHECK();
+  return out;
+}
+
+}  // namespace prof
+
+// ------------------------------------------------------------------ host API
+rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64_t seed) {
+  using namespace prof;
+  if (!tr) throw InvalidArgument("profile: trace is null");
+  if (tr->num_samples < 1 || tr->num_tables == 0)  // profiler.cpp:62-63
+    throw InvalidArgument("profile: trace is empty");
+  if (!(rate > 0.0 && rate <= 1.0))  // profiler.cpp:64-65
+    throw InvalidArgument("profile: sample_rate must be in (0, 1]");
+  if ((tr->ids == nullptr) == (tr->raw_ids == nullptr))
+    throw InvalidArgument("profile: exactly one of ids / raw_ids must be given");
+  const uint32_t J = tr->num_tables;
+  const bool raw = tr->raw_ids != nullptr;
+  const bool on_dev = tr->location == RS_MEM_DEVICE;
+  const uint64_t R = tr->num_records, N = tr->num_ids;
+  if (N >= (uint64_t(1) << 32))
+    throw InvalidArgument("profile: more than 2^32-1 ids per call (u32 row counters)");
+  for (uint32_t j = 0; j < J; ++j) {
+    if (tr->tables[j].hash_size < 1 || tr->tables[j].hash_size > 0x7FFFFFFFULL)
+      throw InvalidArgument("profile: table hash_size must be in [1, 2^31-1]");
+  }
+  cudaStream_t st = ctx->stream;
+
+  // table-id lookup (sorted ids -> index), per-table hash params
+  std::vector<uint32_t> order(J);
+  std::iota(order.begin(), order.end(), 0u);
+  std::sort(order.begin(), order.end(),
+            [&](uint32_t a, uint32_t b) { return tr->tables[a].table_id < tr->tables[b].table_id; });
+  std::vector<uint32_t> sids(J), sidx(J);
+  std::vector<uint64_t> hs(J), mg(J);
+  for (uint32_t i = 0; i < J; ++i) {
+    sids[i] = tr->tables[order[i]].table_id;
+    sidx[i] = order[i];
+  }
+  for (uint32_t j = 0; j < J; ++j) {
+    hs[j] = tr->tables[j].hash_size;
+    mg[j] = FastMod::make(hs[j]).m;
+  }
+  // table groups: sum(H) per group < 2^31 (u32 compaction positions / keys)
+  std::vector<uint32_t> gstart{0};
+  {
+    uint64_t acc = 0;
+    for (uint32_t j = 0; j < J; ++j) {
+      if (acc + hs[j] > 0x7FFFFFFFULL && j > gstart.back()) {
+        gstart.push_back(j);
+        acc = 0;
+      }
+      acc += hs[j];
+    }
+    gstart.push_back(J);
+  }
+  uint64_t maxH = 0;
+  for (size_t g = 0; g + 1 < gstart.size(); ++g) {
+    uint64_t s = 0;
+    for (uint32_t j = gstart[g]; j < gstart[g + 1]; ++j) s += hs[j];
+    maxH = std::max(maxH, s);
+  }
+
+  size_t need = Scratch::bytes_for(R, 8) * 2 + Scratch::bytes_for(R, 4) * 2 +
+                Scratch::bytes_for(N, raw ? 8 : 4) + Scratch::bytes_for(J, 8) * 8 +
+                Scratch::bytes_for(maxH + 1, 4) * 6 + Scratch::bytes_for(maxH + 1, 8) * 3 +
+                radix_sort_scratch_bytes(maxH + 1) + (size_t(J) * 101 + 4096) * 8 + (8 << 20);
+  Scratch scr = ctx->scratch(need);
+
+  const uint64_t* d_rs = on_dev ? tr->rec_sample : stage(tr->rec_sample, R, false, scr, st);
+  const uint32_t* d_rt = on_dev ? tr->rec_table : stage(tr->rec_table, R, false, scr, st);
+  const uint64_t* d_ro = on_dev ? tr->rec_offset : stage(tr->rec_offset, R, false, scr, st);
+  const uint32_t* d_rl = on_dev ? tr->rec_len : stage(tr->rec_len, R, false, scr, st);
+  const uint32_t* d_ids = nullptr;
+  const uint64_t* d_raw = nullptr;
+  if (raw) d_raw = on_dev ? tr->raw_ids : stage(tr->raw_ids, N, false, scr, st);
+  else d_ids = on_dev ? tr->ids : stage(tr->ids, N, false, scr, st);
+
+  uint32_t* d_sids = stage(sids.data(), J, false, scr, st);
+  uint32_t* d_sidx = stage(sidx.data(), J, false, scr, st);
+  uint64_t* d_hs = stage(hs.data(), J, false, scr, st);
+  uint64_t* d_mg = stage(mg.data(), J, false, scr, st);
+  auto* d_pres = scr.take<unsigned long long>(J);
+  auto* d_acc = scr.take<unsigned long long>(J);
+  auto* d_sel = scr.take<unsigned long long>(1);
+  auto* d_err = scr.take<unsigned>(1);
+  RS_CUDA(cudaMemsetAsync(d_pres, 0, J * 8, st));
+  RS_CUDA(cudaMemsetAsync(d_acc, 0, J * 8, st));
+  RS_CUDA(cudaMemsetAsync(d_sel, 0, 8, st));
+  RS_CUDA(cudaMemsetAsync(d_err, 0, 4, st));
+
+  const int sms = sm_count();
+  {
+    unsigned g = unsigned(std::min<uint64_t>((tr->num_samples + 255) / 256, uint64_t(sms) * 8));
+    count_selected<<<std::max(1u, g), 256, 0, st>>>(tr->num_samples, rate, seed, d_sel);
+  }
+
+  auto* res = new rs_profile;
+  res->J = J;
+  res->table_ids.resize(J);
+  res->coverage.resize(J);
+  res->avg_pooling.resize(J);
+  res->distinct.assign(J, 0);
+  res->total.assign(J, 0);
+  res->present.assign(J, 0);
+  res->icdf.assign(size_t(J) * 101, 0);
+  res->start.assign(J + 1, 0);
+  try {
+    std::vector<uint64_t> h_tot(J), h_pres(J);
+    unsigned h_err = 0;
+    unsigned long long h_sel = 0;
+    std::vector<std::vector<uint32_t>> g_rows;
+    std::vector<std::vector<double>> g_cdf;
+    for (size_t g = 0; g + 1 < gstart.size(); ++g) {
+      const uint32_t t_lo = gstart[g], t_hi = gstart[g + 1], Jg = t_hi - t_lo;
+      size_t mark = scr.used;
+      std::vector<uint64_t> base_all(J, 0), base_g(Jg + 1, 0);
+      for (uint32_t j = t_lo; j < t_hi; ++j) base_g[j - t_lo + 1] = base_g[j - t_lo] + hs[j];
+      for (uint32_t j = t_lo; j < t_hi; ++j) base_all[j] = base_g[j - t_lo];
+      uint64_t* d_base = stage(base_all.data(), J, false, scr, st);
+      uint32_t* d_cnt = scr.take<uint32_t>(base_g[Jg] + 1);
+      RS_CUDA(cudaMemsetAsync(d_cnt, 0, base_g[Jg] * 4, st));
+      Tables tp{d_sids, d_sidx, d_base, d_hs, d_mg, J, t_lo, t_hi};
+      const uint64_t warps = (R + 31) / 32;
+      unsigned grid = unsigned(std::min<uint64_t>((warps + 7) / 8, uint64_t(sms) * 8));
+      grid = std::max(1u, grid);
+      size_t smem = J <= kMaxSmemTables ? size_t(J) * 8 : 0;
+      const bool cr = g == 0;
+      if (raw)
+        hash_hist<true, true><<<grid, kHistThreads, smem, st>>>(d_rs, d_rt, d_ro, d_rl, R, d_ids,
+                                                               d_raw, tp, rate, seed, cr, d_cnt,
+                                                               d_pres, d_acc, d_err);
+      else
+        hash_hist<false, true><<<grid, kHistThreads, smem, st>>>(d_rs, d_rt, d_ro, d_rl, R, d_ids,
+                                                                d_raw, tp, rate, seed, cr, d_cnt,
+                                                                d_pres, d_acc, d_err);
+      RS_LAUNCH_CHECK();
+      if (g == 0) {
+        // errors, selection and per-table totals are known after the first group
+        auto* hb = ctx->pinned_buf<uint64_t>(2 * size_t(J) + 2);
+        RS_CUDA(cudaMemcpyAsync(hb, d_acc, J * 8, cudaMemcpyDeviceToHost, st));
+        RS_CUDA(cudaMemcpyAsync(hb + J, d_pres, J * 8, cudaMemcpyDeviceToHost, st));
+        RS_CUDA(cudaMemcpyAsync(hb + 2 * J, d_sel, 8, cudaMemcpyDeviceToHost, st));
+        RS_CUDA(cudaMemcpyAsync(hb + 2 * J + 1, d_err, 4, cudaMemcpyDeviceToHost, st));
+        ctx->sync();
+        for (uint32_t j = 0; j < J; ++j) {
+          h_tot[j] = hb[j];
+          h_pres[j] = hb[J + j];
+        }
+        h_sel = hb[2 * J];
+        h_err = uint32_t(hb[2 * J + 1]);
+        if (h_sel == 0) throw InvalidArgument("profile: sample selected zero samples");
+        if (h_err & kErrUnknownTable)
+          throw OutOfRange("profile: record references a table id absent from trace.tables");
+        if (h_err & kErrRowRange)
+          throw InvalidArgument("profile: hashed id outside its table's hash_size");
+      }
+      RankDevice rk = rank_group(ctx, scr, d_cnt, base_g, Jg, d_acc + t_lo);
+      std::vector<uint64_t> tstart(Jg + 1);
+      g_rows.emplace_back(rk.n);
+      g_cdf.emplace_back(rk.n);
+      RS_CUDA(cudaMemcpyAsync(tstart.data(), rk.tstart, (Jg + 1) * 8, cudaMemcpyDeviceToHost, st));
+      RS_CUDA(cudaMemcpyAsync(res->icdf.data() + size_t(t_lo) * 101, rk.icdf,
+                              size_t(Jg) * 101 * 8, cudaMemcpyDeviceToHost, st));
+      if (rk.n) {
+        RS_CUDA(cudaMemcpyAsync(g_rows.back().data(), rk.rows, rk.n * 4, cudaMemcpyDeviceToHost, st));
+        RS_CUDA(cudaMemcpyAsync(g_cdf.back().data(), rk.cdf, rk.n * 8, cudaMemcpyDeviceToHost, st));
+      }
+      ctx->sync();
+      for (uint32_t j = t_lo; j < t_hi; ++j) res->distinct[j] = tstart[j - t_lo + 1] - tstart[j - t_lo];
+      scr.used = mark;
+    }
+    // assemble (tables are group-contiguous, so concatenation keeps order)
+    for (uint32_t j = 0; j < J; ++j) res->start[j + 1] = res->start[j] + res->distinct[j];
+    res->rows.reserve(res->start[J]);
+    res->cdf.reserve(res->start[J]);
+    for (size_t g = 0; g < g_rows.size(); ++g) {
+      res->rows.insert(res->rows.end(), g_rows[g].begin(), g_rows[g].end());
+      res->cdf.insert(res->cdf.end(), g_cdf[g].begin(), g_cdf[g].end());
+    }
+    res->selected = h_sel;
+    for (uint32_t j = 0; j < J; ++j) {  // profiler.cpp:114-121
+      res->table_ids[j] = tr->tables[j].table_id;
+      res->total[j] = h_tot[j];
+      res->present[j] = h_pres[j];
+      res->coverage[j] = double(h_pres[j]) / double(h_sel);
+      res->avg_pooling[j] = h_pres[j] ? double(h_tot[j]) / double(h_pres[j]) : 0.0;
+    }
+    const size_t nd = res->rows.size();
+    RS_CUDA(cudaMalloc(&res->d_rows, (nd ? nd : 1) * 4));
+    if (nd)
+      RS_CUDA(cudaMemcpyAsync(res->d_rows, res->rows.data(), nd * 4, cudaMemcpyHostToDevice, st));
+    ctx->sync();
+  } catch (...) {
+    delete res;
+    throw;
+  }
+  return res;
+}
+
+void hash_ids(rs_context* ctx, const uint64_t* raw, uint64_t n, uint64_t H, uint32_t* out,
+              int location) {
+  if (H == 0) throw InvalidArgument("hash_value: hash_size must be >= 1");
+  if (H > 0xFFFFFFFFULL)
+    throw InvalidArgument("hash_ids: hash_size must be < 2^32 (u32 rows)");
+  if (n == 0) return;
+  cudaStream_t st = ctx->stream;
+  Scratch scr = ctx->scratch(location == RS_MEM_DEVICE ? 4096 : n * 12 + 4096);
+  const uint64_t* d_raw = location == RS_MEM_DEVICE ? raw : stage(raw, n, false, scr, st);
+  uint32_t* d_out = location == RS_MEM_DEVICE ? out : scr.take<uint32_t>(n);
+  unsigned g = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(sm_count()) * 16));
+  prof::hash_ids_kernel<<<g, 256, 0, st>>>(d_raw, n, H, FastMod::make(H).m, d_out);
+  RS_LAUNCH_CHECK();
+  if (location != RS_MEM_DEVICE) {
+    RS_CUDA(cudaMemcpyAsync(out, d_out, n * 4, cudaMemcpyDeviceToHost, st));
+    ctx->sync();
+  }
+}
+
+uint32_t profile_tables(const rs_profile* p) { return p->J; }
+uint64_t profile_selected(const rs_profile* p) { return p->selected; }
+void profile_free(rs_profile* p) { delete p; }
+
+void profile_view(const rs_profile* p, uint32_t j, rs_feature_stats* o) {
+  if (j >= p->J) throw InvalidArgument("profile: table index out of range");
+  o->table_id = p->table_ids[j];
+  o->coverage = p->coverage[j];
+  o->avg_pooling = p->avg_pooling[j];
+  o->distinct_rows_accessed = p->distinct[j];
+  o->total_accesses = p->total[j];
+  o->icdf_steps = p->icdf.data() + size_t(j) * 101;
+  o->access_cdf = p->cdf.data() + p->start[j];
+  o->rows_by_rank = p->rows.data() + p->start[j];
+  o->d_rows_by_rank = p->d_rows + p->start[j];
+}
+
+__global__ void narrow_counts(const uint64_t* __restrict__ in, uint64_t n, uint32_t* __restrict__ out,
+                              unsigned long long* __restrict__ total, unsigned* __restrict__ err) {
+  uint64_t s = 0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    uint64_t v = in[i];
+    if (v > 0xFFFFFFFFULL) atomicOr(err, 1u);
+    out[i] = uint32_t(v);
+    s += v;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(total, (unsigned long long)s);
+}
+
+void build_icdf(rs_context* ctx, const uint64_t* counts, uint64_t n, int location, uint64_t* out101) {
+  cudaStream_t st = ctx->stream;
+  Scratch scr = ctx->scratch(n * 40 + radix_sort_scratch_bytes(n + 1) + (8 << 20));
+  const uint64_t* d_in = location == RS_MEM_DEVICE ? counts : stage(counts, n, false, scr, st);
+  uint32_t* d_c = scr.take<uint32_t>(n + 1);
+  auto* d_tot = scr.take<unsigned long long>(1);
+  auto* d_err = scr.take<unsigned>(1);
+  RS_CUDA(cudaMemsetAsync(d_tot, 0, 8, st));
+  RS_CUDA(cudaMemsetAsync(d_err, 0, 4, st));
+  if (n) {
+    unsigned g = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(sm_count()) * 8));
+    narrow_counts<<<g, 256, 0, st>>>(d_in, n, d_c, d_tot, d_err);
+    RS_LAUNCH_CHECK();
+  }
+  auto* hb = ctx->pinned_buf<uint64_t>(2);
+  RS_CUDA(cudaMemcpyAsync(hb, d_tot, 8, cudaMemcpyDeviceToHost, st));
+  RS_CUDA(cudaMemcpyAsync(hb + 1, d_err, 4, cudaMemcpyDeviceToHost, st));
+  ctx->sync();
+  if (hb[0] == 0) throw InvalidArgument("build_icdf: all access counts are zero");  // :52-53
+  if (uint32_t(hb[1])) throw InvalidArgument("build_icdf: per-row counts must be < 2^32");
+  std::vector<uint64_t> base{0, n};
+  prof::RankDevice rk = prof::rank_group(ctx, scr, d_c, base, 1, d_tot);
+  RS_CUDA(cudaMemcpyAsync(out101, rk.icdf, 101 * 8, cudaMemcpyDeviceToHost, st));
+  ctx->sync();
+}
+
+}  // namespace rs

@@ -1,0 +1,331 @@
+// Device-wide scan and stable LSD radix sort (hand-written, sm_100a).
+//
+// Used by the profiler's rank stage (K2: stable sort by descending count over
+// row-ascending input gives the reference's (count desc, row asc) order,
+// core/src/profiler.cpp:136-139) and by the EmbeddingBag backward (K5: stable
+// sort of lookups by row so each row's gradient is reduced in a fixed order).
+//
+// Scan: reduce-then-scan in three launches (tile sums -> single-CTA scan of
+// tile sums -> tile scan + carry-in).  Radix sort: 8-bit digits, per pass
+// upsweep (per-tile digit counts) -> scan of the digit-major count matrix ->
+// downsweep (stable in-tile ranking with warp ballots, scatter).  No atomics
+// and no inter-CTA spinning, so there is no forward-progress hazard.
+#pragma once
+
+#include "common.cuh"
+
+namespace rs {
+
+// ----------------------------------------------------------------- scratch
+// Minimal bump allocator over a caller-owned device arena.
+struct Scratch {
+  char* base = nullptr;
+  size_t cap = 0;
+  size_t used = 0;
+  template <class T>
+  T* take(size_t n) {
+    size_t off = (used + 255) & ~size_t(255);
+    size_t bytes = n * sizeof(T);
+    if (off + bytes > cap)
+      throw Error(-9, "scratch arena exhausted (" + std::to_string(off + bytes) +
+                          " > " + std::to_string(cap) + " bytes)");
+    used = off + bytes;
+    return reinterpret_cast<T*>(base + off);
+  }
+  static size_t bytes_for(size_t n, size_t elem) { return ((n * elem + 255) & ~size_t(255)); }
+};
+
+// ----------------------------------------------------------------- scan
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;  // 4096
+
+template <class T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan of one value per thread; returns the block total
+// in `total`.  Safe to call repeatedly (trailing barrier guards the smem).
+template <class T, int NT>
+__device__ __forceinline__ T block_excl_scan(T v, T& total) {
+  __shared__ T warp_tot[NT / 32];
+  __shared__ T tot_s;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  T inc = warp_incl_scan(v);
+  if (lane == 31) warp_tot[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    T x = lane < NT / 32 ? warp_tot[lane] : T(0);
+    T xi = warp_incl_scan(x);
+    if (lane < NT / 32) warp_tot[lane] = xi - x;
+    if (lane == 31) tot_s = xi;
+  }
+  __syncthreads();
+  T res = inc - v + warp_tot[w];
+  total = tot_s;
+  __syncthreads();
+  return res;
+}
+
+// in[i] may be read through a transform (e.g. "count != 0" flags).
+template <class T, class In>
+__global__ void __launch_bounds__(kScanThreads) scan_tile_sums(In in, size_t n, T* tile_sums) {
+  const size_t base = size_t(blockIdx.x) * kScanTile;
+  T s = 0;
+#pragma unroll 4
+  for (int i = 0; i < kScanItems; ++i) {
+    size_t k = base + size_t(i) * kScanThreads + threadIdx.x;
+    if (k < n) s += T(in(k));
+  }
+  T tot;
+  block_excl_scan<T, kScanThreads>(s, tot);
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
+}
+
+// Single CTA exclusive scan of tile sums (n <= 1024 * 64).
+template <class T>
+__global__ void __launch_bounds__(1024) scan_tile_sums_excl(T* sums, size_t n, T* grand_total) {
+  const int per = int((n + 1023) / 1024);
+  T loc[64];
+  T s = 0;
+  for (int i = 0; i < per; ++i) {
+    size_t k = size_t(threadIdx.x) * per + i;
+    loc[i] = k < n ? sums[k] : T(0);
+    s += loc[i];
+  }
+  T tot;
+  T pre = block_excl_scan<T, 1024>(s, tot);
+  for (int i = 0; i < per; ++i) {
+    size_t k = size_t(threadIdx.x) * per + i;
+    if (k < n) sums[k] = pre;
+    pre += loc[i];
+  }
+  if (threadIdx.x == 0 && grand_total) *grand_total = tot;
+}
+
+// Exclusive scan of a tile with carry-in; elements are processed in
+// blocked-per-thread order so each thread owns kScanItems consecutive items.
+template <class T, class In>
+__global__ void __launch_bounds__(kScanThreads) scan_tiles(In in, size_t n, const T* tile_pre, T* out) {
+  const size_t base = size_t(blockIdx.x) * kScanTile + size_t(threadIdx.x) * kScanItems;
+  T v[kScanItems];
+  T s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    size_t k = base + i;
+    v[i] = k < n ? T(in(k)) : T(0);
+    s += v[i];
+  }
+  T tot;
+  T pre = block_excl_scan<T, kScanThreads>(s, tot) + tile_pre[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    size_t k = base + i;
+    if (k < n) out[k] = pre;
+    pre += v[i];
+  }
+}
+
+template <class T>
+struct ArrayIn {
+  const T* p;
+  __device__ __forceinline__ T operator()(size_t k) const { return p[k]; }
+};
+
+inline size_t scan_scratch_bytes(size_t n, size_t elem) {
+  size_t tiles = (n + kScanTile - 1) / kScanTile;
+  return Scratch::bytes_for(tiles + 1, elem) * 3 + 4096;
+}
+
+template <class T, class In>
+void exclusive_scan(In in, size_t n, T* out, T* total, Scratch& scr, cudaStream_t st);
+
+// In-place exclusive scan of per-tile sums (single CTA when it fits, else
+// recursively through exclusive_scan).
+template <class T>
+void scan_sums_inplace(T* sums, size_t tiles, T* total, Scratch& scr, cudaStream_t st) {
+  if (tiles <= size_t(1024) * 64) {
+    scan_tile_sums_excl<T><<<1, 1024, 0, st>>>(sums, tiles, total);
+    RS_LAUNCH_CHECK();
+    return;
+  }
+  size_t mark = scr.used;
+  T* tmp = scr.take<T>(tiles);
+  exclusive_scan<T>(ArrayIn<T>{sums}, tiles, tmp, total, scr, st);
+  RS_CUDA(cudaMemcpyAsync(sums, tmp, tiles * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  scr.used = mark;
+}
+
+// out[k] = sum_{i<k} in(i); optionally *total (device) = sum of all.
+template <class T, class In>
+void exclusive_scan(In in, size_t n, T* out, T* total, Scratch& scr, cudaStream_t st) {
+  size_t tiles = (n + kScanTile - 1) / kScanTile;
+  if (tiles == 0) {
+    if (total) RS_CUDA(cudaMemsetAsync(total, 0, sizeof(T), st));
+    return;
+  }
+  size_t mark = scr.used;
+  T* sums = scr.take<T>(tiles);
+  scan_tile_sums<T, In><<<unsigned(tiles), kScanThreads, 0, st>>>(in, n, sums);
+  scan_sums_inplace<T>(sums, tiles, total, scr, st);
+  scan_tiles<T, In><<<unsigned(tiles), kScanThreads, 0, st>>>(in, n, sums, out);
+  RS_LAUNCH_CHECK();
+  scr.used = mark;
+}
+
+// ----------------------------------------------------------------- radix sort
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortItems = 8;                       // rounds per warp
+constexpr int kSortTile = kSortThreads * kSortItems;  // 2048 keys per CTA
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
+
+// Peers of this lane with the same `bits`-wide digit, via bit-split ballots.
+template <int BITS>
+__device__ __forceinline__ unsigned digit_peers(unsigned d, bool valid) {
+  unsigned m = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+    unsigned bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+    m &= ((d >> b) & 1u) ? bb : ~bb;
+  }
+  return valid ? m : 0u;
+}
+
+// Per-tile digit counts, written digit-major: counts[d * ntiles + tile].
+static __global__ void __launch_bounds__(kSortThreads)
+radix_upsweep(const uint32_t* __restrict__ keys, size_t n, int shift, int nbits,
+              uint32_t* __restrict__ counts, unsigned ntiles) {
+  __shared__ uint32_t wc[kSortWarps][kRadix];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = lane; i < kRadix; i += 32) wc[w][i] = 0;
+  __syncwarp();
+  const unsigned mask = (1u << nbits) - 1u;
+  const size_t wbase = size_t(blockIdx.x) * kSortTile + size_t(w) * 32 * kSortItems;
+#pragma unroll
+  for (int r = 0; r < kSortItems; ++r) {
+    size_t k = wbase + size_t(r) * 32 + lane;
+    bool valid = k < n;
+    unsigned d = valid ? (keys[k] >> shift) & mask : 0u;
+    unsigned peers = digit_peers<kRadixBits>(d, valid);
+    if (valid && (peers & lanemask_lt()) == 0) wc[w][d] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < kRadix; d += kSortThreads) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int ww = 0; ww < kSortWarps; ++ww) s += wc[ww][d];
+    counts[size_t(d) * ntiles + blockIdx.x] = s;
+  }
+}
+
+// Stable scatter: offsets[d * ntiles + tile] holds the global start of digit d
+// for this tile (exclusive scan of the digit-major count matrix).
+template <bool HAS_VALUES>
+static __global__ void __launch_bounds__(kSortThreads)
+radix_downsweep(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+                size_t n, int shift, int nbits, const uint32_t* __restrict__ offsets,
+                unsigned ntiles, uint32_t* __restrict__ keys_out,
+                uint32_t* __restrict__ vals_out) {
+  __shared__ uint32_t wc[kSortWarps][kRadix];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = lane; i < kRadix; i += 32) wc[w][i] = 0;
+  __syncwarp();
+  const unsigned mask = (1u << nbits) - 1u;
+  const size_t wbase = size_t(blockIdx.x) * kSortTile + size_t(w) * 32 * kSortItems;
+  uint32_t kk[kSortItems], vv[kSortItems], rank[kSortItems];
+#pragma unroll
+  for (int r = 0; r < kSortItems; ++r) {
+    size_t k = wbase + size_t(r) * 32 + lane;
+    bool valid = k < n;
+    kk[r] = valid ? keys_in[k] : 0u;
+    if (HAS_VALUES) vv[r] = valid ? vals_in[k] : 0u;
+    unsigned d = (kk[r] >> shift) & mask;
+    unsigned peers = digit_peers<kRadixBits>(d, valid);
+    unsigned leader = peers ? __ffs(peers) - 1 : 0;
+    uint32_t base = 0;
+    if (valid && lane == int(leader)) base = wc[w][d];
+    // every lane fetches the base from its own leader
+    uint32_t b2 = __shfl_sync(0xffffffffu, base, leader);
+    rank[r] = b2 + __popc(peers & lanemask_lt());
+    if (valid && lane == int(leader)) wc[w][d] = base + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per-digit exclusive offsets across warps, plus this tile's global base
+  for (int d = threadIdx.x; d < kRadix; d += kSortThreads) {
+    uint32_t run = offsets[size_t(d) * ntiles + blockIdx.x];
+#pragma unroll
+    for (int ww = 0; ww < kSortWarps; ++ww) {
+      uint32_t c = wc[ww][d];
+      wc[ww][d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kSortItems; ++r) {
+    size_t k = wbase + size_t(r) * 32 + lane;
+    if (k < n) {
+      unsigned d = (kk[r] >> shift) & mask;
+      uint32_t pos = wc[w][d] + rank[r];
+      keys_out[pos] = kk[r];
+      if (HAS_VALUES) vals_out[pos] = vv[r];
+    }
+  }
+}
+
+inline size_t radix_sort_scratch_bytes(size_t n) {
+  size_t tiles = (n + kSortTile - 1) / kSortTile;
+  size_t cnt = tiles * kRadix;
+  return Scratch::bytes_for(cnt, 4) * 2 + scan_scratch_bytes(cnt, 4) +
+         Scratch::bytes_for(n, 4) * 2 + 4096;
+}
+
+// Stable ascending sort of (keys, vals) on bits [0, end_bit).  Sorted data
+// ends in (keys, vals) — ping-pong buffers come from scratch.  n < 2^32.
+inline void radix_sort_pairs(uint32_t* keys, uint32_t* vals, size_t n, int end_bit,
+                             Scratch& scr, cudaStream_t st) {
+  if (n <= 1 || end_bit <= 0) return;
+  if (n >= (size_t(1) << 32)) throw Error(-1, "radix_sort_pairs: n >= 2^32");
+  const unsigned ntiles = unsigned((n + kSortTile - 1) / kSortTile);
+  size_t mark = scr.used;
+  uint32_t* counts = scr.take<uint32_t>(size_t(ntiles) * kRadix);
+  uint32_t* offs = scr.take<uint32_t>(size_t(ntiles) * kRadix);
+  uint32_t* k2 = scr.take<uint32_t>(n);
+  uint32_t* v2 = vals ? scr.take<uint32_t>(n) : nullptr;
+  uint32_t *ki = keys, *vi = vals, *ko = k2, *vo = v2;
+  for (int shift = 0; shift < end_bit; shift += kRadixBits) {
+    int nb = end_bit - shift < kRadixBits ? end_bit - shift : kRadixBits;
+    radix_upsweep<<<ntiles, kSortThreads, 0, st>>>(ki, n, shift, nb, counts, ntiles);
+    size_t m2 = scr.used;
+    exclusive_scan<uint32_t>(ArrayIn<uint32_t>{counts}, size_t(ntiles) * kRadix, offs,
+                             (uint32_t*)nullptr, scr, st);
+    scr.used = m2;
+    if (vals)
+      radix_downsweep<true><<<ntiles, kSortThreads, 0, st>>>(ki, vi, n, shift, nb, offs,
+                                                             ntiles, ko, vo);
+    else
+      radix_downsweep<false><<<ntiles, kSortThreads, 0, st>>>(ki, nullptr, n, shift, nb,
+                                                              offs, ntiles, ko, nullptr);
+    RS_LAUNCH_CHECK();
+    std::swap(ki, ko);
+    std::swap(vi, vo);
+  }
+  if (ki != keys) {
+    RS_CUDA(cudaMemcpyAsync(keys, ki, n * 4, cudaMemcpyDeviceToDevice, st));
+    if (vals) RS_CUDA(cudaMemcpyAsync(vals, vi, n * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  scr.used = mark;
+}
+
+}  // namespace rs

@@ -1,0 +1,135 @@
+"""GPU parity: HP1 profiler kernels (K0 hash, K1 histogram, K2 rank/CDF/ICDF)
+against the reference goldens and the oracle — bit-exact."""
+import numpy as np
+import pytest
+
+from conftest import assert_stats_equal, golden_stats, golden_trace, load_golden
+
+import paper_2201_10095_b200 as sp
+from paper_2201_10095_b200.types import TableSpec, Trace
+
+pytestmark = pytest.mark.gpu
+
+
+def test_hash_ids_goldens(cuda_ctx):
+    cases = load_golden("hash_value.json")["cases"]
+    by_h = {}
+    for raw, H, want in cases:
+        by_h.setdefault(int(H), []).append((int(raw), int(want)))
+    for H, rows in by_h.items():
+        if H > 0xFFFFFFFF:
+            continue
+        raw = np.array([r for r, _ in rows], np.uint64)
+        got = sp.hash_ids(raw, H, ctx=cuda_ctx)
+        assert list(got) == [w for _, w in rows]
+
+
+def test_hash_ids_device_large(cuda_ctx, coracle):
+    import torch
+
+    rng = np.random.default_rng(1)
+    raw = rng.integers(0, 2**63, 1 << 20, dtype=np.int64).astype(np.uint64) * np.uint64(2) + np.uint64(1)
+    for H in (1, 7, 1_000_000, 99_999_989, 0x7FFFFFFF):
+        got = sp.hash_ids(torch.from_numpy(raw.view(np.int64)).cuda(), H, ctx=cuda_ctx)
+        assert np.array_equal(got.cpu().numpy().view(np.uint32), coracle.hash_batch(raw, H))
+
+
+@pytest.mark.parametrize("name", list(load_golden("profile.json")))
+def test_profile_goldens(cuda_ctx, name):
+    case = load_golden("profile.json")[name]
+    tr = golden_trace(case["trace"], case.get("raw_ids"))
+    got = sp.profile(tr, case["rate"], case["seed"], ctx=cuda_ctx)
+    assert_stats_equal(got, golden_stats(case["stats"]))
+
+
+def test_profile_device_trace_and_hash_utilization(cuda_ctx):
+    import torch
+
+    case = load_golden("profile.json")["generated_r1.0_s0"]
+    tr = golden_trace(case["trace"])
+    dev = Trace(tr.tables, tr.num_samples,
+                *[torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a.view(np.int32)).cuda()
+                  for a in (tr.rec_sample, tr.rec_table, tr.rec_offset, tr.rec_len, tr.ids)])
+    got = sp.profile(dev, 1.0, 0, ctx=cuda_ctx)
+    assert_stats_equal(got, golden_stats(case["stats"]))
+    for st, spec, draw in zip(got, tr.tables, case["distinct_raw"]):
+        s, c = sp.hash_utilization(st, spec, draw)
+        assert s == (spec.hash_size - st.distinct_rows_accessed) / spec.hash_size
+        assert c == (draw - st.distinct_rows_accessed) / spec.hash_size
+
+
+def test_profile_errors(cuda_ctx):
+    case = load_golden("profile.json")["worked_example"]
+    tr = golden_trace(case["trace"])
+    with pytest.raises(sp.InvalidArgument):
+        sp.profile(tr, 0.0, 0, ctx=cuda_ctx)
+    with pytest.raises(sp.InvalidArgument):
+        sp.profile(tr, 1.5, 0, ctx=cuda_ctx)
+    with pytest.raises(sp.InvalidArgument):  # selects zero samples
+        sp.profile(tr, 1e-12, 0, ctx=cuda_ctx)
+    empty = Trace([], 0, np.zeros(0, np.uint64), np.zeros(0, np.uint32), np.zeros(0, np.uint64),
+                  np.zeros(0, np.uint32), ids=np.zeros(0, np.uint32))
+    with pytest.raises(sp.InvalidArgument):
+        sp.profile(empty, 0.5, 0, ctx=cuda_ctx)
+    bad = Trace(tr.tables[:1], tr.num_samples, tr.rec_sample, tr.rec_table, tr.rec_offset,
+                tr.rec_len, ids=tr.ids)
+    with pytest.raises(sp.TableIndexError):  # std::out_of_range, profiler.cpp:103
+        sp.profile(bad, 1.0, 0, ctx=cuda_ctx)
+
+
+def test_build_icdf_goldens(cuda_ctx):
+    for case in load_golden("build_icdf.json")["cases"]:
+        assert list(sp.build_icdf(case["counts"], ctx=cuda_ctx)) == case["icdf"]
+    with pytest.raises(sp.InvalidArgument):
+        sp.build_icdf([0, 0, 0], ctx=cuda_ctx)
+
+
+def _zipf_trace(rng, J, H, S, pool, alpha=1.05):
+    """Hashed Zipf trace in the reference layout (records sample-major)."""
+    ranks = np.arange(1, 200_001, dtype=np.float64)
+    p = ranks ** -alpha
+    p /= p.sum()
+    tables = [TableSpec(j * 2 + 1, 200_000, H, 64, 4) for j in range(J)]
+    R = S * J
+    rec_len = np.full(R, pool, np.uint32)
+    rec_sample = np.repeat(np.arange(S, dtype=np.uint64), J)
+    rec_table = np.tile(np.array([t.table_id for t in tables], np.uint32), S)
+    rec_offset = (np.arange(R, dtype=np.uint64) * pool)
+    raw = rng.choice(200_000, size=R * pool, p=p).astype(np.uint64)
+    return tables, Trace(tables, S, rec_sample, rec_table, rec_offset, rec_len, raw_ids=raw)
+
+
+def test_profile_large_vs_oracle(cuda_ctx, coracle):
+    """cfg1-shaped (8 tables, H=1e6, pooling 20) at 4096 samples, rates 1 and 0.01."""
+    rng = np.random.default_rng(7)
+    tables, rt = _zipf_trace(rng, 8, 1_000_000, 4096, 20)
+    for rate, seed in [(1.0, 0), (0.01, 7), (0.3, 123)]:
+        got = sp.profile(rt, rate, seed, ctx=cuda_ctx)  # raw ids hashed on the GPU
+        want = coracle.profile(tables, rt.num_samples, rt.rec_sample, rt.rec_table, rt.rec_offset,
+                               rt.rec_len, None, rate, seed, raw_ids=rt.raw_ids)
+        assert_stats_equal(got, want)
+
+
+def test_profile_many_tables_and_ragged(cuda_ctx, coracle):
+    """Ragged records, empty records, tables never touched, non-contiguous offsets."""
+    rng = np.random.default_rng(9)
+    J = 37
+    tables = [TableSpec(1000 - 7 * j, 10, int(rng.integers(1, 5000)), 4, 4) for j in range(J)]
+    S = 3000
+    recs = []
+    ids = []
+    for s in range(S):
+        for j in rng.choice(J - 2, size=int(rng.integers(0, 6)), replace=False):
+            L = int(rng.integers(0, 40))
+            recs.append((s, tables[j].table_id, len(ids), L))
+            ids += list(rng.integers(0, tables[j].hash_size, L))
+    order = rng.permutation(len(recs))  # offsets stay valid, record order scrambled
+    recs = [recs[i] for i in order]
+    tr = Trace(tables, S, np.array([r[0] for r in recs], np.uint64),
+               np.array([r[1] for r in recs], np.uint32), np.array([r[2] for r in recs], np.uint64),
+               np.array([r[3] for r in recs], np.uint32), ids=np.array(ids, np.uint32))
+    for rate, seed in [(1.0, 0), (0.5, 3)]:
+        got = sp.profile(tr, rate, seed, ctx=cuda_ctx)
+        want = coracle.profile(tables, S, tr.rec_sample, tr.rec_table, tr.rec_offset, tr.rec_len,
+                               tr.ids, rate, seed)
+        assert_stats_equal(got, want)
