@@ -53,8 +53,10 @@ const char* rs_last_error(void);
 
 /* ------------------------------------------------------------- context */
 typedef struct rs_context rs_context;
-/* stream == NULL creates a private non-blocking stream. */
-int rs_context_create(int device, void* stream, rs_context** out);
+/* Runs on `stream` (a cudaStream_t; NULL = the legacy default stream), or on
+ * a private non-blocking stream when flags has RS_CTX_PRIVATE_STREAM. */
+#define RS_CTX_PRIVATE_STREAM 1
+int rs_context_create(int device, void* stream, int flags, rs_context** out);
 int rs_context_destroy(rs_context* ctx);
 int rs_context_synchronize(rs_context* ctx);
 
@@ -236,6 +238,12 @@ int rs_emb_read_rows(rs_emb* e, uint32_t t, const uint32_t* rows, uint64_t n,
                      float* out, float* momentum_out);
 /* Bytes of HBM / pinned host memory held by the tiers. */
 int rs_emb_memory(const rs_emb* e, uint64_t* hbm_bytes, uint64_t* host_bytes);
+
+/* ------------------------------------------------------------- primitives
+ * The device-wide stable LSD radix sort behind K2 and K5 (device buffers,
+ * sorted in place on bits [0, end_bit); vals may be NULL). */
+int rs_radix_sort_pairs(rs_context* ctx, uint32_t* keys, uint32_t* vals, uint64_t n,
+                        int end_bit);
 
 /* ------------------------------------------------------------- synthetic workload
  * Bench/test INPUT generation — not part of the reference boundary.  Mirrors

@@ -280,13 +280,17 @@ static float rowwise_sumsq(const float* g, uint32_t D) {
   return part[0];
 }
 
-typedef struct { uint32_t row; uint64_t pos; } lk_t;
+/* One lookup of the batch: global key = key_base[t] + row (key_base = sum of
+ * earlier tables' hash sizes), l = position in the table-major index list. */
+typedef struct { uint64_t key; uint64_t l; } lk_t;
 static int cmp_lk(const void* a, const void* b) {
   const lk_t* x = (const lk_t*)a;
   const lk_t* y = (const lk_t*)b;
-  if (x->row != y->row) return x->row < y->row ? -1 : 1;
-  return x->pos < y->pos ? -1 : (x->pos > y->pos);
+  if (x->key != y->key) return x->key < y->key ? -1 : 1;
+  return x->l < y->l ? -1 : (x->l > y->l);
 }
+
+#define OR_CHUNK 64 /* csrc/emb.cu kChunk */
 
 int or_emb_backward(uint32_t T, uint64_t B, const uint32_t* D,
                     const uint64_t* H, const uint64_t* col_off,
@@ -294,50 +298,78 @@ int or_emb_backward(uint32_t T, uint64_t B, const uint32_t* D,
                     const uint32_t* indices, const float* grad_out, int opt,
                     float lr, float eps, float* const* W,
                     float* const* momentum) {
-  for (uint32_t t = 0; t < T; ++t) {
-    uint64_t l0 = offsets[t * B], l1 = offsets[t * B + B];
-    uint64_t n = l1 - l0;
-    if (n == 0) continue;
-    lk_t* lk = (lk_t*)malloc(sizeof(lk_t) * n);
-    uint64_t* bag = (uint64_t*)malloc(sizeof(uint64_t) * n);
+  const uint64_t L = offsets[(uint64_t)T * B];
+  if (L == 0) return ST_OK;
+  uint64_t* kb = (uint64_t*)malloc(sizeof(uint64_t) * (T + 1));
+  kb[0] = 0;
+  for (uint32_t t = 0; t < T; ++t) kb[t + 1] = kb[t] + H[t];
+  lk_t* lk = (lk_t*)malloc(sizeof(lk_t) * L);
+  uint64_t* bag = (uint64_t*)malloc(sizeof(uint64_t) * L);
+  uint32_t* tab = (uint32_t*)malloc(sizeof(uint32_t) * L);
+  for (uint32_t t = 0; t < T; ++t)
     for (uint64_t b = 0; b < B; ++b)
-      for (uint64_t l = offsets[t * B + b]; l < offsets[t * B + b + 1]; ++l)
-        bag[l - l0] = b;
-    for (uint64_t i = 0; i < n; ++i) {
-      lk[i].row = indices[l0 + i];
-      lk[i].pos = i;
-      if (lk[i].row >= H[t]) { free(lk); free(bag); return ST_INVALID; }
-    }
-    qsort(lk, n, sizeof(lk_t), cmp_lk);
-    float* g = (float*)malloc(sizeof(float) * D[t]);
-    uint64_t i = 0;
-    while (i < n) {
-      uint32_t row = lk[i].row;
-      for (uint32_t d = 0; d < D[t]; ++d) g[d] = 0.0f;
-      for (; i < n && lk[i].row == row; ++i) {
-        const float* go = grad_out + bag[lk[i].pos] * grad_stride + col_off[t];
-        for (uint32_t d = 0; d < D[t]; ++d) g[d] = g[d] + go[d];
+      for (uint64_t l = offsets[t * B + b]; l < offsets[t * B + b + 1]; ++l) {
+        if (indices[l] >= H[t]) { free(kb); free(lk); free(bag); free(tab); return ST_INVALID; }
+        lk[l].key = kb[t] + indices[l];
+        lk[l].l = l;
+        bag[l] = b;
+        tab[l] = t;
       }
-      float* w = W[t] + (uint64_t)row * D[t];
-      if (opt == 0) {
-        for (uint32_t d = 0; d < D[t]; ++d) {
-          float step = lr * g[d];
-          w[d] = w[d] - step;
-        }
-      } else {
-        float s = rowwise_sumsq(g, D[t]);
-        float m = momentum[t][row] + s / (float)D[t];
-        momentum[t][row] = m;
-        float mult = lr / (sqrtf(m) + eps);
-        for (uint32_t d = 0; d < D[t]; ++d) {
-          float step = mult * g[d];
-          w[d] = w[d] - step;
-        }
+  qsort(lk, L, sizeof(lk_t), cmp_lk); /* stable by construction (l breaks ties) */
+  uint32_t dmax = 0;
+  for (uint32_t t = 0; t < T; ++t) dmax = D[t] > dmax ? D[t] : dmax;
+  float* g = (float*)malloc(sizeof(float) * dmax);
+  float* piece = (float*)malloc(sizeof(float) * dmax);
+  uint64_t i = 0;
+  while (i < L) {
+    const uint64_t key = lk[i].key;
+    const uint32_t t = tab[lk[i].l];
+    const uint32_t row = (uint32_t)(key - kb[t]);
+    const uint32_t d = D[t];
+    uint64_t e = i;
+    while (e < L && lk[e].key == key) ++e;
+    /* The kernel's reduction order: the segment [i, e) of the sorted list is
+     * cut at multiples of OR_CHUNK; every piece is summed in sorted order
+     * from +0.0f, and the pieces are then added left to right (the first
+     * piece is the accumulator). */
+    int first = 1;
+    uint64_t p = i;
+    while (p < e) {
+      uint64_t pe = (p / OR_CHUNK + 1) * OR_CHUNK;
+      if (pe > e) pe = e;
+      for (uint32_t k = 0; k < d; ++k) piece[k] = 0.0f;
+      for (uint64_t q = p; q < pe; ++q) {
+        const float* go = grad_out + bag[lk[q].l] * grad_stride + col_off[t];
+        for (uint32_t k = 0; k < d; ++k) piece[k] = piece[k] + go[k];
+      }
+      if (first) memcpy(g, piece, sizeof(float) * d);
+      else for (uint32_t k = 0; k < d; ++k) g[k] = g[k] + piece[k];
+      first = 0;
+      p = pe;
+    }
+    float* w = W[t] + (uint64_t)row * d;
+    if (opt == 0) {
+      for (uint32_t k = 0; k < d; ++k) {
+        float step = lr * g[k];
+        w[k] = w[k] - step;
+      }
+    } else {
+      float s = rowwise_sumsq(g, d);
+      float m = momentum[t][row] + s / (float)d;
+      momentum[t][row] = m;
+      float mult = lr / (sqrtf(m) + eps);
+      for (uint32_t k = 0; k < d; ++k) {
+        float step = mult * g[k];
+        w[k] = w[k] - step;
       }
     }
-    free(g);
-    free(bag);
-    free(lk);
+    i = e;
   }
+  free(piece);
+  free(g);
+  free(tab);
+  free(bag);
+  free(lk);
+  free(kb);
   return ST_OK;
 }

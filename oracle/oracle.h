@@ -97,9 +97,13 @@ int or_emb_forward(uint32_t T, uint64_t B, const uint32_t* D,
                    const uint64_t* offsets, const uint32_t* indices,
                    const float* const* W, float* out);
 
-/* Backward + optimizer, per table: for every distinct row r, in ascending
- * row order, g = sum over its lookups in ascending lookup order of
- * grad_out[b, col_off[t] : +D] (fp32, from +0.0f).  Then
+/* Backward + optimizer.  All lookups of the batch are ordered stably by
+ * global key (sum of earlier tables' hash sizes + row); for each distinct
+ * (table, row) the gradient g = sum of grad_out[b, col_off[t] : +D] over its
+ * lookups, accumulated in fp32 in the kernel's fixed order: the row's run in
+ * the sorted list is cut at multiples of 64 positions (csrc/emb.cu kChunk),
+ * each piece is summed in sorted order from +0.0f and the pieces are added
+ * left to right.  Then
  *   opt 0 (row-wise SGD):  w[d] = w[d] - lr*g[d]
  *   opt 1 (exact row-wise Adagrad, FBGEMM semantics):
  *       s = sum_d g[d]^2   (per-lane then xor-butterfly order, see oracle.c)

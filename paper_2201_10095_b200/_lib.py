@@ -84,7 +84,7 @@ class rs_gen_table(C.Structure):
 _SIGS = {
     "rs_abi_version": ([], i32),
     "rs_last_error": ([], C.c_char_p),
-    "rs_context_create": ([i32, P, P], i32),
+    "rs_context_create": ([i32, P, i32, P], i32),
     "rs_context_destroy": ([P], i32),
     "rs_context_synchronize": ([P], i32),
     "rs_hash_value": ([u64, u64, P], i32),
@@ -105,6 +105,7 @@ _SIGS = {
     "rs_emb_backward": ([P, u64, P, P, P, f32], i32),
     "rs_emb_read_rows": ([P, u32, P, u64, P, P], i32),
     "rs_emb_memory": ([P, P, P], i32),
+    "rs_radix_sort_pairs": ([P, P, P, u64, i32], i32),
     "rs_gen_batch": ([P, u32, P, u64, u64, u64, P, P, u64, P], i32),
     "rs_kjt_to_records": ([P, u32, P, u64, u64, P, P, P, P, P, P], i32),
 }

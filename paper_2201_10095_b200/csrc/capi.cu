@@ -64,13 +64,13 @@ extern "C" {
 int rs_abi_version(void) { return RS_ABI_VERSION; }
 const char* rs_last_error(void) { return g_err.c_str(); }
 
-int rs_context_create(int device, void* stream, rs_context** out) {
+int rs_context_create(int device, void* stream, int flags, rs_context** out) {
   return guarded([&] {
     need(out, "out");
     RS_CUDA(cudaSetDevice(device));
     auto* c = new rs_context;
     c->device = device;
-    if (stream) {
+    if (!(flags & RS_CTX_PRIVATE_STREAM)) {
       c->stream = static_cast<cudaStream_t>(stream);
     } else {
       cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
@@ -248,6 +248,16 @@ int rs_emb_read_rows(rs_emb* e, uint32_t t, const uint32_t* rows, uint64_t n, fl
       need(out, "out");
     }
     rs::emb_read_rows(e, t, rows, n, out, mom);
+  });
+}
+
+int rs_radix_sort_pairs(rs_context* c, uint32_t* keys, uint32_t* vals, uint64_t n, int end_bit) {
+  return guarded([&] {
+    need(c, "ctx");
+    if (n) need(keys, "keys");
+    if (end_bit < 0 || end_bit > 32) throw rs::InvalidArgument("radix_sort: end_bit in [0, 32]");
+    rs::Scratch scr = c->scratch(rs::radix_sort_scratch_bytes(n) + (4 << 20));
+    rs::radix_sort_pairs(keys, vals, n, end_bit, scr, c->stream);
   });
 }
 

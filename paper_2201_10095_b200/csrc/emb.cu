@@ -184,7 +184,7 @@ keygen_kernel(const TableDev* __restrict__ tables, uint32_t T, uint64_t B,
         const uint32_t l = s0 + q;  // bags are contiguous in table-major CSR
         const uint32_t idx = indices[l];
         if (idx >= Hk) atomicOr(err, 1u);
-        keys[l] = kb + (idx < Hk ? idx : 0u);
+        keys[l] = kbk + (idx < Hk ? idx : 0u);
         vals[l] = uint32_t(gk % B);
       }
     }
@@ -226,6 +226,12 @@ __device__ __forceinline__ void apply_update(const BwdArgs& a, const TableDev& t
   const int lane = threadIdx.x & 31;
   const uint32_t V = td.dim >> 2;
   const int32_t e = td.remap[row];
+#ifdef RS_DEBUG_BWD
+  if (row >= td.hash_size || (e >= 0 ? uint64_t(e) >= td.hbm_rows : uint64_t(-int64_t(e) - 1) >= td.slow_rows))
+    printf("apply_update: row %u H %llu e %d hbm %llu slow %llu dim %u kb %u\n", row,
+           (unsigned long long)td.hash_size, e, (unsigned long long)td.hbm_rows,
+           (unsigned long long)td.slow_rows, td.dim, td.key_base);
+#endif
   float4* w = reinterpret_cast<float4*>(row_ptr(td, e));
   float mult = a.lr;
   if (a.opt == RS_OPT_ROWWISE_ADAGRAD) {

@@ -25,7 +25,8 @@ class Context:
             stream = torch.cuda.current_stream(device)
         self.torch_stream = stream
         h = C.c_void_p()
-        _lib.check(_lib.lib().rs_context_create(device, C.c_void_p(stream.cuda_stream), C.byref(h)))
+        _lib.check(_lib.lib().rs_context_create(device, C.c_void_p(stream.cuda_stream), 0,
+                                                C.byref(h)))
         self.h = h
 
     def synchronize(self):
