@@ -50,6 +50,8 @@ extern "C" {
 
 int rs_abi_version(void);
 const char* rs_last_error(void);
+/* Kernel launches issued by this library so far (process-wide diagnostic). */
+uint64_t rs_launch_counter(void);
 
 /* ------------------------------------------------------------- context */
 typedef struct rs_context rs_context;

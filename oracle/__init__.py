@@ -456,6 +456,36 @@ class _RefLib:
         return rep
 
 
+def emb_step_cpu(B, dims, hash_sizes, offsets, indices, weights, momentum, opt, lr, eps,
+                 threads):
+    """One oracle fwd + (grad = pooled) + bwd over all tables, tables spread over
+    `threads` host threads (ctypes releases the GIL).  Used only by bench.py's
+    CPU baseline / reference arm.  Returns the pooled output."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    c = C()
+    T = len(dims)
+    offsets = np.ascontiguousarray(offsets, np.uint64)
+    indices = np.ascontiguousarray(indices, np.uint32)
+    cols = np.concatenate([[0], np.cumsum(dims)[:-1]]).astype(np.int64)
+    stride = int(np.sum(dims))
+    pooled = np.zeros((B, stride), np.float32)
+
+    def one(t):
+        o = offsets[t * B:(t + 1) * B + 1]
+        lo, hi = int(o[0]), int(o[-1])
+        ot = np.ascontiguousarray(o - o[0])
+        it = np.ascontiguousarray(indices[lo:hi])
+        y = c.emb_forward(B, [dims[t]], ot, it, [weights[t]])
+        pooled[:, cols[t]:cols[t] + dims[t]] = y
+        c.emb_backward(B, [dims[t]], ot, it, y, [weights[t]],
+                       None if momentum is None else [momentum[t]], opt, lr, eps)
+
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(one, range(T)))
+    return pooled
+
+
 _c = None
 _r = None
 

@@ -83,6 +83,7 @@ class rs_gen_table(C.Structure):
 
 _SIGS = {
     "rs_abi_version": ([], i32),
+    "rs_launch_counter": ([], u64),
     "rs_last_error": ([], C.c_char_p),
     "rs_context_create": ([i32, P, i32, P], i32),
     "rs_context_destroy": ([P], i32),

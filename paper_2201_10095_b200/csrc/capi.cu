@@ -57,11 +57,16 @@ void need(const void* p, const char* what) {
 
 namespace rs {
 void set_error(const std::string& m) { g_err = m; }
+uint64_t& launch_counter() {
+  static uint64_t n = 0;
+  return n;
+}
 }  // namespace rs
 
 extern "C" {
 
 int rs_abi_version(void) { return RS_ABI_VERSION; }
+uint64_t rs_launch_counter(void) { return rs::launch_counter(); }
 const char* rs_last_error(void) { return g_err.c_str(); }
 
 int rs_context_create(int device, void* stream, int flags, rs_context** out) {

@@ -37,6 +37,11 @@ struct CudaError : Error {
 
 #define RS_LAUNCH_CHECK() RS_CUDA(cudaGetLastError())
 
+// Process-wide count of kernel launches issued by this library (exported as
+// rs_launch_counter() so benches can report how many of OUR kernels ran).
+uint64_t& launch_counter();
+#define RS_COUNT(n) (::rs::launch_counter() += (n))
+
 // ---------------------------------------------------------------- hashing
 // SplitMix64 finalizer, inc/rng.hpp:27-31 (constants are the published ones).
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {

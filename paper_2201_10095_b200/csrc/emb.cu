@@ -681,6 +681,7 @@ static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint
   const unsigned grid = unsigned(std::min<uint64_t>(blocks, uint64_t(sm_count()) * 64));
   emb::forward_kernel<G, VPL><<<std::max(1u, grid), emb::kFwdThreads, 0, e->ctx->stream>>>(
       e->d_tables, c.d_list, uint32_t(c.tables.size()), B, off, idx, out, e->total_dim, hits);
+  RS_COUNT(1);
 }
 
 void emb_forward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx, float* out,
@@ -710,6 +711,7 @@ static void launch_bwd(rs_emb* e, const emb::BwdArgs& a) {
   const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((nch + 7) / 8, uint64_t(sm_count()) * 32)));
   emb::bwd_chunk_kernel<VPL><<<grid, 256, 0, e->ctx->stream>>>(a);
   emb::bwd_finalize_kernel<VPL><<<grid, 256, 0, e->ctx->stream>>>(a);
+  RS_COUNT(2);
 }
 
 void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx, const float* grad,
@@ -729,6 +731,7 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
     const uint64_t nb = uint64_t(e->T) * B;
     unsigned g = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((nb / 32 + 7) / 8, uint64_t(sm_count()) * 16)));
     emb::keygen_kernel<<<g, 256, 0, st>>>(e->d_tables, e->T, B, off, idx, e->keys, e->vals, e->d_err);
+    RS_COUNT(1);
   }
   Scratch scr;
   scr.base = e->sort_scratch;

@@ -153,6 +153,7 @@ template <class T>
 void scan_sums_inplace(T* sums, size_t tiles, T* total, Scratch& scr, cudaStream_t st) {
   if (tiles <= size_t(1024) * 64) {
     scan_tile_sums_excl<T><<<1, 1024, 0, st>>>(sums, tiles, total);
+    RS_COUNT(1);
     RS_LAUNCH_CHECK();
     return;
   }
@@ -176,6 +177,7 @@ void exclusive_scan(In in, size_t n, T* out, T* total, Scratch& scr, cudaStream_
   scan_tile_sums<T, In><<<unsigned(tiles), kScanThreads, 0, st>>>(in, n, sums);
   scan_sums_inplace<T>(sums, tiles, total, scr, st);
   scan_tiles<T, In><<<unsigned(tiles), kScanThreads, 0, st>>>(in, n, sums, out);
+  RS_COUNT(2);
   RS_LAUNCH_CHECK();
   scr.used = mark;
 }
@@ -317,6 +319,7 @@ inline void radix_sort_pairs(uint32_t* keys, uint32_t* vals, size_t n, int end_b
     else
       radix_downsweep<false><<<ntiles, kSortThreads, 0, st>>>(ki, nullptr, n, shift, nb,
                                                               offs, ntiles, ko, nullptr);
+    RS_COUNT(2);
     RS_LAUNCH_CHECK();
     std::swap(ki, ko);
     std::swap(vi, vo);
