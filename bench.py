@@ -48,6 +48,9 @@ def parse():
     p.add_argument("--greedy-steps", type=int, default=3)
     p.add_argument("--no-flush", action="store_true", help="skip the L2 flush between steps")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--hbm-fraction", type=float, default=0.4,
+                   help="M*cap_hbm as a fraction of all table bytes (configs/example_2x.cfg:2-3)")
+    p.add_argument("--only", default=None, choices=[None, "recshard", "greedy"])
     p.add_argument("--no-cpu", action="store_true")
     return p.parse_args()
 
@@ -415,7 +418,7 @@ def main():
     B = args.batch
     hbm_peak, peak_kind = measured_peaks()
     bw_uvm = h2d_bandwidth(torch, dev)
-    system = wl.system_for(specs, world, B, hbm_peak * 1e9, bw_uvm)
+    system = wl.system_for(specs, world, B, hbm_peak * 1e9, bw_uvm, args.hbm_fraction)
     tables = [w.table for w in specs]
 
     # ---- HP1: profile the training data on the GPU (whole-sample rate 1.0)
@@ -435,10 +438,11 @@ def main():
     gre = planner.greedy_shard([planner.table_fixed_cost(t, None, "size") for t in tables], tables,
                                stats, system, "greedy-size")
 
-    r = run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, rec, system,
+    first = gre if args.only == "greedy" else rec
+    r = run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, first, system,
                  args.steps, args.warmup, True, B)
     g = None
-    if not args.no_greedy:
+    if not args.no_greedy and args.only is None:
         g = run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, gre, system,
                      args.greedy_steps, 1, False, B)
     prof.close()

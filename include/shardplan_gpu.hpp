@@ -1,0 +1,223 @@
+// shardplan_gpu.hpp — the reference's C++ value API over the C-ABI.
+//
+// A drop-in for callers of the reference library (tools/shardplan.cpp,
+// tests/acceptance_main.cpp): include this next to the reference headers and
+// call shardplan::gpu::profile / build_icdf / hash_utilization / hash_value /
+// build_remap / translate / simulate with exactly the reference's argument
+// types and semantics; errors rethrow the reference's exception types
+// (include/shardplan/error.hpp:38-72, plus std::out_of_range for an unknown
+// table in profile, core/src/profiler.cpp:103).
+//
+// Requires the reference's public headers on the include path (the types are
+// the reference's own: shardplan::Trace, FeatureStats, PlanEntry, ...).
+#pragma once
+
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "shardplan/profiler.hpp"
+#include "shardplan/remap.hpp"
+#include "shardplan/simulator.hpp"
+#include "shardplan_gpu.h"
+
+namespace shardplan::gpu {
+
+[[noreturn]] inline void rethrow(int status) {
+  const std::string m = rs_last_error();
+  switch (status) {
+    case RS_ERR_INVALID_ARGUMENT: throw InvalidArgument(m);
+    case RS_ERR_PARSE: throw ParseError(m);
+    case RS_ERR_INFEASIBLE: throw InfeasibleError(m);
+    case RS_ERR_IO: throw IoError(m);
+    case RS_ERR_OUT_OF_RANGE: throw std::out_of_range(m);
+    default: throw Error(m);
+  }
+}
+
+inline void check(int status) {
+  if (status != RS_OK) rethrow(status);
+}
+
+/// One rs_context per device, on a private stream (calls are synchronous
+/// from the caller's point of view, like the reference functions).
+class Context {
+ public:
+  explicit Context(int device = 0) {
+    check(rs_context_create(device, nullptr, RS_CTX_PRIVATE_STREAM, &ctx_));
+  }
+  ~Context() { rs_context_destroy(ctx_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  rs_context* get() const { return ctx_; }
+
+  static Context& instance(int device = 0) {
+    thread_local std::unique_ptr<Context> c;
+    if (!c) c = std::make_unique<Context>(device);
+    return *c;
+  }
+
+ private:
+  rs_context* ctx_ = nullptr;
+};
+
+namespace detail {
+// Structure-of-arrays view of a reference Trace (inc/workload.hpp:41-58).
+struct TraceSoA {
+  std::vector<rs_table_spec> specs;
+  std::vector<uint64_t> sample, offset;
+  std::vector<uint32_t> table, len;
+  rs_trace view{};
+
+  explicit TraceSoA(const Trace& t) {
+    for (const auto& s : t.tables)
+      specs.push_back({s.table_id, s.cardinality, s.hash_size, s.dim, s.elem_bytes});
+    const size_t R = t.records.size();
+    sample.resize(R);
+    offset.resize(R);
+    table.resize(R);
+    len.resize(R);
+    for (size_t r = 0; r < R; ++r) {
+      sample[r] = t.records[r].sample;
+      table[r] = t.records[r].table;
+      offset[r] = t.records[r].offset;
+      len[r] = t.records[r].len;
+    }
+    view.num_tables = static_cast<uint32_t>(specs.size());
+    view.tables = specs.data();
+    view.num_samples = t.num_samples;
+    view.num_records = R;
+    view.rec_sample = sample.data();
+    view.rec_table = table.data();
+    view.rec_offset = offset.data();
+    view.rec_len = len.data();
+    view.num_ids = t.ids.size();
+    view.ids = t.ids.data();
+    view.raw_ids = nullptr;
+    view.location = RS_MEM_HOST;
+  }
+};
+}  // namespace detail
+
+/// inc/workload.hpp:28-31
+inline uint32_t hash_value(uint64_t raw_id, uint64_t hash_size) {
+  uint32_t out = 0;
+  check(rs_hash_value(raw_id, hash_size, &out));
+  return out;
+}
+
+/// include/shardplan/profiler.hpp:49-50 — K1 + K2 on the GPU.
+inline std::vector<FeatureStats> profile(const Trace& trace, double sample_rate, uint64_t seed) {
+  if (trace.num_samples < 1 || trace.tables.empty())  // profiler.cpp:62-63
+    throw InvalidArgument("profile: trace is empty");
+  detail::TraceSoA soa(trace);
+  rs_profile* p = nullptr;
+  check(rs_profile_run(Context::instance().get(), &soa.view, sample_rate, seed, &p));
+  std::unique_ptr<rs_profile, int (*)(rs_profile*)> guard(p, rs_profile_destroy);
+  uint32_t J = 0;
+  check(rs_profile_num_tables(p, &J));
+  std::vector<FeatureStats> out(J);
+  for (uint32_t j = 0; j < J; ++j) {
+    rs_feature_stats v{};
+    check(rs_profile_get(p, j, &v));
+    FeatureStats& s = out[j];
+    s.table_id = v.table_id;
+    s.coverage = v.coverage;
+    s.avg_pooling = v.avg_pooling;
+    s.distinct_rows_accessed = v.distinct_rows_accessed;
+    s.total_accesses = v.total_accesses;
+    s.icdf_steps.assign(v.icdf_steps, v.icdf_steps + kIcdfPercentSteps + 1);
+    s.access_cdf.assign(v.access_cdf, v.access_cdf + v.distinct_rows_accessed);
+    s.rows_by_rank.assign(v.rows_by_rank, v.rows_by_rank + v.distinct_rows_accessed);
+  }
+  return out;
+}
+
+/// include/shardplan/profiler.hpp:54
+inline std::vector<uint64_t> build_icdf(std::span<const uint64_t> counts_per_row) {
+  std::vector<uint64_t> out(kIcdfPercentSteps + 1);
+  check(rs_build_icdf(Context::instance().get(), counts_per_row.data(), counts_per_row.size(),
+                      RS_MEM_HOST, out.data()));
+  return out;
+}
+
+/// include/shardplan/profiler.hpp:58-60
+inline std::pair<double, double> hash_utilization(const FeatureStats& stats, const TableSpec& spec,
+                                                  uint64_t distinct_raw_ids_seen) {
+  std::pair<double, double> r;
+  check(rs_hash_utilization(stats.distinct_rows_accessed, spec.hash_size, distinct_raw_ids_seen,
+                            &r.first, &r.second));
+  return r;
+}
+
+/// include/shardplan/remap.hpp:54-55 — K3 on the GPU.
+inline RemapTable build_remap(const PlanEntry& entry, const FeatureStats& stats,
+                              const TableSpec& spec, const RemapOptions& opts = {}) {
+  if (stats.rows_by_rank.size() != stats.distinct_rows_accessed && spec.hash_size <= kMaxHashSize &&
+      entry.hbm_rows <= spec.hash_size)  // remap.cpp:52-56 (after the bound checks)
+    throw InvalidArgument(strfmt("table %u: stats lack row-level ranking (loaded from a stats "
+                                 "file?); re-profile the trace",
+                                 spec.table_id));
+  RemapTable r;
+  r.table_id = spec.table_id;
+  r.hash_size = spec.hash_size;
+  r.hbm_rows = entry.hbm_rows;
+  r.entries.resize(spec.hash_size <= kMaxHashSize ? spec.hash_size : 0);
+  check(rs_build_remap(Context::instance().get(), spec.table_id, spec.hash_size, entry.hbm_rows,
+                       stats.rows_by_rank.data(), stats.distinct_rows_accessed, RS_MEM_HOST,
+                       opts.omit_unaccessed ? 1 : 0, r.entries.data(), RS_MEM_HOST,
+                       &r.slow_rows_allocated));
+  return r;
+}
+
+/// core/src/remap.cpp:107-116 (host decode of the sign-bit encoding)
+inline std::pair<Tier, uint64_t> translate(const RemapTable& remap, uint64_t original_index) {
+  if (original_index >= remap.hash_size)
+    throw InvalidArgument(strfmt("translate: index %llu out of range for table %u",
+                                 (unsigned long long)original_index, remap.table_id));
+  const int32_t v = remap.entries[original_index];
+  if (v >= 0) return {Tier::kFast, static_cast<uint64_t>(v)};
+  return {Tier::kSlow, static_cast<uint64_t>(-(int64_t)v - 1)};
+}
+
+/// include/shardplan/simulator.hpp:45-47 — tier counts on the GPU.
+inline SimReport simulate(const Trace& trace, const ShardingPlan& plan,
+                          const std::vector<RemapTable>& remaps, const SystemSpec& system,
+                          uint64_t batch_size) {
+  detail::TraceSoA soa(trace);
+  std::vector<rs_plan_entry> ents;
+  for (const auto& e : plan.entries)
+    ents.push_back({e.table_id, e.gpu, e.step, e.hbm_rows, e.pct, e.mem_bytes});
+  std::vector<rs_remap_view> rv;
+  for (const auto& r : remaps)
+    rv.push_back({r.table_id, r.hash_size, r.hbm_rows, r.entries.data(), RS_MEM_HOST});
+  rs_system_spec sys{system.num_gpus, system.batch_size, system.cap_hbm_bytes,
+                     system.cap_dram_bytes, system.bw_hbm, system.bw_uvm};
+  SimReport rep;
+  const uint32_t M = system.num_gpus;
+  std::vector<double> gh(M ? M : 1), gu(M ? M : 1), gc(M ? M : 1);
+  rep.table_fast_fraction.resize(trace.tables.size());
+  rs_sim_report out{};
+  out.gpu_hbm_accesses = gh.data();
+  out.gpu_uvm_accesses = gu.data();
+  out.gpu_est_iter_cost = gc.data();
+  out.table_fast_fraction = rep.table_fast_fraction.data();
+  check(rs_simulate(Context::instance().get(), &soa.view, static_cast<uint32_t>(ents.size()),
+                    ents.data(), static_cast<uint32_t>(rv.size()), rv.data(), &sys, batch_size,
+                    &out));
+  rep.gpus.resize(M);
+  for (uint32_t g = 0; g < M; ++g) rep.gpus[g] = {gh[g], gu[g], gc[g]};
+  rep.batches = out.batches;
+  rep.total_accesses = out.total_accesses;
+  rep.min_cost = out.min_cost;
+  rep.max_cost = out.max_cost;
+  rep.mean_cost = out.mean_cost;
+  rep.stddev_cost = out.stddev_cost;
+  rep.uvm_access_fraction = out.uvm_access_fraction;
+  return rep;
+}
+
+}  // namespace shardplan::gpu

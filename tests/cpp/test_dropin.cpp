@@ -1,0 +1,173 @@
+// C++ drop-in parity: the reference's own calls, made twice — once into the
+// unmodified reference library (shardplan::) and once through the GPU shim
+// (shardplan::gpu::, include/shardplan_gpu.hpp) — must agree bit for bit.
+// Mirrors the reference tests (tests/test_profiler.cpp, test_remap.cpp,
+// test_simulator.cpp, test_workload.cpp) without doctest.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+
+#include "shardplan/baselines.hpp"
+#include "shardplan/milp.hpp"
+#include "shardplan_gpu.hpp"
+
+using namespace shardplan;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(c)                                                          \
+  do {                                                                    \
+    if (c) ++g_pass;                                                      \
+    else {                                                                \
+      ++g_fail;                                                           \
+      std::fprintf(stderr, "%s:%d CHECK failed: %s\n", __FILE__, __LINE__, #c); \
+    }                                                                     \
+  } while (0)
+
+template <class E, class F>
+static bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+static bool same(double a, double b) { return std::memcmp(&a, &b, sizeof a) == 0; }
+
+static bool stats_equal(const std::vector<FeatureStats>& a, const std::vector<FeatureStats>& b) {
+  if (a.size() != b.size()) return false;
+  for (size_t j = 0; j < a.size(); ++j) {
+    const auto &x = a[j], &y = b[j];
+    if (x.table_id != y.table_id || !same(x.coverage, y.coverage) ||
+        !same(x.avg_pooling, y.avg_pooling) ||
+        x.distinct_rows_accessed != y.distinct_rows_accessed ||
+        x.total_accesses != y.total_accesses || x.icdf_steps != y.icdf_steps ||
+        x.rows_by_rank != y.rows_by_rank || x.access_cdf.size() != y.access_cdf.size())
+      return false;
+    for (size_t r = 0; r < x.access_cdf.size(); ++r)
+      if (!same(x.access_cdf[r], y.access_cdf[r])) return false;
+  }
+  return true;
+}
+
+static Trace worked_example() {  // tests/test_profiler.cpp:30-49
+  Trace t;
+  t.tables = {TableSpec{0, 1000, 100, 4, 4}, TableSpec{1, 1000, 100, 4, 4}};
+  t.num_samples = 3;
+  auto add = [&](uint64_t s, uint32_t tab, std::initializer_list<uint32_t> ids) {
+    t.records.push_back({s, tab, t.ids.size(), static_cast<uint32_t>(ids.size())});
+    t.ids.insert(t.ids.end(), ids);
+  };
+  add(0, 0, {1, 5, 9, 15});
+  add(0, 1, {2, 4, 8});
+  add(1, 0, {5, 7, 9, 30});
+  add(2, 0, {1, 5, 9});
+  return t;
+}
+
+int main() {
+  // hash_value goldens (tests/test_workload.cpp:50-57)
+  CHECK(gpu::hash_value(42, 1ULL << 32) == 3564271138ULL);
+  CHECK(gpu::hash_value(7, 1000) == 604);
+  CHECK(throws<InvalidArgument>([] { gpu::hash_value(1, 0); }));
+  SplitMix64 rng(99);
+  for (int i = 0; i < 10000; ++i) {
+    uint64_t raw = rng.next(), h = 1 + rng.next_below(0x7FFFFFFF);
+    if (gpu::hash_value(raw, h) != hash_value(raw, h)) {
+      CHECK(false);
+      break;
+    }
+  }
+
+  // Fig. 3 worked example (tests/test_profiler.cpp:53-62)
+  {
+    Trace t = worked_example();
+    auto g = gpu::profile(t, 1.0, 0);
+    CHECK(stats_equal(g, profile(t, 1.0, 0)));
+    CHECK(g[0].total_accesses == 11 && g[0].distinct_rows_accessed == 6);
+    CHECK(throws<InvalidArgument>([&] { gpu::profile(t, 0.0, 0); }));
+    CHECK(throws<InvalidArgument>([&] { gpu::profile(Trace{}, 0.5, 0); }));
+    CHECK(throws<InvalidArgument>([&] { gpu::profile(t, 1e-12, 0); }));
+    Trace bad = t;
+    bad.tables.pop_back();
+    CHECK(throws<std::out_of_range>([&] { gpu::profile(bad, 1.0, 0); }));
+  }
+
+  // generated traces, full and sampled profiles
+  std::vector<WorkloadSpec> specs(3);
+  specs[0].table = {0, 4000, 3000, 16, 4};
+  specs[0].gen = {1.3, 6.0, 0.9, PoolingLaw::kPoisson};
+  specs[1].table = {1, 9000, 8000, 8, 4};
+  specs[1].gen = {1.1, 3.0, 0.5, PoolingLaw::kLognormal};
+  specs[2].table = {2, 2000, 1500, 32, 2};
+  specs[2].gen = {0.9, 2.0, 1.0, PoolingLaw::kConstant};
+  Trace t = generate_trace(specs, 20000, 5);
+  for (auto [rate, seed] : {std::pair{1.0, 0ULL}, {0.01, 1ULL}, {0.37, 12ULL}})
+    CHECK(stats_equal(gpu::profile(t, rate, seed), profile(t, rate, seed)));
+
+  // build_icdf vs the reference on random vectors (tests/test_profiler.cpp:103-119)
+  for (int trial = 0; trial < 200; ++trial) {
+    size_t n = 1 + rng.next_below(1000);
+    std::vector<uint64_t> c(n);
+    bool any = false;
+    for (auto& x : c) any |= (x = rng.next_below(100)) > 0;
+    if (!any) c[0] = 1;
+    if (gpu::build_icdf(c) != build_icdf(c)) {
+      CHECK(false);
+      break;
+    }
+  }
+  CHECK(throws<InvalidArgument>([] { gpu::build_icdf(std::vector<uint64_t>(5, 0)); }));
+
+  // plans -> remaps -> simulate (tests/test_simulator.cpp:40-58 pipeline)
+  auto stats = profile(t, 1.0, 0);
+  std::vector<TableSpec> tabs;
+  for (auto& w : specs) tabs.push_back(w.table);
+  SystemSpec sys{2, 256, 0, 1ULL << 30, 1.555e12, 1.6e10};
+  uint64_t total = 0;
+  for (auto& s : tabs) total += s.bytes();
+  sys.cap_hbm_bytes = total / 3;
+  auto inst = build_instance(stats, tabs, sys, {}, 20);
+  std::vector<double> costs;
+  for (size_t j = 0; j < tabs.size(); ++j)
+    costs.push_back(table_fixed_cost(tabs[j], &stats[j], CostKind::kSize));
+  for (const ShardingPlan& plan : {solve(inst, 2.0), greedy_shard(costs, tabs, stats, sys)}) {
+    std::vector<RemapTable> ref_r, gpu_r;
+    for (size_t j = 0; j < tabs.size(); ++j) {
+      for (bool omit : {false, true}) {
+        RemapOptions o;
+        o.omit_unaccessed = omit;
+        auto a = build_remap(plan.entries[j], stats[j], tabs[j], o);
+        auto b = gpu::build_remap(plan.entries[j], stats[j], tabs[j], o);
+        CHECK(a.entries == b.entries && a.slow_rows_allocated == b.slow_rows_allocated);
+      }
+      ref_r.push_back(build_remap(plan.entries[j], stats[j], tabs[j]));
+      gpu_r.push_back(gpu::build_remap(plan.entries[j], stats[j], tabs[j]));
+      for (uint64_t i = 0; i < tabs[j].hash_size; i += 97)
+        CHECK(gpu::translate(gpu_r[j], i) == translate(ref_r[j], i));
+    }
+    for (uint64_t B : {256ULL, 1000ULL, 20000ULL}) {
+      auto a = simulate(t, plan, ref_r, sys, B);
+      auto b = gpu::simulate(t, plan, gpu_r, sys, B);
+      bool eq = a.batches == b.batches && a.total_accesses == b.total_accesses &&
+                same(a.min_cost, b.min_cost) && same(a.max_cost, b.max_cost) &&
+                same(a.mean_cost, b.mean_cost) && same(a.stddev_cost, b.stddev_cost) &&
+                same(a.uvm_access_fraction, b.uvm_access_fraction);
+      for (size_t g = 0; g < a.gpus.size(); ++g)
+        eq = eq && same(a.gpus[g].hbm_accesses, b.gpus[g].hbm_accesses) &&
+             same(a.gpus[g].uvm_accesses, b.gpus[g].uvm_accesses) &&
+             same(a.gpus[g].est_iter_cost, b.gpus[g].est_iter_cost);
+      for (size_t j = 0; j < a.table_fast_fraction.size(); ++j)
+        eq = eq && (same(a.table_fast_fraction[j], b.table_fast_fraction[j]) ||
+                    (std::isnan(a.table_fast_fraction[j]) && std::isnan(b.table_fast_fraction[j])));
+      CHECK(eq);
+    }
+    CHECK(throws<InvalidArgument>([&] { gpu::simulate(t, plan, gpu_r, sys, 1 << 30); }));
+  }
+  std::printf("drop-in parity: %d checks passed, %d failed\n", g_pass, g_fail);
+  return g_fail ? 1 : 0;
+}

@@ -13,7 +13,7 @@ HEADER = os.path.join(ROOT, "include", "shardplan_gpu.h")
 
 def declared_functions():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(rs_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^(?:int|const char\*|uint64_t)\s+(rs_\w+)\s*\(", src, re.M)))
 
 
 def test_header_declares_the_boundary():
