@@ -253,10 +253,17 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
     pooled = torch.empty(B, max(1, D_local), dtype=torch.float32, device=dev)
     hits = torch.zeros(2 * max(1, T), dtype=torch.int64, device=dev)
     flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    recv = torch.empty(B // world * sum(dims_all), dtype=torch.float32, device=dev) if world > 1 else None
-    gback = torch.empty(B * max(1, D_local), dtype=torch.float32, device=dev) if world > 1 else None
+    ex = None
+    if world > 1:
+        from paper_2201_10095_b200.sharded import Exchange
+
+        ex = Exchange(plan, [w.table.dim for w in specs], world, rank, B, dev)
+
+    nvtx = os.environ.get("BENCH_NVTX") == "1"
 
     def step(i, ev=None):
+        if nvtx:
+            torch.cuda.nvtx.range_push("bench_step")
         off, idx, n = batches[i % len(batches)] if T else (None, None, 0)
         if ev:
             ev[0].record()
@@ -265,19 +272,17 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
         if ev:
             ev[1].record()
         g = pooled
-        if world > 1:  # pooled rows to sample owners and gradients back (NCCL all-to-all)
-            bl = B // world
-            dist.all_to_all_single(recv, pooled.reshape(-1)[:B * D_local],
-                                   [d * bl for d in dims_all], [bl * D_local] * world)
-            dist.all_to_all_single(gback[:B * D_local], recv, [bl * D_local] * world,
-                                   [d * bl for d in dims_all])
-            g = gback[:B * D_local].view(B, max(1, D_local))
+        if ex is not None:  # pooled rows to sample owners, gradients back (NCCL all-to-all)
+            y = ex.to_owners(pooled)  # loss 0.5*||y||^2 on this rank's samples: grad = y
+            g = ex.to_tables(y)
         if ev:
             ev[2].record()
         if T:
             op.backward(off, idx, g, B, LR)
         if ev:
             ev[3].record()
+        if nvtx:
+            torch.cuda.nvtx.range_pop()
 
     for i in range(warmup):
         step(i)
@@ -333,8 +338,7 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
             abs(rep.uvm_access_fraction - hh[1::2].sum() / max(1, hh.sum())) == 0.0
             and rep.total_accesses == int(hh.sum()))
     if do_e2e and T:
-        res["e2e"] = run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, D_local,
-                             dims_all, recv, gback)
+        res["e2e"] = run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex)
     if op:
         op.close()
     del remaps, batches
@@ -342,7 +346,7 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
     return res
 
 
-def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, D_local, dims_all, recv, gback):
+def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex):
     """Same step through the public API with host inputs: pinned host offsets +
     indices copied H2D every step, the hit counters (the step's UVM metric)
     read back D2H."""
@@ -361,13 +365,8 @@ def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, D_local, di
         bi = ho.numel() * 4 + hi.numel() * 4
         op.forward(d_off, d_idx, B, out=pooled, hits=hits)
         g = pooled
-        if world > 1:
-            bl = B // world
-            dist.all_to_all_single(recv, pooled.reshape(-1)[:B * D_local],
-                                   [d * bl for d in dims_all], [bl * D_local] * world)
-            dist.all_to_all_single(gback[:B * D_local], recv, [bl * D_local] * world,
-                                   [d * bl for d in dims_all])
-            g = gback[:B * D_local].view(B, max(1, D_local))
+        if ex is not None:
+            g = ex.to_tables(ex.to_owners(pooled))
         op.backward(d_off, d_idx, g, B, LR)
         h_hits.copy_(hits, non_blocking=True)
 
