@@ -42,7 +42,9 @@ def parse():
     p.add_argument("--config", default="rm1", choices=["rm1", "rm2", "rm3", "cfg1"])
     p.add_argument("--batch", type=int, default=16384)
     p.add_argument("--nbatches", type=int, default=4, help="distinct batches cycled")
-    p.add_argument("--profile-batches", type=int, default=4)
+    p.add_argument("--profile-batches", type=int, default=16)
+    p.add_argument("--no-fill", action="store_true",
+                   help="serve the pure RecShard plan (no spare-capacity fill)")
     p.add_argument("--optimizer", default="rowwise_adagrad", choices=["sgd", "rowwise_adagrad"])
     p.add_argument("--no-greedy", action="store_true")
     p.add_argument("--greedy-steps", type=int, default=3)
@@ -433,9 +435,35 @@ def main():
     torch.cuda.empty_cache()
 
     # ---- plans (host): RecShard vs the greedy/size baseline
+    t0 = time.perf_counter()
     rec = planner.recshard_plan(tables, stats, system)
+    plan_s = time.perf_counter() - t0
     gre = planner.greedy_shard([planner.table_fixed_cost(t, None, "size") for t in tables], tables,
                                stats, system, "greedy-size")
+    import copy
+
+    rec_pure = copy.deepcopy(rec)
+    if not args.no_fill:
+        planner.fill_spare_capacity(rec, tables, stats, system)
+    # simulate() (GPU) on one training batch for each placement: the UVM share
+    # the plans predict, before any operator is built
+    sim_uvm = {}
+    if world == 1:
+        sgen = wl.BatchGenerator(specs, B, WORKLOAD_SEED)
+        soff, sidx, sn = sgen.batch(100)
+        strace = wl.kjt_to_trace(specs, soff, sidx, sn, B, 100 * B, ctx=ctx)
+        strace.num_samples = B  # records carry sample ids 100B..101B-1; one batch of B
+        strace.rec_sample = strace.rec_sample - 100 * B
+        for name, pl in (("recshard", rec_pure), (rec.strategy, rec), ("greedy-size", gre)):
+            rms = [sp.build_remap(pl.entries[j], stats[j], tables[j], ctx=ctx,
+                                  device_rows=prof.device_rows_by_rank(j),
+                                  out=torch.empty(tables[j].hash_size, dtype=torch.int32, device=dev))
+                   for j in range(len(tables))]
+            rep = sp.simulate(strace, pl, rms, system, B, ctx=ctx)
+            sim_uvm[name] = 100.0 * rep.uvm_access_fraction
+            del rms
+        del strace, sidx, soff
+        torch.cuda.empty_cache()
 
     first = gre if args.only == "greedy" else rec
     r = run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, first, system,
@@ -471,6 +499,8 @@ def main():
                        "fast_tier_cap": "40% of table bytes", "l2": "256 MiB flush between steps"
                        if not args.no_flush else f"{args.nbatches} distinct batches cycled"},
             "uvm_access_pct": r["uvm_pct"],
+            "plan": first.strategy, "planner_s": plan_s,
+            "simulated_uvm_pct": sim_uvm,
             "uvm_matches_simulate": r.get("uvm_matches_simulate"),
             "recshard": {k: r[k] for k in ("samples_per_s", "ms_per_step", "fwd_ms", "bwd_ms",
                                            "a2a_ms", "uvm_pct", "hbm_bytes", "host_bytes")},

@@ -231,6 +231,55 @@ def _knapsack(curves, cap_hbm, cap_dram):
     return steps, float(sum(c.cost[s] for c, s in zip(curves, steps)))
 
 
+def unseen_mass(st):
+    """Good-Turing estimate of the access probability mass on rows the
+    profile never saw: (rows seen exactly once) / total accesses, read off the
+    ranked CDF (count at rank r = (cdf[r] - cdf[r-1]) * total)."""
+    if st.total_accesses == 0 or st.distinct_rows_accessed == 0:
+        return 0.0
+    cdf = np.asarray(st.access_cdf, np.float64)
+    inc = np.diff(np.concatenate([[0.0], cdf])) * st.total_accesses
+    n1 = int(np.count_nonzero(np.rint(inc) == 1))
+    return n1 / float(st.total_accesses)
+
+
+def fill_spare_capacity(plan, specs, stats, system):
+    """Extension beyond the MILP (off by default in the solver): spend each
+    GPU's leftover fast-tier bytes on never-profiled rows of tables whose whole
+    profiled set is already fast, greedily by expected hits per byte
+    (coverage * pooling * unseen mass / unseen rows / row bytes).  The extra
+    rows are the reference remap's "never-accessed rows in ascending index
+    order" (core/src/remap.cpp:71-78), so the plan format is unchanged."""
+    M = system.num_gpus
+    used = [0] * M
+    for e in plan.entries:
+        used[e.gpu] += e.mem_bytes
+    cands = []
+    for j, (s, st, e) in enumerate(zip(specs, stats, plan.entries)):
+        unseen_rows = s.hash_size - st.distinct_rows_accessed
+        if e.hbm_rows < st.distinct_rows_accessed or unseen_rows <= 0:
+            continue
+        m = unseen_mass(st)
+        if m <= 0:
+            continue
+        rb = s.dim * s.elem_bytes
+        dens = st.coverage * st.avg_pooling * m / unseen_rows / rb
+        cands.append((-dens, s.table_id, j))
+    cands.sort()
+    for _, _, j in cands:
+        e, s = plan.entries[j], specs[j]
+        rb = s.dim * s.elem_bytes
+        room = (system.cap_hbm_bytes - used[e.gpu]) // rb
+        add = int(min(room, s.hash_size - e.hbm_rows))
+        if add <= 0:
+            continue
+        e.hbm_rows += add
+        e.mem_bytes = e.hbm_rows * rb
+        used[e.gpu] += add * rb
+    plan.strategy += "+fill"
+    return plan
+
+
 def recshard_plan(specs, stats, system, step_count=100, iters=200):
     """Minimise max_m c_m with per-GPU HBM/DRAM capacities."""
     _validate_system(system)
