@@ -290,7 +290,8 @@ static int cmp_lk(const void* a, const void* b) {
   return x->l < y->l ? -1 : (x->l > y->l);
 }
 
-#define OR_CHUNK 64 /* csrc/emb.cu kChunk */
+#define OR_CHUNK 64 /* csrc/emb_bwd.cuh kChunk */
+#define OR_SUPER 64 /* csrc/emb_bwd.cuh kSuper (chunks per superchunk) */
 
 int or_emb_backward(uint32_t T, uint64_t B, const uint32_t* D,
                     const uint64_t* H, const uint64_t* col_off,
@@ -320,6 +321,7 @@ int or_emb_backward(uint32_t T, uint64_t B, const uint32_t* D,
   for (uint32_t t = 0; t < T; ++t) dmax = D[t] > dmax ? D[t] : dmax;
   float* g = (float*)malloc(sizeof(float) * dmax);
   float* piece = (float*)malloc(sizeof(float) * dmax);
+  float* gs = (float*)malloc(sizeof(float) * dmax);
   uint64_t i = 0;
   while (i < L) {
     const uint64_t key = lk[i].key;
@@ -332,8 +334,11 @@ int or_emb_backward(uint32_t T, uint64_t B, const uint32_t* D,
      * cut at multiples of OR_CHUNK; every piece is summed in sorted order
      * from +0.0f, and the pieces are then added left to right (the first
      * piece is the accumulator). */
-    int first = 1;
-    uint64_t p = i;
+    /* level 2/3: pieces of one superchunk (OR_CHUNK*OR_SUPER positions) are
+     * summed left to right (first piece = accumulator) into a group sum; the
+     * group sums are then summed left to right (first = accumulator). */
+    int first_group = 1, first_piece = 1;
+    uint64_t p = i, group = (uint64_t)-1;
     while (p < e) {
       uint64_t pe = (p / OR_CHUNK + 1) * OR_CHUNK;
       if (pe > e) pe = e;
@@ -342,11 +347,23 @@ int or_emb_backward(uint32_t T, uint64_t B, const uint32_t* D,
         const float* go = grad_out + bag[lk[q].l] * grad_stride + col_off[t];
         for (uint32_t k = 0; k < d; ++k) piece[k] = piece[k] + go[k];
       }
-      if (first) memcpy(g, piece, sizeof(float) * d);
-      else for (uint32_t k = 0; k < d; ++k) g[k] = g[k] + piece[k];
-      first = 0;
+      const uint64_t grp = p / ((uint64_t)OR_CHUNK * OR_SUPER);
+      if (grp != group) {
+        if (group != (uint64_t)-1) { /* close the previous group into g */
+          if (first_group) memcpy(g, gs, sizeof(float) * d);
+          else for (uint32_t k = 0; k < d; ++k) g[k] = g[k] + gs[k];
+          first_group = 0;
+        }
+        group = grp;
+        first_piece = 1;
+      }
+      if (first_piece) memcpy(gs, piece, sizeof(float) * d);
+      else for (uint32_t k = 0; k < d; ++k) gs[k] = gs[k] + piece[k];
+      first_piece = 0;
       p = pe;
     }
+    if (first_group) memcpy(g, gs, sizeof(float) * d);
+    else for (uint32_t k = 0; k < d; ++k) g[k] = g[k] + gs[k];
     float* w = W[t] + (uint64_t)row * d;
     if (opt == 0) {
       for (uint32_t k = 0; k < d; ++k) {
@@ -365,6 +382,7 @@ int or_emb_backward(uint32_t T, uint64_t B, const uint32_t* D,
     }
     i = e;
   }
+  free(gs);
   free(piece);
   free(g);
   free(tab);

@@ -191,232 +191,13 @@ keygen_kernel(const TableDev* __restrict__ tables, uint32_t T, uint64_t B,
   }
 }
 
-constexpr int kChunk = 64;
+}  // namespace emb
+}  // namespace rs
 
-struct BwdArgs {
-  const TableDev* tables;
-  const uint32_t* key_base_sorted;  // key_base per table, ascending (T entries)
-  uint32_t T;
-  const uint32_t* keys;
-  const uint32_t* vals;
-  uint64_t L;
-  const float* grad;
-  uint64_t stride;
-  float* part;       // [nchunks][2][dmax]
-  uint32_t dmax;
-  float lr, eps;
-  int opt;
-};
+#include "emb_bwd.cuh"
 
-__device__ __forceinline__ uint32_t table_of_key(const BwdArgs& a, uint32_t key) {
-  uint32_t lo = 0, hi = a.T;
-  while (lo + 1 < hi) {
-    uint32_t mid = (lo + hi) >> 1;
-    if (a.key_base_sorted[mid] <= key) lo = mid;
-    else hi = mid;
-  }
-  return lo;
-}
-
-// Apply the optimizer to one row with its full gradient g (VPL float4 per lane,
-// vec = lane + vv*32).  Arithmetic order matches or_emb_backward.
-template <int VPL>
-__device__ __forceinline__ void apply_update(const BwdArgs& a, const TableDev& td, uint32_t row,
-                                             const float4 (&g)[VPL]) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t V = td.dim >> 2;
-  const int32_t e = td.remap[row];
-#ifdef RS_DEBUG_BWD
-  if (row >= td.hash_size || (e >= 0 ? uint64_t(e) >= td.hbm_rows : uint64_t(-int64_t(e) - 1) >= td.slow_rows))
-    printf("apply_update: row %u H %llu e %d hbm %llu slow %llu dim %u kb %u\n", row,
-           (unsigned long long)td.hash_size, e, (unsigned long long)td.hbm_rows,
-           (unsigned long long)td.slow_rows, td.dim, td.key_base);
-#endif
-  float4* w = reinterpret_cast<float4*>(row_ptr(td, e));
-  float mult = a.lr;
-  if (a.opt == RS_OPT_ROWWISE_ADAGRAD) {
-    float s = 0.f;
-#pragma unroll
-    for (int vv = 0; vv < VPL; ++vv) {
-      if (uint32_t(lane + vv * 32) < V) {
-        s = __fadd_rn(s, __fmul_rn(g[vv].x, g[vv].x));
-        s = __fadd_rn(s, __fmul_rn(g[vv].y, g[vv].y));
-        s = __fadd_rn(s, __fmul_rn(g[vv].z, g[vv].z));
-        s = __fadd_rn(s, __fmul_rn(g[vv].w, g[vv].w));
-      }
-    }
-    const int L = lanes_for(td.dim);
-    for (int o = L >> 1; o >= 1; o >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
-    float* mp = mom_ptr(td, e);
-    const float m = __fadd_rn(*mp, __fdiv_rn(s, float(td.dim)));
-    __syncwarp();
-    if (lane == 0) *mp = m;
-    mult = __fdiv_rn(a.lr, __fadd_rn(__fsqrt_rn(m), a.eps));
-  }
-#pragma unroll
-  for (int vv = 0; vv < VPL; ++vv) {
-    const uint32_t vec = lane + vv * 32;
-    if (vec < V) {
-      float4 x = w[vec];
-      x.x = __fsub_rn(x.x, __fmul_rn(mult, g[vv].x));
-      x.y = __fsub_rn(x.y, __fmul_rn(mult, g[vv].y));
-      x.z = __fsub_rn(x.z, __fmul_rn(mult, g[vv].z));
-      x.w = __fsub_rn(x.w, __fmul_rn(mult, g[vv].w));
-      w[vec] = x;
-    }
-  }
-}
-
-template <int VPL>
-__device__ __forceinline__ void store_part(const BwdArgs& a, uint64_t chunk, int slot, uint32_t V,
-                                           const float4 (&g)[VPL]) {
-  const int lane = threadIdx.x & 31;
-  float4* p = reinterpret_cast<float4*>(a.part + (chunk * 2 + slot) * a.dmax);
-#pragma unroll
-  for (int vv = 0; vv < VPL; ++vv)
-    if (uint32_t(lane + vv * 32) < V) p[lane + vv * 32] = g[vv];
-}
-
-// One warp per chunk of kChunk sorted positions.
-template <int VPL>
-__global__ void __launch_bounds__(256) bwd_chunk_kernel(BwdArgs a) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t nchunks = (a.L + kChunk - 1) / kChunk;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t c = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; c < nchunks; c += nwarps) {
-    const uint64_t c0 = c * kChunk;
-    const uint64_t c1 = min(c0 + kChunk, a.L);
-    uint32_t kr[kChunk / 32], vr[kChunk / 32];
-#pragma unroll
-    for (int h = 0; h < kChunk / 32; ++h) {
-      const uint64_t i = c0 + h * 32 + lane;
-      kr[h] = i < c1 ? a.keys[i] : 0xFFFFFFFFu;
-      vr[h] = i < c1 ? a.vals[i] : 0u;
-    }
-    const uint32_t key_before = c0 > 0 ? a.keys[c0 - 1] : 0xFFFFFFFFu;
-    const uint32_t key_after = c1 < a.L ? a.keys[c1] : 0xFFFFFFFFu;
-    uint32_t cur = __shfl_sync(0xffffffffu, kr[0], 0);
-    uint32_t t = table_of_key(a, cur);
-    TableDev td = a.tables[t];
-    uint32_t tend = t + 1 < a.T ? a.key_base_sorted[t + 1] : 0xFFFFFFFFu;
-    uint64_t piece_start = c0;
-    float4 acc[VPL];
-#pragma unroll
-    for (int vv = 0; vv < VPL; ++vv) acc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
-    const uint32_t n = uint32_t(c1 - c0);
-    auto flush = [&](uint64_t pend) {
-      const bool before = piece_start == c0 && cur == key_before;
-      const bool after = pend == c1 && cur == key_after;
-      const uint32_t V = td.dim >> 2;
-      if (!before && !after) apply_update<VPL>(a, td, cur - td.key_base, acc);
-      else store_part<VPL>(a, c, before ? 0 : 1, V, acc);
-    };
-    for (uint32_t j = 0; j < n; j += 8) {
-      float4 v[8][VPL];
-      uint32_t ku[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t pos = j + u;
-        const uint32_t src = pos & 31;
-        uint32_t kk = 0, bb = 0;
-#pragma unroll
-        for (int h = 0; h < kChunk / 32; ++h) {
-          const uint32_t k2 = __shfl_sync(0xffffffffu, kr[h], src);
-          const uint32_t b2 = __shfl_sync(0xffffffffu, vr[h], src);
-          if (pos / 32 == uint32_t(h)) {
-            kk = k2;
-            bb = b2;
-          }
-        }
-        ku[u] = kk;
-        // table of this key (sorted keys: tables only advance)
-        uint32_t tt = t;
-        if (pos < n) {
-          while (kk >= (tt + 1 < a.T ? a.key_base_sorted[tt + 1] : 0xFFFFFFFFu)) ++tt;
-        }
-        const TableDev& tdu = a.tables[tt];
-        const float4* gr = reinterpret_cast<const float4*>(a.grad + uint64_t(bb) * a.stride + tdu.col);
-        const uint32_t Vu = tdu.dim >> 2;
-#pragma unroll
-        for (int vv = 0; vv < VPL; ++vv) {
-          const uint32_t vec = lane + vv * 32;
-          v[u][vv] = (pos < n && vec < Vu) ? ld_nc_f4(gr + vec) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t pos = j + u;
-        if (pos >= n) break;
-        if (ku[u] != cur) {
-          flush(c0 + pos);
-          cur = ku[u];
-          piece_start = c0 + pos;
-#pragma unroll
-          for (int vv = 0; vv < VPL; ++vv) acc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (cur >= tend) {
-            t = table_of_key(a, cur);
-            td = a.tables[t];
-            tend = t + 1 < a.T ? a.key_base_sorted[t + 1] : 0xFFFFFFFFu;
-          }
-        }
-#pragma unroll
-        for (int vv = 0; vv < VPL; ++vv) {
-          acc[vv].x = __fadd_rn(acc[vv].x, v[u][vv].x);
-          acc[vv].y = __fadd_rn(acc[vv].y, v[u][vv].y);
-          acc[vv].z = __fadd_rn(acc[vv].z, v[u][vv].z);
-          acc[vv].w = __fadd_rn(acc[vv].w, v[u][vv].w);
-        }
-      }
-    }
-    flush(c1);
-  }
-}
-
-// Segments that cross chunk edges: the chunk holding the segment's first
-// position sums its tail piece and the following chunks' head pieces in order.
-template <int VPL>
-__global__ void __launch_bounds__(256) bwd_finalize_kernel(BwdArgs a) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t nchunks = (a.L + kChunk - 1) / kChunk;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t c = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; c < nchunks; c += nwarps) {
-    const uint64_t c0 = c * kChunk;
-    const uint64_t c1 = min(c0 + kChunk, a.L);
-    if (c1 >= a.L) continue;
-    const uint32_t kl = a.keys[c1 - 1];
-    if (a.keys[c1] != kl) continue;  // last segment ends inside this chunk
-    // does the segment start inside this chunk?
-    const bool starts_before = (a.keys[c0] == kl) && c0 > 0 && a.keys[c0 - 1] == kl;
-    if (starts_before) continue;
-    const uint32_t t = table_of_key(a, kl);
-    const TableDev td = a.tables[t];
-    const uint32_t V = td.dim >> 2;
-    float4 acc[VPL];
-    const float4* p = reinterpret_cast<const float4*>(a.part + (c * 2 + 1) * a.dmax);
-#pragma unroll
-    for (int vv = 0; vv < VPL; ++vv) {
-      const uint32_t vec = lane + vv * 32;
-      acc[vv] = vec < V ? p[vec] : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    for (uint64_t c2 = c + 1; c2 < nchunks; ++c2) {
-      const float4* q = reinterpret_cast<const float4*>(a.part + (c2 * 2) * a.dmax);
-#pragma unroll
-      for (int vv = 0; vv < VPL; ++vv) {
-        const uint32_t vec = lane + vv * 32;
-        if (vec < V) {
-          const float4 x = q[vec];
-          acc[vv].x = __fadd_rn(acc[vv].x, x.x);
-          acc[vv].y = __fadd_rn(acc[vv].y, x.y);
-          acc[vv].z = __fadd_rn(acc[vv].z, x.z);
-          acc[vv].w = __fadd_rn(acc[vv].w, x.w);
-        }
-      }
-      const uint64_t e2 = min((c2 + 1) * kChunk, a.L);
-      if (e2 >= a.L || a.keys[e2] != kl || a.keys[e2 - 1] != kl) break;
-    }
-    apply_update<VPL>(a, td, kl - td.key_base, acc);
-  }
-}
+namespace rs {
+namespace emb {
 
 // ------------------------------------------------------------------ init / read
 __global__ void init_kernel(TableDev td, uint32_t table_id, uint64_t seed, float scale) {
@@ -500,6 +281,7 @@ struct rs_emb {
   uint32_t* keys = nullptr;
   uint32_t* vals = nullptr;
   float* part = nullptr;
+  float* spart = nullptr;
   unsigned* d_err = nullptr;
   char* sort_scratch = nullptr;
   size_t sort_scratch_bytes = 0;
@@ -515,6 +297,7 @@ struct rs_emb {
     if (keys) cudaFree(keys);
     if (vals) cudaFree(vals);
     if (part) cudaFree(part);
+    if (spart) cudaFree(spart);
     if (d_err) cudaFree(d_err);
     if (sort_scratch) cudaFree(sort_scratch);
   }
@@ -618,10 +401,16 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
     while (e->key_bits < 32 && (uint64_t(1) << e->key_bits) < uint64_t(kb)) ++e->key_bits;
     RS_CUDA(cudaMalloc(&e->d_tables, sizeof(TableDev) * T));
     RS_CUDA(cudaMemcpyAsync(e->d_tables, e->h_tables.data(), sizeof(TableDev) * T, cudaMemcpyHostToDevice, st));
-    std::vector<uint32_t> kbs(T);
-    for (uint32_t t = 0; t < T; ++t) kbs[t] = e->h_tables[t].key_base;
-    RS_CUDA(cudaMalloc(&e->d_key_base_sorted, 4 * T));
-    RS_CUDA(cudaMemcpyAsync(e->d_key_base_sorted, kbs.data(), 4 * T, cudaMemcpyHostToDevice, st));
+    // backward table arrays: key_base[T+1] (sentinel = total keys), col[T], dim[T]
+    std::vector<uint32_t> kbs(3 * size_t(T) + 1);
+    for (uint32_t t = 0; t < T; ++t) {
+      kbs[t] = e->h_tables[t].key_base;
+      kbs[T + 1 + t] = uint32_t(e->h_tables[t].col);
+      kbs[2 * T + 1 + t] = e->h_tables[t].dim;
+    }
+    kbs[T] = kb;
+    RS_CUDA(cudaMalloc(&e->d_key_base_sorted, 4 * kbs.size()));
+    RS_CUDA(cudaMemcpyAsync(e->d_key_base_sorted, kbs.data(), 4 * kbs.size(), cudaMemcpyHostToDevice, st));
     // forward classes
     for (uint32_t t = 0; t < T; ++t) {
       const int G = lanes_for(tabs[t].dim);
@@ -651,6 +440,8 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
     RS_CUDA(cudaMalloc(&e->vals, L * 4));
     const size_t nch = (L + emb::kChunk - 1) / emb::kChunk;
     RS_CUDA(cudaMalloc(&e->part, nch * 2 * e->dmax * 4));
+    const size_t nsup = (nch + emb::kSuper - 1) / emb::kSuper;
+    RS_CUDA(cudaMalloc(&e->spart, nsup * 2 * e->dmax * 4));
     e->sort_scratch_bytes = radix_sort_scratch_bytes(L) + (4 << 20);
     RS_CUDA(cudaMalloc(&e->sort_scratch, e->sort_scratch_bytes));
     RS_CUDA(cudaStreamSynchronize(st));
@@ -705,13 +496,17 @@ void emb_forward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx
   RS_LAUNCH_CHECK();
 }
 
-template <int VPL>
+template <int VPL, int PEND>
 static void launch_bwd(rs_emb* e, const emb::BwdArgs& a) {
   const uint64_t nch = (a.L + emb::kChunk - 1) / emb::kChunk;
-  const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((nch + 7) / 8, uint64_t(sm_count()) * 32)));
-  emb::bwd_chunk_kernel<VPL><<<grid, 256, 0, e->ctx->stream>>>(a);
-  emb::bwd_finalize_kernel<VPL><<<grid, 256, 0, e->ctx->stream>>>(a);
-  RS_COUNT(2);
+  const uint64_t nsup = (nch + emb::kSuper - 1) / emb::kSuper;
+  const uint64_t cap = uint64_t(sm_count()) * 16;
+  const unsigned g1 = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((nch + 7) / 8, cap)));
+  const unsigned g2 = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((nsup + 7) / 8, cap)));
+  emb::bwd_chunk_kernel<VPL, PEND><<<g1, emb::kBwdThreads, 0, e->ctx->stream>>>(a);
+  emb::bwd_super_kernel<VPL, PEND><<<g2, emb::kBwdThreads, 0, e->ctx->stream>>>(a);
+  emb::bwd_final_kernel<VPL, PEND><<<g2, emb::kBwdThreads, 0, e->ctx->stream>>>(a);
+  RS_COUNT(3);
 }
 
 void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx, const float* grad,
@@ -737,13 +532,14 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
   scr.base = e->sort_scratch;
   scr.cap = e->sort_scratch_bytes;
   radix_sort_pairs(e->keys, e->vals, L, int(e->key_bits), scr, st);
-  emb::BwdArgs a{e->d_tables, e->d_key_base_sorted, e->T, e->keys, e->vals, L, grad,
-                 e->total_dim, e->part, e->dmax, lr, e->eps, e->opt};
+  const uint32_t* tb = e->d_key_base_sorted;
+  emb::BwdArgs a{e->d_tables, tb, tb + e->T + 1, tb + 2 * e->T + 1, e->T, e->keys, e->vals, L,
+                 grad, e->total_dim, e->part, e->spart, e->dmax, lr, e->eps, e->opt};
   switch (e->bwd_vpl) {
-    case 1: launch_bwd<1>(e, a); break;
-    case 2: launch_bwd<2>(e, a); break;
-    case 4: launch_bwd<4>(e, a); break;
-    case 8: launch_bwd<8>(e, a); break;
+    case 1: launch_bwd<1, 4>(e, a); break;
+    case 2: launch_bwd<2, 2>(e, a); break;
+    case 4: launch_bwd<4, 1>(e, a); break;
+    case 8: launch_bwd<8, 1>(e, a); break;
     default: throw Error(-9, "emb_backward: unsupported dim");
   }
   RS_LAUNCH_CHECK();

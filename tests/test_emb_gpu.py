@@ -50,6 +50,7 @@ CASES = [
     ([64, 128, 32], [1000, 3000, 257], [0.5, 0.2, 1.0], 256, 30),
     ([256, 96, 4], [500, 800, 64], [0.0, 0.7, 0.3], 100, 12),
     ([64], [50], [0.4], 1024, 40),  # heavy duplicates: long row segments cross chunks
+    ([64, 128], [4, 3], [0.5, 0.34], 2048, 30),  # segments of ~15K: cross superchunks
 ]
 
 
