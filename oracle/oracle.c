@@ -290,7 +290,7 @@ static int cmp_lk(const void* a, const void* b) {
   return x->l < y->l ? -1 : (x->l > y->l);
 }
 
-#define OR_CHUNK 64 /* csrc/emb_bwd.cuh kChunk */
+#define OR_CHUNK 32 /* csrc/emb_bwd.cuh kChunk */
 #define OR_SUPER 64 /* csrc/emb_bwd.cuh kSuper (chunks per superchunk) */
 
 int or_emb_backward(uint32_t T, uint64_t B, const uint32_t* D,

@@ -102,8 +102,8 @@ int or_emb_forward(uint32_t T, uint64_t B, const uint32_t* D,
  * (table, row) the gradient g = sum of grad_out[b, col_off[t] : +D] over its
  * lookups, accumulated in fp32 in the kernel's fixed tree
  * (csrc/emb_bwd.cuh): the row's run in the sorted list is cut at multiples of
- * 64 positions; each piece is summed in sorted order from +0.0f; the pieces
- * falling in one 4096-position superchunk are added left to right (first
+ * 32 positions; each piece is summed in sorted order from +0.0f; the pieces
+ * falling in one 2048-position superchunk are added left to right (first
  * piece as the accumulator), and the superchunk sums are added left to right
  * (first as the accumulator).  Then
  *   opt 0 (row-wise SGD):  w[d] = w[d] - lr*g[d]

@@ -496,14 +496,21 @@ void emb_forward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx
   RS_LAUNCH_CHECK();
 }
 
-template <int VPL, int PEND>
+template <int VPL, int U, int PEND>
 static void launch_bwd(rs_emb* e, const emb::BwdArgs& a) {
   const uint64_t nch = (a.L + emb::kChunk - 1) / emb::kChunk;
   const uint64_t nsup = (nch + emb::kSuper - 1) / emb::kSuper;
   const uint64_t cap = uint64_t(sm_count()) * 16;
   const unsigned g1 = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((nch + 7) / 8, cap)));
   const unsigned g2 = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((nsup + 7) / 8, cap)));
-  emb::bwd_chunk_kernel<VPL, PEND><<<g1, emb::kBwdThreads, 0, e->ctx->stream>>>(a);
+  const int stage_bytes = emb::kBwdWarps * U * 32 * VPL * int(sizeof(float4));
+  static bool attr_set = false;
+  if (!attr_set) {
+    RS_CUDA(cudaFuncSetAttribute(emb::bwd_chunk_kernel<VPL, U>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes));
+    attr_set = true;
+  }
+  emb::bwd_chunk_kernel<VPL, U><<<g1, emb::kBwdThreads, stage_bytes, e->ctx->stream>>>(a);
   emb::bwd_super_kernel<VPL, PEND><<<g2, emb::kBwdThreads, 0, e->ctx->stream>>>(a);
   emb::bwd_final_kernel<VPL, PEND><<<g2, emb::kBwdThreads, 0, e->ctx->stream>>>(a);
   RS_COUNT(3);
@@ -536,10 +543,10 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
   emb::BwdArgs a{e->d_tables, tb, tb + e->T + 1, tb + 2 * e->T + 1, e->T, e->keys, e->vals, L,
                  grad, e->total_dim, e->part, e->spart, e->dmax, lr, e->eps, e->opt};
   switch (e->bwd_vpl) {
-    case 1: launch_bwd<1, 4>(e, a); break;
-    case 2: launch_bwd<2, 2>(e, a); break;
-    case 4: launch_bwd<4, 1>(e, a); break;
-    case 8: launch_bwd<8, 1>(e, a); break;
+    case 1: launch_bwd<1, 8, 4>(e, a); break;
+    case 2: launch_bwd<2, 8, 2>(e, a); break;
+    case 4: launch_bwd<4, 4, 1>(e, a); break;
+    case 8: launch_bwd<8, 2, 1>(e, a); break;
     default: throw Error(-9, "emb_backward: unsupported dim");
   }
   RS_LAUNCH_CHECK();

@@ -5,24 +5,25 @@
 // is one contiguous segment of the sorted list in lookup order.
 //
 // Fixed reduction tree (restated by oracle.c or_emb_backward):
-//   level 1  the list is cut into 64-position chunks; a warp per chunk sums
+//   level 1  the list is cut into 32-position chunks; a warp per chunk sums
 //            each piece (segment ∩ chunk) over its positions in order from
-//            +0.0f, gathering grad_out rows 8 at a time;
+//            +0.0f with a segmented running sum;
 //   level 2  64-chunk superchunks: a warp sums, left to right, the chunk-edge
 //            pieces of every segment that crosses a chunk edge inside it;
 //   level 3  segments crossing superchunk edges: the superchunk holding the
 //            segment's start sums its piece and the following superchunks'
 //            pieces left to right.
 // A segment is updated (row-wise SGD or exact row-wise Adagrad) by the level
-// that completes it.  Updates are batched PEND at a time per warp so the
-// dependent remap -> row -> state loads of different rows overlap.  No float
-// atomics; results are bitwise reproducible.
+// that completes it.  Level 1 stages the segments completing in a batch of
+// positions in shared memory and updates them together, so the dependent
+// remap -> row -> state loads of different rows overlap.  No float atomics;
+// results are bitwise reproducible.
 #pragma once
 
 namespace rs {
 namespace emb {
 
-constexpr int kChunk = 64;
+constexpr int kChunk = 32;
 constexpr int kSuper = 64;
 constexpr uint64_t kSpan = uint64_t(kChunk) * kSuper;
 constexpr uint32_t kSmemTables = 2048;
@@ -89,8 +90,48 @@ __device__ __forceinline__ void add4(float4& a, const float4& b) {
   a.w = __fadd_rn(a.w, b.w);
 }
 
-// Pending complete segments of one warp: key, table and the gradient slice
-// (VPL float4 per lane, vec = lane + vv*32).
+// One row's optimizer step given its full gradient slice g (vec = lane+vv*32)
+// and the row's current values w / state m already loaded.  Arithmetic order
+// matches or_emb_backward.
+template <int VPL>
+__device__ __forceinline__ void update_row(const BwdArgs& a, uint32_t dim, const float4 (&g)[VPL],
+                                           float4 (&w)[VPL], float m_old, float* mp, float4* wp) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t V = dim >> 2;
+  float mult = a.lr;
+  if (a.opt == RS_OPT_ROWWISE_ADAGRAD) {
+    float q = 0.f;
+#pragma unroll
+    for (int vv = 0; vv < VPL; ++vv) {
+      if (uint32_t(lane + vv * 32) < V) {
+        q = __fadd_rn(q, __fmul_rn(g[vv].x, g[vv].x));
+        q = __fadd_rn(q, __fmul_rn(g[vv].y, g[vv].y));
+        q = __fadd_rn(q, __fmul_rn(g[vv].z, g[vv].z));
+        q = __fadd_rn(q, __fmul_rn(g[vv].w, g[vv].w));
+      }
+    }
+    const int Lw = lanes_for(dim);
+    for (int o = Lw >> 1; o >= 1; o >>= 1) q = __fadd_rn(q, __shfl_xor_sync(0xffffffffu, q, o));
+    const float m = __fadd_rn(m_old, __fdiv_rn(q, float(dim)));
+    if (lane == 0) *mp = m;
+    mult = __fdiv_rn(a.lr, __fadd_rn(__fsqrt_rn(m), a.eps));
+  }
+#pragma unroll
+  for (int vv = 0; vv < VPL; ++vv) {
+    const uint32_t vec = lane + vv * 32;
+    if (vec < V) {
+      float4 x = w[vv];
+      x.x = __fsub_rn(x.x, __fmul_rn(mult, g[vv].x));
+      x.y = __fsub_rn(x.y, __fmul_rn(mult, g[vv].y));
+      x.z = __fsub_rn(x.z, __fmul_rn(mult, g[vv].z));
+      x.w = __fsub_rn(x.w, __fmul_rn(mult, g[vv].w));
+      wp[vec] = x;
+    }
+  }
+}
+
+// Pending complete segments of one warp (levels 2 and 3): key, table and the
+// gradient slice (VPL float4 per lane, vec = lane + vv*32).
 template <int VPL, int PEND>
 struct Pending {
   uint32_t key[PEND];
@@ -110,8 +151,6 @@ struct Pending {
     ++n;
   }
 
-  // Row-wise SGD / exact row-wise Adagrad on every pending row; the loads of
-  // all rows are issued before any row is updated.
   __device__ __forceinline__ void flush(const BwdArgs& a) {
     if (n == 0) return;
     const int lane = threadIdx.x & 31;
@@ -121,59 +160,28 @@ struct Pending {
       if (s == lane && s < n) my_e = a.tables[tab[s]].remap[key[s] - a.tables[tab[s]].key_base];
     float4 w[PEND][VPL];
     float mom[PEND];
-    float4* wp[PEND];
-    float* mp[PEND];
-    uint32_t Vs[PEND], Ds[PEND];
 #pragma unroll
     for (int s = 0; s < PEND; ++s) {
       const int32_t e = __shfl_sync(0xffffffffu, my_e, s);
       if (s < n) {
         const TableDev& td = a.tables[tab[s]];
-        Ds[s] = td.dim;
-        Vs[s] = td.dim >> 2;
-        wp[s] = reinterpret_cast<float4*>(row_ptr(td, e));
-        mp[s] = a.opt == RS_OPT_ROWWISE_ADAGRAD ? mom_ptr(td, e) : nullptr;
+        const float4* wp = reinterpret_cast<const float4*>(row_ptr(td, e));
 #pragma unroll
         for (int vv = 0; vv < VPL; ++vv) {
           const uint32_t vec = lane + vv * 32;
-          w[s][vv] = vec < Vs[s] ? wp[s][vec] : make_float4(0.f, 0.f, 0.f, 0.f);
+          w[s][vv] = vec < (td.dim >> 2) ? wp[vec] : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        mom[s] = mp[s] ? *mp[s] : 0.f;
+        mom[s] = a.opt == RS_OPT_ROWWISE_ADAGRAD ? *mom_ptr(td, e) : 0.f;
       }
     }
 #pragma unroll
     for (int s = 0; s < PEND; ++s) {
+      const int32_t e = __shfl_sync(0xffffffffu, my_e, s);
       if (s < n) {
-        float mult = a.lr;
-        if (a.opt == RS_OPT_ROWWISE_ADAGRAD) {
-          float q = 0.f;
-#pragma unroll
-          for (int vv = 0; vv < VPL; ++vv) {
-            if (uint32_t(lane + vv * 32) < Vs[s]) {
-              q = __fadd_rn(q, __fmul_rn(g[s][vv].x, g[s][vv].x));
-              q = __fadd_rn(q, __fmul_rn(g[s][vv].y, g[s][vv].y));
-              q = __fadd_rn(q, __fmul_rn(g[s][vv].z, g[s][vv].z));
-              q = __fadd_rn(q, __fmul_rn(g[s][vv].w, g[s][vv].w));
-            }
-          }
-          const int Lw = lanes_for(Ds[s]);
-          for (int o = Lw >> 1; o >= 1; o >>= 1) q = __fadd_rn(q, __shfl_xor_sync(0xffffffffu, q, o));
-          const float m = __fadd_rn(mom[s], __fdiv_rn(q, float(Ds[s])));
-          if (lane == 0) *mp[s] = m;
-          mult = __fdiv_rn(a.lr, __fadd_rn(__fsqrt_rn(m), a.eps));
-        }
-#pragma unroll
-        for (int vv = 0; vv < VPL; ++vv) {
-          const uint32_t vec = lane + vv * 32;
-          if (vec < Vs[s]) {
-            float4 x = w[s][vv];
-            x.x = __fsub_rn(x.x, __fmul_rn(mult, g[s][vv].x));
-            x.y = __fsub_rn(x.y, __fmul_rn(mult, g[s][vv].y));
-            x.z = __fsub_rn(x.z, __fmul_rn(mult, g[s][vv].z));
-            x.w = __fsub_rn(x.w, __fmul_rn(mult, g[s][vv].w));
-            wp[s][vec] = x;
-          }
-        }
+        const TableDev& td = a.tables[tab[s]];
+        update_row<VPL>(a, td.dim, g[s], w[s], mom[s],
+                        a.opt == RS_OPT_ROWWISE_ADAGRAD ? mom_ptr(td, e) : nullptr,
+                        reinterpret_cast<float4*>(row_ptr(td, e)));
       }
     }
     n = 0;
@@ -201,92 +209,155 @@ __device__ __forceinline__ void load_vec(const float* base, uint32_t V, float4 (
 }
 
 // ---------------------------------------------------------------- level 1
-template <int VPL, int PEND>
+// Warp per 32-position chunk.  Lane j owns position j's key, sample and
+// table column; head/tail flags come from the neighbouring keys.  Rows are
+// gathered U at a time and folded into a segmented running sum (reset to
+// +0.0f at heads).  Pieces that end inside the chunk and started inside it
+// are complete segments: their sums are staged in shared memory and the
+// batch is updated together.  Edge pieces go to the level-2 buffer.
+template <int VPL, int U>
 __global__ void __launch_bounds__(kBwdThreads, 2) bwd_chunk_kernel(BwdArgs a) {
   __shared__ TabSmem ts;
-  __shared__ uint32_t s_k[kBwdWarps][kChunk], s_v[kBwdWarps][kChunk];
+  extern __shared__ float4 stage_mem[];  // [warps][U][32*VPL]
   const TabView tv = load_tables(a, ts);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float4* stage = stage_mem + size_t(w) * U * 32 * VPL;
   const uint64_t nchunks = (a.L + kChunk - 1) / kChunk;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  Pending<VPL, PEND> pend;
   for (uint64_t c = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; c < nchunks; c += nwarps) {
     const uint64_t c0 = c * kChunk;
-    const uint64_t c1 = min(c0 + kChunk, a.L);
-    const uint32_t n = uint32_t(c1 - c0);
-    __syncwarp();
-#pragma unroll
-    for (int h = 0; h < kChunk / 32; ++h) {
-      const uint64_t i = c0 + h * 32 + lane;
-      s_k[w][h * 32 + lane] = i < c1 ? a.keys[i] : 0xFFFFFFFFu;
-      s_v[w][h * 32 + lane] = i < c1 ? a.vals[i] : 0u;
-    }
+    const uint32_t n = uint32_t(min(uint64_t(kChunk), a.L - c0));
+    const bool valid = uint32_t(lane) < n;
+    const uint32_t k = valid ? a.keys[c0 + lane] : 0xFFFFFFFFu;
+    const uint32_t b = valid ? a.vals[c0 + lane] : 0u;
     const uint32_t key_before = c0 > 0 ? a.keys[c0 - 1] : 0xFFFFFFFFu;
-    const uint32_t key_after = c1 < a.L ? a.keys[c1] : 0xFFFFFFFFu;
-    __syncwarp();
-    uint32_t cur = s_k[w][0];
-    uint32_t t = tv.find(cur);
-    uint32_t tend = tv.kb[t + 1];
-    uint32_t V = tv.dim[t] >> 2;
-    uint32_t tg = t;  // gather-side table cursor (keys ascend)
+    const uint32_t key_after = c0 + n < a.L ? a.keys[c0 + n] : 0xFFFFFFFFu;
+    uint32_t kp = __shfl_up_sync(0xffffffffu, k, 1);
+    uint32_t kn = __shfl_down_sync(0xffffffffu, k, 1);
+    if (lane == 0) kp = key_before;
+    if (uint32_t(lane) == n - 1) kn = key_after;
+    const unsigned heads = __ballot_sync(0xffffffffu, valid && k != kp);
+    const unsigned tails = __ballot_sync(0xffffffffu, valid && k != kn);
+    // per-lane table (warp-uniform fast path when the chunk sits in one table)
+    const uint32_t k0 = __shfl_sync(0xffffffffu, k, 0);
+    const uint32_t kl = __shfl_sync(0xffffffffu, k, n - 1);
+    uint32_t t = tv.find(k0);
+    if (kl >= tv.kb[t + 1]) t = valid ? tv.find(k) : t;
+    const uint32_t col = tv.col[t];
+    const uint32_t dimv = tv.dim[t];
     float4 acc[VPL];
 #pragma unroll
     for (int vv = 0; vv < VPL; ++vv) acc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
-    auto end_piece = [&](uint32_t pend_pos) {
-      const bool before = cur == key_before;
-      const bool after = pend_pos == n && cur == key_after;
-      if (!before && !after) {
-        pend.push(cur, t, acc);
-        if (pend.n == PEND) pend.flush(a);
-      } else {
-        store_vec<VPL>(a.part + (c * 2 + (before ? 0 : 1)) * a.dmax, V, acc);
+    for (uint32_t jb = 0; jb < n; jb += U) {
+      float4 v[U][VPL];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t pos = jb + u;
+        const uint32_t bu = __shfl_sync(0xffffffffu, b, pos & 31);
+        const uint32_t cu = __shfl_sync(0xffffffffu, col, pos & 31);
+        const uint32_t Vu = __shfl_sync(0xffffffffu, dimv, pos & 31) >> 2;
+        const float4* gr = reinterpret_cast<const float4*>(a.grad + uint64_t(bu) * a.stride + cu);
+#pragma unroll
+        for (int vv = 0; vv < VPL; ++vv) {
+          const uint32_t vec = lane + vv * 32;
+          v[u][vv] = (pos < n && vec < Vu) ? ld_nc_f4(gr + vec) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
-    };
-    for (uint32_t j = 0; j < n; j += 8) {
-      float4 v[8][VPL];
-      uint32_t ku[8];
+      int ns = 0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t pos = j + u;
-        ku[u] = 0xFFFFFFFFu;
-#pragma unroll
-        for (int vv = 0; vv < VPL; ++vv) v[u][vv] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int u = 0; u < U; ++u) {
+        const uint32_t pos = jb + u;
         if (pos < n) {
-          const uint32_t k = s_k[w][pos];
-          const uint32_t b = s_v[w][pos];
-          while (k >= tv.kb[tg + 1]) ++tg;
-          ku[u] = k;
-          const float4* gr = reinterpret_cast<const float4*>(a.grad + uint64_t(b) * a.stride + tv.col[tg]);
-          const uint32_t Vu = tv.dim[tg] >> 2;
+          if ((heads >> pos) & 1u) {
 #pragma unroll
-          for (int vv = 0; vv < VPL; ++vv) {
-            const uint32_t vec = lane + vv * 32;
-            if (vec < Vu) v[u][vv] = ld_nc_f4(gr + vec);
+            for (int vv = 0; vv < VPL; ++vv) acc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int vv = 0; vv < VPL; ++vv) add4(acc[vv], v[u][vv]);
+          if ((tails >> pos) & 1u) {
+            const uint32_t Vu = __shfl_sync(0xffffffffu, dimv, pos) >> 2;
+            if ((heads & (0xFFFFFFFFu >> (31 - pos))) == 0) {
+              // began before this chunk, ends here: head edge piece
+              store_vec<VPL>(a.part + (c * 2) * a.dmax, Vu, acc);
+            } else {
+#pragma unroll
+              for (int vv = 0; vv < VPL; ++vv)
+                if (uint32_t(lane + vv * 32) < Vu) stage[ns * 32 * VPL + lane + vv * 32] = acc[vv];
+              ++ns;
+            }
           }
         }
       }
+      // keys / tables of the staged complete segments (in position order)
+      if (ns) {
+        const unsigned bm = (tails >> jb) & ((U >= 32) ? 0xFFFFFFFFu : ((1u << U) - 1u));
+        // drop a leading head-edge piece (it was not staged)
+        const unsigned upto = bm;
+        unsigned staged = 0;
+        int s = 0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t pos = j + u;
-        if (pos >= n) break;
-        if (ku[u] != cur) {
-          end_piece(pos);
-          cur = ku[u];
+        for (int u = 0; u < U; ++u) {
+          const uint32_t pos = jb + u;
+          if (((upto >> u) & 1u) && (heads & (0xFFFFFFFFu >> (31 - pos))) != 0) staged |= 1u << u;
+        }
+        // lane s (< ns) takes the s-th staged position
+        uint32_t my_pos = 0;
+        unsigned rem = staged;
+        for (s = 0; s < ns; ++s) {
+          const int u = __ffs(rem) - 1;
+          rem &= rem - 1;
+          if (lane == s) my_pos = jb + u;
+        }
+        const uint32_t my_key = __shfl_sync(0xffffffffu, k, my_pos & 31);
+        const uint32_t my_t = __shfl_sync(0xffffffffu, t, my_pos & 31);
+        int32_t my_e = 0;
+        if (lane < ns) {
+          const TableDev& td = a.tables[my_t];
+          my_e = td.remap[my_key - td.key_base];
+        }
+        // issue every row / state load of the batch, then update
+        float4 wv[U][VPL];
+        float mom[U];
 #pragma unroll
-          for (int vv = 0; vv < VPL; ++vv) acc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (cur >= tend) {
-            t = tv.find(cur);
-            tend = tv.kb[t + 1];
-            V = tv.dim[t] >> 2;
+        for (int q = 0; q < U; ++q) {
+          const int32_t e = __shfl_sync(0xffffffffu, my_e, q);
+          const uint32_t tq = __shfl_sync(0xffffffffu, my_t, q);
+          if (q < ns) {
+            const TableDev& td = a.tables[tq];
+            const float4* wp = reinterpret_cast<const float4*>(row_ptr(td, e));
+#pragma unroll
+            for (int vv = 0; vv < VPL; ++vv) {
+              const uint32_t vec = lane + vv * 32;
+              wv[q][vv] = vec < (td.dim >> 2) ? wp[vec] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            mom[q] = a.opt == RS_OPT_ROWWISE_ADAGRAD ? *mom_ptr(td, e) : 0.f;
           }
         }
+        __syncwarp();
 #pragma unroll
-        for (int vv = 0; vv < VPL; ++vv) add4(acc[vv], v[u][vv]);
+        for (int q = 0; q < U; ++q) {
+          const int32_t e = __shfl_sync(0xffffffffu, my_e, q);
+          const uint32_t tq = __shfl_sync(0xffffffffu, my_t, q);
+          if (q < ns) {
+            const TableDev& td = a.tables[tq];
+            float4 g[VPL];
+#pragma unroll
+            for (int vv = 0; vv < VPL; ++vv) g[vv] = stage[q * 32 * VPL + lane + vv * 32];
+            update_row<VPL>(a, td.dim, g, wv[q], mom[q],
+                            a.opt == RS_OPT_ROWWISE_ADAGRAD ? mom_ptr(td, e) : nullptr,
+                            reinterpret_cast<float4*>(row_ptr(td, e)));
+          }
+        }
+        __syncwarp();
       }
     }
-    end_piece(n);
+    // the last piece continues into the next chunk: tail edge piece (or the
+    // whole chunk is the middle of a segment: head edge piece)
+    if (!((tails >> (n - 1)) & 1u)) {
+      const uint32_t Vl = __shfl_sync(0xffffffffu, dimv, n - 1) >> 2;
+      store_vec<VPL>(a.part + (c * 2 + (heads == 0 ? 0 : 1)) * a.dmax, Vl, acc);
+    }
   }
-  pend.flush(a);
 }
 
 // ---------------------------------------------------------------- level 2
@@ -350,13 +421,13 @@ __global__ void __launch_bounds__(kBwdThreads, 2) bwd_super_kernel(BwdArgs a) {
       for (int slot = 0; slot < 2; ++slot) {
         const bool has = slot == 0 ? e0 : e1;
         if (!has) continue;
-        const uint32_t k = slot == 0 ? f0 : f1;
+        const uint32_t kk = slot == 0 ? f0 : f1;
         float4 x[VPL];
-        if (!open || k != run) {
+        if (!open || kk != run) {
           close();
-          run = k;
+          run = kk;
           open = true;
-          t = tv.find(k);
+          t = tv.find(kk);
           V = tv.dim[t] >> 2;
           load_vec<VPL>(a.part + (c * 2 + slot) * a.dmax, V, acc);
         } else {
@@ -384,7 +455,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) bwd_final_kernel(BwdArgs a) {
     const uint64_t P0 = s * kSpan, P1 = min(P0 + kSpan, a.L);
     if (P1 >= a.L) continue;
     const uint32_t kl = a.keys[P1 - 1];
-    if (a.keys[P1] != kl) continue;                              // ends inside
+    if (a.keys[P1] != kl) continue;                                    // ends inside
     if (P0 > 0 && a.keys[P0 - 1] == kl && a.keys[P0] == kl) continue;  // middle piece
     const uint32_t t = tv.find(kl);
     const uint32_t V = tv.dim[t] >> 2;
