@@ -237,21 +237,24 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
     # algorithmic bytes per batch (fwd: rows + index + remap entry per lookup,
     # offsets, pooled output; bwd: grad read once, indices, unique rows RMW +
     # Adagrad state).  Per-table lookup counts and unique rows from the batch.
-    fwd_bytes, bwd_bytes, lookups = [], [], []
+    fwd_bytes, bwd_bytes, lookups, uniques = [], [], [], []
     for off, idx, n in batches:
         o = off.cpu().numpy().view(np.uint32).astype(np.int64)
         ih = idx[:n].cpu().numpy().view(np.uint32)
         fb = 4 * (T * B + 1) + 4 * B * D_local
         bb = 4 * B * D_local + 4 * n
+        uq = 0
         for t, w in enumerate(lspecs):
             lt = int(o[(t + 1) * B] - o[t * B])
             rb = 4 * w.table.dim
             fb += lt * (rb + 8)
             u = np.unique(ih[o[t * B]:o[(t + 1) * B]]).size
+            uq += u
             bb += u * 2 * rb + (8 * u if args.optimizer != "sgd" else 0)
         fwd_bytes.append(fb)
         bwd_bytes.append(bb)
         lookups.append(n)
+        uniques.append(uq)
     pooled = torch.empty(B, max(1, D_local), dtype=torch.float32, device=dev)
     hits = torch.zeros(2 * max(1, T), dtype=torch.int64, device=dev)
     flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -324,7 +327,8 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
                a2a_ms=float(np.mean(a2a_ms)), launches=launches, clocks=clk,
                fwd_bytes=float(np.mean([fwd_bytes[i % len(batches)] for i in range(steps)])) if T else 0,
                bwd_bytes=float(np.mean([bwd_bytes[i % len(batches)] for i in range(steps)])) if T else 0,
-               lookups=float(np.mean(lookups)) if T else 0, hbm_bytes=hbm_b, host_bytes=host_b,
+               lookups=float(np.mean(lookups)) if T else 0,
+               unique_rows=float(np.mean(uniques)) if T else 0, hbm_bytes=hbm_b, host_bytes=host_b,
                tables=T)
     # accounting check: the forward's hit counters equal simulate() on the same batch
     if T and world == 1:
@@ -503,6 +507,7 @@ def main():
             "simulated_uvm_pct": sim_uvm,
             "uvm_matches_simulate": r.get("uvm_matches_simulate"),
             "recshard": {k: r[k] for k in ("samples_per_s", "ms_per_step", "fwd_ms", "bwd_ms",
+                                           "lookups", "unique_rows",
                                            "a2a_ms", "uvm_pct", "hbm_bytes", "host_bytes")},
             "greedy": None if g is None else {k: g[k] for k in ("samples_per_s", "ms_per_step",
                                                                  "fwd_ms", "bwd_ms", "uvm_pct")},

@@ -304,13 +304,21 @@ int or_emb_backward(uint32_t T, uint64_t B, const uint32_t* D,
   uint64_t* kb = (uint64_t*)malloc(sizeof(uint64_t) * (T + 1));
   kb[0] = 0;
   for (uint32_t t = 0; t < T; ++t) kb[t + 1] = kb[t] + H[t];
+  /* chunks restart at each table's first sorted position tpos[t] =
+   * offsets[t*B]; global chunk ids cb[t] + (pos - tpos[t]) / OR_CHUNK */
+  uint64_t* cb = (uint64_t*)malloc(sizeof(uint64_t) * (T + 1));
+  cb[0] = 0;
+  for (uint32_t t = 0; t < T; ++t) {
+    const uint64_t lt = offsets[(uint64_t)(t + 1) * B] - offsets[(uint64_t)t * B];
+    cb[t + 1] = cb[t] + (lt + OR_CHUNK - 1) / OR_CHUNK;
+  }
   lk_t* lk = (lk_t*)malloc(sizeof(lk_t) * L);
   uint64_t* bag = (uint64_t*)malloc(sizeof(uint64_t) * L);
   uint32_t* tab = (uint32_t*)malloc(sizeof(uint32_t) * L);
   for (uint32_t t = 0; t < T; ++t)
     for (uint64_t b = 0; b < B; ++b)
       for (uint64_t l = offsets[t * B + b]; l < offsets[t * B + b + 1]; ++l) {
-        if (indices[l] >= H[t]) { free(kb); free(lk); free(bag); free(tab); return ST_INVALID; }
+        if (indices[l] >= H[t]) { free(cb); free(kb); free(lk); free(bag); free(tab); return ST_INVALID; }
         lk[l].key = kb[t] + indices[l];
         lk[l].l = l;
         bag[l] = b;
@@ -340,14 +348,15 @@ int or_emb_backward(uint32_t T, uint64_t B, const uint32_t* D,
     int first_group = 1, first_piece = 1;
     uint64_t p = i, group = (uint64_t)-1;
     while (p < e) {
-      uint64_t pe = (p / OR_CHUNK + 1) * OR_CHUNK;
+      const uint64_t tp = offsets[(uint64_t)t * B];
+      uint64_t pe = tp + ((p - tp) / OR_CHUNK + 1) * OR_CHUNK;
       if (pe > e) pe = e;
       for (uint32_t k = 0; k < d; ++k) piece[k] = 0.0f;
       for (uint64_t q = p; q < pe; ++q) {
         const float* go = grad_out + bag[lk[q].l] * grad_stride + col_off[t];
         for (uint32_t k = 0; k < d; ++k) piece[k] = piece[k] + go[k];
       }
-      const uint64_t grp = p / ((uint64_t)OR_CHUNK * OR_SUPER);
+      const uint64_t grp = (cb[t] + (p - tp) / OR_CHUNK) / OR_SUPER;
       if (grp != group) {
         if (group != (uint64_t)-1) { /* close the previous group into g */
           if (first_group) memcpy(g, gs, sizeof(float) * d);
@@ -389,5 +398,6 @@ int or_emb_backward(uint32_t T, uint64_t B, const uint32_t* D,
   free(bag);
   free(lk);
   free(kb);
+  free(cb);
   return ST_OK;
 }

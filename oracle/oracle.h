@@ -101,11 +101,13 @@ int or_emb_forward(uint32_t T, uint64_t B, const uint32_t* D,
  * global key (sum of earlier tables' hash sizes + row); for each distinct
  * (table, row) the gradient g = sum of grad_out[b, col_off[t] : +D] over its
  * lookups, accumulated in fp32 in the kernel's fixed tree
- * (csrc/emb_bwd.cuh): the row's run in the sorted list is cut at multiples of
- * 32 positions; each piece is summed in sorted order from +0.0f; the pieces
- * falling in one 2048-position superchunk are added left to right (first
- * piece as the accumulator), and the superchunk sums are added left to right
- * (first as the accumulator).  Then
+ * (csrc/emb_bwd.cuh): table t's lookups occupy sorted positions from
+ * tpos = offsets[t*B]; the row's run is cut every 32 positions counted from
+ * tpos (chunk id = chunks of earlier tables + (pos - tpos) / 32); each piece
+ * is summed in sorted order from +0.0f; the pieces whose chunk ids fall in one
+ * 64-chunk superchunk are added left to right (first piece as the
+ * accumulator), and the superchunk sums are added left to right (first as the
+ * accumulator).  Then
  *   opt 0 (row-wise SGD):  w[d] = w[d] - lr*g[d]
  *   opt 1 (exact row-wise Adagrad, FBGEMM semantics):
  *       s = sum_d g[d]^2   (per-lane then xor-butterfly order, see oracle.c)

@@ -282,6 +282,9 @@ struct rs_emb {
   uint32_t* vals = nullptr;
   float* part = nullptr;
   float* spart = nullptr;
+  uint32_t* d_meta = nullptr;
+  uint32_t* h_meta = nullptr;
+  size_t meta_words = 0;
   unsigned* d_err = nullptr;
   char* sort_scratch = nullptr;
   size_t sort_scratch_bytes = 0;
@@ -298,6 +301,8 @@ struct rs_emb {
     if (vals) cudaFree(vals);
     if (part) cudaFree(part);
     if (spart) cudaFree(spart);
+    if (d_meta) cudaFree(d_meta);
+    if (h_meta) cudaFreeHost(h_meta);
     if (d_err) cudaFree(d_err);
     if (sort_scratch) cudaFree(sort_scratch);
   }
@@ -438,12 +443,18 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
     const size_t L = std::max<uint64_t>(max_lookups, 1);
     RS_CUDA(cudaMalloc(&e->keys, L * 4));
     RS_CUDA(cudaMalloc(&e->vals, L * 4));
-    const size_t nch = (L + emb::kChunk - 1) / emb::kChunk;
+    const size_t nch = (L + emb::kChunk - 1) / emb::kChunk + T;  // per-table rounding
     RS_CUDA(cudaMalloc(&e->part, nch * 2 * e->dmax * 4));
     const size_t nsup = (nch + emb::kSuper - 1) / emb::kSuper;
     RS_CUDA(cudaMalloc(&e->spart, nsup * 2 * e->dmax * 4));
     e->sort_scratch_bytes = radix_sort_scratch_bytes(L) + (4 << 20);
     RS_CUDA(cudaMalloc(&e->sort_scratch, e->sort_scratch_bytes));
+    // per-backward metadata: tpos[T+1] | cbase[T+1] | per class cls_cbase[n_c+1]
+    size_t meta = 2 * (size_t(T) + 1);
+    for (const auto& c : e->classes) meta += c.tables.size() + 1;
+    e->meta_words = meta;
+    RS_CUDA(cudaMalloc(&e->d_meta, meta * 4));
+    RS_CUDA(cudaHostAlloc(&e->h_meta, meta * 4, cudaHostAllocDefault));
     RS_CUDA(cudaStreamSynchronize(st));
   } catch (...) {
     delete e;
@@ -496,38 +507,72 @@ void emb_forward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx
   RS_LAUNCH_CHECK();
 }
 
-template <int VPL, int U, int PEND>
-static void launch_bwd(rs_emb* e, const emb::BwdArgs& a) {
-  const uint64_t nch = (a.L + emb::kChunk - 1) / emb::kChunk;
-  const uint64_t nsup = (nch + emb::kSuper - 1) / emb::kSuper;
-  const uint64_t cap = uint64_t(sm_count()) * 16;
-  const unsigned g1 = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((nch + 7) / 8, cap)));
-  const unsigned g2 = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((nsup + 7) / 8, cap)));
-  const int stage_bytes = emb::kBwdWarps * U * 32 * VPL * int(sizeof(float4));
+// Level 1 for one (G, VPL) table class.
+template <int G, int VPL>
+static void launch_chunk(rs_emb* e, const emb::BwdArgs& a, const rs_emb::Class& c,
+                         const uint32_t* d_cls_cbase, uint64_t class_chunks) {
+  constexpr int U = G >= 8 ? (VPL <= 2 ? 8 : (VPL == 4 ? 4 : 2)) : G;
+  constexpr int NGRP = emb::kBwdWarps * (32 / G);
+  if (class_chunks == 0) return;
+  const int stage_bytes = NGRP * U * G * VPL * int(sizeof(float4)) +
+                          NGRP * (2 * emb::kChunk + 2) * int(sizeof(uint32_t));
   static bool attr_set = false;
   if (!attr_set) {
-    RS_CUDA(cudaFuncSetAttribute(emb::bwd_chunk_kernel<VPL, U>,
+    RS_CUDA(cudaFuncSetAttribute(emb::bwd_chunk_kernel<G, VPL, U>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes));
     attr_set = true;
   }
-  emb::bwd_chunk_kernel<VPL, U><<<g1, emb::kBwdThreads, stage_bytes, e->ctx->stream>>>(a);
+  const uint64_t cap = uint64_t(sm_count()) * 16;
+  const unsigned g1 = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((class_chunks + NGRP - 1) / NGRP, cap)));
+  emb::bwd_chunk_kernel<G, VPL, U><<<g1, emb::kBwdThreads, stage_bytes, e->ctx->stream>>>(
+      a, c.d_list, d_cls_cbase, uint32_t(c.tables.size()));
+  RS_COUNT(1);
+}
+
+// Levels 2 and 3 (full warps, VPL of the widest table).
+template <int VPL, int PEND>
+static void launch_edges(rs_emb* e, const emb::BwdArgs& a) {
+  const uint64_t nsup = (a.nchunks + emb::kSuper - 1) / emb::kSuper;
+  const uint64_t cap = uint64_t(sm_count()) * 16;
+  const unsigned g2 = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((nsup + 7) / 8, cap)));
   emb::bwd_super_kernel<VPL, PEND><<<g2, emb::kBwdThreads, 0, e->ctx->stream>>>(a);
   emb::bwd_final_kernel<VPL, PEND><<<g2, emb::kBwdThreads, 0, e->ctx->stream>>>(a);
-  RS_COUNT(3);
+  RS_COUNT(2);
 }
 
 void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx, const float* grad,
                   float lr) {
   if (B == 0 || B > e->max_batch) throw InvalidArgument("emb_backward: batch outside [1, max_batch]");
   cudaStream_t st = e->ctx->stream;
-  uint32_t L = 0;
-  RS_CUDA(cudaMemcpyAsync(&L, off + uint64_t(e->T) * B, 4, cudaMemcpyDeviceToHost, st));
-  uint32_t L0 = 0;
-  RS_CUDA(cudaMemcpyAsync(&L0, off, 4, cudaMemcpyDeviceToHost, st));
+  const uint32_t T = e->T;
+  uint32_t* tpos = e->h_meta;  // offsets[t*B], t = 0..T
+  RS_CUDA(cudaMemcpy2DAsync(tpos, 4, off, size_t(B) * 4, 4, T + 1, cudaMemcpyDeviceToHost, st));
   RS_CUDA(cudaStreamSynchronize(st));
-  if (L0 != 0) throw InvalidArgument("emb_backward: offsets must start at 0");
+  const uint32_t L = tpos[T];
+  if (tpos[0] != 0) throw InvalidArgument("emb_backward: offsets must start at 0");
   if (L > e->max_lookups) throw InvalidArgument("emb_backward: more lookups than max_lookups");
   if (L == 0) return;
+  // chunk bases: per table ceil(L_t / 32) chunks, numbered in table order
+  uint32_t* cbase = tpos + T + 1;
+  cbase[0] = 0;
+  for (uint32_t t = 0; t < T; ++t) {
+    if (tpos[t + 1] < tpos[t]) throw InvalidArgument("emb_backward: offsets must be non-decreasing");
+    cbase[t + 1] = cbase[t] + (tpos[t + 1] - tpos[t] + emb::kChunk - 1) / emb::kChunk;
+  }
+  uint32_t* w = cbase + T + 1;
+  std::vector<uint64_t> class_chunks;
+  std::vector<size_t> class_off;
+  for (const auto& c : e->classes) {
+    class_off.push_back(size_t(w - e->h_meta));
+    w[0] = 0;
+    for (size_t j = 0; j < c.tables.size(); ++j) {
+      const uint32_t t = c.tables[j];
+      w[j + 1] = w[j] + (cbase[t + 1] - cbase[t]);
+    }
+    class_chunks.push_back(w[c.tables.size()]);
+    w += c.tables.size() + 1;
+  }
+  RS_CUDA(cudaMemcpyAsync(e->d_meta, e->h_meta, e->meta_words * 4, cudaMemcpyHostToDevice, st));
   RS_CUDA(cudaMemsetAsync(e->d_err, 0, 4, st));
   {
     const uint64_t nb = uint64_t(e->T) * B;
@@ -539,14 +584,29 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
   scr.base = e->sort_scratch;
   scr.cap = e->sort_scratch_bytes;
   radix_sort_pairs(e->keys, e->vals, L, int(e->key_bits), scr, st);
-  const uint32_t* tb = e->d_key_base_sorted;
-  emb::BwdArgs a{e->d_tables, tb, tb + e->T + 1, tb + 2 * e->T + 1, e->T, e->keys, e->vals, L,
+  emb::BwdArgs a{e->d_tables, T, e->d_meta, e->d_meta + T + 1, cbase[T], e->keys, e->vals,
                  grad, e->total_dim, e->part, e->spart, e->dmax, lr, e->eps, e->opt};
+  for (size_t ci = 0; ci < e->classes.size(); ++ci) {
+    const auto& c = e->classes[ci];
+    const uint32_t* dcb = e->d_meta + class_off[ci];
+    switch (c.G * 100 + c.VPL) {
+      case 101: launch_chunk<1, 1>(e, a, c, dcb, class_chunks[ci]); break;
+      case 201: launch_chunk<2, 1>(e, a, c, dcb, class_chunks[ci]); break;
+      case 401: launch_chunk<4, 1>(e, a, c, dcb, class_chunks[ci]); break;
+      case 801: launch_chunk<8, 1>(e, a, c, dcb, class_chunks[ci]); break;
+      case 1601: launch_chunk<16, 1>(e, a, c, dcb, class_chunks[ci]); break;
+      case 3201: launch_chunk<32, 1>(e, a, c, dcb, class_chunks[ci]); break;
+      case 3202: launch_chunk<32, 2>(e, a, c, dcb, class_chunks[ci]); break;
+      case 3204: launch_chunk<32, 4>(e, a, c, dcb, class_chunks[ci]); break;
+      case 3208: launch_chunk<32, 8>(e, a, c, dcb, class_chunks[ci]); break;
+      default: throw Error(-9, "emb_backward: unsupported lane class");
+    }
+  }
   switch (e->bwd_vpl) {
-    case 1: launch_bwd<1, 8, 4>(e, a); break;
-    case 2: launch_bwd<2, 8, 2>(e, a); break;
-    case 4: launch_bwd<4, 4, 1>(e, a); break;
-    case 8: launch_bwd<8, 2, 1>(e, a); break;
+    case 1: launch_edges<1, 4>(e, a); break;
+    case 2: launch_edges<2, 2>(e, a); break;
+    case 4: launch_edges<4, 1>(e, a); break;
+    case 8: launch_edges<8, 1>(e, a); break;
     default: throw Error(-9, "emb_backward: unsupported dim");
   }
   RS_LAUNCH_CHECK();
