@@ -21,7 +21,9 @@
 //   chunk in sorted order; pieces crossing a chunk edge are combined by the
 //   owning chunk in chunk order.  Fully deterministic, no float atomics.
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
+#include <tuple>
 
 #include "../../include/shardplan_gpu.h"
 #include "context.cuh"
@@ -57,24 +59,45 @@ __device__ __forceinline__ float* mom_ptr(const TableDev& td, int32_t e) {
 }
 
 constexpr int kFwdThreads = 256;
-constexpr int kFwdUnroll = 8;
 
-template <int G, int VPL>
-__global__ void __launch_bounds__(kFwdThreads)
+// Flushes a warp's accumulated (fast, total) lookup counts for table t.
+__device__ __forceinline__ void flush_hits(unsigned long long* hits, uint32_t t, uint32_t fast,
+                                           uint32_t tot) {
+#pragma unroll
+  for (int o2 = 16; o2; o2 >>= 1) {
+    fast += __shfl_xor_sync(0xffffffffu, fast, o2);
+    tot += __shfl_xor_sync(0xffffffffu, tot, o2);
+  }
+  if ((threadIdx.x & 31) == 0 && tot) {
+    atomicAdd(&hits[2 * uint64_t(t)], (unsigned long long)fast);
+    atomicAdd(&hits[2 * uint64_t(t) + 1], (unsigned long long)(tot - fast));
+  }
+}
+
+template <int G, int VPL, int UNR, int MINB>
+__global__ void __launch_bounds__(kFwdThreads, MINB)
 forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__ cls_tables,
                uint32_t ntab, uint64_t B, const uint32_t* __restrict__ offsets,
                const uint32_t* __restrict__ indices, float* __restrict__ out, uint64_t stride,
                unsigned long long* __restrict__ hits) {
   constexpr int BPW = 32 / G;
+  constexpr int kFwdUnroll = UNR;
   const int lane = threadIdx.x & 31;
   const int grp = lane / G, lg = lane % G;
   const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
   const uint64_t wpt = (B + BPW - 1) / BPW;
   const uint64_t total_w = wpt * ntab;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  uint32_t cur_t = 0xFFFFFFFFu, fast = 0, tot = 0;
+  TableDev td{};
   for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < total_w; w += nwarps) {
     const uint32_t t = cls_tables[w / wpt];
-    const TableDev td = tables[t];
+    if (t != cur_t) {
+      if (hits && cur_t != 0xFFFFFFFFu) flush_hits(hits, cur_t, fast, tot);
+      fast = tot = 0;
+      cur_t = t;
+      td = tables[t];
+    }
     const uint32_t V = td.dim >> 2;
     const uint64_t b = (w % wpt) * BPW + grp;
     const bool valid = b < B;
@@ -86,7 +109,7 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
     float4 acc[VPL];
 #pragma unroll
     for (int vv = 0; vv < VPL; ++vv) acc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
-    uint32_t fast = 0;
+    if (lg == 0) tot += e - s;
     for (uint32_t base = s; base < e; base += G) {
       const uint32_t n = min(uint32_t(G), e - base);
       int32_t ent = 0;
@@ -129,19 +152,8 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
         if (vec < V) o[vec] = acc[vv];
       }
     }
-    if (hits) {
-      uint32_t tot = (valid && lg == 0) ? e - s : 0u;
-#pragma unroll
-      for (int o2 = 16; o2; o2 >>= 1) {
-        fast += __shfl_xor_sync(0xffffffffu, fast, o2);
-        tot += __shfl_xor_sync(0xffffffffu, tot, o2);
-      }
-      if (lane == 0 && tot) {
-        atomicAdd(&hits[2 * uint64_t(t)], (unsigned long long)fast);
-        atomicAdd(&hits[2 * uint64_t(t) + 1], (unsigned long long)(tot - fast));
-      }
-    }
   }
+  if (hits && cur_t != 0xFFFFFFFFu) flush_hits(hits, cur_t, fast, tot);
 }
 
 // ------------------------------------------------------------------ backward
@@ -480,9 +492,21 @@ static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint
   constexpr int BPW = 32 / G;
   const uint64_t warps = (B + BPW - 1) / BPW * c.tables.size();
   const uint64_t blocks = (warps * 32 + emb::kFwdThreads - 1) / emb::kFwdThreads;
-  const unsigned grid = unsigned(std::min<uint64_t>(blocks, uint64_t(sm_count()) * 64));
-  emb::forward_kernel<G, VPL><<<std::max(1u, grid), emb::kFwdThreads, 0, e->ctx->stream>>>(
-      e->d_tables, c.d_list, uint32_t(c.tables.size()), B, off, idx, out, e->total_dim, hits);
+  const unsigned grid = std::max(1u, unsigned(std::min<uint64_t>(blocks, uint64_t(sm_count()) * 64)));
+  static const int variant = [] {
+    const char* v = getenv("RS_FWD_VARIANT");
+    return v ? atoi(v) : 0;
+  }();
+  auto args = std::make_tuple(e->d_tables, c.d_list, uint32_t(c.tables.size()), B, off, idx, out,
+                              e->total_dim, hits);
+  auto go = [&](auto kern) {
+    std::apply([&](auto... a) { kern<<<grid, emb::kFwdThreads, 0, e->ctx->stream>>>(a...); }, args);
+  };
+  // (unroll, min blocks/SM): measured on B200 RM1 all-HBM — (4, 6) 1.15 ms,
+  // (2, 8) 1.14, (4, 8) 1.17, (6, 6) 1.22, (8, 6) 1.55, (8, 1) 1.85
+  if (VPL > 1) go(emb::forward_kernel<G, VPL, 8, 1>);
+  else if (variant == 1) go(emb::forward_kernel<G, VPL, 2, 8>);
+  else go(emb::forward_kernel<G, VPL, 4, 6>);
   RS_COUNT(1);
 }
 
@@ -508,25 +532,41 @@ void emb_forward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx
 }
 
 // Level 1 for one (G, VPL) table class.
-template <int G, int VPL>
-static void launch_chunk(rs_emb* e, const emb::BwdArgs& a, const rs_emb::Class& c,
-                         const uint32_t* d_cls_cbase, uint64_t class_chunks) {
-  constexpr int U = G >= 8 ? (VPL <= 2 ? 8 : (VPL == 4 ? 4 : 2)) : G;
+template <int G, int VPL, int U, int MINB>
+static void launch_chunk_v(rs_emb* e, const emb::BwdArgs& a, const rs_emb::Class& c,
+                           const uint32_t* d_cls_cbase, uint64_t class_chunks) {
   constexpr int NGRP = emb::kBwdWarps * (32 / G);
-  if (class_chunks == 0) return;
   const int stage_bytes = NGRP * U * G * VPL * int(sizeof(float4)) +
                           NGRP * (2 * emb::kChunk + 2) * int(sizeof(uint32_t));
   static bool attr_set = false;
   if (!attr_set) {
-    RS_CUDA(cudaFuncSetAttribute(emb::bwd_chunk_kernel<G, VPL, U>,
+    RS_CUDA(cudaFuncSetAttribute(emb::bwd_chunk_kernel<G, VPL, U, MINB>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes));
     attr_set = true;
   }
   const uint64_t cap = uint64_t(sm_count()) * 16;
   const unsigned g1 = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((class_chunks + NGRP - 1) / NGRP, cap)));
-  emb::bwd_chunk_kernel<G, VPL, U><<<g1, emb::kBwdThreads, stage_bytes, e->ctx->stream>>>(
+  emb::bwd_chunk_kernel<G, VPL, U, MINB><<<g1, emb::kBwdThreads, stage_bytes, e->ctx->stream>>>(
       a, c.d_list, d_cls_cbase, uint32_t(c.tables.size()));
   RS_COUNT(1);
+}
+
+template <int G, int VPL>
+static void launch_chunk(rs_emb* e, const emb::BwdArgs& a, const rs_emb::Class& c,
+                         const uint32_t* d_cls_cbase, uint64_t class_chunks) {
+  if (class_chunks == 0) return;
+  static const int variant = [] {
+    const char* v = getenv("RS_BWD_VARIANT");
+    return v ? atoi(v) : 0;
+  }();
+  if constexpr (G >= 8 && VPL == 1) {
+    if (variant == 1) return launch_chunk_v<G, VPL, 4, 4>(e, a, c, d_cls_cbase, class_chunks);
+    if (variant == 2) return launch_chunk_v<G, VPL, 4, 3>(e, a, c, d_cls_cbase, class_chunks);
+    if (variant == 3) return launch_chunk_v<G, VPL, 2, 6>(e, a, c, d_cls_cbase, class_chunks);
+    if (variant == 4) return launch_chunk_v<G, VPL, 8, 3>(e, a, c, d_cls_cbase, class_chunks);
+  }
+  constexpr int U = G >= 8 ? (VPL <= 2 ? 8 : (VPL == 4 ? 4 : 2)) : G;
+  launch_chunk_v<G, VPL, U, 1>(e, a, c, d_cls_cbase, class_chunks);
 }
 
 // Levels 2 and 3 (full warps, VPL of the widest table).

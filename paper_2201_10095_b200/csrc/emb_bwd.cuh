@@ -203,8 +203,8 @@ struct Pending {
 // neighbouring keys; rows are gathered U at a time into a segmented running
 // sum.  Complete segments are staged and updated together per batch; edge
 // pieces go to the level-2 buffer.
-template <int G, int VPL, int U>
-__global__ void __launch_bounds__(kBwdThreads) bwd_chunk_kernel(BwdArgs a, const uint32_t* cls_tables,
+template <int G, int VPL, int U, int MINB>
+__global__ void __launch_bounds__(kBwdThreads, MINB) bwd_chunk_kernel(BwdArgs a, const uint32_t* cls_tables,
                                                                 const uint32_t* cls_cbase, uint32_t ncls) {
   constexpr int GPW = 32 / G;
   constexpr int NGRP = kBwdWarps * GPW;
@@ -252,11 +252,13 @@ __global__ void __launch_bounds__(kBwdThreads) bwd_chunk_kernel(BwdArgs a, const
       heads |= ((hb >> sh) & (G == 32 ? 0xffffffffu : ((1u << G) - 1u))) << (r * G);
       tails |= ((tb2 >> sh) & (G == 32 ? 0xffffffffu : ((1u << G) - 1u))) << (r * G);
     }
-    float4 acc[VPL];
-#pragma unroll
-    for (int vv = 0; vv < VPL; ++vv) acc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (uint32_t jb = 0; jb < n; jb += U) {
-      float4 v[U][VPL];
+    // complete segments end at a tail with a head at or before it (a tail
+    // before the first head ends the piece that began in an earlier chunk)
+    const int fh = heads ? __ffs(heads) - 1 : 32;
+    const unsigned complete = fh >= 32 ? 0u : (tails & ~((1u << fh) - 1u));
+    constexpr unsigned UMASK = U >= 32 ? 0xFFFFFFFFu : ((1u << U) - 1u);
+    // gathers the grad rows of batch jb (U positions) into v
+    auto gather = [&](uint32_t jb, float4 (&v)[U][VPL]) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint32_t pos = jb + u;
@@ -268,8 +270,48 @@ __global__ void __launch_bounds__(kBwdThreads) bwd_chunk_kernel(BwdArgs a, const
           v[u][vv] = (pos < n && vec < V) ? ld_nc_f4(gr + vec) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
-      int ns = 0;
-      unsigned staged = 0;
+    };
+    // lane s of the group loads the remap entry of the s-th complete segment of batch jb
+    auto remap_of = [&](uint32_t jb) -> int32_t {
+      unsigned m = (complete >> jb) & UMASK;
+      int32_t e = 0;
+#pragma unroll
+      for (int s = 0; s < U; ++s) {
+        if (m == 0) break;
+        const int u = __ffs(m) - 1;
+        m &= m - 1;
+        if (lg == s) e = td.remap[sk[jb + u] - td.key_base];
+      }
+      return e;
+    };
+    // Software pipeline per batch: the row/state loads of this batch's
+    // complete segments and the grad gathers + remap loads of the next batch
+    // are all in flight before this batch is summed and updated.
+    float4 acc[VPL];
+#pragma unroll
+    for (int vv = 0; vv < VPL; ++vv) acc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 vA[U][VPL], vB[U][VPL];
+    gather(0, vA);
+    int32_t e_next = remap_of(0);
+    for (uint32_t jb = 0; jb < n; jb += U) {
+      const unsigned cm = (complete >> jb) & UMASK;
+      const int ns = __popc(cm);
+      const int32_t e_cur = e_next;
+      float4 wv[U][VPL];
+      float mom[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int32_t e = __shfl_sync(gmask, e_cur, q % G, G);
+        if (q < ns) {
+          load_vec<G, VPL>(row_ptr(td, e), V, lg, wv[q]);
+          mom[q] = a.opt == RS_OPT_ROWWISE_ADAGRAD ? *mom_ptr(td, e) : 0.f;
+        }
+      }
+      if (jb + U < n) {
+        gather(jb + U, vB);
+        e_next = remap_of(jb + U);
+      }
+      int s = 0;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint32_t pos = jb + u;
@@ -279,55 +321,34 @@ __global__ void __launch_bounds__(kBwdThreads) bwd_chunk_kernel(BwdArgs a, const
             for (int vv = 0; vv < VPL; ++vv) acc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
           }
 #pragma unroll
-          for (int vv = 0; vv < VPL; ++vv) add4(acc[vv], v[u][vv]);
+          for (int vv = 0; vv < VPL; ++vv) add4(acc[vv], vA[u][vv]);
           if ((tails >> pos) & 1u) {
-            if ((heads & (0xFFFFFFFFu >> (31 - pos))) == 0) {
-              store_vec<G, VPL>(a.part + (gc * 2) * a.dmax, V, lg, acc);  // began before: head edge
-            } else {
+            if ((cm >> u) & 1u) {
 #pragma unroll
-              for (int vv = 0; vv < VPL; ++vv) stage[(ns * VPL + vv) * G + lg] = acc[vv];
-              staged |= 1u << u;
-              ++ns;
+              for (int vv = 0; vv < VPL; ++vv) stage[(s * VPL + vv) * G + lg] = acc[vv];
+              ++s;
+            } else {
+              store_vec<G, VPL>(a.part + (gc * 2) * a.dmax, V, lg, acc);  // began before: head edge
             }
           }
         }
       }
-      if (ns) {
-        // lane s of the group takes the s-th staged segment
-        int32_t my_e = 0;
-        {
-          unsigned rem = staged;
-          uint32_t my_pos = 0;
-          for (int s = 0; s < ns; ++s) {
-            const int u = __ffs(rem) - 1;
-            rem &= rem - 1;
-            if (lg == s) my_pos = jb + u;
-          }
-          if (lg < ns) my_e = td.remap[sk[my_pos] - td.key_base];
-        }
-        float4 wv[U][VPL];
-        float mom[U];
+      __syncwarp(gmask);
 #pragma unroll
-        for (int q = 0; q < U; ++q) {
-          const int32_t e = __shfl_sync(gmask, my_e, q % G, G);
-          if (q < ns) {
-            load_vec<G, VPL>(row_ptr(td, e), V, lg, wv[q]);
-            mom[q] = a.opt == RS_OPT_ROWWISE_ADAGRAD ? *mom_ptr(td, e) : 0.f;
-          }
-        }
-        __syncwarp(gmask);
+      for (int q = 0; q < U; ++q) {
+        const int32_t e = __shfl_sync(gmask, e_cur, q % G, G);
+        if (q < ns) {
+          float4 g[VPL];
 #pragma unroll
-        for (int q = 0; q < U; ++q) {
-          const int32_t e = __shfl_sync(gmask, my_e, q % G, G);
-          if (q < ns) {
-            float4 g[VPL];
-#pragma unroll
-            for (int vv = 0; vv < VPL; ++vv) g[vv] = stage[(q * VPL + vv) * G + lg];
-            update_row<G, VPL>(a, td, e, g, wv[q], mom[q], gmask, lg);
-          }
+          for (int vv = 0; vv < VPL; ++vv) g[vv] = stage[(q * VPL + vv) * G + lg];
+          update_row<G, VPL>(a, td, e, g, wv[q], mom[q], gmask, lg);
         }
-        __syncwarp(gmask);
       }
+      __syncwarp(gmask);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int vv = 0; vv < VPL; ++vv) vA[u][vv] = vB[u][vv];
     }
     // the last piece continues into the next chunk: tail edge piece (or the
     // whole chunk is the middle of a segment: head edge piece)

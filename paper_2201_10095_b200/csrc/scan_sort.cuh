@@ -263,26 +263,45 @@ radix_downsweep(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict
     __syncwarp();
   }
   __syncthreads();
-  // per-digit exclusive offsets across warps, plus this tile's global base
-  for (int d = threadIdx.x; d < kRadix; d += kSortThreads) {
-    uint32_t run = offsets[size_t(d) * ntiles + blockIdx.x];
+  // Per digit: offsets of each warp inside the digit, the digit's start inside
+  // the tile, and its global start.  The tile is then re-laid out in shared
+  // memory in (digit, rank) order and written as contiguous per-digit runs, so
+  // the global stores coalesce instead of scattering 4-byte writes.
+  __shared__ uint32_t dstart[kRadix], gbase[kRadix];
+  __shared__ uint32_t sk[kSortTile], sv[HAS_VALUES ? kSortTile : 1];
+  static_assert(kRadix == kSortThreads, "one digit per thread");
+  const int d0 = threadIdx.x;
+  uint32_t cnt = 0;
 #pragma unroll
-    for (int ww = 0; ww < kSortWarps; ++ww) {
-      uint32_t c = wc[ww][d];
-      wc[ww][d] = run;
-      run += c;
-    }
+  for (int ww = 0; ww < kSortWarps; ++ww) {
+    const uint32_t c = wc[ww][d0];
+    wc[ww][d0] = cnt;
+    cnt += c;
   }
+  uint32_t tot_unused;
+  const uint32_t ds = block_excl_scan<uint32_t, kSortThreads>(cnt, tot_unused);
+  dstart[d0] = ds;
+  gbase[d0] = offsets[size_t(d0) * ntiles + blockIdx.x];
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kSortItems; ++r) {
     size_t k = wbase + size_t(r) * 32 + lane;
     if (k < n) {
-      unsigned d = (kk[r] >> shift) & mask;
-      uint32_t pos = wc[w][d] + rank[r];
-      keys_out[pos] = kk[r];
-      if (HAS_VALUES) vals_out[pos] = vv[r];
+      const unsigned d = (kk[r] >> shift) & mask;
+      const uint32_t tp = dstart[d] + wc[w][d] + rank[r];
+      sk[tp] = kk[r];
+      if (HAS_VALUES) sv[tp] = vv[r];
     }
+  }
+  __syncthreads();
+  const size_t tile0 = size_t(blockIdx.x) * kSortTile;
+  const uint32_t tn = uint32_t(min(size_t(kSortTile), n - tile0));
+  for (uint32_t i = threadIdx.x; i < tn; i += kSortThreads) {
+    const uint32_t key = sk[i];
+    const unsigned d = (key >> shift) & mask;
+    const uint32_t pos = gbase[d] + (i - dstart[d]);
+    keys_out[pos] = key;
+    if (HAS_VALUES) vals_out[pos] = sv[i];
   }
 }
 
