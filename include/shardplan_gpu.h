@@ -133,6 +133,11 @@ int rs_profile_destroy(rs_profile* p);
 int rs_build_icdf(rs_context* ctx, const uint64_t* counts, uint64_t n,
                   int location, uint64_t* out101);
 
+/* GenStats.distinct_raw_ids (include/shardplan/workload.hpp:62-64,
+ * core/src/workload.cpp:195-223) for a raw trace: distinct raw values per
+ * table over every record (GPU hash sets).  out: host u64[num_tables]. */
+int rs_count_distinct_raw(rs_context* ctx, const rs_trace* trace, uint64_t* out);
+
 /* core/src/profiler.cpp:163-174  hash_utilization(stats, spec, distinct_raw) */
 int rs_hash_utilization(uint64_t distinct_rows_accessed, uint64_t hash_size,
                         uint64_t distinct_raw_ids_seen, double* sparsity,

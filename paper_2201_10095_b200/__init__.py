@@ -15,7 +15,8 @@ from .types import (FeatureGenSpec, FeatureStats, InfeasibleError, InvalidArgume
                     ParseError, PlanEntry, RemapTable, ShardingPlan, ShardplanError, SimReport,
                     SystemSpec, TableIndexError, TableSpec, Trace, WorkloadSpec, TIER_FAST,
                     TIER_SLOW)
-from .profiler import build_icdf, hash_ids, hash_utilization, hash_value, profile, profile_raw
+from .profiler import (build_icdf, count_distinct_raw, hash_ids, hash_utilization, hash_value,
+                       profile, profile_raw)
 from .remap import build_remap, translate
 from .simulator import simulate
 from .embedding import TieredEmbeddingBag
@@ -25,7 +26,7 @@ __all__ = [
     "FeatureGenSpec", "FeatureStats", "InfeasibleError", "InvalidArgument", "IoError",
     "ParseError", "PlanEntry", "RemapTable", "ShardingPlan", "ShardplanError", "SimReport",
     "SystemSpec", "TableIndexError", "TableSpec", "Trace", "WorkloadSpec", "TIER_FAST",
-    "TIER_SLOW", "build_icdf", "hash_ids", "hash_utilization", "hash_value", "profile",
+    "TIER_SLOW", "build_icdf", "count_distinct_raw", "hash_ids", "hash_utilization", "hash_value", "profile",
     "profile_raw", "build_remap", "translate", "simulate", "TieredEmbeddingBag", "Context",
     "default_context",
 ]

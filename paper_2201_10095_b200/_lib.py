@@ -97,6 +97,7 @@ _SIGS = {
     "rs_profile_destroy": ([P], i32),
     "rs_build_icdf": ([P, P, u64, i32, P], i32),
     "rs_hash_utilization": ([u64, u64, u64, P, P], i32),
+    "rs_count_distinct_raw": ([P, P, P], i32),
     "rs_build_remap": ([P, u32, u64, u64, P, u64, i32, i32, P, i32, P], i32),
     "rs_simulate": ([P, P, u32, P, u32, P, P, u64, P], i32),
     "rs_emb_create": ([P, u32, P, u64, u64, i32, f32, P], i32),

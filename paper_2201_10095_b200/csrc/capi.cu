@@ -13,6 +13,7 @@ namespace rs {
 rs_profile* profile_run(rs_context*, const rs_trace*, double, uint64_t);
 void hash_ids(rs_context*, const uint64_t*, uint64_t, uint64_t, uint32_t*, int);
 void build_icdf(rs_context*, const uint64_t*, uint64_t, int, uint64_t*);
+void count_distinct_raw(rs_context*, const rs_trace*, uint64_t*);
 void build_remap(rs_context*, uint32_t, uint64_t, uint64_t, const uint32_t*, uint64_t, int, int,
                  int32_t*, int, uint64_t*);
 void simulate(rs_context*, const rs_trace*, uint32_t, const rs_plan_entry*, uint32_t,
@@ -166,6 +167,15 @@ int rs_build_icdf(rs_context* c, const uint64_t* counts, uint64_t n, int loc, ui
     need(out101, "out");
     if (n) need(counts, "counts");
     rs::build_icdf(c, counts, n, loc, out101);
+  });
+}
+
+int rs_count_distinct_raw(rs_context* c, const rs_trace* tr, uint64_t* out) {
+  return guarded([&] {
+    need(c, "ctx");
+    need(tr, "trace");
+    need(out, "out");
+    rs::count_distinct_raw(c, tr, out);
   });
 }
 

@@ -186,6 +186,91 @@ __global__ void hash_ids_kernel(const uint64_t* __restrict__ raw, uint64_t n, ui
     out[i] = uint32_t(fast_mod(mix64(raw[i]), H, magic));
 }
 
+// ------------------------------------------------------------------ distinct raw ids
+// GenStats.distinct_raw_ids (core/src/workload.cpp:195-223, an unordered_set
+// per table) on the GPU: one open-addressing hash set of raw u64 values per
+// table (capacity a power of two >= 2x the table's ids), linear probing with
+// atomicCAS; successful inserts are counted.  Exact, order-independent.
+constexpr uint64_t kEmpty = ~0ull;
+
+// Per-table id totals over ALL records (the generator counts every sample).
+__global__ void ids_per_table(const uint32_t* __restrict__ rec_table, const uint32_t* __restrict__ rec_len,
+                              uint64_t R, const uint32_t* __restrict__ sid, const uint32_t* __restrict__ six,
+                              uint32_t J, unsigned long long* __restrict__ out, unsigned* __restrict__ err) {
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < R;
+       r += uint64_t(gridDim.x) * blockDim.x) {
+    const int t = lookup_table(sid, six, J, rec_table[r]);
+    if (t < 0) atomicOr(err, kErrUnknownTable);
+    else atomicAdd(&out[t], (unsigned long long)rec_len[r]);
+  }
+}
+
+__global__ void __launch_bounds__(kHistThreads)
+distinct_raw_kernel(const uint32_t* __restrict__ rec_table, const uint64_t* __restrict__ rec_offset,
+                    const uint32_t* __restrict__ rec_len, uint64_t R, const uint64_t* __restrict__ raw,
+                    const uint32_t* __restrict__ sid, const uint32_t* __restrict__ six, uint32_t J,
+                    const uint64_t* __restrict__ set_base, const uint64_t* __restrict__ set_mask,
+                    unsigned long long* __restrict__ slots, unsigned long long* __restrict__ count,
+                    unsigned* __restrict__ has_max) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t c = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; c * 32 < R; c += nwarps) {
+    const uint64_t r = c * 32 + lane;
+    uint32_t len = 0;
+    uint64_t off = 0;
+    int t = 0;
+    if (r < R) {
+      t = lookup_table(sid, six, J, rec_table[r]);
+      if (t >= 0) {
+        len = rec_len[r];
+        off = rec_offset[r];
+      } else {
+        t = 0;
+      }
+    }
+    const uint32_t incl = warp_incl_scan(len);
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t excl = incl - len;
+    for (uint32_t p = 0; p < total; p += 32) {
+      const uint32_t q = p + lane;
+      int k = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const uint32_t e = __shfl_sync(0xffffffffu, excl, k + step);
+        if (e <= q) k += step;
+      }
+      const uint64_t offk = __shfl_sync(0xffffffffu, off, k);
+      const uint32_t exk = __shfl_sync(0xffffffffu, excl, k);
+      const int tk = __shfl_sync(0xffffffffu, t, k);
+      bool inserted = false;
+      if (q < total) {
+        const uint64_t v = raw[offk + (q - exk)];
+        if (v == kEmpty) {
+          inserted = atomicOr(&has_max[tk], 1u) == 0u;
+        } else {
+          const uint64_t m = set_mask[tk];
+          unsigned long long* s = slots + set_base[tk];
+          uint64_t h = mix64(v) & m;
+          while (true) {
+            const unsigned long long old = atomicCAS(&s[h], kEmpty, (unsigned long long)v);
+            if (old == kEmpty) {
+              inserted = true;
+              break;
+            }
+            if (old == v) break;
+            h = (h + 1) & m;
+          }
+        }
+      }
+      const unsigned act = __ballot_sync(0xffffffffu, inserted);
+      if (inserted) {
+        const unsigned peers = __match_any_sync(act, tk);
+        if ((peers & lanemask_lt()) == 0) atomicAdd(&count[tk], (unsigned long long)__popc(peers));
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ K2
 // Compaction of accessed rows.  Pass 1: per-tile nonzero counts + global max.
 __global__ void __launch_bounds__(kScanThreads)
@@ -585,6 +670,81 @@ void hash_ids(rs_context* ctx, const uint64_t* raw, uint64_t n, uint64_t H, uint
     RS_CUDA(cudaMemcpyAsync(out, d_out, n * 4, cudaMemcpyDeviceToHost, st));
     ctx->sync();
   }
+}
+
+// GenStats.distinct_raw_ids for a raw trace (core/src/workload.cpp:195-223):
+// distinct raw values per table over every record.
+void count_distinct_raw(rs_context* ctx, const rs_trace* tr, uint64_t* out) {
+  using namespace prof;
+  if (!tr || !tr->raw_ids) throw InvalidArgument("count_distinct_raw: trace must carry raw_ids");
+  const uint32_t J = tr->num_tables;
+  const bool on_dev = tr->location == RS_MEM_DEVICE;
+  const uint64_t R = tr->num_records, N = tr->num_ids;
+  cudaStream_t st = ctx->stream;
+  std::vector<uint32_t> order(J), sids(J), sidx(J);
+  std::iota(order.begin(), order.end(), 0u);
+  std::sort(order.begin(), order.end(),
+            [&](uint32_t a, uint32_t b) { return tr->tables[a].table_id < tr->tables[b].table_id; });
+  for (uint32_t i = 0; i < J; ++i) {
+    sids[i] = tr->tables[order[i]].table_id;
+    sidx[i] = order[i];
+  }
+  Scratch s0 = ctx->scratch(Scratch::bytes_for(R, 8) + Scratch::bytes_for(R, 4) * 2 +
+                            Scratch::bytes_for(N, 8) + Scratch::bytes_for(J + 1, 8) * 6 + (4 << 20));
+  const uint32_t* d_rt = on_dev ? tr->rec_table : stage(tr->rec_table, R, false, s0, st);
+  const uint64_t* d_ro = on_dev ? tr->rec_offset : stage(tr->rec_offset, R, false, s0, st);
+  const uint32_t* d_rl = on_dev ? tr->rec_len : stage(tr->rec_len, R, false, s0, st);
+  const uint64_t* d_raw = on_dev ? tr->raw_ids : stage(tr->raw_ids, N, false, s0, st);
+  uint32_t* d_sid = stage(sids.data(), J, false, s0, st);
+  uint32_t* d_six = stage(sidx.data(), J, false, s0, st);
+  auto* d_n = s0.take<unsigned long long>(J);
+  auto* d_err = s0.take<unsigned>(1);
+  RS_CUDA(cudaMemsetAsync(d_n, 0, J * 8, st));
+  RS_CUDA(cudaMemsetAsync(d_err, 0, 4, st));
+  const unsigned g = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((R + 255) / 256, uint64_t(sm_count()) * 8)));
+  ids_per_table<<<g, 256, 0, st>>>(d_rt, d_rl, R, d_sid, d_six, J, d_n, d_err);
+  std::vector<uint64_t> n(J + 1);
+  RS_CUDA(cudaMemcpyAsync(n.data(), d_n, J * 8, cudaMemcpyDeviceToHost, st));
+  RS_CUDA(cudaMemcpyAsync(&n[J], d_err, 4, cudaMemcpyDeviceToHost, st));
+  ctx->sync();
+  if (uint32_t(n[J])) throw OutOfRange("count_distinct_raw: record of a table absent from trace.tables");
+  std::vector<uint64_t> base(J), mask(J);
+  uint64_t total = 0;
+  for (uint32_t j = 0; j < J; ++j) {
+    uint64_t cap = 16;
+    while (cap < 2 * n[j]) cap <<= 1;
+    base[j] = total;
+    mask[j] = cap - 1;
+    total += cap;
+  }
+  const size_t used = s0.used;
+  Scratch scr = ctx->scratch(used + Scratch::bytes_for(total, 8) + Scratch::bytes_for(J, 8) * 4 + (4 << 20));
+  scr.used = used;  // the arena did not move unless it had to grow
+  if (scr.base != s0.base) {
+    // arena reallocated: restage everything
+    scr.used = 0;
+    d_rt = on_dev ? tr->rec_table : stage(tr->rec_table, R, false, scr, st);
+    d_ro = on_dev ? tr->rec_offset : stage(tr->rec_offset, R, false, scr, st);
+    d_rl = on_dev ? tr->rec_len : stage(tr->rec_len, R, false, scr, st);
+    d_raw = on_dev ? tr->raw_ids : stage(tr->raw_ids, N, false, scr, st);
+    d_sid = stage(sids.data(), J, false, scr, st);
+    d_six = stage(sidx.data(), J, false, scr, st);
+  }
+  uint64_t* d_base = stage(base.data(), J, false, scr, st);
+  uint64_t* d_mask = stage(mask.data(), J, false, scr, st);
+  auto* slots = scr.take<unsigned long long>(total);
+  auto* d_cnt = scr.take<unsigned long long>(J);
+  auto* d_hm = scr.take<unsigned>(J);
+  RS_CUDA(cudaMemsetAsync(slots, 0xFF, total * 8, st));
+  RS_CUDA(cudaMemsetAsync(d_cnt, 0, J * 8, st));
+  RS_CUDA(cudaMemsetAsync(d_hm, 0, J * 4, st));
+  const uint64_t warps = (R + 31) / 32;
+  const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((warps + 7) / 8, uint64_t(sm_count()) * 8)));
+  distinct_raw_kernel<<<grid, kHistThreads, 0, st>>>(d_rt, d_ro, d_rl, R, d_raw, d_sid, d_six, J, d_base,
+                                                     d_mask, slots, d_cnt, d_hm);
+  RS_LAUNCH_CHECK();
+  RS_CUDA(cudaMemcpyAsync(out, d_cnt, J * 8, cudaMemcpyDeviceToHost, st));
+  ctx->sync();
 }
 
 uint32_t profile_tables(const rs_profile* p) { return p->J; }

@@ -160,6 +160,19 @@ def build_icdf(counts_per_row, ctx=None) -> np.ndarray:
     return out
 
 
+def count_distinct_raw(trace: Trace, ctx=None) -> np.ndarray:
+    """GenStats.distinct_raw_ids (core/src/workload.cpp:195-223) of a raw trace,
+    counted on the GPU: distinct raw values per table over every record."""
+    if trace.raw_ids is None:
+        raise ValueError("count_distinct_raw needs trace.raw_ids")
+    ctx = ctx or default_context()
+    st, keep = trace_struct(trace)
+    out = np.zeros(max(1, len(trace.tables)), np.uint64)
+    _lib.check(_lib.lib().rs_count_distinct_raw(ctx.h, C.byref(st), ptr(out)))
+    del keep
+    return out[:len(trace.tables)]
+
+
 def hash_utilization(stats: FeatureStats, spec, distinct_raw_ids_seen: int):
     """core/src/profiler.cpp:163-174 — (sparsity_fraction, collision_fraction)."""
     s, c = C.c_double(), C.c_double()

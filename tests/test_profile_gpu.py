@@ -110,6 +110,37 @@ def test_profile_large_vs_oracle(cuda_ctx, coracle):
         assert_stats_equal(got, want)
 
 
+def test_count_distinct_raw(cuda_ctx):
+    """GenStats.distinct_raw_ids on the GPU: numpy unique per table, and the
+    reference generator's own GenStats when the reference library is present."""
+    import oracle
+
+    case = load_golden("profile.json")["raw_trace"]
+    tr = golden_trace(case["trace"], case["raw_ids"])
+    got = sp.count_distinct_raw(tr, ctx=cuda_ctx)
+    for j, t in enumerate(tr.tables):
+        mine = tr.rec_table == t.table_id
+        vals = np.concatenate([tr.raw_ids[o:o + l] for o, l in zip(tr.rec_offset[mine], tr.rec_len[mine])])
+        assert int(got[j]) == np.unique(vals).size
+    rng = np.random.default_rng(3)
+    tables, rt = _zipf_trace(rng, 3, 50_000, 2000, 7)
+    rt.raw_ids[::97] = np.uint64(0xFFFFFFFFFFFFFFFF)  # the hash set's empty sentinel is a valid raw
+    got = sp.count_distinct_raw(rt, ctx=cuda_ctx)
+    for j, t in enumerate(tables):
+        mine = rt.rec_table == t.table_id
+        vals = np.concatenate([rt.raw_ids[o:o + l] for o, l in zip(rt.rec_offset[mine], rt.rec_len[mine])])
+        assert int(got[j]) == np.unique(vals).size
+    if oracle.ref_available():
+        R = oracle.Ref()
+        S = oracle.Spec
+        wl = [(S(0, 5000, 4000, 8, 4), (1.2, 6.0, 0.7, 1)), (S(4, 90000, 30000, 4, 4), (0.8, 3.0, 0.9, 2))]
+        ref = R.generate_trace(wl, 4000, 17, gen_stats=True)
+        raw = R.generate_trace(wl, 4000, 17, raw=True)
+        tr = Trace([TableSpec(**vars(s)) for s in raw.tables], raw.num_samples, raw.rec_sample,
+                   raw.rec_table, raw.rec_offset, raw.rec_len, raw_ids=raw.raw_ids)
+        assert list(sp.count_distinct_raw(tr, ctx=cuda_ctx)) == list(ref.distinct_raw)
+
+
 def test_profile_many_tables_and_ragged(cuda_ctx, coracle):
     """Ragged records, empty records, tables never touched, non-contiguous offsets."""
     rng = np.random.default_rng(9)
