@@ -53,6 +53,9 @@ def parse():
     p.add_argument("--hbm-fraction", type=float, default=0.4,
                    help="M*cap_hbm as a fraction of all table bytes (configs/example_2x.cfg:2-3)")
     p.add_argument("--only", default=None, choices=[None, "recshard", "greedy"])
+    p.add_argument("--profile-ids", type=float, default=1e9,
+                   help="HP1 sweep size (BASELINE configs[4]); 0 disables")
+    p.add_argument("--cpu-profile-ids", type=float, default=5e7)
     p.add_argument("--no-cpu", action="store_true")
     return p.parse_args()
 
@@ -352,6 +355,56 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
     return res
 
 
+def run_profile_sweep(args, torch, ctx, hbm_peak):
+    """HP1 at scale (BASELINE configs[4]): profile() over ~args.profile_ids hashed
+    ids on the cfg1 tables (8 x 1e6 rows, Zipf 1.05, pooling 20), timed end to
+    end (device trace -> FeatureStats on the host), next to the unmodified
+    reference profile() (oracle/_ref, 1 thread) on a bounded sample."""
+    import oracle
+    import paper_2201_10095_b200 as sp
+    from paper_2201_10095_b200 import workload as wl
+
+    specs = wl.cfg1_specs()
+    per_sample = sum(w.gen.mean_pooling for w in specs)
+    S = int(args.profile_ids // per_sample)
+    gen = wl.BatchGenerator(specs, S, WORKLOAD_SEED + 1)
+    off, idx, n = gen.batch(0)
+    tr = wl.kjt_to_trace(specs, off, idx, n, S, 0, ctx=ctx)
+    R = int(tr.rec_sample.numel())
+    sp.profile(tr, 1.0, PROFILE_SEED, ctx=ctx)  # warm-up
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        p = sp.profiler.profile_handle(tr, 1.0, PROFILE_SEED, ctx=ctx)
+        times.append(time.perf_counter() - t0)
+        p.close()
+    secs = float(np.median(times))
+    H = sum(w.table.hash_size for w in specs)
+    alg = 4.0 * n + 24.0 * R + 8.0 * H  # DESIGN.md §4: id + record + (zero + read) per row
+    out = {"workload": "cfg1 tables, rate 1.0", "ids": int(n), "records": R,
+           "seconds": secs, "ids_per_s": n / secs, "algorithmic_gbs": alg / secs / 1e9,
+           "frac_of_hbm": alg / secs / 1e9 / hbm_peak}
+    if oracle.ref_available():
+        m = min(R, int(args.cpu_profile_ids // 20))
+        sub = (tr.rec_sample[:m].cpu().numpy().view(np.uint64), tr.rec_table[:m].cpu().numpy().view(np.uint32),
+               tr.rec_offset[:m].cpu().numpy().view(np.uint64), tr.rec_len[:m].cpu().numpy().view(np.uint32))
+        last = int(sub[2][-1] + sub[3][-1])
+        ids_h = idx[:last].cpu().numpy().view(np.uint32)
+        Rf = oracle.Ref()
+        rt = Rf.trace([oracle.Spec(w.table.table_id, w.table.cardinality, w.table.hash_size,
+                                   w.table.dim, w.table.elem_bytes) for w in specs],
+                      int(sub[0].max()) + 1, *sub, ids_h)
+        cs = Rf.time_profile(rt, 1.0, PROFILE_SEED)
+        Rf.free_trace(rt)
+        out["cpu_reference"] = {"ids_per_s": last / cs, "cores": 1, "kind": "reference",
+                                "sample": f"first {m} records ({last} ids) of the same trace, "
+                                          "unmodified shardplan::profile (single-threaded)"}
+    del tr, idx, off
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex):
     """Same step through the public API with host inputs: pinned host offsets +
     indices copied H2D every step, the hit counters (the step's UVM metric)
@@ -478,6 +531,10 @@ def main():
                      args.greedy_steps, 1, False, B)
     prof.close()
 
+    sweep = None
+    if rank == 0 and world == 1 and args.profile_ids > 0:
+        sweep = run_profile_sweep(args, torch, ctx, hbm_peak)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_emb_baseline(specs, B, args.cpu_seconds, os.cpu_count() or 1, args.optimizer)
@@ -523,6 +580,7 @@ def main():
             "gpu_launches": r["launches"],
             "clocks": r["clocks"],
             "profile": {"ids": pn, "seconds_incl_host": prof_s, "ids_per_s": pn / prof_s},
+            "profiler_sweep": sweep,
             "bw_uvm_h2d_gbs": bw_uvm / 1e9,
         }
         print(json.dumps(line), flush=True)

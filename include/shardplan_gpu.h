@@ -240,6 +240,17 @@ int rs_emb_forward(rs_emb* e, uint64_t batch, const uint32_t* offsets,
 /* K5: backward + optimizer update, deterministic (sorted-segment reduction). */
 int rs_emb_backward(rs_emb* e, uint64_t batch, const uint32_t* offsets,
                     const uint32_t* indices, const float* grad_pooled, float lr);
+/* HBM staging of slow-tier rows, overlapped with compute: after
+ * rs_emb_enable_uvm_cache(nslots), rs_emb_prefetch(batch k+1) — called while
+ * batch k computes — copies batch k+1's slow rows (deduplicated) into HBM on a
+ * side stream; the forward/backward of that batch use the staged copies and a
+ * side-stream write-back returns updated rows to the host tier.  At most one
+ * batch ahead; results are bit-identical to the zero-copy path.  nslots should
+ * be >= 2x the unique slow rows of one batch.  rs_emb_flush writes every
+ * staged row back (read_rows / init_weights do so implicitly). */
+int rs_emb_enable_uvm_cache(rs_emb* e, uint32_t nslots);
+int rs_emb_prefetch(rs_emb* e, uint64_t batch, const uint32_t* offsets, const uint32_t* indices);
+int rs_emb_flush(rs_emb* e);
 /* Reads rows by ORIGINAL id into host memory (parity checks). */
 int rs_emb_read_rows(rs_emb* e, uint32_t t, const uint32_t* rows, uint64_t n,
                      float* out, float* momentum_out);

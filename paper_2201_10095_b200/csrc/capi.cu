@@ -23,6 +23,9 @@ void emb_init_weights(rs_emb*, uint64_t, float);
 void emb_forward(rs_emb*, uint64_t, const uint32_t*, const uint32_t*, float*, uint64_t*);
 void emb_backward(rs_emb*, uint64_t, const uint32_t*, const uint32_t*, const float*, float);
 void emb_read_rows(rs_emb*, uint32_t, const uint32_t*, uint64_t, float*, float*);
+void emb_enable_cache(rs_emb*, uint32_t);
+void emb_prefetch(rs_emb*, uint64_t, const uint32_t*, const uint32_t*);
+void emb_flush(rs_emb*);
 void emb_memory(const rs_emb*, uint64_t*, uint64_t*);
 void profile_view(const rs_profile*, uint32_t, rs_feature_stats*);
 uint32_t profile_tables(const rs_profile*);
@@ -252,6 +255,28 @@ int rs_emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* 
     need(off, "offsets");
     need(grad, "grad");
     rs::emb_backward(e, B, off, idx, grad, lr);
+  });
+}
+
+int rs_emb_enable_uvm_cache(rs_emb* e, uint32_t nslots) {
+  return guarded([&] {
+    need(e, "emb");
+    rs::emb_enable_cache(e, nslots);
+  });
+}
+
+int rs_emb_prefetch(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx) {
+  return guarded([&] {
+    need(e, "emb");
+    need(off, "offsets");
+    rs::emb_prefetch(e, B, off, idx);
+  });
+}
+
+int rs_emb_flush(rs_emb* e) {
+  return guarded([&] {
+    need(e, "emb");
+    rs::emb_flush(e);
   });
 }
 

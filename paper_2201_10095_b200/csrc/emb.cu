@@ -43,6 +43,11 @@ struct TableDev {
   uint32_t key_base; // backward key space offset
   uint64_t hbm_rows;
   uint64_t slow_rows;
+  // HBM staging of slow-tier rows (uvm_cache.cuh); slot_of == nullptr means
+  // slow rows are read/written zero-copy in host memory.
+  uint32_t* slot_of;
+  float* staging;
+  uint64_t stage_stride;
 };
 
 __host__ __device__ inline int lanes_for(uint32_t dim) {
@@ -51,8 +56,17 @@ __host__ __device__ inline int lanes_for(uint32_t dim) {
   return int(L);
 }
 
-__device__ __forceinline__ float* row_ptr(const TableDev& td, int32_t e) {
+// Row of remap entry e in the host tier (no staging).
+__device__ __forceinline__ float* row_ptr_host(const TableDev& td, int32_t e) {
   return e >= 0 ? td.fast + uint64_t(e) * td.dim : td.slow + uint64_t(-int64_t(e) - 1) * td.dim;
+}
+// Row of remap entry e as the hot paths see it: slow rows come from their HBM
+// staging slot when the batch was prefetched (uvm_cache.cuh).
+__device__ __forceinline__ float* row_ptr(const TableDev& td, int32_t e) {
+  if (e >= 0) return td.fast + uint64_t(e) * td.dim;
+  const uint64_t s = uint64_t(-int64_t(e) - 1);
+  if (td.slot_of) return td.staging + uint64_t(td.slot_of[s]) * td.stage_stride;
+  return td.slow + s * td.dim;
 }
 __device__ __forceinline__ float* mom_ptr(const TableDev& td, int32_t e) {
   return e >= 0 ? td.mom_fast + uint64_t(e) : td.mom_slow + uint64_t(-int64_t(e) - 1);
@@ -207,6 +221,7 @@ keygen_kernel(const TableDev* __restrict__ tables, uint32_t T, uint64_t B,
 }  // namespace rs
 
 #include "emb_bwd.cuh"
+#include "uvm_cache.cuh"
 
 namespace rs {
 namespace emb {
@@ -227,7 +242,7 @@ __global__ void init_kernel(TableDev td, uint32_t table_id, uint64_t seed, float
       x[k] = __fmul_rn(__fsub_rn(__fmul_rn(float(u), 0x1.0p-24f), 0.5f), scale);
     }
     const int32_t e = td.remap[row];
-    float4* w = reinterpret_cast<float4*>(row_ptr(td, e));
+    float4* w = reinterpret_cast<float4*>(row_ptr_host(td, e));
     w[vec] = make_float4(x[0], x[1], x[2], x[3]);
     if (vec == 0 && td.mom_fast) *mom_ptr(td, e) = 0.f;
   }
@@ -242,7 +257,7 @@ __global__ void read_rows_kernel(TableDev td, const uint32_t* __restrict__ rows,
     const uint32_t vec = uint32_t(i % V);
     const int32_t e = td.remap[rows[r]];
     reinterpret_cast<float4*>(out + r * td.dim)[vec] =
-        reinterpret_cast<const float4*>(row_ptr(td, e))[vec];
+        reinterpret_cast<const float4*>(row_ptr_host(td, e))[vec];
     if (mom_out && vec == 0) mom_out[r] = td.mom_fast ? *mom_ptr(td, e) : 0.f;
   }
 }
@@ -292,6 +307,26 @@ struct rs_emb {
   // backward buffers
   uint32_t* keys = nullptr;
   uint32_t* vals = nullptr;
+  // HBM staging of slow rows (uvm_cache.cuh)
+  uint32_t nslots = 0;
+  float* staging = nullptr;
+  uint32_t* slot_of = nullptr;  // sum(slow_rows)
+  uint32_t* slot_gen = nullptr;
+  uint32_t* slot_tab = nullptr;
+  uint32_t* slot_row = nullptr;
+  uint32_t* free_stack = nullptr;
+  uint32_t* copy_list = nullptr;
+  int* free_top = nullptr;
+  unsigned* ncopy = nullptr;
+  unsigned* cache_err = nullptr;
+  TableDev* d_tables_c = nullptr;
+  const TableDev* cur_tables = nullptr;  // tables the running forward/backward use
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_main = nullptr, ev_bwd = nullptr, ev_gather[2] = {nullptr, nullptr};
+  std::vector<uint64_t> pending;  // prefetched generations, oldest first
+  int64_t cur_gen = -1;           // staged generation of the running step (-1: zero-copy)
+  uint64_t next_gen = 0;
+  bool staged_dirty = false;
   float* part = nullptr;
   float* spart = nullptr;
   uint32_t* d_meta = nullptr;
@@ -317,6 +352,16 @@ struct rs_emb {
     if (h_meta) cudaFreeHost(h_meta);
     if (d_err) cudaFree(d_err);
     if (sort_scratch) cudaFree(sort_scratch);
+    if (side) {
+      cudaStreamSynchronize(side);
+      cudaStreamDestroy(side);
+    }
+    for (cudaEvent_t ev : {ev_main, ev_bwd, ev_gather[0], ev_gather[1]})
+      if (ev) cudaEventDestroy(ev);
+    for (void* p : {(void*)staging, (void*)slot_of, (void*)slot_gen, (void*)slot_tab, (void*)slot_row,
+                    (void*)free_stack, (void*)copy_list, (void*)free_top, (void*)ncopy, (void*)cache_err,
+                    (void*)d_tables_c})
+      if (p) cudaFree(p);
   }
 };
 
@@ -364,12 +409,14 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
         throw InvalidArgument("emb: sum of hash sizes must be < 2^31 per operator (split the tables)");
       key_acc += x.hash_size;
     }
+    // Adagrad state (4 B/row) of BOTH tiers lives in HBM: a slow-tier row's
+    // update then costs one PCIe row read + write instead of four transfers.
     if (opt == RS_OPT_ROWWISE_ADAGRAD) {
       for (uint32_t t = 0; t < T; ++t) {
         mfoff[t] = fb;
         fb += align256(tabs[t].hbm_rows * 4);
-        mhoff[t] = hb;
-        hb += align256(tabs[t].slow_rows * 4);
+        mhoff[t] = fb;
+        fb += align256(tabs[t].slow_rows * 4);
       }
     }
     e->fast_bytes = std::max<size_t>(fb, 256);
@@ -394,7 +441,7 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
       d.fast = reinterpret_cast<float*>(e->fast_pool + foff[t]);
       d.slow = reinterpret_cast<float*>(e->host_pool_dev + hoff[t]);
       d.mom_fast = opt == RS_OPT_ROWWISE_ADAGRAD ? reinterpret_cast<float*>(e->fast_pool + mfoff[t]) : nullptr;
-      d.mom_slow = opt == RS_OPT_ROWWISE_ADAGRAD ? reinterpret_cast<float*>(e->host_pool_dev + mhoff[t]) : nullptr;
+      d.mom_slow = opt == RS_OPT_ROWWISE_ADAGRAD ? reinterpret_cast<float*>(e->fast_pool + mhoff[t]) : nullptr;
       d.hash_size = x.hash_size;
       d.col = col;
       d.dim = x.dim;
@@ -475,7 +522,141 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
   return e;
 }
 
+// ------------------------------------------------------------------ slow-row staging
+void emb_enable_cache(rs_emb* e, uint32_t nslots) {
+  if (e->nslots) throw InvalidArgument("emb: the slow-row cache is already enabled");
+  if (nslots == 0 || nslots >= emb::kClaim) throw InvalidArgument("emb: nslots out of range");
+  cudaStream_t st = e->ctx->stream;
+  uint64_t total_slow = 0;
+  for (const auto& d : e->h_tables) total_slow += d.slow_rows;
+  const uint64_t stride = e->dmax;
+  RS_CUDA(cudaMalloc(&e->staging, uint64_t(nslots) * stride * 4));
+  RS_CUDA(cudaMalloc(&e->slot_of, std::max<uint64_t>(total_slow, 1) * 4));
+  RS_CUDA(cudaMalloc(&e->slot_gen, uint64_t(nslots) * 4));
+  RS_CUDA(cudaMalloc(&e->slot_tab, uint64_t(nslots) * 4));
+  RS_CUDA(cudaMalloc(&e->slot_row, uint64_t(nslots) * 4));
+  RS_CUDA(cudaMalloc(&e->free_stack, uint64_t(nslots) * 4));
+  RS_CUDA(cudaMalloc(&e->copy_list, uint64_t(nslots) * 4));
+  RS_CUDA(cudaMalloc(&e->free_top, 4));
+  RS_CUDA(cudaMalloc(&e->ncopy, 4));
+  RS_CUDA(cudaMalloc(&e->cache_err, 4));
+  RS_CUDA(cudaMemsetAsync(e->slot_of, 0xFF, std::max<uint64_t>(total_slow, 1) * 4, st));
+  RS_CUDA(cudaMemsetAsync(e->slot_gen, 0, uint64_t(nslots) * 4, st));
+  RS_CUDA(cudaMemsetAsync(e->cache_err, 0, 4, st));
+  std::vector<uint32_t> fs(nslots);
+  std::iota(fs.begin(), fs.end(), 0u);
+  RS_CUDA(cudaMemcpyAsync(e->free_stack, fs.data(), uint64_t(nslots) * 4, cudaMemcpyHostToDevice, st));
+  const int top = int(nslots);
+  RS_CUDA(cudaMemcpyAsync(e->free_top, &top, 4, cudaMemcpyHostToDevice, st));
+  std::vector<TableDev> tc = e->h_tables;
+  uint64_t base = 0;
+  for (auto& d : tc) {
+    d.slot_of = e->slot_of + base;
+    d.staging = e->staging;
+    d.stage_stride = stride;
+    base += d.slow_rows;
+  }
+  RS_CUDA(cudaMalloc(&e->d_tables_c, sizeof(TableDev) * e->T));
+  RS_CUDA(cudaMemcpyAsync(e->d_tables_c, tc.data(), sizeof(TableDev) * e->T, cudaMemcpyHostToDevice, st));
+  RS_CUDA(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+  for (cudaEvent_t* ev : {&e->ev_main, &e->ev_bwd, &e->ev_gather[0], &e->ev_gather[1]})
+    RS_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+  RS_CUDA(cudaStreamSynchronize(st));
+  e->nslots = nslots;
+}
+
+static unsigned cache_grid(uint64_t work) {
+  return unsigned(std::max<uint64_t>(1, std::min<uint64_t>((work + 255) / 256, uint64_t(sm_count()) * 8)));
+}
+
+static void check_cache_error(rs_emb* e) {
+  unsigned err = 0;
+  RS_CUDA(cudaMemcpy(&err, e->cache_err, 4, cudaMemcpyDeviceToHost));
+  if (err)
+    throw InvalidArgument("emb: slow-row cache out of slots; enable it with more slots "
+                          "(>= 2x the unique slow rows of a batch)");
+}
+
+// Enqueues the write-back of generation g on the side stream after the
+// backward that used it; rows a pending prefetch still needs stay staged.
+static void enqueue_writeback(rs_emb* e, uint64_t g) {
+  uint32_t keep = 0;
+  for (uint64_t p : e->pending) keep |= 1u << (p & 1);
+  RS_CUDA(cudaEventRecord(e->ev_bwd, e->ctx->stream));
+  RS_CUDA(cudaStreamWaitEvent(e->side, e->ev_bwd, 0));
+  emb::uvm_writeback_kernel<<<cache_grid(uint64_t(e->nslots) * 32 / 32), 256, 0, e->side>>>(
+      e->d_tables_c, e->nslots, 1u << (g & 1), keep, e->slot_gen, e->slot_tab, e->slot_row,
+      e->free_stack, e->free_top, e->staging, e->dmax);
+  RS_COUNT(1);
+  RS_LAUNCH_CHECK();
+}
+
+void emb_prefetch(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx) {
+  if (!e->nslots) throw InvalidArgument("emb_prefetch: enable the slow-row cache first");
+  if (B == 0 || B > e->max_batch) throw InvalidArgument("emb_prefetch: batch outside [1, max_batch]");
+  const uint64_t g = e->next_gen;
+  const bool clash = (e->cur_gen >= 0 && (uint64_t(e->cur_gen) & 1) == (g & 1)) ||
+                     std::any_of(e->pending.begin(), e->pending.end(),
+                                 [&](uint64_t p) { return (p & 1) == (g & 1); });
+  if (clash) throw InvalidArgument("emb_prefetch: at most one batch may be prefetched ahead");
+  ++e->next_gen;
+  // inputs are produced on the caller's stream
+  RS_CUDA(cudaEventRecord(e->ev_main, e->ctx->stream));
+  RS_CUDA(cudaStreamWaitEvent(e->side, e->ev_main, 0));
+  RS_CUDA(cudaMemsetAsync(e->ncopy, 0, 4, e->side));
+  emb::uvm_claim_kernel<<<unsigned(uint64_t(sm_count()) * 8), 256, 0, e->side>>>(
+      e->d_tables_c, e->T, B, off, idx, 1u << (g & 1), e->slot_gen, e->slot_tab, e->slot_row,
+      e->free_stack, e->free_top, e->copy_list, e->ncopy, e->cache_err);
+  emb::uvm_fill_kernel<<<unsigned(uint64_t(sm_count()) * 8), 256, 0, e->side>>>(
+      e->d_tables_c, e->slot_tab, e->slot_row, e->copy_list, e->ncopy, e->staging, e->dmax);
+  RS_COUNT(2);
+  RS_LAUNCH_CHECK();
+  RS_CUDA(cudaEventRecord(e->ev_gather[g & 1], e->side));
+  e->pending.push_back(g);
+  e->staged_dirty = true;
+}
+
+// Writes every staged row back and drops pending prefetches (they would
+// refetch); afterwards the host tier is authoritative again.
+void emb_flush(rs_emb* e) {
+  if (!e->nslots || !e->staged_dirty) return;
+  cudaStream_t st = e->ctx->stream;
+  RS_CUDA(cudaEventRecord(e->ev_main, e->side));
+  RS_CUDA(cudaStreamWaitEvent(st, e->ev_main, 0));
+  emb::uvm_writeback_kernel<<<cache_grid(e->nslots), 256, 0, st>>>(
+      e->d_tables_c, e->nslots, 3u, 0u, e->slot_gen, e->slot_tab, e->slot_row, e->free_stack,
+      e->free_top, e->staging, e->dmax);
+  RS_COUNT(1);
+  RS_LAUNCH_CHECK();
+  RS_CUDA(cudaStreamSynchronize(st));
+  check_cache_error(e);
+  e->pending.clear();
+  e->cur_gen = -1;
+  e->staged_dirty = false;
+}
+
+// Picks the tables for a forward: the oldest prefetched batch (staged rows)
+// or, without a prefetch, the zero-copy path.
+static void begin_step(rs_emb* e) {
+  if (e->cur_gen >= 0) {  // previous staged forward without a backward
+    const uint64_t g = uint64_t(e->cur_gen);
+    e->cur_gen = -1;
+    enqueue_writeback(e, g);
+  }
+  if (!e->pending.empty()) {
+    const uint64_t g = e->pending.front();
+    e->pending.erase(e->pending.begin());
+    e->cur_gen = int64_t(g);
+    RS_CUDA(cudaStreamWaitEvent(e->ctx->stream, e->ev_gather[g & 1], 0));
+    e->cur_tables = e->d_tables_c;
+  } else {
+    emb_flush(e);
+    e->cur_tables = e->d_tables;
+  }
+}
+
 void emb_init_weights(rs_emb* e, uint64_t seed, float scale) {
+  emb_flush(e);
   cudaStream_t st = e->ctx->stream;
   for (uint32_t t = 0; t < e->T; ++t) {
     const TableDev& d = e->h_tables[t];
@@ -497,7 +678,7 @@ static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint
     const char* v = getenv("RS_FWD_VARIANT");
     return v ? atoi(v) : 0;
   }();
-  auto args = std::make_tuple(e->d_tables, c.d_list, uint32_t(c.tables.size()), B, off, idx, out,
+  auto args = std::make_tuple(e->cur_tables, c.d_list, uint32_t(c.tables.size()), B, off, idx, out,
                               e->total_dim, hits);
   auto go = [&](auto kern) {
     std::apply([&](auto... a) { kern<<<grid, emb::kFwdThreads, 0, e->ctx->stream>>>(a...); }, args);
@@ -513,6 +694,7 @@ static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint
 void emb_forward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx, float* out,
                  uint64_t* hits) {
   if (B == 0 || B > e->max_batch) throw InvalidArgument("emb_forward: batch outside [1, max_batch]");
+  begin_step(e);
   auto* h = reinterpret_cast<unsigned long long*>(hits);
   for (const auto& c : e->classes) {
     switch (c.G * 100 + c.VPL) {
@@ -583,6 +765,25 @@ static void launch_edges(rs_emb* e, const emb::BwdArgs& a) {
 void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx, const float* grad,
                   float lr) {
   if (B == 0 || B > e->max_batch) throw InvalidArgument("emb_backward: batch outside [1, max_batch]");
+  // a backward belongs to the last forward's batch: staged rows if that batch
+  // was prefetched, else the zero-copy path
+  if (e->cur_gen < 0) {
+    emb_flush(e);
+    e->cur_tables = e->d_tables;
+  }
+  struct Release {
+    rs_emb* e;
+    ~Release() {
+      if (e->cur_gen >= 0) {
+        const uint64_t g = uint64_t(e->cur_gen);
+        e->cur_gen = -1;
+        try {
+          enqueue_writeback(e, g);
+        } catch (...) {
+        }
+      }
+    }
+  } release{e};
   cudaStream_t st = e->ctx->stream;
   const uint32_t T = e->T;
   uint32_t* tpos = e->h_meta;  // offsets[t*B], t = 0..T
@@ -624,7 +825,7 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
   scr.base = e->sort_scratch;
   scr.cap = e->sort_scratch_bytes;
   radix_sort_pairs(e->keys, e->vals, L, int(e->key_bits), scr, st);
-  emb::BwdArgs a{e->d_tables, T, e->d_meta, e->d_meta + T + 1, cbase[T], e->keys, e->vals,
+  emb::BwdArgs a{e->cur_tables, T, e->d_meta, e->d_meta + T + 1, cbase[T], e->keys, e->vals,
                  grad, e->total_dim, e->part, e->spart, e->dmax, lr, e->eps, e->opt};
   for (size_t ci = 0; ci < e->classes.size(); ++ci) {
     const auto& c = e->classes[ci];
@@ -654,6 +855,12 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
 
 void emb_read_rows(rs_emb* e, uint32_t t, const uint32_t* rows, uint64_t n, float* out, float* mom) {
   if (t >= e->T) throw InvalidArgument("emb_read_rows: table index out of range");
+  if (e->cur_gen >= 0) {  // a staged forward without its backward yet
+    const uint64_t g = uint64_t(e->cur_gen);
+    e->cur_gen = -1;
+    enqueue_writeback(e, g);
+  }
+  emb_flush(e);
   cudaStream_t st = e->ctx->stream;
   const TableDev& d = e->h_tables[t];
   for (uint64_t i = 0; i < n; ++i)

@@ -81,6 +81,19 @@ class TieredEmbeddingBag:
         _lib.check(_lib.lib().rs_emb_backward(self.h, C.c_uint64(batch), ptr(offsets), ptr(indices),
                                               ptr(grad), C.c_float(lr)))
 
+    def enable_uvm_cache(self, nslots: int):
+        """HBM staging of slow-tier rows with side-stream prefetch/write-back
+        (csrc/uvm_cache.cuh); nslots >= 2x the unique slow rows of a batch."""
+        _lib.check(_lib.lib().rs_emb_enable_uvm_cache(self.h, C.c_uint32(nslots)))
+
+    def prefetch(self, offsets, indices, batch: int):
+        """Stage the next batch's slow rows while the current batch runs."""
+        self._check_dev(offsets, indices)
+        _lib.check(_lib.lib().rs_emb_prefetch(self.h, C.c_uint64(batch), ptr(offsets), ptr(indices)))
+
+    def flush(self):
+        _lib.check(_lib.lib().rs_emb_flush(self.h))
+
     def read_rows(self, t: int, rows):
         rows = np.ascontiguousarray(rows, np.uint32)
         out = np.empty((rows.size, self.dims[t]), np.float32)

@@ -138,6 +138,82 @@ def test_backward_deterministic(cuda_ctx, coracle):
         assert np.array_equal(ma.view(np.uint32), mb.view(np.uint32))
 
 
+def _train(cuda_ctx, coracle, cached, steps=5, nslots=4096):
+    """Fwd+bwd over distinct batches; with `cached`, batch k+1 is prefetched
+    (slow rows staged in HBM) while batch k runs."""
+    import torch
+
+    dims, Hs, frac, B, ml = ([64, 128, 32], [300, 500, 2000], [0.3, 0.1, 0.5], 128, 12)
+    rng = np.random.default_rng(11)
+    specs, remaps, _, _, _, _, _ = _setup(coracle, dims, Hs, frac, B, ml, rng)
+    batches = []
+    for k in range(steps):
+        r2 = np.random.default_rng(100 + k)
+        lens = r2.integers(0, ml + 1, len(dims) * B)
+        off = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint32)
+        idx = np.concatenate([np.minimum(r2.zipf(1.3, L) - 1, Hs[i // B] - 1)
+                              for i, L in enumerate(lens)]).astype(np.uint32)
+        batches.append((torch.from_numpy(off.view(np.int32)).cuda(),
+                        torch.from_numpy(idx.view(np.int32)).cuda(), idx.size))
+    op = sp.TieredEmbeddingBag(specs, remaps, B, max(b[2] for b in batches), "rowwise_adagrad",
+                               ctx=cuda_ctx)
+    op.init_weights(SEED, SCALE)
+    if cached:
+        op.enable_uvm_cache(nslots)
+        op.prefetch(batches[0][0], batches[0][1], B)
+    outs = []
+    for k in range(steps):
+        off, idx, _ = batches[k]
+        y = op.forward(off, idx, B)
+        if cached and k + 1 < steps:
+            op.prefetch(batches[k + 1][0], batches[k + 1][1], B)
+        outs.append(y.clone())
+        op.backward(off, idx, y * 0.5 + 0.01, B, 0.05)
+    torch.cuda.synchronize()
+    rows = [op.read_rows(t, np.arange(s.hash_size, dtype=np.uint32)) for t, s in enumerate(specs)]
+    op.close()
+    return outs, rows
+
+
+def test_uvm_cache_bit_identical_to_zero_copy(cuda_ctx, coracle):
+    """Slow rows staged in HBM with side-stream prefetch/write-back (one batch
+    ahead) give exactly the zero-copy results, incl. rows shared by
+    consecutive batches and slot reuse under a small cache."""
+    ref_out, ref_rows = _train(cuda_ctx, coracle, cached=False)
+    for nslots in (4096, 1200):
+        out, rows = _train(cuda_ctx, coracle, cached=True, nslots=nslots)
+        for a, b in zip(out, ref_out):
+            assert torch_equal(a, b)
+        for (wa, ma), (wb, mb) in zip(rows, ref_rows):
+            assert np.array_equal(wa.view(np.uint32), wb.view(np.uint32))
+            assert np.array_equal(ma.view(np.uint32), mb.view(np.uint32))
+
+
+def torch_equal(a, b):
+    import torch
+
+    return bool(torch.equal(a.view(torch.int32), b.view(torch.int32)))
+
+
+def test_uvm_cache_errors(cuda_ctx, coracle):
+    import torch
+
+    rng = np.random.default_rng(5)
+    specs, remaps, offsets, idx, d_off, d_idx, _ = _setup(coracle, [64], [1000], [0.0], 64, 10, rng)
+    op = sp.TieredEmbeddingBag(specs, remaps, 64, idx.size, "sgd", ctx=cuda_ctx)
+    with pytest.raises(sp.InvalidArgument):  # prefetch needs the cache
+        op.prefetch(d_off, d_idx, 64)
+    op.enable_uvm_cache(4)  # far fewer slots than slow rows in the batch
+    op.prefetch(d_off, d_idx, 64)
+    op.prefetch(d_off, d_idx, 64)  # the next batch and the one after: two live
+    with pytest.raises(sp.InvalidArgument):  # a third would be two batches ahead
+        op.prefetch(d_off, d_idx, 64)
+    with pytest.raises(sp.InvalidArgument):  # out of slots is reported
+        op.flush()
+    torch.cuda.synchronize()
+    op.close()
+
+
 def test_operator_rejects_bad_inputs(cuda_ctx):
     spec = TableSpec(0, 10, 10, 6, 4)  # dim not a multiple of 4
     r = sp.RemapTable(0, 10, 10, 0, np.arange(10, dtype=np.int32))
