@@ -198,8 +198,10 @@ class _COracle:
         return out
 
     def emb_backward(self, B, dims, offsets, indices, grad_out, weights,
-                     momentum, opt, lr, eps):
-        """Updates ``weights`` / ``momentum`` (lists of numpy arrays) in place."""
+                     momentum, opt, lr, eps, remaps=None):
+        """Updates ``weights`` / ``momentum`` (lists of numpy arrays) in place.
+        ``remaps``: per table (entries int32[H], hbm_rows) of the operator's
+        placement — lookups are reduced in storage-slot order; None = identity."""
         T = len(dims)
         D = _u32(dims)
         Hs = _u64([w.shape[0] for w in weights])
@@ -214,10 +216,15 @@ class _COracle:
         if momentum is None:
             momentum = [np.zeros(1, np.float32) for _ in weights]
         ma = (_P * T)(*[m.ctypes.data for m in momentum])
+        ra, hb = None, None
+        if remaps is not None:
+            ents = [np.ascontiguousarray(r[0], np.int32) for r in remaps]
+            ra = (_P * T)(*[e.ctypes.data for e in ents])
+            hb = _u64([r[1] for r in remaps])
         st = self.lib.or_emb_backward(C_.c_uint32(T), C_.c_uint64(B), _ptr(D), _ptr(Hs),
                                       _ptr(col), C_.c_uint64(stride), _ptr(off), _ptr(idx),
                                       _ptr(g), C_.c_int(opt), C_.c_float(lr),
-                                      C_.c_float(eps), wa, ma)
+                                      C_.c_float(eps), wa, ma, ra, _ptr(hb))
         if st:
             raise OracleError(st)
 

@@ -280,8 +280,9 @@ static float rowwise_sumsq(const float* g, uint32_t D) {
   return part[0];
 }
 
-/* One lookup of the batch: global key = key_base[t] + row (key_base = sum of
- * earlier tables' hash sizes), l = position in the table-major index list. */
+/* One lookup of the batch: global key = key_base[t] + storage slot (key_base =
+ * sum of earlier tables' hash sizes), l = position in the table-major index
+ * list. */
 typedef struct { uint64_t key; uint64_t l; } lk_t;
 static int cmp_lk(const void* a, const void* b) {
   const lk_t* x = (const lk_t*)a;
@@ -298,7 +299,8 @@ int or_emb_backward(uint32_t T, uint64_t B, const uint32_t* D,
                     uint64_t grad_stride, const uint64_t* offsets,
                     const uint32_t* indices, const float* grad_out, int opt,
                     float lr, float eps, float* const* W,
-                    float* const* momentum) {
+                    float* const* momentum, const int32_t* const* remap,
+                    const uint64_t* hbm_rows) {
   const uint64_t L = offsets[(uint64_t)T * B];
   if (L == 0) return ST_OK;
   uint64_t* kb = (uint64_t*)malloc(sizeof(uint64_t) * (T + 1));
@@ -319,7 +321,13 @@ int or_emb_backward(uint32_t T, uint64_t B, const uint32_t* D,
     for (uint64_t b = 0; b < B; ++b)
       for (uint64_t l = offsets[t * B + b]; l < offsets[t * B + b + 1]; ++l) {
         if (indices[l] >= H[t]) { free(cb); free(kb); free(lk); free(bag); free(tab); return ST_INVALID; }
-        lk[l].key = kb[t] + indices[l];
+        uint64_t slot = indices[l];
+        if (remap) {
+          const int32_t e = remap[t][indices[l]];
+          slot = e >= 0 ? (uint64_t)e : hbm_rows[t] + (uint64_t)(-(int64_t)e - 1);
+          if (slot >= H[t]) { free(cb); free(kb); free(lk); free(bag); free(tab); return ST_INVALID; }
+        }
+        lk[l].key = kb[t] + slot;
         lk[l].l = l;
         bag[l] = b;
         tab[l] = t;
@@ -334,7 +342,7 @@ int or_emb_backward(uint32_t T, uint64_t B, const uint32_t* D,
   while (i < L) {
     const uint64_t key = lk[i].key;
     const uint32_t t = tab[lk[i].l];
-    const uint32_t row = (uint32_t)(key - kb[t]);
+    const uint32_t row = indices[lk[i].l]; /* the remap is a bijection: one row per slot */
     const uint32_t d = D[t];
     uint64_t e = i;
     while (e < L && lk[e].key == key) ++e;

@@ -98,7 +98,11 @@ int or_emb_forward(uint32_t T, uint64_t B, const uint32_t* D,
                    const float* const* W, float* out);
 
 /* Backward + optimizer.  All lookups of the batch are ordered stably by
- * global key (sum of earlier tables' hash sizes + row); for each distinct
+ * global key = (sum of earlier tables' hash sizes) + slot, where slot is the
+ * row's storage slot in the operator's tiers (csrc/emb.cu keygen_kernel):
+ * remap entry e >= 0 -> e, e < 0 -> hbm_rows[t] + (-e - 1)
+ * (include/shardplan/remap.hpp:27-29 encoding).  remap == NULL means the
+ * identity placement (slot = row).  For each distinct
  * (table, row) the gradient g = sum of grad_out[b, col_off[t] : +D] over its
  * lookups, accumulated in fp32 in the kernel's fixed tree
  * (csrc/emb_bwd.cuh): table t's lookups occupy sorted positions from
@@ -119,7 +123,8 @@ int or_emb_backward(uint32_t T, uint64_t B, const uint32_t* D,
                     uint64_t grad_stride, const uint64_t* offsets,
                     const uint32_t* indices, const float* grad_out, int opt,
                     float lr, float eps, float* const* W,
-                    float* const* momentum);
+                    float* const* momentum, const int32_t* const* remap,
+                    const uint64_t* hbm_rows);
 
 #ifdef __cplusplus
 }

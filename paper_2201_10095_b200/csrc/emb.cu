@@ -71,6 +71,15 @@ __device__ __forceinline__ float* row_ptr(const TableDev& td, int32_t e) {
 __device__ __forceinline__ float* mom_ptr(const TableDev& td, int32_t e) {
   return e >= 0 ? td.mom_fast + uint64_t(e) : td.mom_slow + uint64_t(-int64_t(e) - 1);
 }
+// Backward keys are storage slots: key = key_base + (e >= 0 ? e : hbm_rows + (-e - 1)),
+// a bijection of the remap entries onto [key_base, key_base + hbm_rows + slow_rows).
+__device__ __forceinline__ uint32_t slot_of_entry(const TableDev& td, int32_t e) {
+  return e >= 0 ? uint32_t(e) : uint32_t(td.hbm_rows + uint64_t(-int64_t(e) - 1));
+}
+__device__ __forceinline__ int32_t entry_of_key(const TableDev& td, uint32_t key) {
+  const uint32_t s = key - td.key_base;
+  return s < td.hbm_rows ? int32_t(s) : int32_t(-int64_t(s - td.hbm_rows) - 1);
+}
 
 constexpr int kFwdThreads = 256;
 
@@ -171,8 +180,10 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
 }
 
 // ------------------------------------------------------------------ backward
-// keys[l] = key_base[t] + index, vals[l] = sample b, for every lookup l of
-// bag (t, b); warps flatten 32 bags' lookups so stores stay coalesced.
+// keys[l] = key_base[t] + storage slot of remap[index], vals[l] = sample b, for
+// every lookup l of bag (t, b); warps flatten 32 bags' lookups so stores stay
+// coalesced.  Keying by slot lets the backward address rows without a remap
+// load and walks each tier in address order.
 __global__ void __launch_bounds__(256)
 keygen_kernel(const TableDev* __restrict__ tables, uint32_t T, uint64_t B,
               const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ indices,
@@ -210,7 +221,8 @@ keygen_kernel(const TableDev* __restrict__ tables, uint32_t T, uint64_t B,
         const uint32_t l = s0 + q;  // bags are contiguous in table-major CSR
         const uint32_t idx = indices[l];
         if (idx >= Hk) atomicOr(err, 1u);
-        keys[l] = kbk + (idx < Hk ? idx : 0u);
+        const TableDev& tdk = tables[gk / B];
+        keys[l] = kbk + slot_of_entry(tdk, tdk.remap[idx < Hk ? idx : 0u]);
         vals[l] = uint32_t(gk % B);
       }
     }
@@ -329,6 +341,9 @@ struct rs_emb {
   bool staged_dirty = false;
   float* part = nullptr;
   float* spart = nullptr;
+  uint32_t* pcount = nullptr;  // [chunks + 1] pieces per chunk
+  uint32_t* pbase = nullptr;   // [chunks + 1] exclusive scan of pcount
+  uint4* pieces = nullptr;     // [max_lookups] piece descriptors
   uint32_t* d_meta = nullptr;
   uint32_t* h_meta = nullptr;
   size_t meta_words = 0;
@@ -348,6 +363,9 @@ struct rs_emb {
     if (vals) cudaFree(vals);
     if (part) cudaFree(part);
     if (spart) cudaFree(spart);
+    if (pcount) cudaFree(pcount);
+    if (pbase) cudaFree(pbase);
+    if (pieces) cudaFree(pieces);
     if (d_meta) cudaFree(d_meta);
     if (h_meta) cudaFreeHost(h_meta);
     if (d_err) cudaFree(d_err);
@@ -405,9 +423,9 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
       e->total_dim += x.dim;
       e->dmax = std::max(e->dmax, x.dim);
       e->table_ids.push_back(x.table_id);
-      if (key_acc + x.hash_size > 0x7FFFFFFFULL)
-        throw InvalidArgument("emb: sum of hash sizes must be < 2^31 per operator (split the tables)");
-      key_acc += x.hash_size;
+      if (key_acc + x.hbm_rows + x.slow_rows > 0x7FFFFFFFULL)
+        throw InvalidArgument("emb: sum of tier rows must be < 2^31 per operator (split the tables)");
+      key_acc += x.hbm_rows + x.slow_rows;
     }
     // Adagrad state (4 B/row) of BOTH tiers lives in HBM: a slow-tier row's
     // update then costs one PCIe row read + write instead of four transfers.
@@ -449,7 +467,7 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
       d.hbm_rows = x.hbm_rows;
       d.slow_rows = x.slow_rows;
       col += x.dim;
-      kb += uint32_t(x.hash_size);
+      kb += uint32_t(x.hbm_rows + x.slow_rows);  // key span = storage slots
       // every remap entry must land inside its tier's allocation
       RS_CUDA(cudaMemsetAsync(e->d_err, 0, 4, st));
       unsigned g = unsigned(std::min<uint64_t>((x.hash_size + 255) / 256, uint64_t(sm_count()) * 8));
@@ -506,10 +524,14 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
     RS_CUDA(cudaMalloc(&e->part, nch * 2 * e->dmax * 4));
     const size_t nsup = (nch + emb::kSuper - 1) / emb::kSuper;
     RS_CUDA(cudaMalloc(&e->spart, nsup * 2 * e->dmax * 4));
+    RS_CUDA(cudaMalloc(&e->pcount, (nch + 1) * 4));
+    RS_CUDA(cudaMalloc(&e->pbase, (nch + 1) * 4));
+    RS_CUDA(cudaMalloc(&e->pieces, L * sizeof(uint4)));
     e->sort_scratch_bytes = radix_sort_scratch_bytes(L) + (4 << 20);
     RS_CUDA(cudaMalloc(&e->sort_scratch, e->sort_scratch_bytes));
     // per-backward metadata: tpos[T+1] | cbase[T+1] | per class cls_cbase[n_c+1]
-    size_t meta = 2 * (size_t(T) + 1);
+    // | wstart[T+1] | wtab[T] (class-major chunk work map)
+    size_t meta = 2 * (size_t(T) + 1) + 2 * size_t(T) + 1;
     for (const auto& c : e->classes) meta += c.tables.size() + 1;
     e->meta_words = meta;
     RS_CUDA(cudaMalloc(&e->d_meta, meta * 4));
@@ -733,6 +755,26 @@ static void launch_chunk_v(rs_emb* e, const emb::BwdArgs& a, const rs_emb::Class
   RS_COUNT(1);
 }
 
+// Level 1, shared-memory staged (rows of <= 32 float4): one CTA per SM.
+template <int G>
+static void launch_chunk_smem(rs_emb* e, const emb::BwdArgs& a, const rs_emb::Class& c,
+                              const uint32_t* d_cls_cbase, uint64_t class_chunks) {
+  constexpr int NW = G >= 4 ? 6 : 4;
+  constexpr int NGRP = NW * (32 / G);
+  constexpr size_t smem = emb::chunk_smem_bytes<G, NW>();
+  static bool attr_set = false;
+  if (!attr_set) {
+    RS_CUDA(cudaFuncSetAttribute(emb::bwd_chunk_smem_kernel<G, NW>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr_set = true;
+  }
+  const unsigned g1 = unsigned(std::max<uint64_t>(
+      1, std::min<uint64_t>((class_chunks + NGRP - 1) / NGRP, uint64_t(sm_count()))));
+  emb::bwd_chunk_smem_kernel<G, NW><<<g1, NW * 32, smem, e->ctx->stream>>>(
+      a, c.d_list, d_cls_cbase, uint32_t(c.tables.size()));
+  RS_COUNT(1);
+}
+
 template <int G, int VPL>
 static void launch_chunk(rs_emb* e, const emb::BwdArgs& a, const rs_emb::Class& c,
                          const uint32_t* d_cls_cbase, uint64_t class_chunks) {
@@ -741,7 +783,11 @@ static void launch_chunk(rs_emb* e, const emb::BwdArgs& a, const rs_emb::Class& 
     const char* v = getenv("RS_BWD_VARIANT");
     return v ? atoi(v) : 0;
   }();
+  if constexpr (VPL == 1) {
+    if (variant == 0) return launch_chunk_smem<G>(e, a, c, d_cls_cbase, class_chunks);
+  }
   if constexpr (G >= 8 && VPL == 1) {
+    if (variant == 5) return launch_chunk_v<G, VPL, 8, 1>(e, a, c, d_cls_cbase, class_chunks);
     if (variant == 1) return launch_chunk_v<G, VPL, 4, 4>(e, a, c, d_cls_cbase, class_chunks);
     if (variant == 2) return launch_chunk_v<G, VPL, 4, 3>(e, a, c, d_cls_cbase, class_chunks);
     if (variant == 3) return launch_chunk_v<G, VPL, 2, 6>(e, a, c, d_cls_cbase, class_chunks);
@@ -749,6 +795,31 @@ static void launch_chunk(rs_emb* e, const emb::BwdArgs& a, const rs_emb::Class& 
   }
   constexpr int U = G >= 8 ? (VPL <= 2 ? 8 : (VPL == 4 ? 4 : 2)) : G;
   launch_chunk_v<G, VPL, U, 1>(e, a, c, d_cls_cbase, class_chunks);
+}
+
+// Level 1 bag pass for one lane class over its chunk work range [wlo, whi).
+template <int G, int VPL, int UNR, int MINB>
+static void launch_pieces_v(rs_emb* e, const emb::BwdArgs& a, uint32_t wlo, uint32_t whi) {
+  const unsigned grid = unsigned(sm_count()) * MINB;
+  emb::bwd_piece_kernel<G, VPL, UNR, MINB><<<grid, emb::kBwdThreads, 0, e->ctx->stream>>>(
+      a, e->pieces, e->pbase, wlo, whi);
+  RS_COUNT(1);
+}
+
+template <int G, int VPL>
+static void launch_pieces(rs_emb* e, const emb::BwdArgs& a, uint32_t wlo, uint32_t whi) {
+  static const int variant = [] {
+    const char* v = getenv("RS_PIECE_VARIANT");
+    return v ? atoi(v) : 0;
+  }();
+  if constexpr (VPL == 1) {
+    if (variant == 1) return launch_pieces_v<G, 1, 4, 3>(e, a, wlo, whi);
+    if (variant == 2) return launch_pieces_v<G, 1, 2, 6>(e, a, wlo, whi);
+    if (variant == 3) return launch_pieces_v<G, 1, 8, 2>(e, a, wlo, whi);
+    return launch_pieces_v<G, 1, 4, 4>(e, a, wlo, whi);
+  } else {
+    return launch_pieces_v<G, VPL, (VPL == 2 ? 2 : 1), 2>(e, a, wlo, whi);
+  }
 }
 
 // Levels 2 and 3 (full warps, VPL of the widest table).
@@ -813,6 +884,20 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
     class_chunks.push_back(w[c.tables.size()]);
     w += c.tables.size() + 1;
   }
+  // class-major work map for the piece scan
+  uint32_t* wstart = w;
+  uint32_t* wtab = w + T + 1;
+  {
+    uint32_t acc = 0, i = 0;
+    for (const auto& c : e->classes)
+      for (uint32_t t : c.tables) {
+        wstart[i] = acc;
+        wtab[i] = t;
+        acc += cbase[t + 1] - cbase[t];
+        ++i;
+      }
+    wstart[T] = acc;
+  }
   RS_CUDA(cudaMemcpyAsync(e->d_meta, e->h_meta, e->meta_words * 4, cudaMemcpyHostToDevice, st));
   RS_CUDA(cudaMemsetAsync(e->d_err, 0, 4, st));
   {
@@ -827,7 +912,42 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
   radix_sort_pairs(e->keys, e->vals, L, int(e->key_bits), scr, st);
   emb::BwdArgs a{e->cur_tables, T, e->d_meta, e->d_meta + T + 1, cbase[T], e->keys, e->vals,
                  grad, e->total_dim, e->part, e->spart, e->dmax, lr, e->eps, e->opt};
-  for (size_t ci = 0; ci < e->classes.size(); ++ci) {
+  static const int variant = [] {
+    const char* v = getenv("RS_BWD_VARIANT");
+    return v ? atoi(v) : 0;
+  }();
+  if (variant == 0) {
+    // level 1 as bags: list the pieces, then one bag pass per lane class
+    const uint32_t W = wstart[T];
+    const size_t woff = size_t(wstart - e->h_meta);
+    emb::WorkMap wm{e->d_meta + woff, e->d_meta + woff + T + 1, T};
+    const unsigned gs = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((uint64_t(W) + 7) / 8, uint64_t(sm_count()) * 16)));
+    emb::bwd_piece_scan_kernel<false><<<gs, 256, 0, st>>>(a, wm, e->pcount, nullptr, nullptr);
+    exclusive_scan<uint32_t>(ArrayIn<uint32_t>{e->pcount}, W, e->pbase, e->pbase + W, scr, st);
+    emb::bwd_piece_scan_kernel<true><<<gs, 256, 0, st>>>(a, wm, nullptr, e->pbase, e->pieces);
+    RS_COUNT(2);
+    uint32_t wlo = 0;
+    for (size_t ci = 0; ci < e->classes.size(); ++ci) {
+      const auto& c = e->classes[ci];
+      const uint32_t whi = wlo + uint32_t(class_chunks[ci]);
+      if (whi > wlo) {
+        switch (c.G * 100 + c.VPL) {
+          case 101: launch_pieces<1, 1>(e, a, wlo, whi); break;
+          case 201: launch_pieces<2, 1>(e, a, wlo, whi); break;
+          case 401: launch_pieces<4, 1>(e, a, wlo, whi); break;
+          case 801: launch_pieces<8, 1>(e, a, wlo, whi); break;
+          case 1601: launch_pieces<16, 1>(e, a, wlo, whi); break;
+          case 3201: launch_pieces<32, 1>(e, a, wlo, whi); break;
+          case 3202: launch_pieces<32, 2>(e, a, wlo, whi); break;
+          case 3204: launch_pieces<32, 4>(e, a, wlo, whi); break;
+          case 3208: launch_pieces<32, 8>(e, a, wlo, whi); break;
+          default: throw Error(-9, "emb_backward: unsupported lane class");
+        }
+      }
+      wlo = whi;
+    }
+  }
+  for (size_t ci = 0; ci < e->classes.size() && variant != 0; ++ci) {
     const auto& c = e->classes[ci];
     const uint32_t* dcb = e->d_meta + class_off[ci];
     switch (c.G * 100 + c.VPL) {

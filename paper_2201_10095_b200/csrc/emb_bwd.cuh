@@ -176,7 +176,7 @@ struct Pending {
     int32_t my_e = 0;
 #pragma unroll
     for (int s = 0; s < PEND; ++s)
-      if (s == lane && s < n) my_e = a.tables[tab[s]].remap[key[s] - a.tables[tab[s]].key_base];
+      if (s == lane && s < n) my_e = entry_of_key(a.tables[tab[s]], key[s]);
     float4 w[PEND][VPL];
     float mom[PEND];
 #pragma unroll
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) bwd_chunk_kernel(BwdArgs a,
         if (m == 0) break;
         const int u = __ffs(m) - 1;
         m &= m - 1;
-        if (lg == s) e = td.remap[sk[jb + u] - td.key_base];
+        if (lg == s) e = entry_of_key(td, sk[jb + u]);
       }
       return e;
     };
@@ -353,6 +353,251 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) bwd_chunk_kernel(BwdArgs a,
     // the last piece continues into the next chunk: tail edge piece (or the
     // whole chunk is the middle of a segment: head edge piece)
     if (!((tails >> (n - 1)) & 1u)) store_vec<G, VPL>(a.part + (gc * 2 + (heads == 0 ? 0 : 1)) * a.dmax, V, lg, acc);
+  }
+}
+
+// ---------------------------------------------------------------- level 1, dim <= 128
+// Shared-memory staged variant for rows of at most 32 float4 (one per lane of
+// a G-lane group).  A group takes a chunk and puts EVERY load of it in flight
+// at once with cp.async: the grad rows of all its positions, then (keys are
+// storage slots, so no remap load) the rows and Adagrad state of its complete
+// segments.  It then sums the pieces from shared memory in position order and
+// applies the updates.  Same reduction tree and arithmetic as
+// bwd_chunk_kernel; registers stay low, the loads have full memory-level
+// parallelism.  Shared memory per group: 2 x 32 x G float4 + 130 words.
+constexpr int kGroupWords = 130;  // sk[34] | sb[32] | se[32] | smo[32]
+
+template <int G, int NW>
+constexpr size_t chunk_smem_bytes() {
+  return size_t(NW) * (32 / G) * (2 * kChunk * G * sizeof(float4) + kGroupWords * 4);
+}
+
+template <int G, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
+bwd_chunk_smem_kernel(BwdArgs a, const uint32_t* cls_tables, const uint32_t* cls_cbase, uint32_t ncls) {
+  constexpr int GPW = 32 / G;
+  constexpr int NGRP = NW * GPW;
+  extern __shared__ float4 sm5[];
+  const int lane = threadIdx.x & 31, lg = lane % G;
+  const int gid = (threadIdx.x >> 5) * GPW + lane / G;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((lane / G) * G));
+  float4* gst = sm5 + size_t(gid) * (2 * kChunk * G);
+  float4* wst = gst + kChunk * G;
+  uint32_t* ub = reinterpret_cast<uint32_t*>(sm5 + size_t(NGRP) * 2 * kChunk * G) + gid * kGroupWords;
+  uint32_t* sk = ub + 1;  // sk[-1] = key before, sk[n] = key after
+  uint32_t* sb = ub + kChunk + 2;
+  int32_t* se = reinterpret_cast<int32_t*>(ub + 2 * kChunk + 2);
+  float* smo = reinterpret_cast<float*>(ub + 3 * kChunk + 2);
+  const bool ada = a.opt == RS_OPT_ROWWISE_ADAGRAD;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  const uint64_t nwork = cls_cbase[ncls];
+  const uint64_t ngroups = uint64_t(gridDim.x) * NGRP;
+  for (uint64_t wi = uint64_t(blockIdx.x) * NGRP + gid; wi < nwork; wi += ngroups) {
+    const uint32_t j = upper_index(cls_cbase, ncls, wi);
+    const uint32_t t = cls_tables[j];
+    const uint32_t k = uint32_t(wi - cls_cbase[j]);
+    const TableDev td = a.tables[t];
+    const uint32_t V = td.dim >> 2;
+    const bool lv = uint32_t(lg) < V;
+    const uint32_t tb = a.tpos[t], te = a.tpos[t + 1];
+    const uint32_t p0 = tb + k * kChunk;
+    const uint32_t n = min(uint32_t(kChunk), te - p0);
+    const uint64_t gc = uint64_t(a.cbase[t]) + k;
+    __syncwarp(gmask);  // the previous chunk's shared-memory reads are done
+    for (uint32_t i = lg; i <= uint32_t(kChunk); i += G) {
+      uint32_t kv = kNoKey;
+      if (i < n) kv = a.keys[p0 + i];
+      else if (i == n && p0 + n < te) kv = a.keys[p0 + n];  // key after (same table)
+      sk[i] = kv;
+      if (i < uint32_t(kChunk)) sb[i] = i < n ? a.vals[p0 + i] : 0u;
+    }
+    if (lg == 0) sk[-1] = p0 > tb ? a.keys[p0 - 1] : kNoKey;
+    __syncwarp(gmask);
+    // 1. every position's grad row (lane lg: float4 lg of the row)
+    if (lv) {
+      const float* gcol = a.grad + td.col + 4 * lg;
+#pragma unroll 8
+      for (uint32_t i = 0; i < n; ++i) cp_async16(gst + i * G + lg, gcol + uint64_t(sb[i]) * a.stride);
+    }
+    cp_async_commit();
+    // 2. segment heads / tails inside the chunk
+    unsigned heads = 0, tails = 0;
+#pragma unroll
+    for (int r = 0; r < kChunk / G; ++r) {
+      const uint32_t i = lg + r * G;
+      const uint32_t kk = sk[i];
+      const bool v = i < n;
+      const unsigned hb = __ballot_sync(gmask, v && kk != sk[i - 1]);
+      const unsigned tb2 = __ballot_sync(gmask, v && kk != sk[i + 1]);
+      const unsigned sh = (lane / G) * G;
+      heads |= ((hb >> sh) & (G == 32 ? 0xffffffffu : ((1u << G) - 1u))) << (r * G);
+      tails |= ((tb2 >> sh) & (G == 32 ? 0xffffffffu : ((1u << G) - 1u))) << (r * G);
+    }
+    const int fh = heads ? __ffs(heads) - 1 : 32;
+    const unsigned complete = fh >= 32 ? 0u : (tails & ~((1u << fh) - 1u));
+    const int ns = __popc(complete);
+    // 3. rows (+ state) of the complete segments, addressed by their slot keys
+    for (uint32_t i = lg; i < n; i += G) {
+      if ((complete >> i) & 1u) {
+        const int r = __popc(complete & ((1u << i) - 1u));
+        const int32_t e = entry_of_key(td, sk[i]);
+        se[r] = e;
+        if (ada) smo[r] = *mom_ptr(td, e);
+      }
+    }
+    __syncwarp(gmask);
+    if (lv)
+      for (int r = 0; r < ns; ++r) cp_async16(wst + r * G + lg, row_ptr(td, se[r]) + 4 * lg);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncwarp(gmask);
+    // 4. pieces in position order from +0.0f; complete segments update their row
+    float4 acc = zero;
+    int r = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+      if ((heads >> i) & 1u) acc = zero;
+      if (lv) add4(acc, gst[i * G + lg]);
+      if ((tails >> i) & 1u) {
+        float4 g1[1] = {acc};
+        if ((complete >> i) & 1u) {
+          float4 w1[1] = {lv ? wst[r * G + lg] : zero};
+          update_row<G, 1>(a, td, se[r], g1, w1, smo[r], gmask, lg);
+          ++r;
+        } else {
+          store_vec<G, 1>(a.part + (gc * 2) * a.dmax, V, lg, g1);  // began before: head edge
+        }
+      }
+    }
+    if (!((tails >> (n - 1)) & 1u)) {
+      float4 g1[1] = {acc};
+      store_vec<G, 1>(a.part + (gc * 2 + (heads == 0 ? 0 : 1)) * a.dmax, V, lg, g1);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- level 1 as bags
+// Level 1 restated as an EmbeddingBag over the grad matrix: every PIECE
+// (segment ∩ chunk) is a bag of <= 32 positions whose "indices" are the
+// samples of its lookups.  A scan pass (warp per chunk, lane per position)
+// lists the pieces; the bag pass gathers each piece's grad rows with the
+// forward's structure (G lanes per piece, UNR row loads in flight, in-order
+// fp32 adds from +0.0f) and either updates the row (the piece is a whole
+// segment: row and state loads are issued first, addressed by the slot key)
+// or stores the edge piece for level 2.  Same tree as bwd_chunk_kernel.
+constexpr uint32_t kPieceComplete = 0, kPieceSlot0 = 1, kPieceSlot1 = 2;
+
+// Chunk work index -> (table, chunk in table), tables in class-major order.
+struct WorkMap {
+  const uint32_t* wstart;  // [nt + 1] first work index of each table
+  const uint32_t* wtab;    // [nt] table index
+  uint32_t nt;
+};
+
+// WRITE = false: counts[wi] = pieces of chunk wi.  WRITE = true: pieces at
+// pbase[wi] (exclusive scan of counts) as {start, global chunk, table, type << 8 | len}.
+template <bool WRITE>
+__global__ void __launch_bounds__(256) bwd_piece_scan_kernel(BwdArgs a, WorkMap m, uint32_t* __restrict__ counts,
+                                                            const uint32_t* __restrict__ pbase,
+                                                            uint4* __restrict__ pieces) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nwork = m.wstart[m.nt];
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t wi = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; wi < nwork; wi += nwarps) {
+    const uint32_t i = upper_index(m.wstart, m.nt, wi);
+    const uint32_t t = m.wtab[i];
+    const uint32_t k = uint32_t(wi - m.wstart[i]);
+    const uint32_t tb = a.tpos[t], te = a.tpos[t + 1];
+    const uint32_t p0 = tb + k * kChunk;
+    const uint32_t n = min(uint32_t(kChunk), te - p0);
+    const bool v = uint32_t(lane) < n;
+    const uint32_t key = v ? a.keys[p0 + lane] : kNoKey;
+    uint32_t kp = __shfl_up_sync(0xffffffffu, key, 1);
+    if (lane == 0) kp = p0 > tb ? a.keys[p0 - 1] : kNoKey;
+    uint32_t kn = __shfl_down_sync(0xffffffffu, key, 1);
+    if (uint32_t(lane) == n - 1) kn = p0 + n < te ? a.keys[p0 + n] : kNoKey;
+    const bool head = v && key != kp;
+    const unsigned starts = __ballot_sync(0xffffffffu, v && (lane == 0 || head));
+    const unsigned tails = __ballot_sync(0xffffffffu, v && key != kn);
+    if (!WRITE) {
+      if (lane == 0) counts[wi] = __popc(starts);
+      continue;
+    }
+    if ((starts >> lane) & 1u) {
+      const unsigned rest = lane < 31 ? (starts >> (lane + 1)) : 0u;
+      const uint32_t e = rest ? uint32_t(lane) + __ffs(rest) : n;  // end (exclusive)
+      const uint32_t type = !head ? kPieceSlot0 : (((tails >> (e - 1)) & 1u) ? kPieceComplete : kPieceSlot1);
+      const uint32_t r = __popc(starts & lanemask_lt());
+      pieces[pbase[wi] + r] = make_uint4(p0 + lane, a.cbase[t] + k, t, (type << 8) | (e - lane));
+    }
+  }
+}
+
+template <int G, int VPL, int UNR, int MINB>
+__global__ void __launch_bounds__(kBwdThreads, MINB)
+bwd_piece_kernel(BwdArgs a, const uint4* __restrict__ pieces, const uint32_t* __restrict__ pbase,
+                 uint32_t w_lo, uint32_t w_hi) {
+  constexpr int BPW = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / G, lg = lane % G;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
+  const uint64_t p_lo = pbase[w_lo], p_hi = pbase[w_hi];
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const bool ada = a.opt == RS_OPT_ROWWISE_ADAGRAD;
+  uint32_t cur_t = 0xFFFFFFFFu;
+  TableDev td{};
+  for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; p_lo + w * BPW < p_hi; w += nwarps) {
+    const uint64_t pi = p_lo + w * BPW + grp;
+    const bool valid = pi < p_hi;
+    const uint4 d = valid ? pieces[pi] : make_uint4(0u, 0u, 0xFFFFFFFFu, 0u);
+    const uint32_t len = d.w & 0xFFu, type = d.w >> 8;
+    if (valid && d.z != cur_t) {
+      cur_t = d.z;
+      td = a.tables[cur_t];
+    }
+    const uint32_t V = td.dim >> 2;
+    const bool upd = valid && type == kPieceComplete;
+    // the row and its state first: the slot key addresses them directly
+    float4 w4[VPL];
+    float m_old = 0.f;
+    int32_t e = 0;
+    if (upd) {
+      e = entry_of_key(td, a.keys[d.x]);
+      const float4* wr = reinterpret_cast<const float4*>(row_ptr(td, e));
+#pragma unroll
+      for (int vv = 0; vv < VPL; ++vv) {
+        const uint32_t vec = lg + vv * G;
+        w4[vv] = vec < V ? wr[vec] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (ada) m_old = *mom_ptr(td, e);
+    }
+    float4 acc[VPL];
+#pragma unroll
+    for (int vv = 0; vv < VPL; ++vv) acc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t base = 0; base < len; base += G) {
+      const uint32_t nn = min(uint32_t(G), len - base);
+      const uint32_t smp = uint32_t(lg) < nn ? a.vals[d.x + base + lg] : 0u;
+      for (uint32_t j = 0; j < nn; j += UNR) {
+        float4 g[UNR][VPL];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const uint32_t bu = __shfl_sync(gmask, smp, int(j) + u, G);
+          const float4* gr = reinterpret_cast<const float4*>(a.grad + uint64_t(bu) * a.stride + td.col);
+#pragma unroll
+          for (int vv = 0; vv < VPL; ++vv) {
+            const uint32_t vec = lg + vv * G;
+            g[u][vv] = (j + u < nn && vec < V) ? ld_nc_f4(gr + vec) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+          if (j + u < nn) {
+#pragma unroll
+            for (int vv = 0; vv < VPL; ++vv) add4(acc[vv], g[u][vv]);
+          }
+      }
+    }
+    if (upd) update_row<G, VPL>(a, td, e, acc, w4, m_old, gmask, lg);
+    else if (valid) store_vec<G, VPL>(a.part + (uint64_t(d.y) * 2 + (type == kPieceSlot1)) * a.dmax, V, lg, acc);
   }
 }
 

@@ -101,7 +101,8 @@ def test_backward_matches_oracle(cuda_ctx, coracle, case, opt):
     mom = [np.zeros(s.hash_size, np.float32) for s in specs]
     for _ in range(2):
         coracle.emb_backward(B, dims, offsets.astype(np.uint64), idx, grad, Ws, mom,
-                             0 if opt == "sgd" else 1, lr, 1e-8)
+                             0 if opt == "sgd" else 1, lr, 1e-8,
+                             remaps=[(r.entries, r.hbm_rows) for r in remaps])
     for t, s in enumerate(specs):
         w, m = op.read_rows(t, np.arange(s.hash_size, dtype=np.uint32))
         # north_star tolerance: 1e-5 relative ...
