@@ -57,6 +57,8 @@ def parse():
                    help="HP1 sweep size (BASELINE configs[4]); 0 disables")
     p.add_argument("--cpu-profile-ids", type=float, default=5e7)
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-prefetch", action="store_true",
+                   help="headline in zero-copy mode only (no slow-row staging pipeline)")
     return p.parse_args()
 
 
@@ -76,50 +78,59 @@ def specs_for(name):
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock + throttle reasons sampled every few ms during the timed region
+    (NVML — the same counters as the recipe's nvidia-smi clocks line)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+             "sw_power_cap": 0x4}
 
-    def __init__(self, device):
-        self.device = device
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+    def __init__(self, device, period=0.005):
+        import threading
+
+        self.samples, self.reasons, self.mx = [], set(), None
+        self.stop_ev = threading.Event()
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
-                                      stdout=self.f, stderr=subprocess.DEVNULL)
+            import pynvml
+
+            pynvml.nvmlInit()
+            idx = device
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                try:
+                    idx = int(vis.split(",")[device])
+                except ValueError:
+                    idx = device
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nv = pynvml
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
         except Exception:
-            self.p = None
+            self.nv = None
+            return
+
+        def poll():
+            while not self.stop_ev.is_set():
+                try:
+                    self.samples.append(float(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)))
+                    r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    for n, bit in self.NAMES.items():
+                        if r & bit:
+                            self.reasons.add(n)
+                except Exception:
+                    pass
+                self.stop_ev.wait(period)
+
+        self.th = threading.Thread(target=poll, daemon=True)
+        self.th.start()
 
     def stop(self):
-        if self.p is None:
+        if self.nv is None:
             return None
-        self.p.terminate()
-        try:
-            self.p.wait(timeout=5)
-        except Exception:
-            self.p.kill()
-        self.f.seek(0)
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.f.read().splitlines():
-            c = [x.strip() for x in line.split(",")]
-            if len(c) < 9:
-                continue
-            try:
-                sm.append(float(c[1]))
-                mx = float(c[2])
-            except ValueError:
-                continue
-            for n, v in zip(names, c[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        os.unlink(self.f.name)
-        if not sm:
+        self.stop_ev.set()
+        self.th.join(timeout=2)
+        if not self.samples:
             return None
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.mx,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
 # ---------------------------------------------------------------------------- reference arm
@@ -266,10 +277,20 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
         from paper_2201_10095_b200.sharded import Exchange
 
         ex = Exchange(plan, [w.table.dim for w in specs], world, rank, B, dev)
-
+    # unique slow-tier rows per batch (sizes the HBM staging of the pipelined mode)
+    slow_u = 0
+    for off, idx, n in batches:
+        o = off.cpu().numpy().view(np.uint32).astype(np.int64)
+        u = 0
+        for t in range(T):
+            seg = idx[int(o[t * B]):int(o[(t + 1) * B])].long()
+            if seg.numel():
+                ent = remaps[t].entries[seg]
+                u += int(torch.unique(seg[ent < 0]).numel())
+        slow_u = max(slow_u, u)
     nvtx = os.environ.get("BENCH_NVTX") == "1"
 
-    def step(i, ev=None):
+    def step(i, cache, ev=None):
         if nvtx:
             torch.cuda.nvtx.range_push("bench_step")
         off, idx, n = batches[i % len(batches)] if T else (None, None, 0)
@@ -277,6 +298,9 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
             ev[0].record()
         if T:
             op.forward(off, idx, B, out=pooled, hits=hits)
+        if cache and i + 1 < cache:  # stage batch i+1's slow rows behind batch i's backward
+            nb = batches[(i + 1) % len(batches)]
+            op.prefetch(nb[0], nb[1], B)
         if ev:
             ev[1].record()
         g = pooled
@@ -292,42 +316,68 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
         if nvtx:
             torch.cuda.nvtx.range_pop()
 
-    for i in range(warmup):
-        step(i)
-    torch.cuda.synchronize()
-    hits.zero_()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks = Clocks(dev.index)
-    L0 = _lib.lib().rs_launch_counter()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
-    for i in range(steps):
-        if flush is not None:
-            flush.zero_()
-        step(i, evs[i])
-    torch.cuda.synchronize()
-    launches = int(_lib.lib().rs_launch_counter() - L0)
-    if world > 1:
-        dist.barrier()
-    clk = clocks.stop()
-    fwd_ms = [e[0].elapsed_time(e[1]) for e in evs]
-    a2a_ms = [e[1].elapsed_time(e[2]) for e in evs]
-    bwd_ms = [e[2].elapsed_time(e[3]) for e in evs]
-    step_ms = [e[0].elapsed_time(e[3]) for e in evs]
-    h = hits.cpu().numpy()
-    fast, slow = int(h[0::2][:T].sum()), int(h[1::2][:T].sum())
-    tot_ms = float(np.sum(step_ms))
-    if world > 1:
-        t = torch.tensor([tot_ms, fast, slow], dtype=torch.float64, device=dev)
-        mx = t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        tot_ms, fast, slow = float(mx[0]), int(t[1]), int(t[2])
-    res = dict(ms_per_step=tot_ms / steps, samples_per_s=B * steps / (tot_ms / 1e3),
-               uvm_pct=100.0 * slow / max(1, fast + slow), fast=fast, slow=slow,
-               fwd_ms=float(np.mean(fwd_ms)), bwd_ms=float(np.mean(bwd_ms)),
-               a2a_ms=float(np.mean(a2a_ms)), launches=launches, clocks=clk,
+    def run(nsteps, cache, evs=None):
+        """nsteps steps; with `cache`, batch 0's staging and the final write-back
+        are inside the run (every slow row is back in host memory at the end)."""
+        if cache and T:
+            op.prefetch(batches[0][0], batches[0][1], B)
+        for i in range(nsteps):
+            if flush is not None and evs is not None:
+                flush.zero_()
+            step(i, nsteps if cache else 0, evs[i] if evs else None)
+        if cache and T:
+            op.flush()
+
+    def timed(cache):
+        run(warmup, cache)
+        torch.cuda.synchronize()
+        hits.zero_()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clocks = Clocks(dev.index)
+        L0 = _lib.lib().rs_launch_counter()
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        run(steps, cache, evs)
+        t1.record()
+        torch.cuda.synchronize()
+        launches = int(_lib.lib().rs_launch_counter() - L0)
+        if world > 1:
+            dist.barrier()
+        clk = clocks.stop()
+        tot_ms = t0.elapsed_time(t1)
+        fwd_ms = [e[0].elapsed_time(e[1]) for e in evs]
+        a2a_ms = [e[1].elapsed_time(e[2]) for e in evs]
+        bwd_ms = [e[2].elapsed_time(e[3]) for e in evs]
+        h = hits.cpu().numpy()
+        fast, slow = int(h[0::2][:T].sum()), int(h[1::2][:T].sum())
+        if world > 1:
+            t = torch.tensor([tot_ms, fast, slow], dtype=torch.float64, device=dev)
+            mx = t.clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            tot_ms, fast, slow = float(mx[0]), int(t[1]), int(t[2])
+        return dict(ms_per_step=tot_ms / steps, samples_per_s=B * steps / (tot_ms / 1e3),
+                    uvm_pct=100.0 * slow / max(1, fast + slow), fast=fast, slow=slow,
+                    fwd_ms=float(np.mean(fwd_ms)), bwd_ms=float(np.mean(bwd_ms)),
+                    a2a_ms=float(np.mean(a2a_ms)), launches=launches, clocks=clk)
+
+    # zero-copy mode (the paper's UVM operator: slow rows read over PCIe inside
+    # the kernels), then the pipelined mode (slow rows staged in HBM one batch
+    # ahead on a side stream, written back behind the next batch)
+    zc = timed(0)
+    pipe = None
+    if T and slow_u and not args.no_prefetch:
+        op.enable_uvm_cache(int(2.5 * slow_u) + 4096)
+        if os.environ.get("BENCH_PROBE") == "1":
+            probe_cache(torch, op, batches, pooled, B)
+        pipe = timed(steps)
+    best = pipe if pipe is not None and pipe["samples_per_s"] > zc["samples_per_s"] else zc
+    res = dict(best)
+    res.update(mode="pipelined" if best is pipe else "zero-copy", zero_copy=zc, pipelined=pipe,
+               slow_unique_rows=slow_u,
                fwd_bytes=float(np.mean([fwd_bytes[i % len(batches)] for i in range(steps)])) if T else 0,
                bwd_bytes=float(np.mean([bwd_bytes[i % len(batches)] for i in range(steps)])) if T else 0,
                lookups=float(np.mean(lookups)) if T else 0,
@@ -347,7 +397,8 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
             abs(rep.uvm_access_fraction - hh[1::2].sum() / max(1, hh.sum())) == 0.0
             and rep.total_accesses == int(hh.sum()))
     if do_e2e and T:
-        res["e2e"] = run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex)
+        res["e2e"] = run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex,
+                             res["mode"] == "pipelined")
     if op:
         op.close()
     del remaps, batches
@@ -405,44 +456,108 @@ def run_profile_sweep(args, torch, ctx, hbm_peak):
     return out
 
 
-def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex):
-    """Same step through the public API with host inputs: pinned host offsets +
-    indices copied H2D every step, the hit counters (the step's UVM metric)
-    read back D2H."""
+def probe_cache(torch, op, batches, pooled, B):
+    """Diagnostics: each stage of the staged pipeline timed alone (synchronised)."""
+    def wall(f):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        f()
+        torch.cuda.synchronize()
+        return 1e3 * (time.perf_counter() - t0)
+    for k in range(3):
+        off, idx, n = batches[k % len(batches)]
+        out = {}
+        out["prefetch_ms"] = wall(lambda: op.prefetch(off, idx, B))
+        out["fwd_staged_ms"] = wall(lambda: op.forward(off, idx, B, out=pooled))
+        out["bwd_staged_ms"] = wall(lambda: op.backward(off, idx, pooled, B, LR))
+        out["writeback_flush_ms"] = wall(lambda: op.flush())
+        out["fwd_zero_copy_ms"] = wall(lambda: op.forward(off, idx, B, out=pooled))
+        out["bwd_zero_copy_ms"] = wall(lambda: op.backward(off, idx, pooled, B, LR))
+        print("probe", json.dumps(out), flush=True)
+
+
+def modes(r):
+    return {m: (None if r.get(k) is None else {x: r[k][x] for x in ("samples_per_s", "ms_per_step",
+                                                                  "fwd_ms", "bwd_ms")})
+            for m, k in (("zero-copy", "zero_copy"), ("pipelined", "pipelined"))}
+
+
+def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex, cache):
+    """Same step through the public API with host inputs: every step's offsets +
+    indices are copied from pinned host memory (a copy stream, two batches
+    ahead, triple-buffered — the data loader's overlap) and the hit counters
+    (the step's UVM metric) are read back D2H.  With `cache`, batch k+1's slow
+    rows are staged while batch k runs, as in the device-resident run."""
+    dev = pooled.device
     host = [(off.cpu().pin_memory(), idx[:max(1, n)].cpu().pin_memory(), n) for off, idx, n in batches]
-    d_off = torch.empty_like(batches[0][0])
-    d_idx = torch.empty(max(b[1].numel() for b in batches), dtype=torch.int32, device=pooled.device)
+    nb = 3
+    bufs = [(torch.empty_like(batches[0][0]),
+             torch.empty(max(b[1].numel() for b in batches), dtype=torch.int32, device=dev))
+            for _ in range(nb)]
+    cs = torch.cuda.Stream(device=dev)
+    main = torch.cuda.current_stream(dev)
+    ev_in = [torch.cuda.Event() for _ in range(nb)]
+    ev_free = [torch.cuda.Event() for _ in range(nb)]
+    used = [False] * nb
     h_hits = torch.empty(hits.numel(), dtype=torch.int64).pin_memory()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    bi = 0
+    bi = [0]
 
-    def one(i):
-        nonlocal bi
-        ho, hi, n = host[i % len(host)]
-        d_off.copy_(ho, non_blocking=True)
-        d_idx[:hi.numel()].copy_(hi, non_blocking=True)
-        bi = ho.numel() * 4 + hi.numel() * 4
-        op.forward(d_off, d_idx, B, out=pooled, hits=hits)
-        g = pooled
-        if ex is not None:
-            g = ex.to_tables(ex.to_owners(pooled))
-        op.backward(d_off, d_idx, g, B, LR)
-        h_hits.copy_(hits, non_blocking=True)
+    def h2d(k, total):
+        if k >= total:
+            return
+        b = k % nb
+        if used[b]:
+            cs.wait_event(ev_free[b])
+        ho, hi, n = host[k % len(host)]
+        with torch.cuda.stream(cs):
+            bufs[b][0].copy_(ho, non_blocking=True)
+            bufs[b][1][:hi.numel()].copy_(hi, non_blocking=True)
+        ev_in[b].record(cs)
+        bi[0] = ho.numel() * 4 + hi.numel() * 4
 
-    one(0)
+    def view(k):
+        b = k % nb
+        return bufs[b][0], bufs[b][1][:host[k % len(host)][1].numel()]
+
+    def run(total):
+        h2d(0, total)
+        h2d(1, total)
+        if cache:
+            main.wait_event(ev_in[0])
+            op.prefetch(*view(0), B)
+        for i in range(total):
+            h2d(i + 2, total)
+            main.wait_event(ev_in[i % nb])
+            d_off, d_idx = view(i)
+            op.forward(d_off, d_idx, B, out=pooled, hits=hits)
+            if cache and i + 1 < total:
+                main.wait_event(ev_in[(i + 1) % nb])
+                op.prefetch(*view(i + 1), B)
+            g = pooled
+            if ex is not None:
+                g = ex.to_tables(ex.to_owners(pooled))
+            op.backward(d_off, d_idx, g, B, LR)
+            h_hits.copy_(hits, non_blocking=True)
+            ev_free[i % nb].record(main)
+            used[i % nb] = True
+        if cache:
+            op.flush()
+
+    run(2)
     torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
-    for i in range(steps):
-        one(i)
+    run(steps)
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e)
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=pooled.device)
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t[0])
-    return {"value": B * steps / (ms / 1e3), "unit": "samples/s", "h2d_bytes_per_step": int(bi),
-            "d2h_bytes_per_step": int(h_hits.numel() * 8), "ms_per_step": ms / steps}
+    return {"value": B * steps / (ms / 1e3), "unit": "samples/s", "h2d_bytes_per_step": int(bi[0]),
+            "d2h_bytes_per_step": int(h_hits.numel() * 8), "ms_per_step": ms / steps,
+            "mode": "pipelined" if cache else "zero-copy"}
 
 
 def main():
@@ -563,12 +678,19 @@ def main():
             "plan": first.strategy, "planner_s": plan_s,
             "simulated_uvm_pct": sim_uvm,
             "uvm_matches_simulate": r.get("uvm_matches_simulate"),
-            "recshard": {k: r[k] for k in ("samples_per_s", "ms_per_step", "fwd_ms", "bwd_ms",
-                                           "lookups", "unique_rows",
-                                           "a2a_ms", "uvm_pct", "hbm_bytes", "host_bytes")},
-            "greedy": None if g is None else {k: g[k] for k in ("samples_per_s", "ms_per_step",
-                                                                 "fwd_ms", "bwd_ms", "uvm_pct")},
+            "operator_mode": r["mode"],
+            "recshard": dict({k: r[k] for k in ("samples_per_s", "ms_per_step", "fwd_ms", "bwd_ms",
+                                                "lookups", "unique_rows", "slow_unique_rows",
+                                                "a2a_ms", "uvm_pct", "hbm_bytes", "host_bytes")},
+                             modes=modes(r)),
+            "greedy": None if g is None else dict({k: g[k] for k in ("samples_per_s", "ms_per_step",
+                                                                     "fwd_ms", "bwd_ms", "uvm_pct",
+                                                                     "slow_unique_rows")},
+                                                  mode=g["mode"], modes=modes(g)),
             "recshard_vs_greedy": None if g is None else r["samples_per_s"] / g["samples_per_s"],
+            "recshard_vs_greedy_by_mode": None if g is None else {
+                m: (r[k]["samples_per_s"] / g[k]["samples_per_s"]) if r.get(k) and g.get(k) else None
+                for m, k in (("zero-copy", "zero_copy"), ("pipelined", "pipelined"))},
             "roofline": {"bound": "hbm", "kernel": "emb forward (gather-pool)",
                          "achieved": fwd_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": fwd_gbs / hbm_peak, "peak_kind": peak_kind,

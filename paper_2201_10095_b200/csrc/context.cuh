@@ -3,11 +3,53 @@
 // (SURVEY §8b threading contract).
 #pragma once
 
+#include <map>
+#include <memory>
+#include <mutex>
 #include <vector>
 
 #include "scan_sort.cuh"
 
+namespace rs {
+// Cache of pinned host blocks.  Results handed to the caller (profile rows /
+// CDFs) live in pinned memory so the D2H copies run at full PCIe speed;
+// cudaHostAlloc costs milliseconds per 100 MB, so blocks are recycled.
+// Shared by the context and the results that hold blocks, so either may go
+// first.
+struct PinnedPool {
+  std::mutex mu;
+  std::multimap<size_t, void*> free_blocks;
+  ~PinnedPool() {
+    for (auto& kv : free_blocks) cudaFreeHost(kv.second);
+  }
+  // returns a block of at least `bytes` (its capacity in *cap)
+  void* take(size_t bytes, size_t* cap) {
+    bytes = std::max<size_t>((bytes + 4095) & ~size_t(4095), 4096);
+    {
+      std::lock_guard<std::mutex> g(mu);
+      auto it = free_blocks.lower_bound(bytes);
+      if (it != free_blocks.end() && it->first <= 2 * bytes + (64 << 20)) {
+        void* p = it->second;
+        *cap = it->first;
+        free_blocks.erase(it);
+        return p;
+      }
+    }
+    void* p = nullptr;
+    RS_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocDefault));
+    *cap = bytes;
+    return p;
+  }
+  void give(void* p, size_t cap) {
+    if (!p) return;
+    std::lock_guard<std::mutex> g(mu);
+    free_blocks.emplace(cap, p);
+  }
+};
+}  // namespace rs
+
 struct rs_context {
+  std::shared_ptr<rs::PinnedPool> host_pool = std::make_shared<rs::PinnedPool>();
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;

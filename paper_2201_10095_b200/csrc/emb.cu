@@ -332,9 +332,12 @@ struct rs_emb {
   unsigned* ncopy = nullptr;
   unsigned* cache_err = nullptr;
   TableDev* d_tables_c = nullptr;
+  uint32_t* d_slow_tabs = nullptr;  // tables with slow rows
+  uint32_t nslow_tabs = 0;
   const TableDev* cur_tables = nullptr;  // tables the running forward/backward use
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_main = nullptr, ev_bwd = nullptr, ev_gather[2] = {nullptr, nullptr};
+  cudaEvent_t ev_main = nullptr, ev_bwd = nullptr, ev_wb = nullptr, ev_gather[2] = {nullptr, nullptr};
+  bool wb_recorded = false;
   std::vector<uint64_t> pending;  // prefetched generations, oldest first
   int64_t cur_gen = -1;           // staged generation of the running step (-1: zero-copy)
   uint64_t next_gen = 0;
@@ -374,11 +377,11 @@ struct rs_emb {
       cudaStreamSynchronize(side);
       cudaStreamDestroy(side);
     }
-    for (cudaEvent_t ev : {ev_main, ev_bwd, ev_gather[0], ev_gather[1]})
+    for (cudaEvent_t ev : {ev_main, ev_bwd, ev_wb, ev_gather[0], ev_gather[1]})
       if (ev) cudaEventDestroy(ev);
     for (void* p : {(void*)staging, (void*)slot_of, (void*)slot_gen, (void*)slot_tab, (void*)slot_row,
                     (void*)free_stack, (void*)copy_list, (void*)free_top, (void*)ncopy, (void*)cache_err,
-                    (void*)d_tables_c})
+                    (void*)d_tables_c, (void*)d_slow_tabs})
       if (p) cudaFree(p);
   }
 };
@@ -580,12 +583,36 @@ void emb_enable_cache(rs_emb* e, uint32_t nslots) {
   }
   RS_CUDA(cudaMalloc(&e->d_tables_c, sizeof(TableDev) * e->T));
   RS_CUDA(cudaMemcpyAsync(e->d_tables_c, tc.data(), sizeof(TableDev) * e->T, cudaMemcpyHostToDevice, st));
-  RS_CUDA(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
-  for (cudaEvent_t* ev : {&e->ev_main, &e->ev_bwd, &e->ev_gather[0], &e->ev_gather[1]})
+  {
+    std::vector<uint32_t> st_list;
+    for (uint32_t t = 0; t < e->T; ++t)
+      if (e->h_tables[t].slow_rows) st_list.push_back(t);
+    e->nslow_tabs = uint32_t(st_list.size());
+    RS_CUDA(cudaMalloc(&e->d_slow_tabs, std::max<size_t>(1, st_list.size()) * 4));
+    if (!st_list.empty())
+      RS_CUDA(cudaMemcpyAsync(e->d_slow_tabs, st_list.data(), st_list.size() * 4, cudaMemcpyHostToDevice, st));
+  }
+  // side stream for the PCIe gathers / write-backs (small grids: they hold
+  // few SM slots while the compute stream runs)
+  {
+    static const int prio_env = [] {
+      const char* v = getenv("RS_SIDE_PRIORITY");
+      return v ? atoi(v) : 0;
+    }();
+    int prio_lo = 0, prio_hi = 0;
+    RS_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    RS_CUDA(cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking,
+                                         prio_env < 0 ? prio_hi : (prio_env > 0 ? prio_lo : 0)));
+  }
+  for (cudaEvent_t* ev : {&e->ev_main, &e->ev_bwd, &e->ev_wb, &e->ev_gather[0], &e->ev_gather[1]})
     RS_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
   RS_CUDA(cudaStreamSynchronize(st));
   e->nslots = nslots;
 }
+
+// Side-stream PCIe kernels use few blocks: enough reads in flight for the
+// bus, few SM slots taken from the compute stream.
+constexpr unsigned kSideBlocks = 32;
 
 static unsigned cache_grid(uint64_t work) {
   return unsigned(std::max<uint64_t>(1, std::min<uint64_t>((work + 255) / 256, uint64_t(sm_count()) * 8)));
@@ -606,11 +633,13 @@ static void enqueue_writeback(rs_emb* e, uint64_t g) {
   for (uint64_t p : e->pending) keep |= 1u << (p & 1);
   RS_CUDA(cudaEventRecord(e->ev_bwd, e->ctx->stream));
   RS_CUDA(cudaStreamWaitEvent(e->side, e->ev_bwd, 0));
-  emb::uvm_writeback_kernel<<<cache_grid(uint64_t(e->nslots) * 32 / 32), 256, 0, e->side>>>(
+  emb::uvm_writeback_kernel<<<unsigned(std::min<uint64_t>(cache_grid(e->nslots), kSideBlocks)), 256, 0, e->side>>>(
       e->d_tables_c, e->nslots, 1u << (g & 1), keep, e->slot_gen, e->slot_tab, e->slot_row,
       e->free_stack, e->free_top, e->staging, e->dmax);
   RS_COUNT(1);
   RS_LAUNCH_CHECK();
+  RS_CUDA(cudaEventRecord(e->ev_wb, e->side));
+  e->wb_recorded = true;
 }
 
 void emb_prefetch(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx) {
@@ -622,14 +651,23 @@ void emb_prefetch(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
                                  [&](uint64_t p) { return (p & 1) == (g & 1); });
   if (clash) throw InvalidArgument("emb_prefetch: at most one batch may be prefetched ahead");
   ++e->next_gen;
-  // inputs are produced on the caller's stream
-  RS_CUDA(cudaEventRecord(e->ev_main, e->ctx->stream));
+  // The claim pass (index + remap read per lookup, an atomic per new slow
+  // row) is short and bandwidth-bound: it runs on the caller's stream, after
+  // the last write-back released its slots.  Only the PCIe gather of the new
+  // rows goes to the side stream, behind the caller's next kernels.
+  cudaStream_t st = e->ctx->stream;
+  if (e->wb_recorded) RS_CUDA(cudaStreamWaitEvent(st, e->ev_wb, 0));
+  RS_CUDA(cudaMemsetAsync(e->ncopy, 0, 4, st));
+  if (e->nslow_tabs) {
+    const uint64_t work = uint64_t(e->nslow_tabs) * ((B + 31) / 32);
+    emb::uvm_claim_kernel<<<unsigned(std::max<uint64_t>(1, std::min<uint64_t>((work + 7) / 8, uint64_t(sm_count()) * 8))),
+                            256, 0, st>>>(
+        e->d_tables_c, e->d_slow_tabs, e->nslow_tabs, B, off, idx, 1u << (g & 1), e->slot_gen,
+        e->slot_tab, e->slot_row, e->free_stack, e->free_top, e->copy_list, e->ncopy, e->cache_err);
+  }
+  RS_CUDA(cudaEventRecord(e->ev_main, st));
   RS_CUDA(cudaStreamWaitEvent(e->side, e->ev_main, 0));
-  RS_CUDA(cudaMemsetAsync(e->ncopy, 0, 4, e->side));
-  emb::uvm_claim_kernel<<<unsigned(uint64_t(sm_count()) * 8), 256, 0, e->side>>>(
-      e->d_tables_c, e->T, B, off, idx, 1u << (g & 1), e->slot_gen, e->slot_tab, e->slot_row,
-      e->free_stack, e->free_top, e->copy_list, e->ncopy, e->cache_err);
-  emb::uvm_fill_kernel<<<unsigned(uint64_t(sm_count()) * 8), 256, 0, e->side>>>(
+  emb::uvm_fill_kernel<<<kSideBlocks, 256, 0, e->side>>>(
       e->d_tables_c, e->slot_tab, e->slot_row, e->copy_list, e->ncopy, e->staging, e->dmax);
   RS_COUNT(2);
   RS_LAUNCH_CHECK();
@@ -800,7 +838,10 @@ static void launch_chunk(rs_emb* e, const emb::BwdArgs& a, const rs_emb::Class& 
 // Level 1 bag pass for one lane class over its chunk work range [wlo, whi).
 template <int G, int VPL, int UNR, int MINB>
 static void launch_pieces_v(rs_emb* e, const emb::BwdArgs& a, uint32_t wlo, uint32_t whi) {
-  const unsigned grid = unsigned(sm_count()) * MINB;
+  // several waves (not one persistent wave): blocks rebalance when a side
+  // stream holds SM slots.  Pieces <= 32 per chunk; typically ~8.
+  const uint64_t est = uint64_t(whi - wlo) * 8 / (uint64_t(emb::kBwdWarps) * (32 / G)) + 1;
+  const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(est, uint64_t(sm_count()) * MINB * 8)));
   emb::bwd_piece_kernel<G, VPL, UNR, MINB><<<grid, emb::kBwdThreads, 0, e->ctx->stream>>>(
       a, e->pieces, e->pbase, wlo, whi);
   RS_COUNT(1);

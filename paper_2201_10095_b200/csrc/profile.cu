@@ -12,6 +12,7 @@
 // CPU and GPU); the ICDF uses the reference's integer test
 // 100*prefix(k) >= i*total (core/src/profiler.cpp:38).
 #include <algorithm>
+#include <cstring>
 #include <numeric>
 
 #include "../../include/shardplan_gpu.h"
@@ -25,11 +26,47 @@ struct rs_profile {
   std::vector<uint64_t> distinct, total, present;
   std::vector<uint64_t> icdf;   // J * 101
   std::vector<uint64_t> start;  // J + 1 offsets into rows / cdf
-  std::vector<uint32_t> rows;
-  std::vector<double> cdf;
+  // rows_by_rank / access_cdf of all tables: pinned host copies (D2H straight
+  // from the rank kernels) and the device ranking (feeds build_remap)
+  // (pinned blocks come from / return to the context's pool; the device
+  // ranking is stream-ordered memory, so neither allocation nor release
+  // synchronises the device)
+  size_t nd = 0;
+  uint32_t* rows = nullptr;
+  double* cdf = nullptr;
   uint32_t* d_rows = nullptr;
+  size_t rows_cap = 0, cdf_cap = 0;
+  std::shared_ptr<rs::PinnedPool> pool;
+  cudaStream_t stream = nullptr;
   ~rs_profile() {
-    if (d_rows) cudaFree(d_rows);
+    if (d_rows) cudaFreeAsync(d_rows, stream);
+    if (pool) {
+      pool->give(rows, rows_cap);
+      pool->give(cdf, cdf_cap);
+    }
+  }
+  // grows the three arrays to hold n more entries (groups append in order)
+  void grow(size_t n, cudaStream_t st) {
+    const size_t m = std::max<size_t>(nd + n, 1);
+    size_t rc = 0, cc = 0;
+    auto* r2 = static_cast<uint32_t*>(pool->take(m * 4, &rc));
+    auto* c2 = static_cast<double*>(pool->take(m * 8, &cc));
+    uint32_t* d2 = nullptr;
+    RS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d2), m * 4, st));
+    if (nd) {
+      RS_CUDA(cudaStreamSynchronize(st));
+      memcpy(r2, rows, nd * 4);
+      memcpy(c2, cdf, nd * 8);
+      RS_CUDA(cudaMemcpyAsync(d2, d_rows, nd * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    if (d_rows) RS_CUDA(cudaFreeAsync(d_rows, st));
+    pool->give(rows, rows_cap);
+    pool->give(cdf, cdf_cap);
+    rows = r2;
+    cdf = c2;
+    d_rows = d2;
+    rows_cap = rc;
+    cdf_cap = cc;
   }
 };
 
@@ -80,43 +117,86 @@ struct Tables {
   uint32_t t_lo, t_hi;    // table-index range counted by this launch
 };
 
-// K1.  Each warp takes 32 records, scans their (selected) lengths, then walks
-// the flattened id stream 32 ids at a time so every lane has work and the id
-// loads are coalesced whenever records are contiguous (the generator's
-// layout).  AGG: warp-aggregate same-row increments with match.any before the
-// global atomic, which takes the Zipf head off the L2 atomic unit.
-template <bool RAW, bool AGG>
+// K1.  Each warp takes 32 records (sample selection, table lookup, length),
+// scans their lengths, and expands them into a shared-memory map of the
+// warp's flattened id stream: for every id its table and its position in the
+// ids array (32 lanes write one record at a time, so any length mix costs
+// ~2 stores per 32 ids).  The ids are then processed 32 at a time with
+// coalesced loads and no per-id record search.
+//
+// Zipf heads: same-address atomics serialise in the L2 atomic unit
+// (B300_MICROARCH.md: "LTS atomic-ALU serializes per-address"), so one hot
+// row hammered from every SM bounds the whole pass.  Large calls therefore
+// run in two phases: a sample of the records (1/64) is counted straight into
+// the global counters; rows whose sample count reaches a threshold form the
+// HOT set (at most kHotMax rows — the Zipf head); the rest of the records run
+// with the hot set in a per-CTA shared-memory hash (read-only keys, no CAS)
+// whose counters take the hot increments, flushed once per CTA at the end.
+// Other rows are counted with global atomics (no contention: the tail is
+// spread).  Integer adds commute, so counts are exact and order-independent.
+constexpr int kHotSlots = 4096;  // power of two
+constexpr int kHotMax = kHotSlots / 2;
+constexpr uint32_t kHotEmpty = 0xFFFFFFFFu;
+constexpr int kWin = 256;         // ids per warp window of the expansion map
+constexpr int kHistWarps = kHistThreads / 32;
+
+__device__ __forceinline__ uint32_t hot_hash(uint32_t addr) { return (addr * 2654435761u) >> 20; }
+
+template <bool RAW, bool HOT>
 __global__ void __launch_bounds__(kHistThreads)
 hash_hist(const uint64_t* __restrict__ rec_sample, const uint32_t* __restrict__ rec_table,
           const uint64_t* __restrict__ rec_offset, const uint32_t* __restrict__ rec_len,
-          uint64_t R, const uint32_t* __restrict__ ids, const uint64_t* __restrict__ raw,
-          Tables tp, double rate, uint64_t seed, bool count_records,
-          uint32_t* __restrict__ counters, unsigned long long* __restrict__ present,
-          unsigned long long* __restrict__ accesses, unsigned* __restrict__ err) {
+          uint64_t r_lo, uint64_t r_hi, const uint32_t* __restrict__ ids,
+          const uint64_t* __restrict__ raw, Tables tp, double rate, uint64_t seed,
+          bool count_records, const uint32_t* __restrict__ hot_list,
+          const unsigned* __restrict__ n_hot, uint32_t* __restrict__ counters,
+          unsigned long long* __restrict__ present, unsigned long long* __restrict__ accesses,
+          unsigned* __restrict__ err, int dbg) {
   extern __shared__ uint32_t sm[];
+  uint32_t* hkeys = sm;
+  uint32_t* hvals = sm + (HOT ? kHotSlots : 0);
+  uint32_t* mtab = sm + (HOT ? 2 * kHotSlots : 0);       // [warps][kWin] table index
+  uint32_t* msrc = mtab + kHistWarps * kWin;              // [warps][kWin] ids position
   const bool use_sm = count_records && tp.J <= kMaxSmemTables;
-  uint32_t* pres_s = sm;
-  uint32_t* acc_s = sm + (use_sm ? tp.J : 0);
+  uint32_t* pres_s = msrc + kHistWarps * kWin;
+  uint32_t* acc_s = pres_s + (use_sm ? tp.J : 0);
+  if (HOT) {
+    for (uint32_t i = threadIdx.x; i < kHotSlots; i += blockDim.x) {
+      hkeys[i] = kHotEmpty;
+      hvals[i] = 0;
+    }
+  }
   if (use_sm)
-    for (uint32_t i = threadIdx.x; i < 2 * tp.J; i += blockDim.x) sm[i] = 0;
+    for (uint32_t i = threadIdx.x; i < 2 * tp.J; i += blockDim.x) pres_s[i] = 0;
   __syncthreads();
+  if (HOT) {
+    const uint32_t nh = min(*n_hot, uint32_t(kHotMax));
+    for (uint32_t i = threadIdx.x; i < nh; i += blockDim.x) {
+      const uint32_t a = hot_list[i];
+      uint32_t h = hot_hash(a);
+      while (atomicCAS(&hkeys[h], kHotEmpty, a) != kHotEmpty) h = (h + 1) & (kHotSlots - 1);
+    }
+    __syncthreads();
+  }
 
   const int lane = threadIdx.x & 31;
+  uint32_t* wtab = mtab + (threadIdx.x >> 5) * kWin;
+  uint32_t* wsrc = msrc + (threadIdx.x >> 5) * kWin;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t c = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; c * 32 < R;
+  for (uint64_t c = r_lo / 32 + ((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); c * 32 < r_hi;
        c += nwarps) {
     const uint64_t r = c * 32 + lane;
     uint32_t len = 0;
-    uint64_t off = 0;
+    uint32_t off = 0;
     int t = 0;
-    if (r < R && sample_selected(rec_sample[r], rate, seed)) {
+    if (r >= r_lo && r < r_hi && sample_selected(rec_sample[r], rate, seed)) {
       t = lookup_table(tp.sorted_ids, tp.sorted_idx, tp.J, rec_table[r]);
       if (t < 0) {
         atomicOr(err, kErrUnknownTable);
         t = 0;
       } else {
         len = rec_len[r];
-        off = rec_offset[r];
+        off = uint32_t(rec_offset[r]);  // < 2^32 ids per call (checked on the host)
         if (count_records) {
           if (use_sm) {
             atomicAdd(&pres_s[t], 1u);
@@ -132,48 +212,77 @@ hash_hist(const uint64_t* __restrict__ rec_sample, const uint32_t* __restrict__ 
     const uint32_t incl = warp_incl_scan(len);
     const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
     const uint32_t excl = incl - len;
-    for (uint32_t p = 0; p < total; p += 32) {
-      const uint32_t q = p + lane;
-      int k = 0;
-#pragma unroll
-      for (int step = 16; step >= 1; step >>= 1) {
-        uint32_t e = __shfl_sync(0xffffffffu, excl, k + step);
-        if (e <= q) k += step;
+    for (uint32_t w0 = 0; w0 < total; w0 += kWin) {
+      const uint32_t w1 = min(total, w0 + uint32_t(kWin));
+      // expand: record k's ids inside [w0, w1)
+      __syncwarp();
+      for (int k = 0; k < 32; ++k) {
+        const uint32_t ek = __shfl_sync(0xffffffffu, excl, k);
+        const uint32_t lk = __shfl_sync(0xffffffffu, len, k);
+        const uint32_t ok = __shfl_sync(0xffffffffu, off, k);
+        const int tk = __shfl_sync(0xffffffffu, t, k);
+        const uint32_t s = max(ek, w0), e = min(ek + lk, w1);
+        for (uint32_t q = s + lane; q < e; q += 32) {
+          wtab[q - w0] = uint32_t(tk);
+          wsrc[q - w0] = ok + (q - ek);
+        }
       }
-      const uint64_t offk = __shfl_sync(0xffffffffu, off, k);
-      const uint32_t exk = __shfl_sync(0xffffffffu, excl, k);
-      const int tk = __shfl_sync(0xffffffffu, t, k);
-      bool ok = q < total;
-      uint64_t addr = 0;
-      if (ok) {
-        const uint64_t idx = offk + (q - exk);
+      __syncwarp();
+      for (uint32_t q = w0 + lane; q < w1; q += 32) {
+        const uint32_t tk = wtab[q - w0];
+        const uint32_t idx = wsrc[q - w0];
         const uint64_t H = tp.hsize[tk];
         uint64_t row;
         if (RAW) row = fast_mod(mix64(raw[idx]), H, tp.magic[tk]);
         else row = ld_stream_u32(ids + idx);
         if (row >= H) {
           atomicOr(err, kErrRowRange);
-          ok = false;
+          continue;
+        }
+        const uint32_t addr = uint32_t(tp.base[tk] + row);
+        if (HOT) {
+          uint32_t h = hot_hash(addr);
+          while (true) {
+            const uint32_t kk = hkeys[h];
+            if (kk == addr) {
+              if (!(dbg & 2)) atomicAdd(&hvals[h], 1u);
+              break;
+            }
+            if (kk == kHotEmpty) {
+              if (!(dbg & 1)) atomicAdd(&counters[addr], 1u);
+              break;
+            }
+            h = (h + 1) & (kHotSlots - 1);
+          }
         } else {
-          addr = tp.base[tk] + row;
+          atomicAdd(&counters[addr], 1u);
         }
-      }
-      if (AGG) {
-        const unsigned am = __ballot_sync(0xffffffffu, ok);
-        if (ok) {
-          const unsigned peers = __match_any_sync(am, addr);
-          if ((peers & lanemask_lt()) == 0) atomicAdd(&counters[addr], uint32_t(__popc(peers)));
-        }
-      } else if (ok) {
-        atomicAdd(&counters[addr], 1u);
       }
     }
+  }
+  if (HOT) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < kHotSlots; i += blockDim.x)
+      if (hvals[i]) atomicAdd(&counters[hkeys[i]], hvals[i]);
   }
   if (use_sm) {
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < tp.J; i += blockDim.x) {
       if (pres_s[i]) atomicAdd(&present[i], (unsigned long long)pres_s[i]);
       if (acc_s[i]) atomicAdd(&accesses[i], (unsigned long long)acc_s[i]);
+    }
+  }
+}
+
+// Hot-set selection after the sample phase: rows with count >= thr (group-local
+// addresses), appended up to kHotMax.
+__global__ void hot_select(const uint32_t* __restrict__ counters, uint64_t n, uint32_t thr,
+                          uint32_t* __restrict__ hot_list, unsigned* __restrict__ n_hot) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    if (counters[i] >= thr) {
+      const unsigned k = atomicAdd(n_hot, 1u);
+      if (k < unsigned(kHotMax)) hot_list[k] = uint32_t(i);
     }
   }
 }
@@ -394,6 +503,11 @@ __global__ void icdf_kernel(const uint64_t* __restrict__ cum_excl, const uint64_
   icdf[size_t(t) * 101 + p] = lo;
 }
 
+template <class K>
+inline void set_smem_attr(K kern, size_t bytes) {
+  if (bytes > 48 * 1024) RS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+}
+
 struct RankDevice {
   uint32_t* rows;     // n
   double* cdf;        // n
@@ -551,6 +665,8 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
   }
 
   auto* res = new rs_profile;
+  res->pool = ctx->host_pool;
+  res->stream = st;
   res->J = J;
   res->table_ids.resize(J);
   res->coverage.resize(J);
@@ -564,8 +680,6 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
     std::vector<uint64_t> h_tot(J), h_pres(J);
     unsigned h_err = 0;
     unsigned long long h_sel = 0;
-    std::vector<std::vector<uint32_t>> g_rows;
-    std::vector<std::vector<double>> g_cdf;
     for (size_t g = 0; g + 1 < gstart.size(); ++g) {
       const uint32_t t_lo = gstart[g], t_hi = gstart[g + 1], Jg = t_hi - t_lo;
       size_t mark = scr.used;
@@ -579,16 +693,42 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
       const uint64_t warps = (R + 31) / 32;
       unsigned grid = unsigned(std::min<uint64_t>((warps + 7) / 8, uint64_t(sms) * 8));
       grid = std::max(1u, grid);
-      size_t smem = J <= kMaxSmemTables ? size_t(J) * 8 : 0;
+      const size_t rsm = (J <= kMaxSmemTables ? size_t(J) * 8 : 0) + size_t(2) * kHistWarps * kWin * 4;
       const bool cr = g == 0;
-      if (raw)
-        hash_hist<true, true><<<grid, kHistThreads, smem, st>>>(d_rs, d_rt, d_ro, d_rl, R, d_ids,
-                                                               d_raw, tp, rate, seed, cr, d_cnt,
-                                                               d_pres, d_acc, d_err);
-      else
-        hash_hist<false, true><<<grid, kHistThreads, smem, st>>>(d_rs, d_rt, d_ro, d_rl, R, d_ids,
-                                                                d_raw, tp, rate, seed, cr, d_cnt,
-                                                                d_pres, d_acc, d_err);
+      auto run = [&](auto kern, uint64_t lo, uint64_t hi, size_t smem, const uint32_t* hl, const unsigned* nh) {
+        set_smem_attr(kern, smem);
+        static const int dbg = getenv("RS_HIST_DBG") ? atoi(getenv("RS_HIST_DBG")) : 0;
+        kern<<<grid, kHistThreads, smem, st>>>(d_rs, d_rt, d_ro, d_rl, lo, hi, d_ids, d_raw, tp, rate, seed, cr,
+                                               hl, nh, d_cnt, d_pres, d_acc, d_err, dbg);
+        RS_COUNT(1);
+      };
+      // two phases when the call is large enough for a sample to find the head
+      const uint64_t Rs = N >= (uint64_t(1) << 22) && R >= 64 * 32 ? (R / 64 + 31) / 32 * 32 : R;
+      if (Rs < R) {
+        uint32_t* d_hot = scr.take<uint32_t>(kHotMax);
+        unsigned* d_nh = scr.take<unsigned>(1);
+        RS_CUDA(cudaMemsetAsync(d_nh, 0, 4, st));
+        if (raw) run(hash_hist<true, false>, 0, Rs, rsm, nullptr, nullptr);
+        else run(hash_hist<false, false>, 0, Rs, rsm, nullptr, nullptr);
+        // expected sample ids ~ N * Rs / R: rows at >= 1/8192 of the sample
+        const uint32_t thr = uint32_t(std::max<uint64_t>(8, uint64_t(double(N) * double(Rs) / double(R) / 8192.0)));
+        const unsigned gs = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((base_g[Jg] + 255) / 256, uint64_t(sms) * 8)));
+        hot_select<<<gs, 256, 0, st>>>(d_cnt, base_g[Jg], thr, d_hot, d_nh);
+        RS_COUNT(1);
+        if (getenv("RS_HIST_DEBUG")) {
+          unsigned nh = 0;
+          RS_CUDA(cudaMemcpyAsync(&nh, d_nh, 4, cudaMemcpyDeviceToHost, st));
+          ctx->sync();
+          fprintf(stderr, "hist: R=%llu Rs=%llu N=%llu thr=%u n_hot=%u\n", (unsigned long long)R,
+                  (unsigned long long)Rs, (unsigned long long)N, thr, nh);
+        }
+        const size_t smem = 2 * kHotSlots * 4 + rsm;
+        if (raw) run(hash_hist<true, true>, Rs, R, smem, d_hot, d_nh);
+        else run(hash_hist<false, true>, Rs, R, smem, d_hot, d_nh);
+      } else {
+        if (raw) run(hash_hist<true, false>, 0, R, rsm, nullptr, nullptr);
+        else run(hash_hist<false, false>, 0, R, rsm, nullptr, nullptr);
+      }
       RS_LAUNCH_CHECK();
       if (g == 0) {
         // errors, selection and per-table totals are known after the first group
@@ -612,27 +752,23 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
       }
       RankDevice rk = rank_group(ctx, scr, d_cnt, base_g, Jg, d_acc + t_lo);
       std::vector<uint64_t> tstart(Jg + 1);
-      g_rows.emplace_back(rk.n);
-      g_cdf.emplace_back(rk.n);
+      const size_t at = res->nd;
+      res->grow(rk.n, st);
       RS_CUDA(cudaMemcpyAsync(tstart.data(), rk.tstart, (Jg + 1) * 8, cudaMemcpyDeviceToHost, st));
       RS_CUDA(cudaMemcpyAsync(res->icdf.data() + size_t(t_lo) * 101, rk.icdf,
                               size_t(Jg) * 101 * 8, cudaMemcpyDeviceToHost, st));
       if (rk.n) {
-        RS_CUDA(cudaMemcpyAsync(g_rows.back().data(), rk.rows, rk.n * 4, cudaMemcpyDeviceToHost, st));
-        RS_CUDA(cudaMemcpyAsync(g_cdf.back().data(), rk.cdf, rk.n * 8, cudaMemcpyDeviceToHost, st));
+        RS_CUDA(cudaMemcpyAsync(res->rows + at, rk.rows, rk.n * 4, cudaMemcpyDeviceToHost, st));
+        RS_CUDA(cudaMemcpyAsync(res->cdf + at, rk.cdf, rk.n * 8, cudaMemcpyDeviceToHost, st));
+        RS_CUDA(cudaMemcpyAsync(res->d_rows + at, rk.rows, rk.n * 4, cudaMemcpyDeviceToDevice, st));
       }
+      res->nd = at + rk.n;
       ctx->sync();
       for (uint32_t j = t_lo; j < t_hi; ++j) res->distinct[j] = tstart[j - t_lo + 1] - tstart[j - t_lo];
       scr.used = mark;
     }
     // assemble (tables are group-contiguous, so concatenation keeps order)
     for (uint32_t j = 0; j < J; ++j) res->start[j + 1] = res->start[j] + res->distinct[j];
-    res->rows.reserve(res->start[J]);
-    res->cdf.reserve(res->start[J]);
-    for (size_t g = 0; g < g_rows.size(); ++g) {
-      res->rows.insert(res->rows.end(), g_rows[g].begin(), g_rows[g].end());
-      res->cdf.insert(res->cdf.end(), g_cdf[g].begin(), g_cdf[g].end());
-    }
     res->selected = h_sel;
     for (uint32_t j = 0; j < J; ++j) {  // profiler.cpp:114-121
       res->table_ids[j] = tr->tables[j].table_id;
@@ -641,10 +777,7 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
       res->coverage[j] = double(h_pres[j]) / double(h_sel);
       res->avg_pooling[j] = h_pres[j] ? double(h_tot[j]) / double(h_pres[j]) : 0.0;
     }
-    const size_t nd = res->rows.size();
-    RS_CUDA(cudaMalloc(&res->d_rows, (nd ? nd : 1) * 4));
-    if (nd)
-      RS_CUDA(cudaMemcpyAsync(res->d_rows, res->rows.data(), nd * 4, cudaMemcpyHostToDevice, st));
+    if (!res->d_rows) res->grow(0, st);
     ctx->sync();
   } catch (...) {
     delete res;
@@ -759,8 +892,8 @@ void profile_view(const rs_profile* p, uint32_t j, rs_feature_stats* o) {
   o->distinct_rows_accessed = p->distinct[j];
   o->total_accesses = p->total[j];
   o->icdf_steps = p->icdf.data() + size_t(j) * 101;
-  o->access_cdf = p->cdf.data() + p->start[j];
-  o->rows_by_rank = p->rows.data() + p->start[j];
+  o->access_cdf = p->cdf + p->start[j];
+  o->rows_by_rank = p->rows + p->start[j];
   o->d_rows_by_rank = p->d_rows + p->start[j];
 }
 

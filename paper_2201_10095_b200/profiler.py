@@ -80,11 +80,39 @@ def trace_struct(trace: Trace):
     return st, (arrs, specs)
 
 
-class Profile:
-    """Owning handle of one profile() result; ``stats`` are host copies and
-    ``device_rows_by_rank(j)`` exposes the device ranking (feeds build_remap)."""
+class _Owner:
+    """Owns one rs_profile; freed when the Profile and every array viewing its
+    pinned buffers are gone (the stats arrays are zero-copy views)."""
 
     def __init__(self, h):
+        self.h = h
+
+    def __del__(self):  # pragma: no cover - interpreter teardown
+        try:
+            if self.h:
+                _lib.lib().rs_profile_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def _view(owner, p, n, ctype, dtype):
+    """numpy view of n elements at ctypes pointer p that keeps `owner` alive."""
+    if n == 0:
+        return np.zeros(0, dtype)
+    arr = (ctype * n).from_address(C.cast(p, C.c_void_p).value)
+    arr._owner = owner
+    return np.frombuffer(arr, dtype=dtype)
+
+
+class Profile:
+    """Handle of one profile() result.  ``stats`` hold zero-copy numpy views of
+    the pinned host arrays the kernels wrote (no host-side copy of the
+    per-row CDFs/rankings); ``device_rows_by_rank(j)`` exposes the device
+    ranking (feeds build_remap)."""
+
+    def __init__(self, h):
+        self._owner = _Owner(h)
         self.h = h
         L = _lib.lib()
         n = C.c_uint32()
@@ -99,28 +127,23 @@ class Profile:
             _lib.check(L.rs_profile_get(h, j, C.byref(v)))
             d = int(v.distinct_rows_accessed)
             icdf = np.ctypeslib.as_array(v.icdf_steps, shape=(101,)).copy()
-            cdf = (np.ctypeslib.as_array(v.access_cdf, shape=(d,)).copy() if d
-                   else np.zeros(0, np.float64))
-            rbr = (np.ctypeslib.as_array(v.rows_by_rank, shape=(d,)).copy() if d
-                   else np.zeros(0, np.uint32))
+            cdf = _view(self._owner, v.access_cdf, d, C.c_double, np.float64)
+            rbr = _view(self._owner, v.rows_by_rank, d, C.c_uint32, np.uint32)
             self.stats.append(FeatureStats(int(v.table_id), float(v.coverage),
                                            float(v.avg_pooling), d, int(v.total_accesses),
                                            icdf, cdf, rbr))
             self._dev.append(v.d_rows_by_rank)
 
     def device_rows_by_rank(self, j):
+        if self._owner is None:
+            raise ValueError("profile handle closed")
         return self._dev[j]
 
     def close(self):
-        if self.h:
-            _lib.lib().rs_profile_destroy(self.h)
-            self.h = None
-
-    def __del__(self):  # pragma: no cover
-        try:
-            self.close()
-        except Exception:
-            pass
+        """Drops this handle's reference; the buffers are freed once no stats
+        array views them any more."""
+        self._owner = None
+        self.h = None
 
 
 def profile_handle(trace: Trace, sample_rate: float, seed: int, ctx=None) -> Profile:
