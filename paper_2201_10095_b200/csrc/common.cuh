@@ -92,10 +92,23 @@ __device__ __forceinline__ float4 ld_nc_f4(const float4* p) {
   return r;
 }
 
-// Streaming 4-byte load that does not allocate in L1.
+// Streaming loads: no L1 allocation, and L2 evict-first so a large input
+// stream does not push resident working sets (counters, remaps) out of L2.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
   uint32_t r;
-  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+               : "=r"(r) : "l"(p), "l"(l2_evict_first_policy()));
+  return r;
+}
+__device__ __forceinline__ uint64_t ld_stream_u64(const uint64_t* p) {
+  uint64_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;"
+               : "=l"(r) : "l"(p), "l"(l2_evict_first_policy()));
   return r;
 }
 

@@ -134,13 +134,13 @@ struct Tables {
 // whose counters take the hot increments, flushed once per CTA at the end.
 // Other rows are counted with global atomics (no contention: the tail is
 // spread).  Integer adds commute, so counts are exact and order-independent.
-constexpr int kHotSlots = 4096;  // power of two
+constexpr int kHotSlots = 8192;  // power of two
 constexpr int kHotMax = kHotSlots / 2;
 constexpr uint32_t kHotEmpty = 0xFFFFFFFFu;
 constexpr int kWin = 256;         // ids per warp window of the expansion map
 constexpr int kHistWarps = kHistThreads / 32;
 
-__device__ __forceinline__ uint32_t hot_hash(uint32_t addr) { return (addr * 2654435761u) >> 20; }
+__device__ __forceinline__ uint32_t hot_hash(uint32_t addr) { return (addr * 2654435761u) >> 19; }
 
 template <bool RAW, bool HOT>
 __global__ void __launch_bounds__(kHistThreads)
@@ -151,7 +151,7 @@ hash_hist(const uint64_t* __restrict__ rec_sample, const uint32_t* __restrict__ 
           bool count_records, const uint32_t* __restrict__ hot_list,
           const unsigned* __restrict__ n_hot, uint32_t* __restrict__ counters,
           unsigned long long* __restrict__ present, unsigned long long* __restrict__ accesses,
-          unsigned* __restrict__ err, int dbg) {
+          unsigned* __restrict__ err) {
   extern __shared__ uint32_t sm[];
   uint32_t* hkeys = sm;
   uint32_t* hvals = sm + (HOT ? kHotSlots : 0);
@@ -228,34 +228,49 @@ hash_hist(const uint64_t* __restrict__ rec_sample, const uint32_t* __restrict__ 
         }
       }
       __syncwarp();
-      for (uint32_t q = w0 + lane; q < w1; q += 32) {
-        const uint32_t tk = wtab[q - w0];
-        const uint32_t idx = wsrc[q - w0];
-        const uint64_t H = tp.hsize[tk];
-        uint64_t row;
-        if (RAW) row = fast_mod(mix64(raw[idx]), H, tp.magic[tk]);
-        else row = ld_stream_u32(ids + idx);
-        if (row >= H) {
-          atomicOr(err, kErrRowRange);
-          continue;
+      // all of the window's id loads in flight, then the counts
+      constexpr int IPW = kWin / 32;
+      uint32_t addr[IPW];
+      bool ok[IPW];
+#pragma unroll
+      for (int u = 0; u < IPW; ++u) {
+        const uint32_t q = w0 + lane + 32 * u;
+        ok[u] = q < w1;
+        addr[u] = 0;
+        if (ok[u]) {
+          const uint32_t tk = wtab[q - w0];
+          const uint32_t idx = wsrc[q - w0];
+          const uint64_t H = tp.hsize[tk];
+          uint64_t row;
+          if (RAW) row = fast_mod(mix64(ld_stream_u64(raw + idx)), H, tp.magic[tk]);
+          else row = ld_stream_u32(ids + idx);
+          if (row >= H) {
+            atomicOr(err, kErrRowRange);
+            ok[u] = false;
+          } else {
+            addr[u] = uint32_t(tp.base[tk] + row);
+          }
         }
-        const uint32_t addr = uint32_t(tp.base[tk] + row);
+      }
+#pragma unroll
+      for (int u = 0; u < IPW; ++u) {
+        if (!ok[u]) continue;
         if (HOT) {
-          uint32_t h = hot_hash(addr);
+          uint32_t h = hot_hash(addr[u]);
           while (true) {
             const uint32_t kk = hkeys[h];
-            if (kk == addr) {
-              if (!(dbg & 2)) atomicAdd(&hvals[h], 1u);
+            if (kk == addr[u]) {
+              atomicAdd(&hvals[h], 1u);
               break;
             }
             if (kk == kHotEmpty) {
-              if (!(dbg & 1)) atomicAdd(&counters[addr], 1u);
+              atomicAdd(&counters[addr[u]], 1u);
               break;
             }
             h = (h + 1) & (kHotSlots - 1);
           }
         } else {
-          atomicAdd(&counters[addr], 1u);
+          atomicAdd(&counters[addr[u]], 1u);
         }
       }
     }
@@ -697,9 +712,8 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
       const bool cr = g == 0;
       auto run = [&](auto kern, uint64_t lo, uint64_t hi, size_t smem, const uint32_t* hl, const unsigned* nh) {
         set_smem_attr(kern, smem);
-        static const int dbg = getenv("RS_HIST_DBG") ? atoi(getenv("RS_HIST_DBG")) : 0;
         kern<<<grid, kHistThreads, smem, st>>>(d_rs, d_rt, d_ro, d_rl, lo, hi, d_ids, d_raw, tp, rate, seed, cr,
-                                               hl, nh, d_cnt, d_pres, d_acc, d_err, dbg);
+                                               hl, nh, d_cnt, d_pres, d_acc, d_err);
         RS_COUNT(1);
       };
       // two phases when the call is large enough for a sample to find the head
@@ -710,18 +724,11 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
         RS_CUDA(cudaMemsetAsync(d_nh, 0, 4, st));
         if (raw) run(hash_hist<true, false>, 0, Rs, rsm, nullptr, nullptr);
         else run(hash_hist<false, false>, 0, Rs, rsm, nullptr, nullptr);
-        // expected sample ids ~ N * Rs / R: rows at >= 1/8192 of the sample
-        const uint32_t thr = uint32_t(std::max<uint64_t>(8, uint64_t(double(N) * double(Rs) / double(R) / 8192.0)));
+        // expected sample ids ~ N * Rs / R: rows at >= 1/32768 of the sample
+        const uint32_t thr = uint32_t(std::max<uint64_t>(8, uint64_t(double(N) * double(Rs) / double(R) / 32768.0)));
         const unsigned gs = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((base_g[Jg] + 255) / 256, uint64_t(sms) * 8)));
         hot_select<<<gs, 256, 0, st>>>(d_cnt, base_g[Jg], thr, d_hot, d_nh);
         RS_COUNT(1);
-        if (getenv("RS_HIST_DEBUG")) {
-          unsigned nh = 0;
-          RS_CUDA(cudaMemcpyAsync(&nh, d_nh, 4, cudaMemcpyDeviceToHost, st));
-          ctx->sync();
-          fprintf(stderr, "hist: R=%llu Rs=%llu N=%llu thr=%u n_hot=%u\n", (unsigned long long)R,
-                  (unsigned long long)Rs, (unsigned long long)N, thr, nh);
-        }
         const size_t smem = 2 * kHotSlots * 4 + rsm;
         if (raw) run(hash_hist<true, true>, Rs, R, smem, d_hot, d_nh);
         else run(hash_hist<false, true>, Rs, R, smem, d_hot, d_nh);
