@@ -838,10 +838,8 @@ static void launch_chunk(rs_emb* e, const emb::BwdArgs& a, const rs_emb::Class& 
 // Level 1 bag pass for one lane class over its chunk work range [wlo, whi).
 template <int G, int VPL, int UNR, int MINB>
 static void launch_pieces_v(rs_emb* e, const emb::BwdArgs& a, uint32_t wlo, uint32_t whi) {
-  // several waves (not one persistent wave): blocks rebalance when a side
-  // stream holds SM slots.  Pieces <= 32 per chunk; typically ~8.
   const uint64_t est = uint64_t(whi - wlo) * 8 / (uint64_t(emb::kBwdWarps) * (32 / G)) + 1;
-  const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(est, uint64_t(sm_count()) * MINB * 8)));
+  const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(est, uint64_t(sm_count()) * MINB)));
   emb::bwd_piece_kernel<G, VPL, UNR, MINB><<<grid, emb::kBwdThreads, 0, e->ctx->stream>>>(
       a, e->pieces, e->pbase, wlo, whi);
   RS_COUNT(1);

@@ -494,7 +494,7 @@ struct WorkMap {
 };
 
 // WRITE = false: counts[wi] = pieces of chunk wi.  WRITE = true: pieces at
-// pbase[wi] (exclusive scan of counts) as {start, global chunk, table, type << 8 | len}.
+// pbase[wi] (exclusive scan of counts) as {start, global chunk, key, table << 8 | type << 6 | len - 1}.
 template <bool WRITE>
 __global__ void __launch_bounds__(256) bwd_piece_scan_kernel(BwdArgs a, WorkMap m, uint32_t* __restrict__ counts,
                                                             const uint32_t* __restrict__ pbase,
@@ -527,7 +527,8 @@ __global__ void __launch_bounds__(256) bwd_piece_scan_kernel(BwdArgs a, WorkMap 
       const uint32_t e = rest ? uint32_t(lane) + __ffs(rest) : n;  // end (exclusive)
       const uint32_t type = !head ? kPieceSlot0 : (((tails >> (e - 1)) & 1u) ? kPieceComplete : kPieceSlot1);
       const uint32_t r = __popc(starts & lanemask_lt());
-      pieces[pbase[wi] + r] = make_uint4(p0 + lane, a.cbase[t] + k, t, (type << 8) | (e - lane));
+      // {first position, global chunk, slot key, table << 8 | type << 6 | (len - 1)}
+      pieces[pbase[wi] + r] = make_uint4(p0 + lane, a.cbase[t] + k, key, (t << 8) | (type << 6) | (e - lane - 1));
     }
   }
 }
@@ -545,13 +546,20 @@ bwd_piece_kernel(BwdArgs a, const uint4* __restrict__ pieces, const uint32_t* __
   const bool ada = a.opt == RS_OPT_ROWWISE_ADAGRAD;
   uint32_t cur_t = 0xFFFFFFFFu;
   TableDev td{};
-  for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; p_lo + w * BPW < p_hi; w += nwarps) {
+  uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  // the next piece's descriptor is loaded while this one runs
+  uint4 dn = p_lo + w * BPW + grp < p_hi ? pieces[p_lo + w * BPW + grp] : make_uint4(0u, 0u, 0u, 0xFFFFFFFFu);
+  for (; p_lo + w * BPW < p_hi; w += nwarps) {
     const uint64_t pi = p_lo + w * BPW + grp;
     const bool valid = pi < p_hi;
-    const uint4 d = valid ? pieces[pi] : make_uint4(0u, 0u, 0xFFFFFFFFu, 0u);
-    const uint32_t len = d.w & 0xFFu, type = d.w >> 8;
-    if (valid && d.z != cur_t) {
-      cur_t = d.z;
+    const uint4 d = dn;
+    {
+      const uint64_t pn = pi + nwarps * BPW;
+      dn = pn < p_hi ? pieces[pn] : make_uint4(0u, 0u, 0u, 0xFFFFFFFFu);
+    }
+    const uint32_t len = (d.w & 63u) + 1, type = (d.w >> 6) & 3u, tt = d.w >> 8;
+    if (valid && tt != cur_t) {
+      cur_t = tt;
       td = a.tables[cur_t];
     }
     const uint32_t V = td.dim >> 2;
@@ -561,7 +569,7 @@ bwd_piece_kernel(BwdArgs a, const uint4* __restrict__ pieces, const uint32_t* __
     float m_old = 0.f;
     int32_t e = 0;
     if (upd) {
-      e = entry_of_key(td, a.keys[d.x]);
+      e = entry_of_key(td, d.z);
       const float4* wr = reinterpret_cast<const float4*>(row_ptr(td, e));
 #pragma unroll
       for (int vv = 0; vv < VPL; ++vv) {
@@ -573,7 +581,7 @@ bwd_piece_kernel(BwdArgs a, const uint4* __restrict__ pieces, const uint32_t* __
     float4 acc[VPL];
 #pragma unroll
     for (int vv = 0; vv < VPL; ++vv) acc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (uint32_t base = 0; base < len; base += G) {
+    for (uint32_t base = 0; valid && base < len; base += G) {
       const uint32_t nn = min(uint32_t(G), len - base);
       const uint32_t smp = uint32_t(lg) < nn ? a.vals[d.x + base + lg] : 0u;
       for (uint32_t j = 0; j < nn; j += UNR) {
