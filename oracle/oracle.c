@@ -291,8 +291,8 @@ static int cmp_lk(const void* a, const void* b) {
   return x->l < y->l ? -1 : (x->l > y->l);
 }
 
-#define OR_CHUNK 32 /* csrc/emb_bwd.cuh kChunk */
-#define OR_SUPER 64 /* csrc/emb_bwd.cuh kSuper (chunks per superchunk) */
+#define OR_CHUNK 32 /* csrc/emb_bwd.cuh kChunk (positions per piece) */
+#define OR_GROUP 64 /* csrc/emb_bwd.cuh kGroupPieces (pieces per group) */
 
 int or_emb_backward(uint32_t T, uint64_t B, const uint32_t* D,
                     const uint64_t* H, const uint64_t* col_off,
@@ -306,26 +306,18 @@ int or_emb_backward(uint32_t T, uint64_t B, const uint32_t* D,
   uint64_t* kb = (uint64_t*)malloc(sizeof(uint64_t) * (T + 1));
   kb[0] = 0;
   for (uint32_t t = 0; t < T; ++t) kb[t + 1] = kb[t] + H[t];
-  /* chunks restart at each table's first sorted position tpos[t] =
-   * offsets[t*B]; global chunk ids cb[t] + (pos - tpos[t]) / OR_CHUNK */
-  uint64_t* cb = (uint64_t*)malloc(sizeof(uint64_t) * (T + 1));
-  cb[0] = 0;
-  for (uint32_t t = 0; t < T; ++t) {
-    const uint64_t lt = offsets[(uint64_t)(t + 1) * B] - offsets[(uint64_t)t * B];
-    cb[t + 1] = cb[t] + (lt + OR_CHUNK - 1) / OR_CHUNK;
-  }
   lk_t* lk = (lk_t*)malloc(sizeof(lk_t) * L);
   uint64_t* bag = (uint64_t*)malloc(sizeof(uint64_t) * L);
   uint32_t* tab = (uint32_t*)malloc(sizeof(uint32_t) * L);
   for (uint32_t t = 0; t < T; ++t)
     for (uint64_t b = 0; b < B; ++b)
       for (uint64_t l = offsets[t * B + b]; l < offsets[t * B + b + 1]; ++l) {
-        if (indices[l] >= H[t]) { free(cb); free(kb); free(lk); free(bag); free(tab); return ST_INVALID; }
+        if (indices[l] >= H[t]) { free(kb); free(lk); free(bag); free(tab); return ST_INVALID; }
         uint64_t slot = indices[l];
         if (remap) {
           const int32_t e = remap[t][indices[l]];
           slot = e >= 0 ? (uint64_t)e : hbm_rows[t] + (uint64_t)(-(int64_t)e - 1);
-          if (slot >= H[t]) { free(cb); free(kb); free(lk); free(bag); free(tab); return ST_INVALID; }
+          if (slot >= H[t]) { free(kb); free(lk); free(bag); free(tab); return ST_INVALID; }
         }
         lk[l].key = kb[t] + slot;
         lk[l].l = l;
@@ -346,41 +338,36 @@ int or_emb_backward(uint32_t T, uint64_t B, const uint32_t* D,
     const uint32_t d = D[t];
     uint64_t e = i;
     while (e < L && lk[e].key == key) ++e;
-    /* The kernel's reduction order: the segment [i, e) of the sorted list is
-     * cut at multiples of OR_CHUNK; every piece is summed in sorted order
-     * from +0.0f, and the pieces are then added left to right (the first
-     * piece is the accumulator). */
-    /* level 2/3: pieces of one superchunk (OR_CHUNK*OR_SUPER positions) are
-     * summed left to right (first piece = accumulator) into a group sum; the
-     * group sums are then summed left to right (first = accumulator). */
-    int first_group = 1, first_piece = 1;
-    uint64_t p = i, group = (uint64_t)-1;
+    /* The kernel's reduction tree (csrc/emb_bwd.cuh), anchored at the
+     * segment's first sorted position i, length L = e - i: pieces of
+     * OR_CHUNK positions from i, each summed in sorted order from +0.0f; for
+     * L <= OR_CHUNK the single piece is g.  Otherwise groups of OR_GROUP
+     * consecutive pieces are added left to right (first piece as the
+     * accumulator) and g = the group sums left to right (first as the
+     * accumulator). */
+    int first_group = 1;
+    uint64_t p = i;
     while (p < e) {
-      const uint64_t tp = offsets[(uint64_t)t * B];
-      uint64_t pe = tp + ((p - tp) / OR_CHUNK + 1) * OR_CHUNK;
-      if (pe > e) pe = e;
-      for (uint32_t k = 0; k < d; ++k) piece[k] = 0.0f;
-      for (uint64_t q = p; q < pe; ++q) {
-        const float* go = grad_out + bag[lk[q].l] * grad_stride + col_off[t];
-        for (uint32_t k = 0; k < d; ++k) piece[k] = piece[k] + go[k];
-      }
-      const uint64_t grp = (cb[t] + (p - tp) / OR_CHUNK) / OR_SUPER;
-      if (grp != group) {
-        if (group != (uint64_t)-1) { /* close the previous group into g */
-          if (first_group) memcpy(g, gs, sizeof(float) * d);
-          else for (uint32_t k = 0; k < d; ++k) g[k] = g[k] + gs[k];
-          first_group = 0;
+      uint64_t ge = p + (uint64_t)OR_CHUNK * OR_GROUP;
+      if (ge > e) ge = e;
+      int first_piece = 1;
+      for (uint64_t q0 = p; q0 < ge; q0 += OR_CHUNK) {
+        uint64_t pe = q0 + OR_CHUNK;
+        if (pe > ge) pe = ge;
+        for (uint32_t k = 0; k < d; ++k) piece[k] = 0.0f;
+        for (uint64_t q = q0; q < pe; ++q) {
+          const float* go = grad_out + bag[lk[q].l] * grad_stride + col_off[t];
+          for (uint32_t k = 0; k < d; ++k) piece[k] = piece[k] + go[k];
         }
-        group = grp;
-        first_piece = 1;
+        if (first_piece) memcpy(gs, piece, sizeof(float) * d);
+        else for (uint32_t k = 0; k < d; ++k) gs[k] = gs[k] + piece[k];
+        first_piece = 0;
       }
-      if (first_piece) memcpy(gs, piece, sizeof(float) * d);
-      else for (uint32_t k = 0; k < d; ++k) gs[k] = gs[k] + piece[k];
-      first_piece = 0;
-      p = pe;
+      if (first_group) memcpy(g, gs, sizeof(float) * d);
+      else for (uint32_t k = 0; k < d; ++k) g[k] = g[k] + gs[k];
+      first_group = 0;
+      p = ge;
     }
-    if (first_group) memcpy(g, gs, sizeof(float) * d);
-    else for (uint32_t k = 0; k < d; ++k) g[k] = g[k] + gs[k];
     float* w = W[t] + (uint64_t)row * d;
     if (opt == 0) {
       for (uint32_t k = 0; k < d; ++k) {
@@ -406,6 +393,5 @@ int or_emb_backward(uint32_t T, uint64_t B, const uint32_t* D,
   free(bag);
   free(lk);
   free(kb);
-  free(cb);
   return ST_OK;
 }

@@ -102,15 +102,13 @@ int or_emb_forward(uint32_t T, uint64_t B, const uint32_t* D,
  * row's storage slot in the operator's tiers (csrc/emb.cu keygen_kernel):
  * remap entry e >= 0 -> e, e < 0 -> hbm_rows[t] + (-e - 1)
  * (include/shardplan/remap.hpp:27-29 encoding).  remap == NULL means the
- * identity placement (slot = row).  For each distinct
- * (table, row) the gradient g = sum of grad_out[b, col_off[t] : +D] over its
- * lookups, accumulated in fp32 in the kernel's fixed tree
- * (csrc/emb_bwd.cuh): table t's lookups occupy sorted positions from
- * tpos = offsets[t*B]; the row's run is cut every 32 positions counted from
- * tpos (chunk id = chunks of earlier tables + (pos - tpos) / 32); each piece
- * is summed in sorted order from +0.0f; the pieces whose chunk ids fall in one
- * 64-chunk superchunk are added left to right (first piece as the
- * accumulator), and the superchunk sums are added left to right (first as the
+ * identity placement (slot = row).  For each distinct (table, slot) — a
+ * SEGMENT of the sorted list starting at position s, length L — the gradient
+ * g = sum of grad_out[b, col_off[t] : +D] over its lookups, accumulated in
+ * fp32 in the kernel's fixed tree (csrc/emb_bwd.cuh): pieces of 32 positions
+ * from s, each summed in sorted order from +0.0f (L <= 32: g is that sum);
+ * groups of 64 consecutive pieces added left to right (first piece as the
+ * accumulator); g = the group sums left to right (first as the
  * accumulator).  Then
  *   opt 0 (row-wise SGD):  w[d] = w[d] - lr*g[d]
  *   opt 1 (exact row-wise Adagrad, FBGEMM semantics):

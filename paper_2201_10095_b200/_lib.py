@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libshardplan_gpu.so")
+LIB_PATH = os.environ.get("RS_LIB_PATH") or os.path.join(_HERE, "libshardplan_gpu.so")
 
 RS_OK = 0
 RS_ERR_INVALID_ARGUMENT = -1

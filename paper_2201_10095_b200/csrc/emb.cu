@@ -342,11 +342,18 @@ struct rs_emb {
   int64_t cur_gen = -1;           // staged generation of the running step (-1: zero-copy)
   uint64_t next_gen = 0;
   bool staged_dirty = false;
-  float* part = nullptr;
-  float* spart = nullptr;
-  uint32_t* pcount = nullptr;  // [chunks + 1] pieces per chunk
-  uint32_t* pbase = nullptr;   // [chunks + 1] exclusive scan of pcount
-  uint4* pieces = nullptr;     // [max_lookups] piece descriptors
+  uint32_t* scount = nullptr;  // [windows + 1] segment heads per window
+  uint32_t* sbase = nullptr;   // [windows + 1] exclusive scan of scount
+  uint4* segs = nullptr;       // [max_lookups] segment descriptors
+  size_t long_cap = 0;         // long segments (> 32 positions) <= lookups / 33
+  uint4* longs = nullptr;
+  uint32_t* long_np = nullptr;  // [long_cap + 1] pieces per long segment
+  uint32_t* long_ng = nullptr;  // [long_cap + 1] groups per long segment
+  uint32_t* pbase = nullptr;    // [long_cap + 1] exclusive scan of long_np
+  uint32_t* gbase = nullptr;    // [long_cap + 1] exclusive scan of long_ng
+  unsigned* n_long = nullptr;
+  float* ppart = nullptr;       // [pieces][dmax] piece sums of long segments
+  float* gpart = nullptr;       // [groups][dmax] group sums of long segments
   uint32_t* d_meta = nullptr;
   uint32_t* h_meta = nullptr;
   size_t meta_words = 0;
@@ -364,11 +371,9 @@ struct rs_emb {
     if (d_key_base_sorted) cudaFree(d_key_base_sorted);
     if (keys) cudaFree(keys);
     if (vals) cudaFree(vals);
-    if (part) cudaFree(part);
-    if (spart) cudaFree(spart);
-    if (pcount) cudaFree(pcount);
-    if (pbase) cudaFree(pbase);
-    if (pieces) cudaFree(pieces);
+    for (void* p : {(void*)scount, (void*)sbase, (void*)segs, (void*)longs, (void*)long_np, (void*)long_ng,
+                    (void*)pbase, (void*)gbase, (void*)n_long, (void*)ppart, (void*)gpart})
+      if (p) cudaFree(p);
     if (d_meta) cudaFree(d_meta);
     if (h_meta) cudaFreeHost(h_meta);
     if (d_err) cudaFree(d_err);
@@ -523,19 +528,26 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
     const size_t L = std::max<uint64_t>(max_lookups, 1);
     RS_CUDA(cudaMalloc(&e->keys, L * 4));
     RS_CUDA(cudaMalloc(&e->vals, L * 4));
-    const size_t nch = (L + emb::kChunk - 1) / emb::kChunk + T;  // per-table rounding
-    RS_CUDA(cudaMalloc(&e->part, nch * 2 * e->dmax * 4));
-    const size_t nsup = (nch + emb::kSuper - 1) / emb::kSuper;
-    RS_CUDA(cudaMalloc(&e->spart, nsup * 2 * e->dmax * 4));
-    RS_CUDA(cudaMalloc(&e->pcount, (nch + 1) * 4));
-    RS_CUDA(cudaMalloc(&e->pbase, (nch + 1) * 4));
-    RS_CUDA(cudaMalloc(&e->pieces, L * sizeof(uint4)));
+    const size_t nch = (L + emb::kChunk - 1) / emb::kChunk + T;  // windows (per-table rounding)
+    RS_CUDA(cudaMalloc(&e->scount, (nch + 1) * 4));
+    RS_CUDA(cudaMalloc(&e->sbase, (nch + 1) * 4));
+    RS_CUDA(cudaMalloc(&e->segs, L * sizeof(uint4)));
+    e->long_cap = L / (emb::kChunk + 1) + 1;
+    RS_CUDA(cudaMalloc(&e->longs, e->long_cap * sizeof(uint4)));
+    RS_CUDA(cudaMalloc(&e->long_np, (e->long_cap + 1) * 4));
+    RS_CUDA(cudaMalloc(&e->long_ng, (e->long_cap + 1) * 4));
+    RS_CUDA(cudaMalloc(&e->pbase, (e->long_cap + 1) * 4));
+    RS_CUDA(cudaMalloc(&e->gbase, (e->long_cap + 1) * 4));
+    RS_CUDA(cudaMalloc(&e->n_long, 4));
+    const size_t max_pieces = L / emb::kChunk + e->long_cap + 1;
+    const size_t max_groups = L / (emb::kChunk * emb::kGroupPieces) + e->long_cap + 1;
+    RS_CUDA(cudaMalloc(&e->ppart, max_pieces * e->dmax * 4));
+    RS_CUDA(cudaMalloc(&e->gpart, max_groups * e->dmax * 4));
     e->sort_scratch_bytes = radix_sort_scratch_bytes(L) + (4 << 20);
     RS_CUDA(cudaMalloc(&e->sort_scratch, e->sort_scratch_bytes));
-    // per-backward metadata: tpos[T+1] | cbase[T+1] | per class cls_cbase[n_c+1]
-    // | wstart[T+1] | wtab[T] (class-major chunk work map)
-    size_t meta = 2 * (size_t(T) + 1) + 2 * size_t(T) + 1;
-    for (const auto& c : e->classes) meta += c.tables.size() + 1;
+    // per-backward metadata: tpos[T+1] | wstart[T+1] | wtab[T] (class-major
+    // window work map)
+    const size_t meta = 3 * size_t(T) + 2;
     e->meta_words = meta;
     RS_CUDA(cudaMalloc(&e->d_meta, meta * 4));
     RS_CUDA(cudaHostAlloc(&e->h_meta, meta * 4, cudaHostAllocDefault));
@@ -773,103 +785,33 @@ void emb_forward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx
   RS_LAUNCH_CHECK();
 }
 
-// Level 1 for one (G, VPL) table class.
-template <int G, int VPL, int U, int MINB>
-static void launch_chunk_v(rs_emb* e, const emb::BwdArgs& a, const rs_emb::Class& c,
-                           const uint32_t* d_cls_cbase, uint64_t class_chunks) {
-  constexpr int NGRP = emb::kBwdWarps * (32 / G);
-  const int stage_bytes = NGRP * U * G * VPL * int(sizeof(float4)) +
-                          NGRP * (2 * emb::kChunk + 2) * int(sizeof(uint32_t));
-  static bool attr_set = false;
-  if (!attr_set) {
-    RS_CUDA(cudaFuncSetAttribute(emb::bwd_chunk_kernel<G, VPL, U, MINB>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes));
-    attr_set = true;
-  }
-  const uint64_t cap = uint64_t(sm_count()) * 16;
-  const unsigned g1 = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((class_chunks + NGRP - 1) / NGRP, cap)));
-  emb::bwd_chunk_kernel<G, VPL, U, MINB><<<g1, emb::kBwdThreads, stage_bytes, e->ctx->stream>>>(
-      a, c.d_list, d_cls_cbase, uint32_t(c.tables.size()));
-  RS_COUNT(1);
-}
-
-// Level 1, shared-memory staged (rows of <= 32 float4): one CTA per SM.
-template <int G>
-static void launch_chunk_smem(rs_emb* e, const emb::BwdArgs& a, const rs_emb::Class& c,
-                              const uint32_t* d_cls_cbase, uint64_t class_chunks) {
-  constexpr int NW = G >= 4 ? 6 : 4;
-  constexpr int NGRP = NW * (32 / G);
-  constexpr size_t smem = emb::chunk_smem_bytes<G, NW>();
-  static bool attr_set = false;
-  if (!attr_set) {
-    RS_CUDA(cudaFuncSetAttribute(emb::bwd_chunk_smem_kernel<G, NW>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr_set = true;
-  }
-  const unsigned g1 = unsigned(std::max<uint64_t>(
-      1, std::min<uint64_t>((class_chunks + NGRP - 1) / NGRP, uint64_t(sm_count()))));
-  emb::bwd_chunk_smem_kernel<G, NW><<<g1, NW * 32, smem, e->ctx->stream>>>(
-      a, c.d_list, d_cls_cbase, uint32_t(c.tables.size()));
-  RS_COUNT(1);
-}
-
-template <int G, int VPL>
-static void launch_chunk(rs_emb* e, const emb::BwdArgs& a, const rs_emb::Class& c,
-                         const uint32_t* d_cls_cbase, uint64_t class_chunks) {
-  if (class_chunks == 0) return;
-  static const int variant = [] {
-    const char* v = getenv("RS_BWD_VARIANT");
-    return v ? atoi(v) : 0;
-  }();
-  if constexpr (VPL == 1) {
-    if (variant == 0) return launch_chunk_smem<G>(e, a, c, d_cls_cbase, class_chunks);
-  }
-  if constexpr (G >= 8 && VPL == 1) {
-    if (variant == 5) return launch_chunk_v<G, VPL, 8, 1>(e, a, c, d_cls_cbase, class_chunks);
-    if (variant == 1) return launch_chunk_v<G, VPL, 4, 4>(e, a, c, d_cls_cbase, class_chunks);
-    if (variant == 2) return launch_chunk_v<G, VPL, 4, 3>(e, a, c, d_cls_cbase, class_chunks);
-    if (variant == 3) return launch_chunk_v<G, VPL, 2, 6>(e, a, c, d_cls_cbase, class_chunks);
-    if (variant == 4) return launch_chunk_v<G, VPL, 8, 3>(e, a, c, d_cls_cbase, class_chunks);
-  }
-  constexpr int U = G >= 8 ? (VPL <= 2 ? 8 : (VPL == 4 ? 4 : 2)) : G;
-  launch_chunk_v<G, VPL, U, 1>(e, a, c, d_cls_cbase, class_chunks);
-}
-
-// Level 1 bag pass for one lane class over its chunk work range [wlo, whi).
+// Short-segment bag pass for one lane class over its window range [wlo, whi).
 template <int G, int VPL, int UNR, int MINB>
-static void launch_pieces_v(rs_emb* e, const emb::BwdArgs& a, uint32_t wlo, uint32_t whi) {
+static void launch_segs_v(rs_emb* e, const emb::BwdArgs& a, uint32_t wlo, uint32_t whi) {
   const uint64_t est = uint64_t(whi - wlo) * 8 / (uint64_t(emb::kBwdWarps) * (32 / G)) + 1;
   const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(est, uint64_t(sm_count()) * MINB)));
-  emb::bwd_piece_kernel<G, VPL, UNR, MINB><<<grid, emb::kBwdThreads, 0, e->ctx->stream>>>(
-      a, e->pieces, e->pbase, wlo, whi);
+  emb::bwd_seg_kernel<G, VPL, UNR, MINB><<<grid, emb::kBwdThreads, 0, e->ctx->stream>>>(
+      a, e->segs, e->sbase, wlo, whi, e->longs, e->long_np, e->long_ng, e->n_long);
   RS_COUNT(1);
 }
 
 template <int G, int VPL>
-static void launch_pieces(rs_emb* e, const emb::BwdArgs& a, uint32_t wlo, uint32_t whi) {
-  static const int variant = [] {
-    const char* v = getenv("RS_PIECE_VARIANT");
-    return v ? atoi(v) : 0;
-  }();
-  if constexpr (VPL == 1) {
-    if (variant == 1) return launch_pieces_v<G, 1, 4, 3>(e, a, wlo, whi);
-    if (variant == 2) return launch_pieces_v<G, 1, 2, 6>(e, a, wlo, whi);
-    if (variant == 3) return launch_pieces_v<G, 1, 8, 2>(e, a, wlo, whi);
-    return launch_pieces_v<G, 1, 4, 4>(e, a, wlo, whi);
-  } else {
-    return launch_pieces_v<G, VPL, (VPL == 2 ? 2 : 1), 2>(e, a, wlo, whi);
-  }
+static void launch_segs(rs_emb* e, const emb::BwdArgs& a, uint32_t wlo, uint32_t whi) {
+  if constexpr (VPL == 1) launch_segs_v<G, 1, 4, 4>(e, a, wlo, whi);
+  else launch_segs_v<G, VPL, (VPL == 2 ? 2 : 1), 2>(e, a, wlo, whi);
 }
 
-// Levels 2 and 3 (full warps, VPL of the widest table).
-template <int VPL, int PEND>
-static void launch_edges(rs_emb* e, const emb::BwdArgs& a) {
-  const uint64_t nsup = (a.nchunks + emb::kSuper - 1) / emb::kSuper;
-  const uint64_t cap = uint64_t(sm_count()) * 16;
-  const unsigned g2 = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((nsup + 7) / 8, cap)));
-  emb::bwd_super_kernel<VPL, PEND><<<g2, emb::kBwdThreads, 0, e->ctx->stream>>>(a);
-  emb::bwd_final_kernel<VPL, PEND><<<g2, emb::kBwdThreads, 0, e->ctx->stream>>>(a);
-  RS_COUNT(2);
+// Long segments: groups of 64 pieces, then one warp per segment (full warps,
+// VPL of the widest table).
+template <int VPL>
+static void launch_long(rs_emb* e, const emb::BwdArgs& a) {
+  const unsigned g = unsigned(sm_count()) * 8;
+  cudaStream_t st = e->ctx->stream;
+  emb::bwd_lpiece_kernel<VPL><<<g, emb::kBwdThreads, 0, st>>>(a, e->longs, e->n_long, e->pbase, e->ppart);
+  emb::bwd_group_kernel<VPL><<<g, emb::kBwdThreads, 0, st>>>(a, e->longs, e->n_long, e->pbase, e->gbase,
+                                                             e->ppart, e->gpart);
+  emb::bwd_long_kernel<VPL><<<g, emb::kBwdThreads, 0, st>>>(a, e->longs, e->n_long, e->gbase, e->gpart);
+  RS_COUNT(3);
 }
 
 void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx, const float* grad,
@@ -903,38 +845,24 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
   if (tpos[0] != 0) throw InvalidArgument("emb_backward: offsets must start at 0");
   if (L > e->max_lookups) throw InvalidArgument("emb_backward: more lookups than max_lookups");
   if (L == 0) return;
-  // chunk bases: per table ceil(L_t / 32) chunks, numbered in table order
-  uint32_t* cbase = tpos + T + 1;
-  cbase[0] = 0;
-  for (uint32_t t = 0; t < T; ++t) {
+  for (uint32_t t = 0; t < T; ++t)
     if (tpos[t + 1] < tpos[t]) throw InvalidArgument("emb_backward: offsets must be non-decreasing");
-    cbase[t + 1] = cbase[t] + (tpos[t + 1] - tpos[t] + emb::kChunk - 1) / emb::kChunk;
-  }
-  uint32_t* w = cbase + T + 1;
+  // class-major window work map: table t has ceil(L_t / 32) windows
+  uint32_t* wstart = tpos + T + 1;
+  uint32_t* wtab = wstart + T + 1;
   std::vector<uint64_t> class_chunks;
-  std::vector<size_t> class_off;
-  for (const auto& c : e->classes) {
-    class_off.push_back(size_t(w - e->h_meta));
-    w[0] = 0;
-    for (size_t j = 0; j < c.tables.size(); ++j) {
-      const uint32_t t = c.tables[j];
-      w[j + 1] = w[j] + (cbase[t + 1] - cbase[t]);
-    }
-    class_chunks.push_back(w[c.tables.size()]);
-    w += c.tables.size() + 1;
-  }
-  // class-major work map for the piece scan
-  uint32_t* wstart = w;
-  uint32_t* wtab = w + T + 1;
   {
     uint32_t acc = 0, i = 0;
-    for (const auto& c : e->classes)
+    for (const auto& c : e->classes) {
+      const uint32_t c0 = acc;
       for (uint32_t t : c.tables) {
         wstart[i] = acc;
         wtab[i] = t;
-        acc += cbase[t + 1] - cbase[t];
+        acc += (tpos[t + 1] - tpos[t] + emb::kChunk - 1) / emb::kChunk;
         ++i;
       }
+      class_chunks.push_back(acc - c0);
+    }
     wstart[T] = acc;
   }
   RS_CUDA(cudaMemcpyAsync(e->d_meta, e->h_meta, e->meta_words * 4, cudaMemcpyHostToDevice, st));
@@ -949,64 +877,48 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
   scr.base = e->sort_scratch;
   scr.cap = e->sort_scratch_bytes;
   radix_sort_pairs(e->keys, e->vals, L, int(e->key_bits), scr, st);
-  emb::BwdArgs a{e->cur_tables, T, e->d_meta, e->d_meta + T + 1, cbase[T], e->keys, e->vals,
-                 grad, e->total_dim, e->part, e->spart, e->dmax, lr, e->eps, e->opt};
-  static const int variant = [] {
-    const char* v = getenv("RS_BWD_VARIANT");
-    return v ? atoi(v) : 0;
-  }();
-  if (variant == 0) {
-    // level 1 as bags: list the pieces, then one bag pass per lane class
-    const uint32_t W = wstart[T];
-    const size_t woff = size_t(wstart - e->h_meta);
-    emb::WorkMap wm{e->d_meta + woff, e->d_meta + woff + T + 1, T};
-    const unsigned gs = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((uint64_t(W) + 7) / 8, uint64_t(sm_count()) * 16)));
-    emb::bwd_piece_scan_kernel<false><<<gs, 256, 0, st>>>(a, wm, e->pcount, nullptr, nullptr);
-    exclusive_scan<uint32_t>(ArrayIn<uint32_t>{e->pcount}, W, e->pbase, e->pbase + W, scr, st);
-    emb::bwd_piece_scan_kernel<true><<<gs, 256, 0, st>>>(a, wm, nullptr, e->pbase, e->pieces);
-    RS_COUNT(2);
-    uint32_t wlo = 0;
-    for (size_t ci = 0; ci < e->classes.size(); ++ci) {
-      const auto& c = e->classes[ci];
-      const uint32_t whi = wlo + uint32_t(class_chunks[ci]);
-      if (whi > wlo) {
-        switch (c.G * 100 + c.VPL) {
-          case 101: launch_pieces<1, 1>(e, a, wlo, whi); break;
-          case 201: launch_pieces<2, 1>(e, a, wlo, whi); break;
-          case 401: launch_pieces<4, 1>(e, a, wlo, whi); break;
-          case 801: launch_pieces<8, 1>(e, a, wlo, whi); break;
-          case 1601: launch_pieces<16, 1>(e, a, wlo, whi); break;
-          case 3201: launch_pieces<32, 1>(e, a, wlo, whi); break;
-          case 3202: launch_pieces<32, 2>(e, a, wlo, whi); break;
-          case 3204: launch_pieces<32, 4>(e, a, wlo, whi); break;
-          case 3208: launch_pieces<32, 8>(e, a, wlo, whi); break;
-          default: throw Error(-9, "emb_backward: unsupported lane class");
-        }
-      }
-      wlo = whi;
-    }
-  }
-  for (size_t ci = 0; ci < e->classes.size() && variant != 0; ++ci) {
+  emb::BwdArgs a{e->cur_tables, T, e->d_meta, e->keys, e->vals, grad, e->total_dim, e->dmax, lr, e->eps, e->opt};
+  // segment list: count heads per window, scan, write descriptors
+  const uint32_t W = wstart[T];
+  const size_t woff = size_t(wstart - e->h_meta);
+  emb::WorkMap wm{e->d_meta + woff, e->d_meta + woff + T + 1, T};
+  const unsigned gs = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((uint64_t(W) + 7) / 8, uint64_t(sm_count()) * 16)));
+  emb::bwd_seg_scan_kernel<false><<<gs, 256, 0, st>>>(a, wm, e->scount, nullptr, nullptr);
+  exclusive_scan<uint32_t>(ArrayIn<uint32_t>{e->scount}, W, e->sbase, e->sbase + W, scr, st);
+  emb::bwd_seg_scan_kernel<true><<<gs, 256, 0, st>>>(a, wm, nullptr, e->sbase, e->segs);
+  RS_COUNT(2);
+  // short segments per lane class (long ones are listed)
+  RS_CUDA(cudaMemsetAsync(e->n_long, 0, 4, st));
+  RS_CUDA(cudaMemsetAsync(e->long_np, 0, (e->long_cap + 1) * 4, st));
+  RS_CUDA(cudaMemsetAsync(e->long_ng, 0, (e->long_cap + 1) * 4, st));
+  uint32_t wlo = 0;
+  for (size_t ci = 0; ci < e->classes.size(); ++ci) {
     const auto& c = e->classes[ci];
-    const uint32_t* dcb = e->d_meta + class_off[ci];
-    switch (c.G * 100 + c.VPL) {
-      case 101: launch_chunk<1, 1>(e, a, c, dcb, class_chunks[ci]); break;
-      case 201: launch_chunk<2, 1>(e, a, c, dcb, class_chunks[ci]); break;
-      case 401: launch_chunk<4, 1>(e, a, c, dcb, class_chunks[ci]); break;
-      case 801: launch_chunk<8, 1>(e, a, c, dcb, class_chunks[ci]); break;
-      case 1601: launch_chunk<16, 1>(e, a, c, dcb, class_chunks[ci]); break;
-      case 3201: launch_chunk<32, 1>(e, a, c, dcb, class_chunks[ci]); break;
-      case 3202: launch_chunk<32, 2>(e, a, c, dcb, class_chunks[ci]); break;
-      case 3204: launch_chunk<32, 4>(e, a, c, dcb, class_chunks[ci]); break;
-      case 3208: launch_chunk<32, 8>(e, a, c, dcb, class_chunks[ci]); break;
-      default: throw Error(-9, "emb_backward: unsupported lane class");
+    const uint32_t whi = wlo + uint32_t(class_chunks[ci]);
+    if (whi > wlo) {
+      switch (c.G * 100 + c.VPL) {
+        case 101: launch_segs<1, 1>(e, a, wlo, whi); break;
+        case 201: launch_segs<2, 1>(e, a, wlo, whi); break;
+        case 401: launch_segs<4, 1>(e, a, wlo, whi); break;
+        case 801: launch_segs<8, 1>(e, a, wlo, whi); break;
+        case 1601: launch_segs<16, 1>(e, a, wlo, whi); break;
+        case 3201: launch_segs<32, 1>(e, a, wlo, whi); break;
+        case 3202: launch_segs<32, 2>(e, a, wlo, whi); break;
+        case 3204: launch_segs<32, 4>(e, a, wlo, whi); break;
+        case 3208: launch_segs<32, 8>(e, a, wlo, whi); break;
+        default: throw Error(-9, "emb_backward: unsupported lane class");
+      }
     }
+    wlo = whi;
   }
+  // long segments: group offsets, group sums, final sums + updates
+  exclusive_scan<uint32_t>(ArrayIn<uint32_t>{e->long_np}, e->long_cap, e->pbase, e->pbase + e->long_cap, scr, st);
+  exclusive_scan<uint32_t>(ArrayIn<uint32_t>{e->long_ng}, e->long_cap, e->gbase, e->gbase + e->long_cap, scr, st);
   switch (e->bwd_vpl) {
-    case 1: launch_edges<1, 4>(e, a); break;
-    case 2: launch_edges<2, 2>(e, a); break;
-    case 4: launch_edges<4, 1>(e, a); break;
-    case 8: launch_edges<8, 1>(e, a); break;
+    case 1: launch_long<1>(e, a); break;
+    case 2: launch_long<2>(e, a); break;
+    case 4: launch_long<4>(e, a); break;
+    case 8: launch_long<8>(e, a); break;
     default: throw Error(-9, "emb_backward: unsupported dim");
   }
   RS_LAUNCH_CHECK();

@@ -190,16 +190,12 @@ constexpr int kSortTile = kSortThreads * kSortItems;  // 2048 keys per CTA
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
 
-// Peers of this lane with the same `bits`-wide digit, via bit-split ballots.
+// Peers of this lane with the same digit (one MATCH.ANY; measured faster than
+// BITS bit-split ballots on B200).
 template <int BITS>
 __device__ __forceinline__ unsigned digit_peers(unsigned d, bool valid) {
-  unsigned m = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-  for (int b = 0; b < BITS; ++b) {
-    unsigned bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-    m &= ((d >> b) & 1u) ? bb : ~bb;
-  }
-  return valid ? m : 0u;
+  const unsigned pm = __match_any_sync(0xffffffffu, valid ? d : 0xFFFFFFFFu);
+  return valid ? pm : 0u;
 }
 
 // Per-tile digit counts, written digit-major: counts[d * ntiles + tile].
@@ -314,6 +310,8 @@ inline size_t radix_sort_scratch_bytes(size_t n) {
 
 // Stable ascending sort of (keys, vals) on bits [0, end_bit).  Sorted data
 // ends in (keys, vals) — ping-pong buffers come from scratch.  n < 2^32.
+// (A one-kernel-per-pass decoupled look-back variant measured slower on B200
+// RM1: 3.00 vs 2.93 ms backward.)
 inline void radix_sort_pairs(uint32_t* keys, uint32_t* vals, size_t n, int end_bit,
                              Scratch& scr, cudaStream_t st) {
   if (n <= 1 || end_bit <= 0) return;
