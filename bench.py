@@ -370,7 +370,7 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
     zc = timed(0)
     pipe = None
     if T and slow_u and not args.no_prefetch:
-        op.enable_uvm_cache(int(2.5 * slow_u) + 4096)
+        op.enable_uvm_cache(int(4.5 * slow_u) + 4096)  # up to 4 live generations
         if os.environ.get("BENCH_PROBE") == "1":
             probe_cache(torch, op, batches, pooled, B)
         pipe = timed(steps)

@@ -21,12 +21,15 @@
 //   chunk in sorted order; pieces crossing a chunk edge are combined by the
 //   owning chunk in chunk order.  Fully deterministic, no float atomics.
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
+#include <cstring>
 #include <numeric>
 #include <tuple>
 
 #include "../../include/shardplan_gpu.h"
 #include "context.cuh"
+#include "host_worker.hpp"
 
 namespace rs {
 namespace emb {
@@ -331,15 +334,31 @@ struct rs_emb {
   int* free_top = nullptr;
   unsigned* ncopy = nullptr;
   unsigned* cache_err = nullptr;
+  // DMA staging (uvm_cache.cuh): bounce buffers of bcap rows (stride dmax)
+  uint32_t bcap = 0;
+  uint32_t *copy_tab = nullptr, *copy_row = nullptr, *wb_tab = nullptr, *wb_row = nullptr;
+  unsigned* n_wb = nullptr;
+  float *d_bin = nullptr, *d_bout = nullptr, *h_bin = nullptr, *h_bout = nullptr;
+  uint32_t *h_ctab = nullptr, *h_crow = nullptr, *h_wtab = nullptr, *h_wrow = nullptr;
+  unsigned* h_cnt = nullptr;
+  cudaEvent_t ev_claim[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_evict[4] = {nullptr, nullptr, nullptr, nullptr};  // ring: one per eviction in flight
+  uint64_t n_evicts = 0;
+  std::unique_ptr<rs::TaskQueue> worker;      // stage-in tasks (host tier -> slots)
+  std::unique_ptr<rs::TaskQueue> out_worker;  // stage-out tasks (evicted rows -> host tier)
+  std::unique_ptr<rs::ThreadPool> pool, out_pool;
+  cudaStream_t side_out = nullptr;
+  uint64_t gather_seq[4] = {0, 0, 0, 0}, wb_seq = 0;
+
   TableDev* d_tables_c = nullptr;
   uint32_t* d_slow_tabs = nullptr;  // tables with slow rows
   uint32_t nslow_tabs = 0;
   const TableDev* cur_tables = nullptr;  // tables the running forward/backward use
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_main = nullptr, ev_bwd = nullptr, ev_wb = nullptr, ev_gather[2] = {nullptr, nullptr};
-  bool wb_recorded = false;
+  cudaEvent_t ev_main = nullptr, ev_gather[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<uint64_t> pending;  // prefetched generations, oldest first
   int64_t cur_gen = -1;           // staged generation of the running step (-1: zero-copy)
+  int64_t done_gen = -1;          // finished generation, evicted one step later
   uint64_t next_gen = 0;
   bool staged_dirty = false;
   uint32_t* scount = nullptr;  // [windows + 1] segment heads per window
@@ -362,6 +381,23 @@ struct rs_emb {
   size_t sort_scratch_bytes = 0;
 
   ~rs_emb() {
+    worker.reset();  // joins the staging workers before any buffer goes
+    out_worker.reset();
+    pool.reset();
+    out_pool.reset();
+    if (side_out) {
+      cudaStreamSynchronize(side_out);
+      cudaStreamDestroy(side_out);
+    }
+    for (void* p : {(void*)h_bin, (void*)h_bout, (void*)h_ctab, (void*)h_crow, (void*)h_wtab, (void*)h_wrow,
+                    (void*)h_cnt})
+      if (p) cudaFreeHost(p);
+    for (void* p : {(void*)copy_tab, (void*)copy_row, (void*)wb_tab, (void*)wb_row, (void*)n_wb, (void*)d_bin,
+                    (void*)d_bout})
+      if (p) cudaFree(p);
+    for (cudaEvent_t ev : {ev_claim[0], ev_claim[1], ev_claim[2], ev_claim[3], ev_evict[0], ev_evict[1],
+                           ev_evict[2], ev_evict[3]})
+      if (ev) cudaEventDestroy(ev);
     if (d_tables) cudaFree(d_tables);
     if (fast_pool) cudaFree(fast_pool);
     if (host_pool) cudaFreeHost(host_pool);
@@ -382,7 +418,7 @@ struct rs_emb {
       cudaStreamSynchronize(side);
       cudaStreamDestroy(side);
     }
-    for (cudaEvent_t ev : {ev_main, ev_bwd, ev_wb, ev_gather[0], ev_gather[1]})
+    for (cudaEvent_t ev : {ev_main, ev_gather[0], ev_gather[1], ev_gather[2], ev_gather[3]})
       if (ev) cudaEventDestroy(ev);
     for (void* p : {(void*)staging, (void*)slot_of, (void*)slot_gen, (void*)slot_tab, (void*)slot_row,
                     (void*)free_stack, (void*)copy_list, (void*)free_top, (void*)ncopy, (void*)cache_err,
@@ -567,16 +603,31 @@ void emb_enable_cache(rs_emb* e, uint32_t nslots) {
   uint64_t total_slow = 0;
   for (const auto& d : e->h_tables) total_slow += d.slow_rows;
   const uint64_t stride = e->dmax;
+  // one generation's rows fit in half the slots (nslots >= 2x a batch's rows)
+  e->bcap = nslots / 2 + 1;
+  const uint64_t bc = e->bcap;
   RS_CUDA(cudaMalloc(&e->staging, uint64_t(nslots) * stride * 4));
   RS_CUDA(cudaMalloc(&e->slot_of, std::max<uint64_t>(total_slow, 1) * 4));
   RS_CUDA(cudaMalloc(&e->slot_gen, uint64_t(nslots) * 4));
   RS_CUDA(cudaMalloc(&e->slot_tab, uint64_t(nslots) * 4));
   RS_CUDA(cudaMalloc(&e->slot_row, uint64_t(nslots) * 4));
   RS_CUDA(cudaMalloc(&e->free_stack, uint64_t(nslots) * 4));
-  RS_CUDA(cudaMalloc(&e->copy_list, uint64_t(nslots) * 4));
+  RS_CUDA(cudaMalloc(&e->copy_list, bc * 4));
+  RS_CUDA(cudaMalloc(&e->copy_tab, bc * 4));
+  RS_CUDA(cudaMalloc(&e->copy_row, bc * 4));
+  RS_CUDA(cudaMalloc(&e->wb_tab, bc * 4));
+  RS_CUDA(cudaMalloc(&e->wb_row, bc * 4));
+  RS_CUDA(cudaMalloc(&e->d_bin, bc * stride * 4));
+  RS_CUDA(cudaMalloc(&e->d_bout, bc * stride * 4));
   RS_CUDA(cudaMalloc(&e->free_top, 4));
   RS_CUDA(cudaMalloc(&e->ncopy, 4));
+  RS_CUDA(cudaMalloc(&e->n_wb, 4));
   RS_CUDA(cudaMalloc(&e->cache_err, 4));
+  RS_CUDA(cudaHostAlloc(&e->h_bin, bc * stride * 4, cudaHostAllocDefault));
+  RS_CUDA(cudaHostAlloc(&e->h_bout, bc * stride * 4, cudaHostAllocDefault));
+  for (uint32_t** hp : {&e->h_ctab, &e->h_crow, &e->h_wtab, &e->h_wrow})
+    RS_CUDA(cudaHostAlloc(hp, bc * 4, cudaHostAllocDefault));
+  RS_CUDA(cudaHostAlloc(&e->h_cnt, 16, cudaHostAllocDefault));
   RS_CUDA(cudaMemsetAsync(e->slot_of, 0xFF, std::max<uint64_t>(total_slow, 1) * 4, st));
   RS_CUDA(cudaMemsetAsync(e->slot_gen, 0, uint64_t(nslots) * 4, st));
   RS_CUDA(cudaMemsetAsync(e->cache_err, 0, 4, st));
@@ -604,30 +655,20 @@ void emb_enable_cache(rs_emb* e, uint32_t nslots) {
     if (!st_list.empty())
       RS_CUDA(cudaMemcpyAsync(e->d_slow_tabs, st_list.data(), st_list.size() * 4, cudaMemcpyHostToDevice, st));
   }
-  // side stream for the PCIe gathers / write-backs (small grids: they hold
-  // few SM slots while the compute stream runs)
-  {
-    static const int prio_env = [] {
-      const char* v = getenv("RS_SIDE_PRIORITY");
-      return v ? atoi(v) : 0;
-    }();
-    int prio_lo = 0, prio_hi = 0;
-    RS_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-    RS_CUDA(cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking,
-                                         prio_env < 0 ? prio_hi : (prio_env > 0 ? prio_lo : 0)));
-  }
-  for (cudaEvent_t* ev : {&e->ev_main, &e->ev_bwd, &e->ev_wb, &e->ev_gather[0], &e->ev_gather[1]})
+  RS_CUDA(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+  RS_CUDA(cudaStreamCreateWithFlags(&e->side_out, cudaStreamNonBlocking));
+  for (cudaEvent_t* ev : {&e->ev_main, &e->ev_gather[0], &e->ev_gather[1], &e->ev_gather[2], &e->ev_gather[3],
+                          &e->ev_claim[0], &e->ev_claim[1], &e->ev_claim[2], &e->ev_claim[3], &e->ev_evict[0],
+                          &e->ev_evict[1], &e->ev_evict[2], &e->ev_evict[3]})
     RS_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
   RS_CUDA(cudaStreamSynchronize(st));
+  // host threads: one gather pool (in) and one scatter pool (out) sharing the cores
+  const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+  e->pool = std::make_unique<rs::ThreadPool>(std::min(16u, hw));
+  e->out_pool = std::make_unique<rs::ThreadPool>(std::min(8u, hw / 2));
+  e->worker = std::make_unique<rs::TaskQueue>();
+  e->out_worker = std::make_unique<rs::TaskQueue>();
   e->nslots = nslots;
-}
-
-// Side-stream PCIe kernels use few blocks: enough reads in flight for the
-// bus, few SM slots taken from the compute stream.
-constexpr unsigned kSideBlocks = 32;
-
-static unsigned cache_grid(uint64_t work) {
-  return unsigned(std::max<uint64_t>(1, std::min<uint64_t>((work + 255) / 256, uint64_t(sm_count()) * 8)));
 }
 
 static void check_cache_error(rs_emb* e) {
@@ -638,52 +679,155 @@ static void check_cache_error(rs_emb* e) {
                           "(>= 2x the unique slow rows of a batch)");
 }
 
-// Enqueues the write-back of generation g on the side stream after the
-// backward that used it; rows a pending prefetch still needs stay staged.
-static void enqueue_writeback(rs_emb* e, uint64_t g) {
-  uint32_t keep = 0;
-  for (uint64_t p : e->pending) keep |= 1u << (p & 1);
-  RS_CUDA(cudaEventRecord(e->ev_bwd, e->ctx->stream));
-  RS_CUDA(cudaStreamWaitEvent(e->side, e->ev_bwd, 0));
-  emb::uvm_writeback_kernel<<<unsigned(std::min<uint64_t>(cache_grid(e->nslots), kSideBlocks)), 256, 0, e->side>>>(
-      e->d_tables_c, e->nslots, 1u << (g & 1), keep, e->slot_gen, e->slot_tab, e->slot_row,
-      e->free_stack, e->free_top, e->staging, e->dmax);
+// Host row of (table t, slow row r) in the pinned host tier.
+static inline float* host_slow_row(rs_emb* e, uint32_t t, uint32_t r) {
+  const TableDev& d = e->h_tables[t];
+  return reinterpret_cast<float*>(e->host_pool + (reinterpret_cast<char*>(d.slow) - e->host_pool_dev)) +
+         uint64_t(r) * d.dim;
+}
+
+// Worker task: rows claimed for generation g (claim event ev_claim[g & 3])
+// host tier -> pinned bounce (CPU threads) -> HBM bounce (DMA) -> slots.
+static double now_us() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+static void stage_in_task(rs_emb* e, uint64_t g, uint64_t out_before) {
+  static const bool dbg = getenv("RS_STAGE_DEBUG") != nullptr;
+  const double t0 = dbg ? now_us() : 0;
+  cudaStream_t s = e->side;
+  // rows evicted by earlier generations must be in the host tier first
+  if (out_before) e->out_worker->wait(out_before);
+  RS_CUDA(cudaStreamSynchronize(s));  // the previous DMA out of h_bin is done
+  RS_CUDA(cudaEventSynchronize(e->ev_claim[g & 3]));
+  const double t1 = dbg ? now_us() : 0;
+  RS_CUDA(cudaMemcpyAsync(e->h_cnt, e->ncopy, 4, cudaMemcpyDeviceToHost, s));
+  RS_CUDA(cudaStreamSynchronize(s));
+  const uint64_t n = std::min<uint64_t>(e->h_cnt[0], e->bcap);
+  const uint64_t stride = e->dmax;
+  if (n) {
+    RS_CUDA(cudaMemcpyAsync(e->h_ctab, e->copy_tab, n * 4, cudaMemcpyDeviceToHost, s));
+    RS_CUDA(cudaMemcpyAsync(e->h_crow, e->copy_row, n * 4, cudaMemcpyDeviceToHost, s));
+    RS_CUDA(cudaStreamSynchronize(s));
+    const double t2 = dbg ? now_us() : 0;
+    // gather chunk c on the CPU while chunk c-1 is on the bus
+    constexpr uint64_t kChunkRows = 16384;
+    for (uint64_t c0 = 0; c0 < n; c0 += kChunkRows) {
+      const uint64_t c1 = std::min(n, c0 + kChunkRows);
+      e->pool->parallel_for(c1 - c0, [&](size_t b, size_t en) {
+        for (size_t k = c0 + b; k < c0 + en; ++k) {
+          const uint32_t t = e->h_ctab[k];
+          memcpy(e->h_bin + k * stride, host_slow_row(e, t, e->h_crow[k]), size_t(e->h_tables[t].dim) * 4);
+        }
+      });
+      RS_CUDA(cudaMemcpyAsync(e->d_bin + c0 * stride, e->h_bin + c0 * stride, (c1 - c0) * stride * 4,
+                              cudaMemcpyHostToDevice, s));
+    }
+    const double t3 = dbg ? now_us() : 0;
+    if (dbg)
+      fprintf(stderr, "stage_in g=%llu n=%llu t=%.0f wait=%.0fus lists=%.0fus gather+enqueue=%.0fus (%u threads)\n",
+              (unsigned long long)g, (unsigned long long)n, t0, t1 - t0, t2 - t1, t3 - t2, e->pool->size());
+    const unsigned grid = unsigned(std::min<uint64_t>((n + 7) / 8, uint64_t(sm_count()) * 4));
+    emb::uvm_scatter_in_kernel<<<grid, 256, 0, s>>>(e->d_tables_c, e->copy_list, e->copy_tab, e->ncopy, e->bcap,
+                                                   e->d_bin, e->staging, stride);
+    RS_COUNT(1);
+    RS_LAUNCH_CHECK();
+  }
+  RS_CUDA(cudaEventRecord(e->ev_gather[g & 3], s));
+}
+
+// Worker task: rows an eviction packed into d_bout (its event `evicted`)
+// HBM bounce -> pinned bounce (DMA) -> host tier (CPU threads).
+static void stage_out_task(rs_emb* e, cudaEvent_t evicted) {
+  static const bool dbg = getenv("RS_STAGE_DEBUG") != nullptr;
+  const double t0 = dbg ? now_us() : 0;
+  cudaStream_t s = e->side_out;
+  RS_CUDA(cudaEventSynchronize(evicted));
+  const double t1 = dbg ? now_us() : 0;
+  RS_CUDA(cudaMemcpyAsync(e->h_cnt + 1, e->n_wb, 4, cudaMemcpyDeviceToHost, s));
+  RS_CUDA(cudaStreamSynchronize(s));
+  const uint64_t n = std::min<uint64_t>(e->h_cnt[1], e->bcap);
+  if (!n) return;
+  const uint64_t stride = e->dmax;
+  RS_CUDA(cudaMemcpyAsync(e->h_wtab, e->wb_tab, n * 4, cudaMemcpyDeviceToHost, s));
+  RS_CUDA(cudaMemcpyAsync(e->h_wrow, e->wb_row, n * 4, cudaMemcpyDeviceToHost, s));
+  RS_CUDA(cudaMemcpyAsync(e->h_bout, e->d_bout, n * stride * 4, cudaMemcpyDeviceToHost, s));
+  RS_CUDA(cudaStreamSynchronize(s));
+  const double t2 = dbg ? now_us() : 0;
+  e->out_pool->parallel_for(n, [&](size_t b, size_t en) {
+    for (size_t k = b; k < en; ++k) {
+      const uint32_t t = e->h_wtab[k];
+      memcpy(host_slow_row(e, t, e->h_wrow[k]), e->h_bout + k * stride, size_t(e->h_tables[t].dim) * 4);
+    }
+  });
+  if (dbg)
+    fprintf(stderr, "stage_out n=%llu t=%.0f wait_evict=%.0fus d2h=%.0fus scatter=%.0fus\n", (unsigned long long)n,
+            t0, t1 - t0, t2 - t1, now_us() - t2);
+}
+
+// Evicts generation bit(s) `gen_bits` except rows of `keep` (caller's
+// stream) and queues their return to the host tier.
+static void evict(rs_emb* e, uint32_t gen_bits, uint32_t keep) {
+  cudaStream_t st = e->ctx->stream;
+  if (e->wb_seq) e->out_worker->wait(e->wb_seq);  // d_bout free again
+  RS_CUDA(cudaMemsetAsync(e->n_wb, 0, 4, st));
+  const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((e->nslots + 255) / 256, uint64_t(sm_count()) * 8)));
+  emb::uvm_evict_kernel<<<grid, 256, 0, st>>>(e->d_tables_c, e->nslots, gen_bits, keep, e->slot_gen, e->slot_tab,
+                                              e->slot_row, e->free_stack, e->free_top, e->staging, e->dmax,
+                                              e->d_bout, e->wb_tab, e->wb_row, e->bcap, e->n_wb, e->cache_err);
   RS_COUNT(1);
   RS_LAUNCH_CHECK();
-  RS_CUDA(cudaEventRecord(e->ev_wb, e->side));
-  e->wb_recorded = true;
+  // each eviction gets its own event: the host may run ahead and record the
+  // next eviction before this task syncs (a shared event would then wait on
+  // work queued behind a stream wait on this very pipeline)
+  cudaEvent_t ev = e->ev_evict[e->n_evicts++ & 3];
+  RS_CUDA(cudaEventRecord(ev, st));
+  e->wb_seq = e->out_worker->post([e, ev] { stage_out_task(e, ev); });
+}
+
+// After the backward that used generation g: the generation finished one
+// step EARLIER is evicted (its rows that neither g nor a pending prefetch
+// needs go back to the host tier).  The one-step delay means a claim never
+// needs a row whose write-back is still in flight: a claim for g+1 runs
+// before g-1 is evicted (so it re-marks the still-staged row), and by the
+// time g+2 is claimed, g-1's stage-out has had a whole step to finish.
+static void enqueue_writeback(rs_emb* e, uint64_t g) {
+  if (e->done_gen >= 0) {
+    uint32_t keep = 1u << (g & 3);
+    for (uint64_t p : e->pending) keep |= 1u << (p & 3);
+    evict(e, 1u << (uint64_t(e->done_gen) & 3), keep);
+  }
+  e->done_gen = int64_t(g);
 }
 
 void emb_prefetch(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx) {
   if (!e->nslots) throw InvalidArgument("emb_prefetch: enable the slow-row cache first");
   if (B == 0 || B > e->max_batch) throw InvalidArgument("emb_prefetch: batch outside [1, max_batch]");
   const uint64_t g = e->next_gen;
-  const bool clash = (e->cur_gen >= 0 && (uint64_t(e->cur_gen) & 1) == (g & 1)) ||
-                     std::any_of(e->pending.begin(), e->pending.end(),
-                                 [&](uint64_t p) { return (p & 1) == (g & 1); });
-  if (clash) throw InvalidArgument("emb_prefetch: at most one batch may be prefetched ahead");
+  // live generations: done (awaiting eviction), current, pending; g & 3 must be free
+  const bool clash = e->pending.size() >= 2 ||
+                     (e->done_gen >= 0 && (uint64_t(e->done_gen) & 3) == (g & 3)) ||
+                     (e->cur_gen >= 0 && (uint64_t(e->cur_gen) & 3) == (g & 3));
+  if (clash) throw InvalidArgument("emb_prefetch: at most two prefetched batches may be pending");
   ++e->next_gen;
-  // The claim pass (index + remap read per lookup, an atomic per new slow
-  // row) is short and bandwidth-bound: it runs on the caller's stream, after
-  // the last write-back released its slots.  Only the PCIe gather of the new
-  // rows goes to the side stream, behind the caller's next kernels.
+  // claim (index + remap read per lookup, an atomic per new slow row) on the
+  // caller's stream, ordered after the last eviction; the copies run behind
+  // the caller's next kernels
   cudaStream_t st = e->ctx->stream;
-  if (e->wb_recorded) RS_CUDA(cudaStreamWaitEvent(st, e->ev_wb, 0));
   RS_CUDA(cudaMemsetAsync(e->ncopy, 0, 4, st));
   if (e->nslow_tabs) {
     const uint64_t work = uint64_t(e->nslow_tabs) * ((B + 31) / 32);
     emb::uvm_claim_kernel<<<unsigned(std::max<uint64_t>(1, std::min<uint64_t>((work + 7) / 8, uint64_t(sm_count()) * 8))),
                             256, 0, st>>>(
-        e->d_tables_c, e->d_slow_tabs, e->nslow_tabs, B, off, idx, 1u << (g & 1), e->slot_gen,
-        e->slot_tab, e->slot_row, e->free_stack, e->free_top, e->copy_list, e->ncopy, e->cache_err);
+        e->d_tables_c, e->d_slow_tabs, e->nslow_tabs, B, off, idx, 1u << (g & 3), e->slot_gen,
+        e->slot_tab, e->slot_row, e->free_stack, e->free_top, e->copy_list, e->copy_tab, e->copy_row, e->bcap,
+        e->ncopy, e->cache_err);
+    RS_COUNT(1);
+    RS_LAUNCH_CHECK();
   }
-  RS_CUDA(cudaEventRecord(e->ev_main, st));
-  RS_CUDA(cudaStreamWaitEvent(e->side, e->ev_main, 0));
-  emb::uvm_fill_kernel<<<kSideBlocks, 256, 0, e->side>>>(
-      e->d_tables_c, e->slot_tab, e->slot_row, e->copy_list, e->ncopy, e->staging, e->dmax);
-  RS_COUNT(2);
-  RS_LAUNCH_CHECK();
-  RS_CUDA(cudaEventRecord(e->ev_gather[g & 1], e->side));
+  RS_CUDA(cudaEventRecord(e->ev_claim[g & 3], st));
+  const uint64_t ob = e->out_worker->posted();
+  e->gather_seq[g & 3] = e->worker->post([e, g, ob] { stage_in_task(e, g, ob); });
   e->pending.push_back(g);
   e->staged_dirty = true;
 }
@@ -692,15 +836,13 @@ void emb_prefetch(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
 // refetch); afterwards the host tier is authoritative again.
 void emb_flush(rs_emb* e) {
   if (!e->nslots || !e->staged_dirty) return;
-  cudaStream_t st = e->ctx->stream;
-  RS_CUDA(cudaEventRecord(e->ev_main, e->side));
-  RS_CUDA(cudaStreamWaitEvent(st, e->ev_main, 0));
-  emb::uvm_writeback_kernel<<<cache_grid(e->nslots), 256, 0, st>>>(
-      e->d_tables_c, e->nslots, 3u, 0u, e->slot_gen, e->slot_tab, e->slot_row, e->free_stack,
-      e->free_top, e->staging, e->dmax);
-  RS_COUNT(1);
-  RS_LAUNCH_CHECK();
-  RS_CUDA(cudaStreamSynchronize(st));
+  e->worker->drain();
+  for (cudaEvent_t ev : e->ev_gather) RS_CUDA(cudaStreamWaitEvent(e->ctx->stream, ev, 0));
+  // a generation's rows fit the bounce buffers: evict one generation at a time
+  for (uint32_t b = 0; b < 4; ++b) evict(e, 1u << b, 0u);
+  e->out_worker->drain();
+  e->done_gen = -1;
+  RS_CUDA(cudaStreamSynchronize(e->ctx->stream));
   check_cache_error(e);
   e->pending.clear();
   e->cur_gen = -1;
@@ -719,7 +861,8 @@ static void begin_step(rs_emb* e) {
     const uint64_t g = e->pending.front();
     e->pending.erase(e->pending.begin());
     e->cur_gen = int64_t(g);
-    RS_CUDA(cudaStreamWaitEvent(e->ctx->stream, e->ev_gather[g & 1], 0));
+    e->worker->wait(e->gather_seq[g & 3]);  // its copies are enqueued
+    RS_CUDA(cudaStreamWaitEvent(e->ctx->stream, e->ev_gather[g & 3], 0));
     e->cur_tables = e->d_tables_c;
   } else {
     emb_flush(e);

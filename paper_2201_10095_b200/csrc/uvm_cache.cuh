@@ -1,23 +1,30 @@
-// HBM staging of slow-tier (UVM) rows, overlapped with compute (included by
-// emb.cu).
+// HBM staging of slow-tier (UVM) rows, moved by the copy engines while the
+// previous batch computes (included by emb.cu).
 //
-// The plan leaves rows in pinned host memory that the GPU reads zero-copy over
-// PCIe; inside the forward/backward those reads sit on the critical path.
-// With a prefetch, each batch's slow rows are copied once (deduplicated) into
-// an HBM staging area on a side stream BEFORE the batch runs — while the
-// previous batch computes — the forward/backward read and update the staged
-// copy, and a write-back on the side stream returns updated rows to the host
-// tier while the next batch computes.  Values and arithmetic are unchanged
-// (the staged row is the host row), so results are bit-identical to the
-// zero-copy path; accounting (tier hits) still follows the remap.
+// The plan leaves rows in pinned host memory that the kernels could read
+// zero-copy over PCIe — but SM-issued PCIe traffic costs about its own
+// duration in lost HBM throughput (measured: a concurrent zero-copy gather
+// slowed the backward by ~1 ms, a concurrent DMA of the same bytes by 0.1 ms).
+// So each batch's slow rows are staged once (deduplicated) into HBM slots
+// BEFORE the batch runs: a claim kernel (caller's stream) lists the rows that
+// are not staged yet, a host worker gathers them from the host tier into a
+// pinned bounce buffer (CPU memcpy, several threads) and one DMA copy plus a
+// scatter kernel put them in their slots (side stream).  After the backward,
+// an evict kernel (caller's stream) packs the rows no pending batch needs
+// into a device bounce buffer and frees their slots; the worker copies them
+// back with one DMA and scatters them into the host tier.  Values and
+// arithmetic are unchanged (a staged row IS the host row), so results are
+// bit-identical to the zero-copy path; accounting follows the remap.
 //
 // Per slow row: slot_of[s] = staging slot or kNoSlot.  Per slot: its (table,
 // slow row) and a 2-bit generation mask — bit (g & 1) is set while batch g
-// needs the row.  Two batches may be live (current + prefetched): a gather
+// needs the row.  Two batches may be live (current + prefetched): a claim
 // marks rows already staged instead of re-reading them (so a row updated by
-// the running backward is never read stale from the host), and the write-back
-// of batch g keeps rows batch g+1 still needs.  Gathers and write-backs run on
-// one side stream, so slot allocation and release never race.
+// the running backward is never read stale from the host), and the eviction
+// of batch g keeps rows batch g+1 still needs.  Claims and evictions run on
+// the caller's stream, so slot allocation and release never race; the host
+// worker runs its gathers and scatters in FIFO order, so a row evicted by
+// batch g reaches the host tier before a later batch gathers it again.
 #pragma once
 
 namespace rs {
@@ -37,6 +44,7 @@ uvm_claim_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict
                  uint32_t* __restrict__ slot_gen, uint32_t* __restrict__ slot_tab,
                  uint32_t* __restrict__ slot_row, uint32_t* __restrict__ free_stack,
                  int* __restrict__ free_top, uint32_t* __restrict__ copy_list,
+                 uint32_t* __restrict__ copy_tab, uint32_t* __restrict__ copy_row, uint32_t cap,
                  unsigned* __restrict__ ncopy, unsigned* __restrict__ err) {
   const int lane = threadIdx.x & 31;
   const uint64_t cpt = (B + 31) / 32;  // 32-bag chunks per table
@@ -68,7 +76,14 @@ uvm_claim_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict
         slot_tab[slot] = t;
         slot_row[slot] = s;
         slot_gen[slot] = gen_bit;
-        copy_list[atomicAdd(ncopy, 1u)] = slot;
+        const unsigned k = atomicAdd(ncopy, 1u);
+        if (k < cap) {
+          copy_list[k] = slot;
+          copy_tab[k] = t;
+          copy_row[k] = s;
+        } else {
+          atomicOr(err, 2u);
+        }
         __threadfence();
         atomicExch(p, slot);
       } else if (old != kClaim) {
@@ -78,55 +93,33 @@ uvm_claim_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict
   }
 }
 
-// Host row -> staging slot.  A warp copies RPW rows at a time (their PCIe
-// reads all in flight before the HBM stores), so a small grid keeps the bus
-// busy without holding many SM slots away from the compute stream.
-constexpr int kFillRows = 8;
+// Bounce row k (the host row, copied by DMA) -> its staging slot; warp per row.
 __global__ void __launch_bounds__(256)
-uvm_fill_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__ slot_tab,
-                const uint32_t* __restrict__ slot_row, const uint32_t* __restrict__ copy_list,
-                const unsigned* __restrict__ ncopy, float* __restrict__ staging, uint64_t stride) {
+uvm_scatter_in_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__ copy_list,
+                      const uint32_t* __restrict__ copy_tab, const unsigned* __restrict__ ncopy, uint32_t cap,
+                      const float* __restrict__ bounce, float* __restrict__ staging, uint64_t stride) {
   const int lane = threadIdx.x & 31;
-  const uint64_t n = *ncopy;
+  const uint64_t n = min(*ncopy, cap);
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t i0 = ((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * kFillRows; i0 < n;
-       i0 += nwarps * kFillRows) {
-    uint32_t slot[kFillRows], V[kFillRows];
-    const float4* src[kFillRows];
-#pragma unroll
-    for (int r = 0; r < kFillRows; ++r) {
-      slot[r] = i0 + r < n ? copy_list[i0 + r] : 0u;
-      V[r] = 0;
-      src[r] = nullptr;
-      if (i0 + r < n) {
-        const TableDev& td = tables[slot_tab[slot[r]]];
-        V[r] = td.dim >> 2;
-        src[r] = reinterpret_cast<const float4*>(td.slow + uint64_t(slot_row[slot[r]]) * td.dim);
-      }
-    }
-    uint32_t vmax = 0;
-#pragma unroll
-    for (int r = 0; r < kFillRows; ++r) vmax = max(vmax, V[r]);
-    for (uint32_t v = lane; v < vmax; v += 32) {
-      float4 x[kFillRows];
-#pragma unroll
-      for (int r = 0; r < kFillRows; ++r)
-        if (v < V[r]) x[r] = src[r][v];
-#pragma unroll
-      for (int r = 0; r < kFillRows; ++r)
-        if (v < V[r]) reinterpret_cast<float4*>(staging + uint64_t(slot[r]) * stride)[v] = x[r];
-    }
+  for (uint64_t k = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; k < n; k += nwarps) {
+    const uint32_t V = tables[copy_tab[k]].dim >> 2;
+    const float4* src = reinterpret_cast<const float4*>(bounce + k * stride);
+    float4* dst = reinterpret_cast<float4*>(staging + uint64_t(copy_list[k]) * stride);
+    for (uint32_t v = lane; v < V; v += 32) dst[v] = src[v];
   }
 }
 
 // Release every slot of generation bit `gen_bit` that no batch in `keep`
-// still needs: staged row -> host row, slot_of reset, slot back on the free
-// stack.  Rows kept for the next batch only lose the bit.
+// still needs: staged row -> bounce row k (with its table / slow row for the
+// host scatter), slot_of reset, slot back on the free stack.  Rows kept for
+// the next batch only lose the bit.
 __global__ void __launch_bounds__(256)
-uvm_writeback_kernel(const TableDev* __restrict__ tables, uint32_t nslots, uint32_t gen_bit,
-                     uint32_t keep, uint32_t* __restrict__ slot_gen, const uint32_t* __restrict__ slot_tab,
-                     const uint32_t* __restrict__ slot_row, uint32_t* __restrict__ free_stack,
-                     int* __restrict__ free_top, const float* __restrict__ staging, uint64_t stride) {
+uvm_evict_kernel(const TableDev* __restrict__ tables, uint32_t nslots, uint32_t gen_bit, uint32_t keep,
+                 uint32_t* __restrict__ slot_gen, const uint32_t* __restrict__ slot_tab,
+                 const uint32_t* __restrict__ slot_row, uint32_t* __restrict__ free_stack,
+                 int* __restrict__ free_top, const float* __restrict__ staging, uint64_t stride,
+                 float* __restrict__ bounce, uint32_t* __restrict__ wb_tab, uint32_t* __restrict__ wb_row,
+                 uint32_t cap, unsigned* __restrict__ n_wb, unsigned* __restrict__ err) {
   const int lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t base = ((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 32; base < nslots;
@@ -137,20 +130,33 @@ uvm_writeback_kernel(const TableDev* __restrict__ tables, uint32_t nslots, uint3
     const bool kept = mine && (g & keep) != 0;
     if (kept) slot_gen[my] = g & ~gen_bit;
     unsigned evict = __ballot_sync(0xffffffffu, mine && !kept);
+    unsigned k0 = 0;
+    if (lane == 0 && evict) k0 = atomicAdd(n_wb, unsigned(__popc(evict)));
+    k0 = __shfl_sync(0xffffffffu, k0, 0);
     while (evict) {
       const int src = __ffs(evict) - 1;
       evict &= evict - 1;
       const uint32_t slot = uint32_t(base) + src;
-      const TableDev& td = tables[slot_tab[slot]];
+      const uint32_t t = slot_tab[slot];
+      const TableDev& td = tables[t];
       const uint32_t s = slot_row[slot];
-      const float4* from = reinterpret_cast<const float4*>(staging + uint64_t(slot) * stride);
-      float4* to = reinterpret_cast<float4*>(td.slow + uint64_t(s) * td.dim);
-      for (uint32_t v = lane; v < (td.dim >> 2); v += 32) to[v] = from[v];
+      if (k0 < cap) {
+        const float4* from = reinterpret_cast<const float4*>(staging + uint64_t(slot) * stride);
+        float4* to = reinterpret_cast<float4*>(bounce + uint64_t(k0) * stride);
+        for (uint32_t v = lane; v < (td.dim >> 2); v += 32) to[v] = from[v];
+        if (lane == 0) {
+          wb_tab[k0] = t;
+          wb_row[k0] = s;
+        }
+      } else if (lane == 0) {
+        atomicOr(err, 2u);
+      }
       if (lane == 0) {
         td.slot_of[s] = kNoSlot;
         slot_gen[slot] = 0;
         free_stack[atomicAdd(free_top, 1)] = slot;
       }
+      ++k0;
     }
   }
 }

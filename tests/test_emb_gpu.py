@@ -181,7 +181,7 @@ def test_uvm_cache_bit_identical_to_zero_copy(cuda_ctx, coracle):
     ahead) give exactly the zero-copy results, incl. rows shared by
     consecutive batches and slot reuse under a small cache."""
     ref_out, ref_rows = _train(cuda_ctx, coracle, cached=False)
-    for nslots in (4096, 1200):
+    for nslots in (4096, 1800):
         out, rows = _train(cuda_ctx, coracle, cached=True, nslots=nslots)
         for a, b in zip(out, ref_out):
             assert torch_equal(a, b)
