@@ -241,13 +241,17 @@ int rs_emb_forward(rs_emb* e, uint64_t batch, const uint32_t* offsets,
 int rs_emb_backward(rs_emb* e, uint64_t batch, const uint32_t* offsets,
                     const uint32_t* indices, const float* grad_pooled, float lr);
 /* HBM staging of slow-tier rows, overlapped with compute: after
- * rs_emb_enable_uvm_cache(nslots), rs_emb_prefetch(batch k+1) — called while
- * batch k computes — copies batch k+1's slow rows (deduplicated) into HBM on a
- * side stream; the forward/backward of that batch use the staged copies and a
- * side-stream write-back returns updated rows to the host tier.  At most one
- * batch ahead; results are bit-identical to the zero-copy path.  nslots should
- * be >= 2x the unique slow rows of one batch.  rs_emb_flush writes every
- * staged row back (read_rows / init_weights do so implicitly). */
+ * rs_emb_enable_uvm_cache(nslots), rs_emb_prefetch(batch k+1) — called after
+ * batch k's forward — lists batch k+1's slow rows that are not staged yet
+ * (claim kernel on the operator's stream); a host worker gathers them from
+ * the host tier and the copy engines move them into HBM slots while batch k's
+ * backward runs.  The forward/backward of batch k+1 use the staged copies;
+ * rows no live batch needs are evicted one step after their last use and
+ * returned to the host tier the same way (DMA + host scatter).  At most two
+ * prefetched batches pending; results are bit-identical to the zero-copy
+ * path.  nslots should be >= 4x the unique slow rows of one batch.
+ * rs_emb_flush writes every staged row back (read_rows / init_weights do so
+ * implicitly). */
 int rs_emb_enable_uvm_cache(rs_emb* e, uint32_t nslots);
 int rs_emb_prefetch(rs_emb* e, uint64_t batch, const uint32_t* offsets, const uint32_t* indices);
 int rs_emb_flush(rs_emb* e);
@@ -256,6 +260,11 @@ int rs_emb_read_rows(rs_emb* e, uint32_t t, const uint32_t* rows, uint64_t n,
                      float* out, float* momentum_out);
 /* Bytes of HBM / pinned host memory held by the tiers. */
 int rs_emb_memory(const rs_emb* e, uint64_t* hbm_bytes, uint64_t* host_bytes);
+/* Kernel-only time of the forward / backward kernel sequences since the last
+ * reset (CUDA events on the operator's stream around the kernels, excluding
+ * slow-row staging waits), and how many calls it covers.  Synchronises. */
+int rs_emb_kernel_times(rs_emb* e, double* fwd_ms, uint64_t* n_fwd, double* bwd_ms, uint64_t* n_bwd,
+                        int reset);
 
 /* ------------------------------------------------------------- primitives
  * The device-wide stable LSD radix sort behind K2 and K5 (device buffers,

@@ -110,6 +110,7 @@ _SIGS = {
     "rs_emb_prefetch": ([P, u64, P, P], i32),
     "rs_emb_flush": ([P], i32),
     "rs_emb_memory": ([P, P, P], i32),
+    "rs_emb_kernel_times": ([P, P, P, P, P, i32], i32),
     "rs_radix_sort_pairs": ([P, P, P, u64, i32], i32),
     "rs_gen_batch": ([P, u32, P, u64, u64, u64, P, P, u64, P], i32),
     "rs_kjt_to_records": ([P, u32, P, u64, u64, P, P, P, P, P, P], i32),

@@ -27,6 +27,7 @@ void emb_enable_cache(rs_emb*, uint32_t);
 void emb_prefetch(rs_emb*, uint64_t, const uint32_t*, const uint32_t*);
 void emb_flush(rs_emb*);
 void emb_memory(const rs_emb*, uint64_t*, uint64_t*);
+void emb_kernel_times(rs_emb*, double*, uint64_t*, double*, uint64_t*, int);
 void profile_view(const rs_profile*, uint32_t, rs_feature_stats*);
 uint32_t profile_tables(const rs_profile*);
 uint64_t profile_selected(const rs_profile*);
@@ -298,6 +299,13 @@ int rs_radix_sort_pairs(rs_context* c, uint32_t* keys, uint32_t* vals, uint64_t 
     if (end_bit < 0 || end_bit > 32) throw rs::InvalidArgument("radix_sort: end_bit in [0, 32]");
     rs::Scratch scr = c->scratch(rs::radix_sort_scratch_bytes(n) + (4 << 20));
     rs::radix_sort_pairs(keys, vals, n, end_bit, scr, c->stream);
+  });
+}
+
+int rs_emb_kernel_times(rs_emb* e, double* fwd_ms, uint64_t* n_fwd, double* bwd_ms, uint64_t* n_bwd, int reset) {
+  return guarded([&] {
+    need(e, "emb");
+    rs::emb_kernel_times(e, fwd_ms, n_fwd, bwd_ms, n_bwd, reset);
   });
 }
 

@@ -356,6 +356,39 @@ struct rs_emb {
   const TableDev* cur_tables = nullptr;  // tables the running forward/backward use
   cudaStream_t side = nullptr;
   cudaEvent_t ev_main = nullptr, ev_gather[4] = {nullptr, nullptr, nullptr, nullptr};
+  // kernel-only timing: event pairs around the forward / backward kernel
+  // sequences (excluding staging waits), harvested by rs_emb_kernel_times
+  struct Timer {
+    static constexpr int kRing = 64;
+    cudaEvent_t ev[kRing][2] = {};
+    int n = 0;
+    double ms = 0;
+    uint64_t count = 0;
+    void begin(cudaStream_t s) {
+      if (n == kRing) harvest();
+      if (!ev[n][0]) {
+        RS_CUDA(cudaEventCreate(&ev[n][0]));
+        RS_CUDA(cudaEventCreate(&ev[n][1]));
+      }
+      RS_CUDA(cudaEventRecord(ev[n][0], s));
+    }
+    void end(cudaStream_t s) { RS_CUDA(cudaEventRecord(ev[n++][1], s)); }
+    void harvest() {
+      for (int i = 0; i < n; ++i) {
+        float t = 0;
+        RS_CUDA(cudaEventSynchronize(ev[i][1]));
+        RS_CUDA(cudaEventElapsedTime(&t, ev[i][0], ev[i][1]));
+        ms += t;
+        ++count;
+      }
+      n = 0;
+    }
+    ~Timer() {
+      for (auto& p : ev)
+        for (cudaEvent_t x : p)
+          if (x) cudaEventDestroy(x);
+    }
+  } t_fwd, t_bwd;
   std::vector<uint64_t> pending;  // prefetched generations, oldest first
   int64_t cur_gen = -1;           // staged generation of the running step (-1: zero-copy)
   int64_t done_gen = -1;          // finished generation, evicted one step later
@@ -910,6 +943,7 @@ void emb_forward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx
                  uint64_t* hits) {
   if (B == 0 || B > e->max_batch) throw InvalidArgument("emb_forward: batch outside [1, max_batch]");
   begin_step(e);
+  e->t_fwd.begin(e->ctx->stream);
   auto* h = reinterpret_cast<unsigned long long*>(hits);
   for (const auto& c : e->classes) {
     switch (c.G * 100 + c.VPL) {
@@ -926,6 +960,20 @@ void emb_forward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx
     }
   }
   RS_LAUNCH_CHECK();
+  e->t_fwd.end(e->ctx->stream);
+}
+
+void emb_kernel_times(rs_emb* e, double* fwd_ms, uint64_t* n_fwd, double* bwd_ms, uint64_t* n_bwd, int reset) {
+  e->t_fwd.harvest();
+  e->t_bwd.harvest();
+  if (fwd_ms) *fwd_ms = e->t_fwd.ms;
+  if (n_fwd) *n_fwd = e->t_fwd.count;
+  if (bwd_ms) *bwd_ms = e->t_bwd.ms;
+  if (n_bwd) *n_bwd = e->t_bwd.count;
+  if (reset) {
+    e->t_fwd.ms = e->t_bwd.ms = 0;
+    e->t_fwd.count = e->t_bwd.count = 0;
+  }
 }
 
 // Short-segment bag pass for one lane class over its window range [wlo, whi).
@@ -1010,6 +1058,7 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
   }
   RS_CUDA(cudaMemcpyAsync(e->d_meta, e->h_meta, e->meta_words * 4, cudaMemcpyHostToDevice, st));
   RS_CUDA(cudaMemsetAsync(e->d_err, 0, 4, st));
+  e->t_bwd.begin(st);
   {
     const uint64_t nb = uint64_t(e->T) * B;
     unsigned g = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((nb / 32 + 7) / 8, uint64_t(sm_count()) * 16)));
@@ -1064,6 +1113,7 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
     case 8: launch_long<8>(e, a); break;
     default: throw Error(-9, "emb_backward: unsupported dim");
   }
+  e->t_bwd.end(st);
   RS_LAUNCH_CHECK();
 }
 

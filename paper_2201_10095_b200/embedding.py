@@ -102,6 +102,15 @@ class TieredEmbeddingBag:
                                                ptr(out), ptr(mom)))
         return out, mom
 
+    def kernel_times(self, reset: bool = False):
+        """(fwd_ms, n_fwd, bwd_ms, n_bwd): summed kernel-only times of the
+        forward / backward kernel sequences (CUDA events on the operator's
+        stream, excluding staging waits) since the last reset."""
+        f, nf, b, nb = C.c_double(), C.c_uint64(), C.c_double(), C.c_uint64()
+        _lib.check(_lib.lib().rs_emb_kernel_times(self.h, C.byref(f), C.byref(nf), C.byref(b),
+                                                  C.byref(nb), int(reset)))
+        return float(f.value), int(nf.value), float(b.value), int(nb.value)
+
     def memory(self):
         a, b = C.c_uint64(), C.c_uint64()
         _lib.check(_lib.lib().rs_emb_memory(self.h, C.byref(a), C.byref(b)))
