@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(kFwdThreads, MINB)
 forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__ cls_tables,
                uint32_t ntab, uint64_t B, const uint32_t* __restrict__ offsets,
                const uint32_t* __restrict__ indices, float* __restrict__ out, uint64_t stride,
-               unsigned long long* __restrict__ hits) {
+               unsigned long long* __restrict__ hits, uint32_t* __restrict__ keys,
+               uint32_t* __restrict__ vals, uint64_t max_keys, unsigned* __restrict__ err) {
   constexpr int BPW = 32 / G;
   constexpr int kFwdUnroll = UNR;
   const int lane = threadIdx.x & 31;
@@ -140,9 +141,24 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
       const uint32_t n = min(uint32_t(G), e - base);
       int32_t ent = 0;
       if (uint32_t(lg) < n) {
-        const uint32_t idx = ld_stream_u32(indices + base + lg);
+        const uint32_t l = base + lg;
+        uint32_t idx = ld_stream_u32(indices + l);
+        if (idx >= td.hash_size) {  // reported by the next backward / rs_emb_check
+          atomicOr(err, 1u);
+          idx = 0;
+        }
         ent = td.remap[idx];
         fast += ent >= 0;
+        // the backward's sort keys, while the remap entry is in hand
+        // (key = table key base + storage slot, value = sample)
+        if (keys) {
+          if (l < max_keys) {
+            keys[l] = td.key_base + slot_of_entry(td, ent);
+            vals[l] = uint32_t(b);
+          } else {
+            atomicOr(err, 2u);
+          }
+        }
       }
       for (uint32_t j = 0; j < n; j += kFwdUnroll) {
         float4 v[kFwdUnroll][VPL];
@@ -322,6 +338,11 @@ struct rs_emb {
   // backward buffers
   uint32_t* keys = nullptr;
   uint32_t* vals = nullptr;
+  // the last forward wrote (keys, vals) for its batch: a backward of the same
+  // (offsets, indices, batch) skips keygen
+  const uint32_t* keys_off = nullptr;
+  const uint32_t* keys_idx = nullptr;
+  uint64_t keys_B = 0;
   // HBM staging of slow rows (uvm_cache.cuh)
   uint32_t nslots = 0;
   float* staging = nullptr;
@@ -616,7 +637,7 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
     RS_CUDA(cudaMalloc(&e->sort_scratch, e->sort_scratch_bytes));
     // per-backward metadata: tpos[T+1] | wstart[T+1] | wtab[T] (class-major
     // window work map)
-    const size_t meta = 3 * size_t(T) + 2;
+    const size_t meta = 3 * size_t(T) + 3;  // + the error word read back with tpos
     e->meta_words = meta;
     RS_CUDA(cudaMalloc(&e->d_meta, meta * 4));
     RS_CUDA(cudaHostAlloc(&e->h_meta, meta * 4, cudaHostAllocDefault));
@@ -927,7 +948,7 @@ static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint
     return v ? atoi(v) : 0;
   }();
   auto args = std::make_tuple(e->cur_tables, c.d_list, uint32_t(c.tables.size()), B, off, idx, out,
-                              e->total_dim, hits);
+                              e->total_dim, hits, e->keys, e->vals, uint64_t(e->max_lookups), e->d_err);
   auto go = [&](auto kern) {
     std::apply([&](auto... a) { kern<<<grid, emb::kFwdThreads, 0, e->ctx->stream>>>(a...); }, args);
   };
@@ -944,6 +965,9 @@ void emb_forward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx
   if (B == 0 || B > e->max_batch) throw InvalidArgument("emb_forward: batch outside [1, max_batch]");
   begin_step(e);
   e->t_fwd.begin(e->ctx->stream);
+  e->keys_off = off;
+  e->keys_idx = idx;
+  e->keys_B = B;
   auto* h = reinterpret_cast<unsigned long long*>(hits);
   for (const auto& c : e->classes) {
     switch (c.G * 100 + c.VPL) {
@@ -1030,8 +1054,19 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
   cudaStream_t st = e->ctx->stream;
   const uint32_t T = e->T;
   uint32_t* tpos = e->h_meta;  // offsets[t*B], t = 0..T
+  uint32_t* herr = e->h_meta + e->meta_words - 1;
   RS_CUDA(cudaMemcpy2DAsync(tpos, 4, off, size_t(B) * 4, 4, T + 1, cudaMemcpyDeviceToHost, st));
+  RS_CUDA(cudaMemcpyAsync(herr, e->d_err, 4, cudaMemcpyDeviceToHost, st));
   RS_CUDA(cudaStreamSynchronize(st));
+  if (*herr) {
+    RS_CUDA(cudaMemsetAsync(e->d_err, 0, 4, st));
+    e->keys_off = nullptr;
+    if (*herr & 1u) throw InvalidArgument("emb: an index is outside its table's hash_size");
+    throw InvalidArgument("emb: more lookups than max_lookups");
+  }
+  // keys from the forward of this very batch?  (the sort below consumes them)
+  const bool have_keys = e->keys_off == off && e->keys_idx == idx && e->keys_B == B;
+  e->keys_off = nullptr;
   const uint32_t L = tpos[T];
   if (tpos[0] != 0) throw InvalidArgument("emb_backward: offsets must start at 0");
   if (L > e->max_lookups) throw InvalidArgument("emb_backward: more lookups than max_lookups");
@@ -1057,9 +1092,8 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
     wstart[T] = acc;
   }
   RS_CUDA(cudaMemcpyAsync(e->d_meta, e->h_meta, e->meta_words * 4, cudaMemcpyHostToDevice, st));
-  RS_CUDA(cudaMemsetAsync(e->d_err, 0, 4, st));
   e->t_bwd.begin(st);
-  {
+  if (!have_keys) {
     const uint64_t nb = uint64_t(e->T) * B;
     unsigned g = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((nb / 32 + 7) / 8, uint64_t(sm_count()) * 16)));
     emb::keygen_kernel<<<g, 256, 0, st>>>(e->d_tables, e->T, B, off, idx, e->keys, e->vals, e->d_err);

@@ -224,3 +224,25 @@ def test_operator_rejects_bad_inputs(cuda_ctx):
     bad = sp.RemapTable(0, 10, 5, 0, np.arange(10, dtype=np.int32))  # entry beyond hbm_rows
     with pytest.raises(sp.InvalidArgument):
         sp.TieredEmbeddingBag([spec], [bad], 4, 16, ctx=cuda_ctx)
+
+
+def test_out_of_range_index_is_reported(cuda_ctx, coracle):
+    """An index >= hash_size never reads out of bounds; the next backward
+    raises InvalidArgument (the reference rejects hashed ids outside H)."""
+    import torch
+
+    rng = np.random.default_rng(8)
+    specs, remaps, offsets, idx, d_off, d_idx, _ = _setup(coracle, [16], [100], [0.5], 8, 4, rng)
+    op = sp.TieredEmbeddingBag(specs, remaps, 8, max(1, idx.size), "sgd", ctx=cuda_ctx)
+    op.init_weights(SEED, SCALE)
+    bad = d_idx.clone()
+    if bad.numel():
+        bad[0] = 100  # == hash_size
+    y = op.forward(d_off, bad, 8)
+    with pytest.raises(sp.InvalidArgument):
+        op.backward(d_off, bad, y, 8, 0.1)
+    # the error is consumed: a clean batch runs again
+    y = op.forward(d_off, d_idx, 8)
+    op.backward(d_off, d_idx, y, 8, 0.1)
+    torch.cuda.synchronize()
+    op.close()
