@@ -943,10 +943,6 @@ static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint
   const uint64_t warps = (B + BPW - 1) / BPW * c.tables.size();
   const uint64_t blocks = (warps * 32 + emb::kFwdThreads - 1) / emb::kFwdThreads;
   const unsigned grid = std::max(1u, unsigned(std::min<uint64_t>(blocks, uint64_t(sm_count()) * 64)));
-  static const int variant = [] {
-    const char* v = getenv("RS_FWD_VARIANT");
-    return v ? atoi(v) : 0;
-  }();
   auto args = std::make_tuple(e->cur_tables, c.d_list, uint32_t(c.tables.size()), B, off, idx, out,
                               e->total_dim, hits, e->keys, e->vals, uint64_t(e->max_lookups), e->d_err);
   auto go = [&](auto kern) {
@@ -955,7 +951,6 @@ static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint
   // (unroll, min blocks/SM): measured on B200 RM1 all-HBM — (4, 6) 1.15 ms,
   // (2, 8) 1.14, (4, 8) 1.17, (6, 6) 1.22, (8, 6) 1.55, (8, 1) 1.85
   if (VPL > 1) go(emb::forward_kernel<G, VPL, 8, 1>);
-  else if (variant == 1) go(emb::forward_kernel<G, VPL, 2, 8>);
   else go(emb::forward_kernel<G, VPL, 4, 6>);
   RS_COUNT(1);
 }

@@ -246,3 +246,40 @@ def test_out_of_range_index_is_reported(cuda_ctx, coracle):
     op.backward(d_off, d_idx, y, 8, 0.1)
     torch.cuda.synchronize()
     op.close()
+
+
+@pytest.mark.parametrize("opt", ["sgd", "rowwise_adagrad"])
+def test_backward_tree_edges(cuda_ctx, coracle, opt):
+    """Segment lengths on every edge of the reduction tree (oracle.h): 1, 31,
+    32 (one piece), 33 (two pieces), 2048 (64 pieces = one group), 2049 (two
+    groups), 4160 — bit-exact vs the oracle, both tiers."""
+    import torch
+
+    counts = [1, 31, 32, 33, 2048, 2049, 4160, 5]
+    H = len(counts)
+    rng = np.random.default_rng(21)
+    idx = np.repeat(np.arange(H, dtype=np.uint32), counts)
+    rng.shuffle(idx)
+    B = idx.size  # one lookup per bag
+    offsets = np.arange(B + 1, dtype=np.uint32)
+    spec = TableSpec(3, H, H, 64, 4)
+    st = sp.FeatureStats(3, 1.0, 1.0, H, B, np.zeros(101, np.uint64), np.zeros(H),
+                         np.arange(H, dtype=np.uint32))
+    remap = sp.build_remap(PlanEntry(3, 0, 0, 4), st, spec)  # rows 0-3 fast, 4-7 slow
+    op = sp.TieredEmbeddingBag([spec], [remap], B, B, opt, eps=1e-8, ctx=cuda_ctx)
+    op.init_weights(SEED, SCALE)
+    grad = rng.standard_normal((B, 64)).astype(np.float32)
+    d_off = torch.from_numpy(offsets.view(np.int32)).cuda()
+    d_idx = torch.from_numpy(idx.view(np.int32)).cuda()
+    op.backward(d_off, d_idx, torch.from_numpy(grad).cuda(), B, 0.05)
+    torch.cuda.synchronize()
+    W = [coracle.init_table(SEED, 3, H, 64, SCALE)]
+    mom = [np.zeros(H, np.float32)]
+    coracle.emb_backward(B, [64], offsets.astype(np.uint64), idx, grad, W, mom,
+                         0 if opt == "sgd" else 1, 0.05, 1e-8,
+                         remaps=[(remap.entries, remap.hbm_rows)])
+    w, m = op.read_rows(0, np.arange(H, dtype=np.uint32))
+    assert np.array_equal(w.view(np.uint32), W[0].view(np.uint32))
+    if opt != "sgd":
+        assert np.array_equal(m.view(np.uint32), mom[0].view(np.uint32))
+    op.close()
