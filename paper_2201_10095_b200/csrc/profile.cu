@@ -289,6 +289,278 @@ hash_hist(const uint64_t* __restrict__ rec_sample, const uint32_t* __restrict__ 
   }
 }
 
+// ------------------------------------------------------------------ K1, partitioned
+// Large calls whose records tile the id pool contiguously (the reference
+// generator's layout and every trace built by kjt_to_trace) avoid global
+// atomics altogether:
+//   P0  per record: info = table index (or kSkip if not selected / not in the
+//       group), present/accesses counted per CTA in shared memory
+//   P1  id tiles (CTA per contiguous id range): expand ids -> row address ->
+//       bucket (address >> bbits); per-CTA bucket counts -> matrix[b][cta]
+//   scan of the bucket-major matrix (bucket regions, per-CTA sub-regions)
+//   P2  same expansion; each id's address appended to its (bucket, CTA)
+//       sub-region (shared-memory cursors)
+//   P3  CTA per (bucket, chunk): histogram of the chunk's addresses in shared
+//       memory (the Zipf head contends only within one SM), flushed to the
+//       global counters once
+// The expansion maps ids to records with a per-tile shared-memory window of
+// record offsets (one binary search per thread, then a forward walk), so ids
+// are read 8 per thread with vector loads.  Counts are exact integers in any
+// order.
+constexpr uint32_t kSkip = 0xFFFFFFFFu;
+constexpr int kPThreads = 256;
+constexpr int kPIds = 8;                         // ids per thread per tile
+constexpr int kPTile = kPThreads * kPIds;        // 2048 ids
+constexpr int kPRecWin = kPTile + 1;             // record window (len-1 records)
+constexpr uint32_t kPMaxBuckets = 8192;  // P1/P2 shared bucket counters (32 KB)
+constexpr int kP3Bits = 15;                      // 32768 counters per bucket (P3 shared histogram)
+
+// P0: contiguity check + per-record info.  bad |= 1 if the records do not
+// tile [0, N) in order.
+__global__ void __launch_bounds__(256)
+rec_info_kernel(const uint64_t* __restrict__ rec_sample, const uint32_t* __restrict__ rec_table,
+                const uint64_t* __restrict__ rec_offset, const uint32_t* __restrict__ rec_len, uint64_t R,
+                uint64_t N, Tables tp, double rate, uint64_t seed, bool count_records,
+                uint32_t* __restrict__ roff, uint32_t* __restrict__ rinfo,
+                unsigned long long* __restrict__ present, unsigned long long* __restrict__ accesses,
+                unsigned* __restrict__ bad, unsigned* __restrict__ err) {
+  extern __shared__ uint32_t pa[];
+  const bool use_sm = count_records && tp.J <= kMaxSmemTables;
+  if (use_sm)
+    for (uint32_t i = threadIdx.x; i < 2 * tp.J; i += blockDim.x) pa[i] = 0;
+  __syncthreads();
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < R; r += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t off = rec_offset[r];
+    const uint32_t len = rec_len[r];
+    const uint64_t nxt = r + 1 < R ? rec_offset[r + 1] : N;
+    if (off + len != nxt || (r == 0 && off != 0)) atomicOr(bad, 1u);
+    roff[r] = uint32_t(off);
+    uint32_t info = kSkip;
+    if (sample_selected(rec_sample[r], rate, seed)) {
+      const int t = lookup_table(tp.sorted_ids, tp.sorted_idx, tp.J, rec_table[r]);
+      if (t < 0) {
+        atomicOr(err, kErrUnknownTable);
+      } else {
+        if (count_records) {
+          if (use_sm) {
+            atomicAdd(&pa[t], 1u);
+            atomicAdd(&pa[tp.J + t], len);
+          } else {
+            atomicAdd(&present[t], 1ull);
+            atomicAdd(&accesses[t], (unsigned long long)len);
+          }
+        }
+        if (uint32_t(t) >= tp.t_lo && uint32_t(t) < tp.t_hi && len) info = uint32_t(t);
+      }
+    }
+    rinfo[r] = info;
+  }
+  if (use_sm) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < tp.J; i += blockDim.x) {
+      if (pa[i]) atomicAdd(&present[i], (unsigned long long)pa[i]);
+      if (pa[tp.J + i]) atomicAdd(&accesses[i], (unsigned long long)pa[tp.J + i]);
+    }
+  }
+}
+
+struct PSmem {
+  uint32_t woff[kPRecWin + 1];  // record offsets of the window (+ end sentinel)
+  uint32_t winfo[kPRecWin];
+  uint32_t r0, nrec;
+};
+
+// Expands tile [a, a + kPTile) of the id pool: fn(addr) for every selected id
+// of an in-group table.  *rcur: first record of the tile (advanced to the
+// first record of the next tile).
+template <bool RAW, class Fn>
+__device__ __forceinline__ void expand_tile(uint64_t a, uint64_t N, uint64_t R, const uint32_t* __restrict__ roff,
+                                            const uint32_t* __restrict__ rinfo, const uint32_t* __restrict__ ids,
+                                            const uint64_t* __restrict__ raw, const Tables& tp, PSmem& sm,
+                                            uint32_t& rcur, unsigned* __restrict__ err, unsigned* __restrict__ bad,
+                                            Fn&& fn) {
+  const uint64_t tend = min(N, a + kPTile);
+  // record window: records from rcur covering [a, tend), loaded 256 at a time
+  const uint32_t r0 = rcur;
+  uint32_t nwin = 0;
+  while (true) {
+    const uint32_t i = nwin + threadIdx.x;
+    const bool in = i < uint32_t(kPRecWin) && r0 + i < R;
+    uint32_t o = 0;
+    if (in) {
+      o = roff[r0 + i];
+      sm.woff[i] = o;
+      sm.winfo[i] = rinfo[r0 + i];
+    }
+    const uint32_t got = uint32_t(min(uint64_t(blockDim.x), min(uint64_t(kPRecWin) - nwin, R - r0 - nwin)));
+    // done once a loaded record starts at or beyond the tile end
+    const int covered = __syncthreads_or(in && o >= tend);
+    nwin += got;
+    if (covered || r0 + nwin >= R) break;
+    if (nwin >= uint32_t(kPRecWin)) {  // > 2048 empty records in one tile: caller falls back
+      if (threadIdx.x == 0) atomicOr(bad, 2u);
+      break;
+    }
+  }
+  if (threadIdx.x == 0) sm.woff[nwin] = r0 + nwin < R ? roff[r0 + nwin] : uint32_t(N);
+  __syncthreads();
+  // ids of this thread: q0 .. q0 + kPIds
+  const uint64_t q0 = a + uint64_t(threadIdx.x) * kPIds;
+  uint32_t idv[kPIds];
+  uint64_t rawv[RAW ? kPIds : 1];
+  if (q0 + kPIds <= tend) {
+    if (RAW) {
+#pragma unroll
+      for (int u = 0; u < kPIds; ++u) rawv[u] = ld_stream_u64(raw + q0 + u);
+    } else {
+      const uint4* p = reinterpret_cast<const uint4*>(ids + q0);
+#pragma unroll
+      for (int v = 0; v < kPIds / 4; ++v) {
+        const uint4 x = __ldcs(p + v);
+        idv[4 * v] = x.x;
+        idv[4 * v + 1] = x.y;
+        idv[4 * v + 2] = x.z;
+        idv[4 * v + 3] = x.w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < kPIds; ++u) {
+      if (q0 + u < tend) {
+        if (RAW) rawv[u] = raw[q0 + u];
+        else idv[u] = ids[q0 + u];
+      }
+    }
+  }
+  if (q0 < tend) {
+    // record of q0: largest k with woff[k] <= q0
+    uint32_t lo = 0, hi = nwin;
+    while (lo + 1 < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (sm.woff[mid] <= q0) lo = mid;
+      else hi = mid;
+    }
+    uint32_t k = lo;
+#pragma unroll
+    for (int u = 0; u < kPIds; ++u) {
+      const uint64_t q = q0 + u;
+      if (q < tend) {
+        while (k + 1 <= nwin && sm.woff[k + 1] <= q) ++k;
+        const uint32_t t = sm.winfo[k];
+        if (t != kSkip) {
+          const uint64_t H = tp.hsize[t];
+          const uint64_t row = RAW ? fast_mod(mix64(rawv[u]), H, tp.magic[t]) : uint64_t(idv[u]);
+          if (row >= H) atomicOr(err, kErrRowRange);
+          else fn(uint32_t(tp.base[t] + row));
+        }
+      }
+    }
+  }
+  // the next tile starts in the record holding id tend
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t lo = 0, hi = nwin;
+    while (lo + 1 < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (sm.woff[mid] <= tend) lo = mid;
+      else hi = mid;
+    }
+    sm.nrec = r0 + lo;
+  }
+  __syncthreads();
+  rcur = sm.nrec;
+}
+
+// First record of id a: largest r with roff[r] <= a.
+__device__ __forceinline__ uint32_t find_record(const uint32_t* __restrict__ roff, uint64_t R, uint64_t a) {
+  uint64_t lo = 0, hi = R;
+  while (lo + 1 < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (roff[mid] <= a) lo = mid;
+    else hi = mid;
+  }
+  return uint32_t(lo);
+}
+
+// P1 (SCATTER = false): bucket counts per CTA -> mat[b * nct + cta].
+// P2 (SCATTER = true): addresses into out[mat_scanned[b * nct + cta] + rank].
+template <bool RAW, bool SCATTER>
+__global__ void __launch_bounds__(kPThreads)
+part_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restrict__ rinfo, uint64_t R, uint64_t N,
+            const uint32_t* __restrict__ ids, const uint64_t* __restrict__ raw, Tables tp, uint32_t nb,
+            uint64_t ids_per_cta, uint32_t* __restrict__ mat, uint32_t* __restrict__ out,
+            unsigned* __restrict__ err, unsigned* __restrict__ bad) {
+  __shared__ PSmem sm;
+  extern __shared__ uint32_t cnt[];  // [nb] counts (P1) or cursors (P2)
+  const uint32_t nct = gridDim.x;
+  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x)
+    cnt[i] = SCATTER ? mat[uint64_t(i) * nct + blockIdx.x] : 0u;
+  const uint64_t a0 = uint64_t(blockIdx.x) * ids_per_cta;
+  const uint64_t a1 = min(N, a0 + ids_per_cta);
+  uint32_t rcur = 0;
+  if (threadIdx.x == 0 && a0 < a1) sm.nrec = find_record(roff, R, a0);
+  __syncthreads();
+  rcur = sm.nrec;
+  for (uint64_t a = a0; a < a1; a += kPTile) {
+    expand_tile<RAW>(a, a1, R, roff, rinfo, ids, raw, tp, sm, rcur, err, bad, [&](uint32_t addr) {
+      const uint32_t b = addr >> kP3Bits;
+      if (SCATTER) out[atomicAdd(&cnt[b], 1u)] = addr;
+      else atomicAdd(&cnt[b], 1u);
+    });
+  }
+  if (!SCATTER) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) mat[uint64_t(i) * nct + blockIdx.x] = cnt[i];
+  }
+}
+
+// bstart[b] = scanned[b * nct] (first position of bucket b), bstart[nb] = total.
+__global__ void part_bstart_kernel(const uint32_t* __restrict__ scanned, uint32_t nb, uint32_t nct,
+                                   const uint32_t* __restrict__ total, uint32_t* __restrict__ bstart) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < nb) bstart[b] = scanned[uint64_t(b) * nct];
+  if (b == nb) bstart[nb] = *total;
+}
+
+// Chunks of each bucket for P3: nchk[b] = ceil(len_b / chunk).
+__global__ void part_chunks_kernel(const uint32_t* __restrict__ bstart, uint32_t nb, uint32_t chunk,
+                                   uint32_t* __restrict__ nchk) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < nb) nchk[b] = (bstart[b + 1] - bstart[b] + chunk - 1) / chunk;
+}
+
+// P3: CTA per (bucket, chunk of the bucket's addresses); bstart[b] = first
+// position of bucket b (bstart[nb] = total), cbase = exclusive scan of the
+// chunk counts (cbase[nb] = total chunks).
+__global__ void __launch_bounds__(512)
+part_hist_kernel(const uint32_t* __restrict__ addrs, const uint32_t* __restrict__ bstart,
+                 const uint32_t* __restrict__ cbase, uint32_t nb, uint32_t chunk,
+                 uint32_t* __restrict__ counters, uint64_t ncounters) {
+  extern __shared__ uint32_t h[];
+  constexpr uint32_t span = 1u << kP3Bits;
+  const uint32_t total = cbase[nb];
+  for (uint32_t w = blockIdx.x; w < total; w += gridDim.x) {
+    uint32_t lo = 0, hi = nb;  // largest b with cbase[b] <= w (non-empty buckets only)
+    while (lo + 1 < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (cbase[mid] <= w) lo = mid;
+      else hi = mid;
+    }
+    while (lo + 1 < nb && cbase[lo + 1] <= w) ++lo;
+    const uint32_t b = lo, c = w - cbase[lo];
+    for (uint32_t i = threadIdx.x; i < span; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const uint32_t p0 = bstart[b] + c * chunk;
+    const uint32_t p1 = min(bstart[b + 1], p0 + chunk);
+    for (uint32_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) atomicAdd(&h[__ldcs(addrs + p) & (span - 1)], 1u);
+    __syncthreads();
+    const uint64_t cb = uint64_t(b) << kP3Bits;
+    for (uint32_t i = threadIdx.x; i < span; i += blockDim.x)
+      if (h[i] && cb + i < ncounters) atomicAdd(&counters[cb + i], h[i]);
+    __syncthreads();
+  }
+}
+
 // Hot-set selection after the sample phase: rows with count >= thr (group-local
 // addresses), appended up to kHotMax.
 __global__ void hot_select(const uint32_t* __restrict__ counters, uint64_t n, uint32_t thr,
@@ -519,6 +791,88 @@ __global__ void icdf_kernel(const uint64_t* __restrict__ cum_excl, const uint64_
 }
 
 template <class K>
+inline void set_smem_attr(K kern, size_t bytes);
+
+// K1 partitioned (P0..P3, see part_kernel).  Returns false (nothing counted,
+// record totals already taken by P0 when count_records) when the records do
+// not tile the id pool; the caller then runs the atomic kernel with
+// count_records = false.
+inline bool part_histogram(rs_context* ctx, Scratch& scr, bool raw, const uint64_t* d_rs, const uint32_t* d_rt,
+                           const uint64_t* d_ro, const uint32_t* d_rl, uint64_t R, uint64_t N,
+                           const uint32_t* d_ids, const uint64_t* d_raw, const Tables& tp, double rate, uint64_t seed,
+                           bool& count_records, uint32_t nb, uint32_t* d_cnt, uint64_t ncounters,
+                           unsigned long long* d_pres, unsigned long long* d_acc, unsigned* d_err) {
+  cudaStream_t st = ctx->stream;
+  const int sms = sm_count();
+  const size_t mark = scr.used;
+  uint32_t* roff = scr.take<uint32_t>(R);
+  uint32_t* rinfo = scr.take<uint32_t>(R);
+  unsigned* d_bad = scr.take<unsigned>(1);
+  RS_CUDA(cudaMemsetAsync(d_bad, 0, 4, st));
+  {
+    const size_t smem = count_records && tp.J <= kMaxSmemTables ? size_t(tp.J) * 8 : 0;
+    set_smem_attr(rec_info_kernel, smem);
+    const unsigned g = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((R + 255) / 256, uint64_t(sms) * 8)));
+    rec_info_kernel<<<g, 256, smem, st>>>(d_rs, d_rt, d_ro, d_rl, R, N, tp, rate, seed, count_records, roff, rinfo,
+                                          d_pres, d_acc, d_bad, d_err);
+    RS_COUNT(1);
+  }
+  count_records = false;  // taken by P0
+  unsigned* hbad = ctx->pinned_buf<unsigned>(1);
+  RS_CUDA(cudaMemcpyAsync(hbad, d_bad, 4, cudaMemcpyDeviceToHost, st));
+  ctx->sync();
+  if (*hbad) {  // records do not tile the id pool
+    scr.used = mark;
+    return false;
+  }
+  const uint32_t nct = uint32_t(sms) * 4;
+  const uint64_t ids_per_cta = ((N + nct - 1) / nct + kPTile - 1) / kPTile * kPTile;
+  uint32_t* mat = scr.take<uint32_t>(size_t(nb) * nct);
+  uint32_t* mscan = scr.take<uint32_t>(size_t(nb) * nct + 1);
+  const size_t psm = size_t(nb) * 4;
+  if (raw) {
+    set_smem_attr(part_kernel<true, false>, psm);
+    part_kernel<true, false><<<nct, kPThreads, psm, st>>>(roff, rinfo, R, N, d_ids, d_raw, tp, nb, ids_per_cta, mat,
+                                                          nullptr, d_err, d_bad);
+  } else {
+    set_smem_attr(part_kernel<false, false>, psm);
+    part_kernel<false, false><<<nct, kPThreads, psm, st>>>(roff, rinfo, R, N, d_ids, d_raw, tp, nb, ids_per_cta, mat,
+                                                           nullptr, d_err, d_bad);
+  }
+  RS_COUNT(1);
+  RS_CUDA(cudaMemcpyAsync(hbad, d_bad, 4, cudaMemcpyDeviceToHost, st));
+  ctx->sync();
+  if (*hbad) {  // a tile held more than 2048 empty records: redo with the atomic kernel
+    RS_CUDA(cudaMemsetAsync(d_err, 0, 4, st));
+    RS_CUDA(cudaMemsetAsync(d_cnt, 0, ncounters * 4, st));
+    scr.used = mark;
+    return false;
+  }
+  exclusive_scan<uint32_t>(ArrayIn<uint32_t>{mat}, size_t(nb) * nct, mscan, mscan + size_t(nb) * nct, scr, st);
+  uint32_t* bstart = scr.take<uint32_t>(nb + 1);
+  part_bstart_kernel<<<(nb + 256) / 256, 256, 0, st>>>(mscan, nb, nct, mscan + size_t(nb) * nct, bstart);
+  uint32_t* addrs = scr.take<uint32_t>(N);
+  if (raw)
+    part_kernel<true, true><<<nct, kPThreads, psm, st>>>(roff, rinfo, R, N, d_ids, d_raw, tp, nb, ids_per_cta, mscan,
+                                                         addrs, d_err, d_bad);
+  else
+    part_kernel<false, true><<<nct, kPThreads, psm, st>>>(roff, rinfo, R, N, d_ids, d_raw, tp, nb, ids_per_cta, mscan,
+                                                          addrs, d_err, d_bad);
+  constexpr uint32_t kChunkAddrs = 1u << 20;
+  uint32_t* nchk = scr.take<uint32_t>(nb + 1);
+  uint32_t* cbase = scr.take<uint32_t>(nb + 1);
+  part_chunks_kernel<<<(nb + 255) / 256, 256, 0, st>>>(bstart, nb, kChunkAddrs, nchk);
+  exclusive_scan<uint32_t>(ArrayIn<uint32_t>{nchk}, nb, cbase, cbase + nb, scr, st);
+  const size_t hsm = size_t(1) << kP3Bits << 2;
+  set_smem_attr(part_hist_kernel, hsm);
+  part_hist_kernel<<<unsigned(sms), 512, hsm, st>>>(addrs, bstart, cbase, nb, kChunkAddrs, d_cnt, ncounters);
+  RS_COUNT(5);
+  RS_LAUNCH_CHECK();
+  scr.used = mark;
+  return true;
+}
+
+template <class K>
 inline void set_smem_attr(K kern, size_t bytes) {
   if (bytes > 48 * 1024) RS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
 }
@@ -648,7 +1002,11 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
   size_t need = Scratch::bytes_for(R, 8) * 2 + Scratch::bytes_for(R, 4) * 2 +
                 Scratch::bytes_for(N, raw ? 8 : 4) + Scratch::bytes_for(J, 8) * 8 +
                 Scratch::bytes_for(maxH + 1, 4) * 6 + Scratch::bytes_for(maxH + 1, 8) * 3 +
-                radix_sort_scratch_bytes(maxH + 1) + (size_t(J) * 101 + 4096) * 8 + (8 << 20);
+                radix_sort_scratch_bytes(maxH + 1) + (size_t(J) * 101 + 4096) * 8 + (8 << 20) +
+                // partitioned histogram: record info, bucket matrix, addresses
+                Scratch::bytes_for(R, 4) * 2 + Scratch::bytes_for(size_t(kPMaxBuckets) * sm_count() * 4, 4) * 2 +
+                Scratch::bytes_for(N, 4) + Scratch::bytes_for(kPMaxBuckets + 1, 4) * 3 +
+                scan_scratch_bytes(size_t(kPMaxBuckets) * sm_count() * 4, 4);
   Scratch scr = ctx->scratch(need);
 
   const uint64_t* d_rs = on_dev ? tr->rec_sample : stage(tr->rec_sample, R, false, scr, st);
@@ -709,16 +1067,27 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
       unsigned grid = unsigned(std::min<uint64_t>((warps + 7) / 8, uint64_t(sms) * 8));
       grid = std::max(1u, grid);
       const size_t rsm = (J <= kMaxSmemTables ? size_t(J) * 8 : 0) + size_t(2) * kHistWarps * kWin * 4;
-      const bool cr = g == 0;
+      bool cr = g == 0;
       auto run = [&](auto kern, uint64_t lo, uint64_t hi, size_t smem, const uint32_t* hl, const unsigned* nh) {
         set_smem_attr(kern, smem);
         kern<<<grid, kHistThreads, smem, st>>>(d_rs, d_rt, d_ro, d_rl, lo, hi, d_ids, d_raw, tp, rate, seed, cr,
                                                hl, nh, d_cnt, d_pres, d_acc, d_err);
         RS_COUNT(1);
       };
-      // two phases when the call is large enough for a sample to find the head
+      // large calls with contiguous records: the partitioned histogram
+      bool done = false;
+      const uint32_t nb = uint32_t((base_g[Jg] + (uint64_t(1) << kP3Bits) - 1) >> kP3Bits);
+      const bool aligned = raw ? (reinterpret_cast<uintptr_t>(d_raw) % 8 == 0)
+                               : (reinterpret_cast<uintptr_t>(d_ids) % 16 == 0);
+      static const bool no_part = getenv("RS_PROFILE_NO_PARTITION") != nullptr;
+      if (!no_part && N >= (uint64_t(1) << 22) && nb <= kPMaxBuckets && aligned && R < (uint64_t(1) << 32)) {
+        done = part_histogram(ctx, scr, raw, d_rs, d_rt, d_ro, d_rl, R, N, d_ids, d_raw, tp, rate, seed, cr, nb,
+                              d_cnt, base_g[Jg], d_pres, d_acc, d_err);
+      }
+      // otherwise two phases when the call is large enough for a sample to find the head
       const uint64_t Rs = N >= (uint64_t(1) << 22) && R >= 64 * 32 ? (R / 64 + 31) / 32 * 32 : R;
-      if (Rs < R) {
+      if (done) {
+      } else if (Rs < R) {
         uint32_t* d_hot = scr.take<uint32_t>(kHotMax);
         unsigned* d_nh = scr.take<unsigned>(1);
         RS_CUDA(cudaMemsetAsync(d_nh, 0, 4, st));

@@ -164,3 +164,44 @@ def test_profile_many_tables_and_ragged(cuda_ctx, coracle):
         want = coracle.profile(tables, S, tr.rec_sample, tr.rec_table, tr.rec_offset, tr.rec_len,
                                tr.ids, rate, seed)
         assert_stats_equal(got, want)
+
+
+def test_profile_partitioned_vs_oracle(cuda_ctx, coracle):
+    """Calls of >= 2^22 ids with contiguous records take the partitioned
+    histogram (P0-P3); ragged/empty records, raw and hashed ids, sampled
+    rates.  A scrambled record order (non-contiguous) falls back to the
+    atomic kernel.  Bit-exact vs the oracle in every case."""
+    import oracle
+
+    rng = np.random.default_rng(31)
+    J, S = 6, 120_000
+    tables = [TableSpec(j + 3, 100_000, int(h), 16, 4)
+              for j, h in enumerate([5_000, 1_000_000, 77_777, 2_000_000, 300, 400_000])]
+    lens = rng.integers(0, 15, S * J).astype(np.uint32)  # includes empty records
+    lens[::7] = 40
+    rec_sample = np.repeat(np.arange(S, dtype=np.uint64), J)
+    rec_table = np.tile(np.array([t.table_id for t in tables], np.uint32), S)
+    rec_offset = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.uint64)
+    N = int(lens.sum())
+    assert N >= (1 << 22)
+    ranks = np.arange(1, 100_001, dtype=np.float64) ** -1.1
+    raw = rng.choice(100_000, size=N, p=ranks / ranks.sum()).astype(np.uint64) * np.uint64(7919)
+    tr_raw = Trace(tables, S, rec_sample, rec_table, rec_offset, lens, raw_ids=raw)
+    hashed = np.empty(N, np.uint32)
+    tab_of = np.repeat(np.tile(np.arange(J), S), lens)
+    for j, t in enumerate(tables):
+        m = tab_of == j
+        hashed[m] = coracle.hash_batch(raw[m], t.hash_size)
+    tr_ids = Trace(tables, S, rec_sample, rec_table, rec_offset, lens, ids=hashed)
+    for tr, rate, seed in [(tr_ids, 1.0, 0), (tr_raw, 1.0, 5), (tr_ids, 0.3, 9)]:
+        got = sp.profile(tr, rate, seed, ctx=cuda_ctx)
+        want = coracle.profile(tables, S, rec_sample, rec_table, rec_offset, lens, hashed, rate, seed)
+        assert_stats_equal(got, want)
+    order = rng.permutation(S * J)
+    tr_s = Trace(tables, S, rec_sample[order], rec_table[order], rec_offset[order], lens[order],
+                 ids=hashed)
+    got = sp.profile(tr_s, 1.0, 0, ctx=cuda_ctx)
+    want = coracle.profile(tables, S, rec_sample[order], rec_table[order], rec_offset[order],
+                           lens[order], hashed, 1.0, 0)
+    assert_stats_equal(got, want)
+    del oracle
