@@ -261,7 +261,7 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
         for t, w in enumerate(lspecs):
             lt = int(o[(t + 1) * B] - o[t * B])
             rb = 4 * w.table.dim
-            fb += lt * (rb + 8)
+            fb += lt * (rb + 8 + 8)  # row + index + remap entry; + key/value written for the backward
             u = np.unique(ih[o[t * B]:o[(t + 1) * B]]).size
             uq += u
             bb += u * 2 * rb + (8 * u if args.optimizer != "sgd" else 0)
@@ -294,13 +294,13 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
         if nvtx:
             torch.cuda.nvtx.range_push("bench_step")
         off, idx, n = batches[i % len(batches)] if T else (None, None, 0)
+        if cache and i + 1 < cache:  # stage batch i+1's slow rows while batch i runs
+            nb = batches[(i + 1) % len(batches)]
+            op.prefetch(nb[0], nb[1], B)
         if ev:
             ev[0].record()
         if T:
             op.forward(off, idx, B, out=pooled, hits=hits)
-        if cache and i + 1 < cache:  # stage batch i+1's slow rows behind batch i's backward
-            nb = batches[(i + 1) % len(batches)]
-            op.prefetch(nb[0], nb[1], B)
         if ev:
             ev[1].record()
         g = pooled
@@ -532,12 +532,12 @@ def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex, cache):
             op.prefetch(*view(0), B)
         for i in range(total):
             h2d(i + 2, total)
-            main.wait_event(ev_in[i % nb])
-            d_off, d_idx = view(i)
-            op.forward(d_off, d_idx, B, out=pooled, hits=hits)
             if cache and i + 1 < total:
                 main.wait_event(ev_in[(i + 1) % nb])
                 op.prefetch(*view(i + 1), B)
+            main.wait_event(ev_in[i % nb])
+            d_off, d_idx = view(i)
+            op.forward(d_off, d_idx, B, out=pooled, hits=hits)
             g = pooled
             if ex is not None:
                 g = ex.to_tables(ex.to_owners(pooled))

@@ -365,10 +365,12 @@ struct rs_emb {
   cudaEvent_t ev_claim[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_evict[4] = {nullptr, nullptr, nullptr, nullptr};  // ring: one per eviction in flight
   uint64_t n_evicts = 0;
+  cudaEvent_t last_claim = nullptr;  // the most recent claim (side stream)
   std::unique_ptr<rs::TaskQueue> worker;      // stage-in tasks (host tier -> slots)
   std::unique_ptr<rs::TaskQueue> out_worker;  // stage-out tasks (evicted rows -> host tier)
   std::unique_ptr<rs::ThreadPool> pool, out_pool;
   cudaStream_t side_out = nullptr;
+  cudaStream_t claim_stream = nullptr;
   uint64_t gather_seq[4] = {0, 0, 0, 0}, wb_seq = 0;
 
   TableDev* d_tables_c = nullptr;
@@ -439,10 +441,11 @@ struct rs_emb {
     out_worker.reset();
     pool.reset();
     out_pool.reset();
-    if (side_out) {
-      cudaStreamSynchronize(side_out);
-      cudaStreamDestroy(side_out);
-    }
+    for (cudaStream_t x : {side_out, claim_stream})
+      if (x) {
+        cudaStreamSynchronize(x);
+        cudaStreamDestroy(x);
+      }
     for (void* p : {(void*)h_bin, (void*)h_bout, (void*)h_ctab, (void*)h_crow, (void*)h_wtab, (void*)h_wrow,
                     (void*)h_cnt})
       if (p) cudaFreeHost(p);
@@ -711,6 +714,7 @@ void emb_enable_cache(rs_emb* e, uint32_t nslots) {
   }
   RS_CUDA(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
   RS_CUDA(cudaStreamCreateWithFlags(&e->side_out, cudaStreamNonBlocking));
+  RS_CUDA(cudaStreamCreateWithFlags(&e->claim_stream, cudaStreamNonBlocking));
   for (cudaEvent_t* ev : {&e->ev_main, &e->ev_gather[0], &e->ev_gather[1], &e->ev_gather[2], &e->ev_gather[3],
                           &e->ev_claim[0], &e->ev_claim[1], &e->ev_claim[2], &e->ev_claim[3], &e->ev_evict[0],
                           &e->ev_evict[1], &e->ev_evict[2], &e->ev_evict[3]})
@@ -824,6 +828,7 @@ static void stage_out_task(rs_emb* e, cudaEvent_t evicted) {
 static void evict(rs_emb* e, uint32_t gen_bits, uint32_t keep) {
   cudaStream_t st = e->ctx->stream;
   if (e->wb_seq) e->out_worker->wait(e->wb_seq);  // d_bout free again
+  if (e->last_claim) RS_CUDA(cudaStreamWaitEvent(st, e->last_claim, 0));  // slot tables settled
   RS_CUDA(cudaMemsetAsync(e->n_wb, 0, 4, st));
   const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((e->nslots + 255) / 256, uint64_t(sm_count()) * 8)));
   emb::uvm_evict_kernel<<<grid, 256, 0, st>>>(e->d_tables_c, e->nslots, gen_bits, keep, e->slot_gen, e->slot_tab,
@@ -865,9 +870,12 @@ void emb_prefetch(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
   if (clash) throw InvalidArgument("emb_prefetch: at most two prefetched batches may be pending");
   ++e->next_gen;
   // claim (index + remap read per lookup, an atomic per new slow row) on the
-  // caller's stream, ordered after the last eviction; the copies run behind
-  // the caller's next kernels
-  cudaStream_t st = e->ctx->stream;
+  // side stream, after everything the caller queued so far (its inputs and
+  // the last eviction) and before the next eviction (enqueue_writeback waits
+  // for it): it overlaps the caller's next kernels
+  RS_CUDA(cudaEventRecord(e->ev_main, e->ctx->stream));
+  cudaStream_t st = e->claim_stream;
+  RS_CUDA(cudaStreamWaitEvent(st, e->ev_main, 0));
   RS_CUDA(cudaMemsetAsync(e->ncopy, 0, 4, st));
   if (e->nslow_tabs) {
     const uint64_t work = uint64_t(e->nslow_tabs) * ((B + 31) / 32);
@@ -880,6 +888,7 @@ void emb_prefetch(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
     RS_LAUNCH_CHECK();
   }
   RS_CUDA(cudaEventRecord(e->ev_claim[g & 3], st));
+  e->last_claim = e->ev_claim[g & 3];
   const uint64_t ob = e->out_worker->posted();
   e->gather_seq[g & 3] = e->worker->post([e, g, ob] { stage_in_task(e, g, ob); });
   e->pending.push_back(g);
