@@ -43,7 +43,6 @@ struct TableDev {
   uint64_t hash_size;
   uint64_t col;      // column offset in pooled rows
   uint32_t dim;
-  uint32_t key_base; // backward key space offset
   uint64_t hbm_rows;
   uint64_t slow_rows;
   // HBM staging of slow-tier rows (uvm_cache.cuh); slot_of == nullptr means
@@ -74,13 +73,15 @@ __device__ __forceinline__ float* row_ptr(const TableDev& td, int32_t e) {
 __device__ __forceinline__ float* mom_ptr(const TableDev& td, int32_t e) {
   return e >= 0 ? td.mom_fast + uint64_t(e) : td.mom_slow + uint64_t(-int64_t(e) - 1);
 }
-// Backward keys are storage slots: key = key_base + (e >= 0 ? e : hbm_rows + (-e - 1)),
-// a bijection of the remap entries onto [key_base, key_base + hbm_rows + slow_rows).
+// Backward keys are storage slots within the table: key = e >= 0 ? e :
+// hbm_rows + (-e - 1), a bijection of the remap entries onto
+// [0, hbm_rows + slow_rows).  Tables keep their CSR position ranges (the
+// backward sorts each table's range on its own).
 __device__ __forceinline__ uint32_t slot_of_entry(const TableDev& td, int32_t e) {
   return e >= 0 ? uint32_t(e) : uint32_t(td.hbm_rows + uint64_t(-int64_t(e) - 1));
 }
 __device__ __forceinline__ int32_t entry_of_key(const TableDev& td, uint32_t key) {
-  const uint32_t s = key - td.key_base;
+  const uint32_t s = key;
   return s < td.hbm_rows ? int32_t(s) : int32_t(-int64_t(s - td.hbm_rows) - 1);
 }
 
@@ -153,7 +154,7 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
         // (key = table key base + storage slot, value = sample)
         if (keys) {
           if (l < max_keys) {
-            keys[l] = td.key_base + slot_of_entry(td, ent);
+            keys[l] = slot_of_entry(td, ent);
             vals[l] = uint32_t(b);
           } else {
             atomicOr(err, 2u);
@@ -199,7 +200,7 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
 }
 
 // ------------------------------------------------------------------ backward
-// keys[l] = key_base[t] + storage slot of remap[index], vals[l] = sample b, for
+// keys[l] = storage slot of remap[index] in table t, vals[l] = sample b, for
 // every lookup l of bag (t, b); warps flatten 32 bags' lookups so stores stay
 // coalesced.  Keying by slot lets the backward address rows without a remap
 // load and walks each tier in address order.
@@ -212,13 +213,12 @@ keygen_kernel(const TableDev* __restrict__ tables, uint32_t T, uint64_t B,
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t c = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; c * 32 < nbags; c += nwarps) {
     const uint64_t g = c * 32 + lane;
-    uint32_t s = 0, len = 0, kb = 0, t = 0;
+    uint32_t s = 0, len = 0, t = 0;
     uint64_t H = 0;
     if (g < nbags) {
       s = offsets[g];
       len = offsets[g + 1] - s;
       t = uint32_t(g / B);
-      kb = tables[t].key_base;
       H = tables[t].hash_size;
     }
     const uint32_t incl = warp_incl_scan(len);
@@ -233,7 +233,6 @@ keygen_kernel(const TableDev* __restrict__ tables, uint32_t T, uint64_t B,
         uint32_t ex = __shfl_sync(0xffffffffu, excl, k + step);
         if (ex <= q) k += step;
       }
-      const uint32_t kbk = __shfl_sync(0xffffffffu, kb, k);
       const uint64_t Hk = __shfl_sync(0xffffffffu, H, k);
       const uint64_t gk = c * 32 + k;
       if (q < total) {
@@ -241,7 +240,7 @@ keygen_kernel(const TableDev* __restrict__ tables, uint32_t T, uint64_t B,
         const uint32_t idx = indices[l];
         if (idx >= Hk) atomicOr(err, 1u);
         const TableDev& tdk = tables[gk / B];
-        keys[l] = kbk + slot_of_entry(tdk, tdk.remap[idx < Hk ? idx : 0u]);
+        keys[l] = slot_of_entry(tdk, tdk.remap[idx < Hk ? idx : 0u]);
         vals[l] = uint32_t(gk % B);
       }
     }
@@ -332,8 +331,11 @@ struct rs_emb {
     uint32_t* d_list = nullptr;
   };
   std::vector<Class> classes;
-  uint32_t* d_key_base_sorted = nullptr;
-  uint32_t key_bits = 0;
+  uint32_t key_bits = 0;  // max over tables of the slot-key width
+  // segmented sort tiles (per table): pos[ntiles+1] | cidx[ntiles] | cstride[ntiles]
+  uint32_t* d_tiles = nullptr;
+  uint32_t* h_tiles = nullptr;
+  size_t tiles_cap = 0;
   int bwd_vpl = 1;
   // backward buffers
   uint32_t* keys = nullptr;
@@ -461,7 +463,8 @@ struct rs_emb {
     if (remap_pool) cudaFree(remap_pool);
     for (auto& c : classes)
       if (c.d_list) cudaFree(c.d_list);
-    if (d_key_base_sorted) cudaFree(d_key_base_sorted);
+    if (d_tiles) cudaFree(d_tiles);
+    if (h_tiles) cudaFreeHost(h_tiles);
     if (keys) cudaFree(keys);
     if (vals) cudaFree(vals);
     for (void* p : {(void*)scount, (void*)sbase, (void*)segs, (void*)longs, (void*)long_np, (void*)long_ng,
@@ -505,7 +508,6 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
   try {
     cudaStream_t st = ctx->stream;
     size_t fb = 0, hb = 0, rb = 0;
-    uint64_t key_acc = 0;
     std::vector<size_t> foff(T), hoff(T), roff(T), mfoff(T), mhoff(T);
     for (uint32_t t = 0; t < T; ++t) {
       const rs_emb_table& x = tabs[t];
@@ -524,9 +526,6 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
       e->total_dim += x.dim;
       e->dmax = std::max(e->dmax, x.dim);
       e->table_ids.push_back(x.table_id);
-      if (key_acc + x.hbm_rows + x.slow_rows > 0x7FFFFFFFULL)
-        throw InvalidArgument("emb: sum of tier rows must be < 2^31 per operator (split the tables)");
-      key_acc += x.hbm_rows + x.slow_rows;
     }
     // Adagrad state (4 B/row) of BOTH tiers lives in HBM: a slow-tier row's
     // update then costs one PCIe row read + write instead of four transfers.
@@ -547,7 +546,6 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
     RS_CUDA(cudaMalloc(&e->remap_pool, std::max<size_t>(rb, 256)));
     RS_CUDA(cudaMalloc(&e->d_err, 16));
     uint64_t col = 0;
-    uint32_t kb = 0;
     e->h_tables.resize(T);
     for (uint32_t t = 0; t < T; ++t) {
       const rs_emb_table& x = tabs[t];
@@ -564,11 +562,9 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
       d.hash_size = x.hash_size;
       d.col = col;
       d.dim = x.dim;
-      d.key_base = kb;
       d.hbm_rows = x.hbm_rows;
       d.slow_rows = x.slow_rows;
       col += x.dim;
-      kb += uint32_t(x.hbm_rows + x.slow_rows);  // key span = storage slots
       // every remap entry must land inside its tier's allocation
       RS_CUDA(cudaMemsetAsync(e->d_err, 0, 4, st));
       unsigned g = unsigned(std::min<uint64_t>((x.hash_size + 255) / 256, uint64_t(sm_count()) * 8));
@@ -581,19 +577,10 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
                               ": remap entry outside the fast/slow tier sizes");
     }
     e->key_bits = 1;
-    while (e->key_bits < 32 && (uint64_t(1) << e->key_bits) < uint64_t(kb)) ++e->key_bits;
+    for (const auto& d : e->h_tables)
+      while (e->key_bits < 32 && (uint64_t(1) << e->key_bits) < d.hbm_rows + d.slow_rows) ++e->key_bits;
     RS_CUDA(cudaMalloc(&e->d_tables, sizeof(TableDev) * T));
     RS_CUDA(cudaMemcpyAsync(e->d_tables, e->h_tables.data(), sizeof(TableDev) * T, cudaMemcpyHostToDevice, st));
-    // backward table arrays: key_base[T+1] (sentinel = total keys), col[T], dim[T]
-    std::vector<uint32_t> kbs(3 * size_t(T) + 1);
-    for (uint32_t t = 0; t < T; ++t) {
-      kbs[t] = e->h_tables[t].key_base;
-      kbs[T + 1 + t] = uint32_t(e->h_tables[t].col);
-      kbs[2 * T + 1 + t] = e->h_tables[t].dim;
-    }
-    kbs[T] = kb;
-    RS_CUDA(cudaMalloc(&e->d_key_base_sorted, 4 * kbs.size()));
-    RS_CUDA(cudaMemcpyAsync(e->d_key_base_sorted, kbs.data(), 4 * kbs.size(), cudaMemcpyHostToDevice, st));
     // forward classes
     for (uint32_t t = 0; t < T; ++t) {
       const int G = lanes_for(tabs[t].dim);
@@ -636,7 +623,10 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
     const size_t max_groups = L / (emb::kChunk * emb::kGroupPieces) + e->long_cap + 1;
     RS_CUDA(cudaMalloc(&e->ppart, max_pieces * e->dmax * 4));
     RS_CUDA(cudaMalloc(&e->gpart, max_groups * e->dmax * 4));
-    e->sort_scratch_bytes = radix_sort_scratch_bytes(L) + (4 << 20);
+    e->sort_scratch_bytes = radix_sort_scratch_bytes(L, T) + (4 << 20);
+    e->tiles_cap = L / kSortTile + T + 2;
+    RS_CUDA(cudaMalloc(&e->d_tiles, 3 * e->tiles_cap * 4));
+    RS_CUDA(cudaHostAlloc(&e->h_tiles, 3 * e->tiles_cap * 4, cudaHostAllocDefault));
     RS_CUDA(cudaMalloc(&e->sort_scratch, e->sort_scratch_bytes));
     // per-backward metadata: tpos[T+1] | wstart[T+1] | wtab[T] (class-major
     // window work map)
@@ -1106,7 +1096,33 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
   Scratch scr;
   scr.base = e->sort_scratch;
   scr.cap = e->sort_scratch_bytes;
-  radix_sort_pairs(e->keys, e->vals, L, int(e->key_bits), scr, st);
+  {
+    // segmented sort: each table's CSR range sorted on its own (slot keys)
+    uint32_t* pos = e->h_tiles;
+    uint32_t nt = 0;
+    std::vector<uint32_t> cidx, cstr;
+    cidx.reserve(e->tiles_cap);
+    cstr.reserve(e->tiles_cap);
+    for (uint32_t t = 0; t < T; ++t) {
+      const uint32_t lt = tpos[t + 1] - tpos[t];
+      const uint32_t ntt = (lt + kSortTile - 1) / kSortTile;
+      for (uint32_t j = 0; j < ntt; ++j) {
+        pos[nt + j] = tpos[t] + j * kSortTile;
+        cidx.push_back(uint32_t(kRadix) * nt + j);
+        cstr.push_back(ntt);
+      }
+      nt += ntt;
+    }
+    pos[nt] = L;
+    memcpy(pos + nt + 1, cidx.data(), nt * 4);
+    memcpy(pos + 2 * nt + 1, cstr.data(), nt * 4);
+    RS_CUDA(cudaMemcpyAsync(e->d_tiles, e->h_tiles, (3 * size_t(nt) + 1) * 4, cudaMemcpyHostToDevice, st));
+    TileMap tm;
+    tm.pos = e->d_tiles;
+    tm.cidx = e->d_tiles + nt + 1;
+    tm.cstride = e->d_tiles + 2 * nt + 1;
+    radix_sort_pairs(e->keys, e->vals, L, int(e->key_bits), scr, st, tm, nt);
+  }
   emb::BwdArgs a{e->cur_tables, T, e->d_meta, e->keys, e->vals, grad, e->total_dim, e->dmax, lr, e->eps, e->opt};
   // segment list: count heads per window, scan, write descriptors
   const uint32_t W = wstart[T];

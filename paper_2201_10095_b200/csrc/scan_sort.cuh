@@ -198,20 +198,40 @@ __device__ __forceinline__ unsigned digit_peers(unsigned d, bool valid) {
   return valid ? pm : 0u;
 }
 
-// Per-tile digit counts, written digit-major: counts[d * ntiles + tile].
+// Tiles of the sort.  Default (pos == nullptr): tile b = [b*kSortTile, ..),
+// counts digit-major (counts[d * ntiles + b]).  Segmented: tile b =
+// [pos[b], pos[b+1]) never crosses a segment, counts laid out
+// [segment][digit][tile in segment] (index cidx[b] + d * cstride[b]), so one
+// global exclusive scan yields each segment's offsets and every segment is
+// sorted in place.
+struct TileMap {
+  const uint32_t* pos = nullptr;
+  const uint32_t* cidx = nullptr;
+  const uint32_t* cstride = nullptr;
+  __device__ __forceinline__ size_t begin(unsigned b) const { return pos ? pos[b] : size_t(b) * kSortTile; }
+  __device__ __forceinline__ size_t end(unsigned b, size_t n) const {
+    return pos ? pos[b + 1] : min(n, size_t(b + 1) * kSortTile);
+  }
+  __device__ __forceinline__ size_t cnt(unsigned b, unsigned d, unsigned ntiles) const {
+    return pos ? size_t(cidx[b]) + size_t(d) * cstride[b] : size_t(d) * ntiles + b;
+  }
+};
+
+// Per-tile digit counts (TileMap layout).
 static __global__ void __launch_bounds__(kSortThreads)
 radix_upsweep(const uint32_t* __restrict__ keys, size_t n, int shift, int nbits,
-              uint32_t* __restrict__ counts, unsigned ntiles) {
+              uint32_t* __restrict__ counts, unsigned ntiles, TileMap tm) {
   __shared__ uint32_t wc[kSortWarps][kRadix];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int i = lane; i < kRadix; i += 32) wc[w][i] = 0;
   __syncwarp();
   const unsigned mask = (1u << nbits) - 1u;
-  const size_t wbase = size_t(blockIdx.x) * kSortTile + size_t(w) * 32 * kSortItems;
+  const size_t tend = tm.end(blockIdx.x, n);
+  const size_t wbase = tm.begin(blockIdx.x) + size_t(w) * 32 * kSortItems;
 #pragma unroll
   for (int r = 0; r < kSortItems; ++r) {
     size_t k = wbase + size_t(r) * 32 + lane;
-    bool valid = k < n;
+    bool valid = k < tend;
     unsigned d = valid ? (keys[k] >> shift) & mask : 0u;
     unsigned peers = digit_peers<kRadixBits>(d, valid);
     if (valid && (peers & lanemask_lt()) == 0) wc[w][d] += __popc(peers);
@@ -222,7 +242,7 @@ radix_upsweep(const uint32_t* __restrict__ keys, size_t n, int shift, int nbits,
     uint32_t s = 0;
 #pragma unroll
     for (int ww = 0; ww < kSortWarps; ++ww) s += wc[ww][d];
-    counts[size_t(d) * ntiles + blockIdx.x] = s;
+    counts[tm.cnt(blockIdx.x, d, ntiles)] = s;
   }
 }
 
@@ -233,18 +253,19 @@ static __global__ void __launch_bounds__(kSortThreads)
 radix_downsweep(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                 size_t n, int shift, int nbits, const uint32_t* __restrict__ offsets,
                 unsigned ntiles, uint32_t* __restrict__ keys_out,
-                uint32_t* __restrict__ vals_out) {
+                uint32_t* __restrict__ vals_out, TileMap tm) {
   __shared__ uint32_t wc[kSortWarps][kRadix];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int i = lane; i < kRadix; i += 32) wc[w][i] = 0;
   __syncwarp();
   const unsigned mask = (1u << nbits) - 1u;
-  const size_t wbase = size_t(blockIdx.x) * kSortTile + size_t(w) * 32 * kSortItems;
+  const size_t tile0 = tm.begin(blockIdx.x), tend = tm.end(blockIdx.x, n);
+  const size_t wbase = tile0 + size_t(w) * 32 * kSortItems;
   uint32_t kk[kSortItems], vv[kSortItems], rank[kSortItems];
 #pragma unroll
   for (int r = 0; r < kSortItems; ++r) {
     size_t k = wbase + size_t(r) * 32 + lane;
-    bool valid = k < n;
+    bool valid = k < tend;
     kk[r] = valid ? keys_in[k] : 0u;
     if (HAS_VALUES) vv[r] = valid ? vals_in[k] : 0u;
     unsigned d = (kk[r] >> shift) & mask;
@@ -277,12 +298,12 @@ radix_downsweep(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict
   uint32_t tot_unused;
   const uint32_t ds = block_excl_scan<uint32_t, kSortThreads>(cnt, tot_unused);
   dstart[d0] = ds;
-  gbase[d0] = offsets[size_t(d0) * ntiles + blockIdx.x];
+  gbase[d0] = offsets[tm.cnt(blockIdx.x, d0, ntiles)];
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kSortItems; ++r) {
     size_t k = wbase + size_t(r) * 32 + lane;
-    if (k < n) {
+    if (k < tend) {
       const unsigned d = (kk[r] >> shift) & mask;
       const uint32_t tp = dstart[d] + wc[w][d] + rank[r];
       sk[tp] = kk[r];
@@ -290,8 +311,7 @@ radix_downsweep(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict
     }
   }
   __syncthreads();
-  const size_t tile0 = size_t(blockIdx.x) * kSortTile;
-  const uint32_t tn = uint32_t(min(size_t(kSortTile), n - tile0));
+  const uint32_t tn = uint32_t(tend - tile0);
   for (uint32_t i = threadIdx.x; i < tn; i += kSortThreads) {
     const uint32_t key = sk[i];
     const unsigned d = (key >> shift) & mask;
@@ -301,8 +321,9 @@ radix_downsweep(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict
   }
 }
 
-inline size_t radix_sort_scratch_bytes(size_t n) {
-  size_t tiles = (n + kSortTile - 1) / kSortTile;
+// extra_tiles: segmented sorts round every segment up to whole tiles
+inline size_t radix_sort_scratch_bytes(size_t n, size_t extra_tiles = 0) {
+  size_t tiles = (n + kSortTile - 1) / kSortTile + extra_tiles;
   size_t cnt = tiles * kRadix;
   return Scratch::bytes_for(cnt, 4) * 2 + scan_scratch_bytes(cnt, 4) +
          Scratch::bytes_for(n, 4) * 2 + 4096;
@@ -313,10 +334,10 @@ inline size_t radix_sort_scratch_bytes(size_t n) {
 // (A one-kernel-per-pass decoupled look-back variant measured slower on B200
 // RM1: 3.00 vs 2.93 ms backward.)
 inline void radix_sort_pairs(uint32_t* keys, uint32_t* vals, size_t n, int end_bit,
-                             Scratch& scr, cudaStream_t st) {
+                             Scratch& scr, cudaStream_t st, TileMap tm = TileMap{}, unsigned seg_tiles = 0) {
   if (n <= 1 || end_bit <= 0) return;
   if (n >= (size_t(1) << 32)) throw Error(-1, "radix_sort_pairs: n >= 2^32");
-  const unsigned ntiles = unsigned((n + kSortTile - 1) / kSortTile);
+  const unsigned ntiles = tm.pos ? seg_tiles : unsigned((n + kSortTile - 1) / kSortTile);
   size_t mark = scr.used;
   uint32_t* counts = scr.take<uint32_t>(size_t(ntiles) * kRadix);
   uint32_t* offs = scr.take<uint32_t>(size_t(ntiles) * kRadix);
@@ -325,17 +346,17 @@ inline void radix_sort_pairs(uint32_t* keys, uint32_t* vals, size_t n, int end_b
   uint32_t *ki = keys, *vi = vals, *ko = k2, *vo = v2;
   for (int shift = 0; shift < end_bit; shift += kRadixBits) {
     int nb = end_bit - shift < kRadixBits ? end_bit - shift : kRadixBits;
-    radix_upsweep<<<ntiles, kSortThreads, 0, st>>>(ki, n, shift, nb, counts, ntiles);
+    radix_upsweep<<<ntiles, kSortThreads, 0, st>>>(ki, n, shift, nb, counts, ntiles, tm);
     size_t m2 = scr.used;
     exclusive_scan<uint32_t>(ArrayIn<uint32_t>{counts}, size_t(ntiles) * kRadix, offs,
                              (uint32_t*)nullptr, scr, st);
     scr.used = m2;
     if (vals)
       radix_downsweep<true><<<ntiles, kSortThreads, 0, st>>>(ki, vi, n, shift, nb, offs,
-                                                             ntiles, ko, vo);
+                                                             ntiles, ko, vo, tm);
     else
       radix_downsweep<false><<<ntiles, kSortThreads, 0, st>>>(ki, nullptr, n, shift, nb,
-                                                              offs, ntiles, ko, nullptr);
+                                                              offs, ntiles, ko, nullptr, tm);
     RS_COUNT(2);
     RS_LAUNCH_CHECK();
     std::swap(ki, ko);
