@@ -9,5 +9,6 @@ timeout -s KILL 900 bash tools/breakdown.sh gpurun_out/launches_step.csv bench_s
 timeout -s KILL 900 bash tools/breakdown.sh gpurun_out/launches_prof.csv profile_call tools/prof_bench.py --ids 1e9 --reps 1 > gpurun_out/breakdown_prof.txt 2>&1; head -12 gpurun_out/breakdown_prof.txt
 NCU_SKIP=2 timeout -s KILL 900 bash tools/ncu_k.sh fwd bench_step forward_kernel bench.py --steps 2 --warmup 1 --no-greedy --no-cpu --profile-ids 0
 NCU_SKIP=2 timeout -s KILL 900 bash tools/ncu_k.sh seg bench_step bwd_seg_kernel bench.py --steps 2 --warmup 1 --no-greedy --no-cpu --profile-ids 0
-NCU_SKIP=1 timeout -s KILL 900 bash tools/ncu_k.sh hist profile_call hash_hist tools/prof_bench.py --ids 2e8 --reps 1
-for r in fwd seg hist; do python tools/ncu_read.py gpurun_out/$r.ncu-rep > gpurun_out/$r.txt 2>&1; cat gpurun_out/$r.txt; done
+NCU_SKIP=0 timeout -s KILL 900 bash tools/ncu_k.sh hist profile_call "part_hist_kernel" tools/prof_bench.py --ids 2e8 --reps 1
+NCU_SKIP=0 timeout -s KILL 900 bash tools/ncu_k.sh scat profile_call "part_kernel" tools/prof_bench.py --ids 2e8 --reps 1
+for r in fwd seg hist scat; do python tools/ncu_read.py gpurun_out/$r.ncu-rep > gpurun_out/$r.txt 2>&1; cat gpurun_out/$r.txt; done
