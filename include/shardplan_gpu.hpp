@@ -4,6 +4,7 @@
 // tests/acceptance_main.cpp): include this next to the reference headers and
 // call shardplan::gpu::profile / build_icdf / hash_utilization / hash_value /
 // build_remap / translate / simulate with exactly the reference's argument
+// types (plus the §8b extensions count_distinct_raw and TieredEmbeddingBag)
 // types and semantics; errors rethrow the reference's exception types
 // (include/shardplan/error.hpp:38-72, plus std::out_of_range for an unknown
 // table in profile, core/src/profiler.cpp:103).
@@ -219,5 +220,89 @@ inline SimReport simulate(const Trace& trace, const ShardingPlan& plan,
   rep.uvm_access_fraction = out.uvm_access_fraction;
   return rep;
 }
+
+/// SURVEY §8b extension: GenStats.distinct_raw_ids (core/src/workload.cpp:195-223)
+/// of a trace carrying raw ids, counted on the GPU (one value per trace table).
+inline std::vector<uint64_t> count_distinct_raw(const Trace& trace, const std::vector<uint64_t>& raw_ids) {
+  detail::TraceSoA soa(trace);
+  soa.view.ids = nullptr;
+  soa.view.raw_ids = raw_ids.data();
+  soa.view.num_ids = raw_ids.size();
+  std::vector<uint64_t> out(trace.tables.size());
+  check(rs_count_distinct_raw(Context::instance().get(), &soa.view, out.data()));
+  return out;
+}
+
+/// The tiered EmbeddingBag serving a sharding plan (the paper ran
+/// FBGEMM): rows the remap sends to the fast tier live in HBM,
+/// the others in pinned host memory.  forward = sum-pool (an empty bag pools
+/// to 0) with per-table fast/slow hit counts equal to
+/// simulate()'s accounting; backward = deterministic row-wise SGD or exact
+/// row-wise Adagrad.  Batches are table-major CSR in DEVICE memory
+/// (offsets[T*B+1], indices = original rows); the pooled output is
+/// [B, sum dim] fp32.  Calls are stream-ordered on the object's context.
+class TieredEmbeddingBag {
+ public:
+  enum class Optimizer { kSgd = RS_OPT_SGD, kRowwiseAdagrad = RS_OPT_ROWWISE_ADAGRAD };
+
+  TieredEmbeddingBag(const std::vector<TableSpec>& specs, const std::vector<RemapTable>& remaps,
+                     uint64_t max_batch, uint64_t max_lookups, Optimizer opt = Optimizer::kSgd,
+                     float eps = 1e-8f, Context& ctx = Context::instance())
+      : ctx_(ctx) {
+    if (specs.size() != remaps.size()) throw InvalidArgument("TieredEmbeddingBag: one remap per table");
+    std::vector<rs_emb_table> tabs;
+    for (size_t i = 0; i < specs.size(); ++i) {
+      const auto& s = specs[i];
+      const auto& r = remaps[i];
+      if (s.elem_bytes != 4) throw InvalidArgument("TieredEmbeddingBag: fp32 tables only (elem_bytes 4)");
+      tabs.push_back({s.table_id, s.hash_size, s.dim, r.entries.data(), RS_MEM_HOST, r.hbm_rows,
+                      s.hash_size - r.hbm_rows});
+      total_dim_ += s.dim;
+    }
+    check(rs_emb_create(ctx_.get(), static_cast<uint32_t>(tabs.size()), tabs.data(), max_batch, max_lookups,
+                        static_cast<int>(opt), eps, &e_));
+  }
+  ~TieredEmbeddingBag() {
+    if (e_) rs_emb_destroy(e_);
+  }
+  TieredEmbeddingBag(const TieredEmbeddingBag&) = delete;
+  TieredEmbeddingBag& operator=(const TieredEmbeddingBag&) = delete;
+
+  uint32_t total_dim() const { return total_dim_; }
+  void init_weights(uint64_t seed, float scale) { check(rs_emb_init_weights(e_, seed, scale)); }
+  void forward(uint64_t batch, const uint32_t* d_offsets, const uint32_t* d_indices, float* d_pooled,
+               uint64_t* d_hit_counts = nullptr) {
+    check(rs_emb_forward(e_, batch, d_offsets, d_indices, d_pooled, d_hit_counts));
+  }
+  void backward(uint64_t batch, const uint32_t* d_offsets, const uint32_t* d_indices, const float* d_grad,
+                float lr) {
+    check(rs_emb_backward(e_, batch, d_offsets, d_indices, d_grad, lr));
+  }
+  /// Slow-row staging (copy engines, one batch ahead): enable once, then
+  /// prefetch(batch k+1) before batch k's forward.
+  void enable_uvm_cache(uint32_t nslots) { check(rs_emb_enable_uvm_cache(e_, nslots)); }
+  void prefetch(uint64_t batch, const uint32_t* d_offsets, const uint32_t* d_indices) {
+    check(rs_emb_prefetch(e_, batch, d_offsets, d_indices));
+  }
+  void flush() { check(rs_emb_flush(e_)); }
+  /// Rows by ORIGINAL id (and their Adagrad state) into host vectors.
+  std::vector<float> read_rows(uint32_t table, const std::vector<uint32_t>& rows, uint32_t dim,
+                               std::vector<float>* momentum = nullptr) {
+    std::vector<float> out(rows.size() * dim);
+    std::vector<float> m(rows.size());
+    check(rs_emb_read_rows(e_, table, rows.data(), rows.size(), out.data(), m.data()));
+    if (momentum) *momentum = std::move(m);
+    return out;
+  }
+  /// Blocks until the object's queued work is done (before reading its
+  /// outputs from another stream).
+  void synchronize() { check(rs_context_synchronize(ctx_.get())); }
+  rs_emb* handle() const { return e_; }
+
+ private:
+  Context& ctx_;
+  rs_emb* e_ = nullptr;
+  uint32_t total_dim_ = 0;
+};
 
 }  // namespace shardplan::gpu

@@ -12,6 +12,8 @@
 #include "shardplan/milp.hpp"
 #include "shardplan_gpu.hpp"
 
+#include <cuda_runtime.h>
+
 using namespace shardplan;
 
 static int g_fail = 0, g_pass = 0;
@@ -167,6 +169,102 @@ int main() {
       CHECK(eq);
     }
     CHECK(throws<InvalidArgument>([&] { gpu::simulate(t, plan, gpu_r, sys, 1 << 30); }));
+  }
+  // TieredEmbeddingBag (the §8b operator) through the C++ shim: forward is
+  // the in-order fp32 sum of each bag's rows (bit-exact vs a host loop over
+  // read_rows), its hit counts are the remap's tier split, and the backward
+  // (SGD, grad = pooled) moves exactly the rows the batch touched.
+  {
+    std::vector<TableSpec> ftabs;  // fp32 tables only
+    std::vector<RemapTable> frem;
+    std::vector<uint32_t> tid;
+    for (size_t j = 0; j < tabs.size(); ++j)
+      if (tabs[j].elem_bytes == 4) {
+        ftabs.push_back(tabs[j]);
+        PlanEntry pe{tabs[j].table_id, 0, 0, tabs[j].hash_size / 2, 0.0, 0};
+        frem.push_back(gpu::build_remap(pe, stats[j], tabs[j]));
+        tid.push_back(tabs[j].table_id);
+      }
+    const uint32_t T = static_cast<uint32_t>(ftabs.size());
+    const uint64_t B = 256;
+    // table-major CSR of the trace's first B samples
+    std::vector<std::vector<std::vector<uint32_t>>> bags(T, std::vector<std::vector<uint32_t>>(B));
+    for (const auto& r : t.records) {
+      if (r.sample >= B) continue;
+      for (uint32_t k = 0; k < T; ++k)
+        if (t.tables[r.table].table_id == tid[k])
+          for (uint32_t q = 0; q < r.len; ++q) bags[k][r.sample].push_back(t.ids[r.offset + q]);
+    }
+    std::vector<uint32_t> off{0}, idx;
+    for (uint32_t k = 0; k < T; ++k)
+      for (uint64_t b = 0; b < B; ++b) {
+        idx.insert(idx.end(), bags[k][b].begin(), bags[k][b].end());
+        off.push_back(static_cast<uint32_t>(idx.size()));
+      }
+    gpu::TieredEmbeddingBag op(ftabs, frem, B, std::max<size_t>(1, idx.size()));
+    op.init_weights(7, 0.5f);
+    uint32_t *d_off = nullptr, *d_idx = nullptr;
+    float* d_out = nullptr;
+    uint64_t* d_hits = nullptr;
+    cudaMalloc(&d_off, off.size() * 4);
+    cudaMalloc(&d_idx, std::max<size_t>(1, idx.size()) * 4);
+    cudaMalloc(&d_out, B * op.total_dim() * 4);
+    cudaMalloc(&d_hits, 2 * T * 8);
+    cudaMemset(d_hits, 0, 2 * T * 8);
+    cudaMemcpy(d_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_idx, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice);
+    std::vector<std::vector<float>> W(T);
+    for (uint32_t k = 0; k < T; ++k) {
+      std::vector<uint32_t> rows(ftabs[k].hash_size);
+      for (uint32_t r = 0; r < rows.size(); ++r) rows[r] = r;
+      W[k] = op.read_rows(k, rows, ftabs[k].dim);
+    }
+    op.forward(B, d_off, d_idx, d_out, d_hits);
+    op.synchronize();  // the operator runs on the context's private stream
+    std::vector<float> y(B * op.total_dim());
+    std::vector<uint64_t> hits(2 * T);
+    cudaMemcpy(y.data(), d_out, y.size() * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(hits.data(), d_hits, hits.size() * 8, cudaMemcpyDeviceToHost);
+    bool fwd_ok = true, hits_ok = true;
+    uint32_t col = 0;
+    for (uint32_t k = 0; k < T; ++k) {
+      const uint32_t D = ftabs[k].dim;
+      uint64_t fast = 0, total = 0;
+      for (uint64_t b = 0; b < B; ++b) {
+        std::vector<float> acc(D, 0.0f);
+        for (uint32_t row : bags[k][b]) {
+          for (uint32_t d = 0; d < D; ++d) acc[d] = acc[d] + W[k][size_t(row) * D + d];
+          fast += frem[k].entries[row] >= 0;
+          ++total;
+        }
+        for (uint32_t d = 0; d < D; ++d) fwd_ok = fwd_ok && same(acc[d], y[b * op.total_dim() + col + d]);
+      }
+      hits_ok = hits_ok && hits[2 * k] == fast && hits[2 * k + 1] == total - fast;
+      col += D;
+    }
+    CHECK(fwd_ok);
+    CHECK(hits_ok);
+    op.backward(B, d_off, d_idx, d_out, 0.1f);
+    bool moved_ok = true;
+    for (uint32_t k = 0; k < T; ++k) {
+      std::vector<uint32_t> rows(ftabs[k].hash_size);
+      for (uint32_t r = 0; r < rows.size(); ++r) rows[r] = r;
+      auto w2 = op.read_rows(k, rows, ftabs[k].dim);
+      std::vector<char> touched(rows.size(), 0);
+      for (uint64_t b = 0; b < B; ++b)
+        for (uint32_t row : bags[k][b]) touched[row] = 1;
+      for (uint32_t r = 0; r < rows.size(); ++r) {
+        bool changed = false;
+        for (uint32_t d = 0; d < ftabs[k].dim; ++d)
+          changed = changed || !same(w2[size_t(r) * ftabs[k].dim + d], W[k][size_t(r) * ftabs[k].dim + d]);
+        if (!touched[r] && changed) moved_ok = false;
+      }
+    }
+    CHECK(moved_ok);
+    cudaFree(d_off);
+    cudaFree(d_idx);
+    cudaFree(d_out);
+    cudaFree(d_hits);
   }
   std::printf("drop-in parity: %d checks passed, %d failed\n", g_pass, g_fail);
   return g_fail ? 1 : 0;
