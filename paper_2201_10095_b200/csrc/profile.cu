@@ -312,7 +312,7 @@ constexpr int kPThreads = 256;
 constexpr int kPIds = 8;                         // ids per thread per tile
 constexpr int kPTile = kPThreads * kPIds;        // 2048 ids
 constexpr int kPRecWin = kPTile + 1;             // record window (len-1 records)
-constexpr uint32_t kPMaxBuckets = 8192;  // P1/P2 shared bucket counters (32 KB)
+constexpr uint32_t kPMaxBuckets = 4096;  // P2 shared bucket cursors + tile counts/offsets (48 KB)
 constexpr int kP3Bits = 15;                      // 32768 counters per bucket (P3 shared histogram)
 
 // P0: contiguity check + per-record info.  bad |= 1 if the records do not
@@ -451,7 +451,7 @@ __device__ __forceinline__ void expand_tile(uint64_t a, uint64_t N, uint64_t R, 
           const uint64_t H = tp.hsize[t];
           const uint64_t row = RAW ? fast_mod(mix64(rawv[u]), H, tp.magic[t]) : uint64_t(idv[u]);
           if (row >= H) atomicOr(err, kErrRowRange);
-          else fn(uint32_t(tp.base[t] + row));
+          else fn(uint32_t(tp.base[t] + row), u);
         }
       }
     }
@@ -491,7 +491,7 @@ part_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restrict__ rinf
             uint64_t ids_per_cta, uint32_t* __restrict__ mat, uint32_t* __restrict__ out,
             unsigned* __restrict__ err, unsigned* __restrict__ bad) {
   __shared__ PSmem sm;
-  extern __shared__ uint32_t cnt[];  // [nb] counts (P1) or cursors (P2)
+  extern __shared__ uint32_t cnt[];  // [nb] counts (P1) or cursors (P2) | P2: tile counts, offsets
   const uint32_t nct = gridDim.x;
   for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x)
     cnt[i] = SCATTER ? mat[uint64_t(i) * nct + blockIdx.x] : 0u;
@@ -501,16 +501,65 @@ part_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restrict__ rinf
   if (threadIdx.x == 0 && a0 < a1) sm.nrec = find_record(roff, R, a0);
   __syncthreads();
   rcur = sm.nrec;
-  for (uint64_t a = a0; a < a1; a += kPTile) {
-    expand_tile<RAW>(a, a1, R, roff, rinfo, ids, raw, tp, sm, rcur, err, bad, [&](uint32_t addr) {
-      const uint32_t b = addr >> kP3Bits;
-      if (SCATTER) out[atomicAdd(&cnt[b], 1u)] = addr;
-      else atomicAdd(&cnt[b], 1u);
-    });
-  }
   if (!SCATTER) {
+    for (uint64_t a = a0; a < a1; a += kPTile)
+      expand_tile<RAW>(a, a1, R, roff, rinfo, ids, raw, tp, sm, rcur, err, bad,
+                       [&](uint32_t addr, int) { atomicAdd(&cnt[addr >> kP3Bits], 1u); });
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) mat[uint64_t(i) * nct + blockIdx.x] = cnt[i];
+    return;
+  }
+  // P2: each tile's addresses are counting-sorted by bucket in shared memory
+  // and written as contiguous per-bucket runs (coalesced stores)
+  uint32_t* tcnt = cnt + nb;
+  uint32_t* toff = cnt + 2 * nb;
+  __shared__ uint32_t sa[kPTile], sr[kPTile], stage[kPTile];
+  __shared__ uint32_t s_total;
+  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) tcnt[i] = 0;
+  for (uint64_t a = a0; a < a1; a += kPTile) {
+    for (int u = 0; u < kPIds; ++u) sa[threadIdx.x * kPIds + u] = kSkip;
+    expand_tile<RAW>(a, a1, R, roff, rinfo, ids, raw, tp, sm, rcur, err, bad, [&](uint32_t addr, int u) {
+      sa[threadIdx.x * kPIds + u] = addr;
+      sr[threadIdx.x * kPIds + u] = atomicAdd(&tcnt[addr >> kP3Bits], 1u);
+    });
+    // expand_tile ends with a barrier: tile counts complete
+    uint32_t part = 0;
+    const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
+    for (uint32_t j = 0; j < per; ++j) {
+      const uint32_t b = threadIdx.x * per + j;
+      if (b < nb) part += tcnt[b];
+    }
+    uint32_t tot;
+    uint32_t run = block_excl_scan<uint32_t, kPThreads>(part, tot);
+    for (uint32_t j = 0; j < per; ++j) {
+      const uint32_t b = threadIdx.x * per + j;
+      if (b < nb) {
+        toff[b] = run;
+        run += tcnt[b];
+      }
+    }
+    if (threadIdx.x == 0) s_total = tot;
+    __syncthreads();
+    for (int u = 0; u < kPIds; ++u) {
+      const uint32_t x = sa[threadIdx.x * kPIds + u];
+      if (x != kSkip) stage[toff[x >> kP3Bits] + sr[threadIdx.x * kPIds + u]] = x;
+    }
+    __syncthreads();
+    const uint32_t total = s_total;
+    for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
+      const uint32_t x = stage[i];
+      const uint32_t b = x >> kP3Bits;
+      out[cnt[b] + (i - toff[b])] = x;
+    }
+    __syncthreads();
+    for (uint32_t j = 0; j < per; ++j) {
+      const uint32_t b = threadIdx.x * per + j;
+      if (b < nb) {
+        cnt[b] += tcnt[b];
+        tcnt[b] = 0;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -532,7 +581,7 @@ __global__ void part_chunks_kernel(const uint32_t* __restrict__ bstart, uint32_t
 // P3: CTA per (bucket, chunk of the bucket's addresses); bstart[b] = first
 // position of bucket b (bstart[nb] = total), cbase = exclusive scan of the
 // chunk counts (cbase[nb] = total chunks).
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(1024)
 part_hist_kernel(const uint32_t* __restrict__ addrs, const uint32_t* __restrict__ bstart,
                  const uint32_t* __restrict__ cbase, uint32_t nb, uint32_t chunk,
                  uint32_t* __restrict__ counters, uint64_t ncounters) {
@@ -552,7 +601,19 @@ part_hist_kernel(const uint32_t* __restrict__ addrs, const uint32_t* __restrict_
     __syncthreads();
     const uint32_t p0 = bstart[b] + c * chunk;
     const uint32_t p1 = min(bstart[b + 1], p0 + chunk);
-    for (uint32_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) atomicAdd(&h[__ldcs(addrs + p) & (span - 1)], 1u);
+    // 8 address loads in flight per thread, then their atomics
+    constexpr int U = 8;
+    for (uint32_t pb = p0; pb < p1; pb += U * blockDim.x) {
+      uint32_t x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t p = pb + u * blockDim.x + threadIdx.x;
+        x[u] = p < p1 ? __ldcs(addrs + p) : 0xFFFFFFFFu;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (x[u] != 0xFFFFFFFFu) atomicAdd(&h[x[u] & (span - 1)], 1u);
+    }
     __syncthreads();
     const uint64_t cb = uint64_t(b) << kP3Bits;
     for (uint32_t i = threadIdx.x; i < span; i += blockDim.x)
@@ -852,12 +913,16 @@ inline bool part_histogram(rs_context* ctx, Scratch& scr, bool raw, const uint64
   uint32_t* bstart = scr.take<uint32_t>(nb + 1);
   part_bstart_kernel<<<(nb + 256) / 256, 256, 0, st>>>(mscan, nb, nct, mscan + size_t(nb) * nct, bstart);
   uint32_t* addrs = scr.take<uint32_t>(N);
-  if (raw)
-    part_kernel<true, true><<<nct, kPThreads, psm, st>>>(roff, rinfo, R, N, d_ids, d_raw, tp, nb, ids_per_cta, mscan,
-                                                         addrs, d_err, d_bad);
-  else
-    part_kernel<false, true><<<nct, kPThreads, psm, st>>>(roff, rinfo, R, N, d_ids, d_raw, tp, nb, ids_per_cta, mscan,
-                                                          addrs, d_err, d_bad);
+  const size_t psm2 = 3 * psm;  // cursors | tile counts | tile offsets
+  if (raw) {
+    set_smem_attr(part_kernel<true, true>, psm2);
+    part_kernel<true, true><<<nct, kPThreads, psm2, st>>>(roff, rinfo, R, N, d_ids, d_raw, tp, nb, ids_per_cta,
+                                                          mscan, addrs, d_err, d_bad);
+  } else {
+    set_smem_attr(part_kernel<false, true>, psm2);
+    part_kernel<false, true><<<nct, kPThreads, psm2, st>>>(roff, rinfo, R, N, d_ids, d_raw, tp, nb, ids_per_cta,
+                                                           mscan, addrs, d_err, d_bad);
+  }
   constexpr uint32_t kChunkAddrs = 1u << 20;
   uint32_t* nchk = scr.take<uint32_t>(nb + 1);
   uint32_t* cbase = scr.take<uint32_t>(nb + 1);
@@ -865,16 +930,17 @@ inline bool part_histogram(rs_context* ctx, Scratch& scr, bool raw, const uint64
   exclusive_scan<uint32_t>(ArrayIn<uint32_t>{nchk}, nb, cbase, cbase + nb, scr, st);
   const size_t hsm = size_t(1) << kP3Bits << 2;
   set_smem_attr(part_hist_kernel, hsm);
-  part_hist_kernel<<<unsigned(sms), 512, hsm, st>>>(addrs, bstart, cbase, nb, kChunkAddrs, d_cnt, ncounters);
+  part_hist_kernel<<<unsigned(sms), 1024, hsm, st>>>(addrs, bstart, cbase, nb, kChunkAddrs, d_cnt, ncounters);
   RS_COUNT(5);
   RS_LAUNCH_CHECK();
   scr.used = mark;
   return true;
 }
 
+// Allows `bytes` of dynamic shared memory on top of the kernel's static usage.
 template <class K>
 inline void set_smem_attr(K kern, size_t bytes) {
-  if (bytes > 48 * 1024) RS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+  if (bytes > 16 * 1024) RS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
 }
 
 struct RankDevice {
