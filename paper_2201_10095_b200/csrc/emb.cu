@@ -1016,7 +1016,7 @@ template <int VPL>
 static void launch_long(rs_emb* e, const emb::BwdArgs& a) {
   const unsigned g = unsigned(sm_count()) * 8;
   cudaStream_t st = e->ctx->stream;
-  emb::bwd_lpiece_kernel<VPL><<<g, emb::kBwdThreads, 0, st>>>(a, e->longs, e->n_long, e->pbase, e->ppart);
+  emb::bwd_lpiece_kernel<16, 2 * VPL><<<g, emb::kBwdThreads, 0, st>>>(a, e->longs, e->n_long, e->pbase, e->ppart);
   emb::bwd_group_kernel<VPL><<<g, emb::kBwdThreads, 0, st>>>(a, e->longs, e->n_long, e->pbase, e->gbase,
                                                              e->ppart, e->gpart);
   emb::bwd_long_kernel<VPL><<<g, emb::kBwdThreads, 0, st>>>(a, e->longs, e->n_long, e->gbase, e->gpart);

@@ -259,48 +259,64 @@ bwd_seg_kernel(BwdArgs a, const uint4* __restrict__ segs, const uint32_t* __rest
 //
 // Warp per piece (32 positions) of a long segment: summed in position order
 // from +0.0f (UNR grad rows in flight), stored to ppart[piece].
-template <int VPL>
+template <int G, int VPL>
 __global__ void __launch_bounds__(kBwdThreads) bwd_lpiece_kernel(BwdArgs a, const uint4* __restrict__ longs,
                                                                 const unsigned* __restrict__ n_long,
                                                                 const uint32_t* __restrict__ pbase,
                                                                 float* __restrict__ ppart) {
+  // G-lane groups (G = 16: two pieces per warp; a dim-128 row is 2 float4
+  // per lane, a dim-64 row 1) — the sums are elementwise, so the lane layout
+  // does not change any result
+  constexpr int BPW = 32 / G;
+  constexpr int UNR = 8;
   const int lane = threadIdx.x & 31;
+  const int grp = lane / G, lg = lane % G;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
   const uint32_t nl = *n_long;
   if (nl == 0) return;
   const uint32_t npieces = pbase[nl];
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t pi = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; pi < npieces; pi += nwarps) {
-    const uint32_t li = upper_index(pbase, nl, pi);
-    const uint4 L = longs[li];  // {start, len, key, table}
-    const TableDev& td = a.tables[L.w];
-    const uint32_t V = td.dim >> 2;
-    const uint32_t pb = L.x + uint32_t(pi - pbase[li]) * kChunk;
-    const uint32_t np = min(L.x + L.y, pb + kChunk) - pb;
-    const uint32_t smp = uint32_t(lane) < np ? a.vals[pb + lane] : 0u;
-    const float* gcol = a.grad + td.col;
+  for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w * BPW < npieces; w += nwarps) {
+    const uint64_t pi = w * BPW + grp;
+    const bool valid = pi < npieces;
+    uint32_t V = 0, np = 0, pb = 0;
+    const float* gcol = a.grad;
+    if (valid) {
+      const uint32_t li = upper_index(pbase, nl, pi);
+      const uint4 L = longs[li];  // {start, len, key, table}
+      const TableDev& td = a.tables[L.w];
+      V = td.dim >> 2;
+      pb = L.x + uint32_t(pi - pbase[li]) * kChunk;
+      np = min(L.x + L.y, pb + kChunk) - pb;
+      gcol = a.grad + td.col;
+    }
     float4 pc[VPL];
 #pragma unroll
     for (int vv = 0; vv < VPL; ++vv) pc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (uint32_t j = 0; j < np; j += 8) {
-      float4 g[8][VPL];
+    for (uint32_t base = 0; base < np; base += G) {
+      const uint32_t nn = min(uint32_t(G), np - base);
+      const uint32_t smp = uint32_t(lg) < nn ? a.vals[pb + base + lg] : 0u;
+      for (uint32_t j = 0; j < nn; j += UNR) {
+        float4 g[UNR][VPL];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t bu = __shfl_sync(0xffffffffu, smp, int(j) + u);
-        const float4* gr = reinterpret_cast<const float4*>(gcol + uint64_t(bu) * a.stride);
+        for (int u = 0; u < UNR; ++u) {
+          const uint32_t bu = __shfl_sync(gmask, smp, int(j) + u, G);
+          const float4* gr = reinterpret_cast<const float4*>(gcol + uint64_t(bu) * a.stride);
 #pragma unroll
-        for (int vv = 0; vv < VPL; ++vv) {
-          const uint32_t vec = lane + vv * 32;
-          g[u][vv] = (j + u < np && vec < V) ? ld_nc_f4(gr + vec) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int vv = 0; vv < VPL; ++vv) {
+            const uint32_t vec = lg + vv * G;
+            g[u][vv] = (j + u < nn && vec < V) ? ld_nc_f4(gr + vec) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
         }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+          if (j + u < nn) {
+#pragma unroll
+            for (int vv = 0; vv < VPL; ++vv) add4(pc[vv], g[u][vv]);
+          }
       }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (j + u < np) {
-#pragma unroll
-          for (int vv = 0; vv < VPL; ++vv) add4(pc[vv], g[u][vv]);
-        }
     }
-    store_vec<32, VPL>(ppart + uint64_t(pi) * a.dmax, V, lane, pc);
+    if (valid) store_vec<G, VPL>(ppart + uint64_t(pi) * a.dmax, V, lg, pc);
   }
 }
 
