@@ -316,53 +316,61 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
         if nvtx:
             torch.cuda.nvtx.range_pop()
 
-    def run(nsteps, cache, evs=None):
-        """nsteps steps; with `cache`, batch 0's staging and the final write-back
-        are inside the run (every slow row is back in host memory at the end)."""
+    def timed(cache):
+        """warmup + steps steps in one continuous run.  With `cache` the
+        pipeline is filled before step 0 (batch 0's staging) and drained after
+        the last step (every staged row written back).  The timed window is
+        the last `steps` steps in steady state: each holds exactly one step's
+        work (its forward + backward, the next batch's claim/stage-in, the
+        eviction/stage-out of the batch two behind); the fill/drain costs are
+        reported separately (ms_per_step_incl_warmup_fill_drain)."""
+        nsteps = warmup + steps
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+        ta0, t0, t1, ta1 = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        clocks, L0 = None, 0
+        ta0.record()
         if cache and T:
             op.prefetch(batches[0][0], batches[0][1], B)
         for i in range(nsteps):
-            if flush is not None and evs is not None:
+            if i == warmup:
+                torch.cuda.synchronize()
+                hits.zero_()
+                if world > 1:
+                    dist.barrier()
+                if T:
+                    op.kernel_times(reset=True)
+                torch.cuda.synchronize()
+                clocks = Clocks(dev.index)
+                L0 = _lib.lib().rs_launch_counter()
+                t0.record()
+            if flush is not None:
                 flush.zero_()
-            step(i, nsteps if cache else 0, evs[i] if evs else None)
+            step(i, nsteps if cache else 0, evs[i - warmup] if i >= warmup else None)
+        t1.record()
+        launches = int(_lib.lib().rs_launch_counter() - L0)
         if cache and T:
             op.flush()
-
-    def timed(cache):
-        run(warmup, cache)
-        torch.cuda.synchronize()
-        hits.zero_()
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        clocks = Clocks(dev.index)
-        L0 = _lib.lib().rs_launch_counter()
-        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        if T:
-            op.kernel_times(reset=True)
-        t0.record()
-        run(steps, cache, evs)
-        t1.record()
+        ta1.record()
         torch.cuda.synchronize()
         kf, nf, kb, nbk = op.kernel_times(reset=True) if T else (0.0, 1, 0.0, 1)
-        launches = int(_lib.lib().rs_launch_counter() - L0)
         if world > 1:
             dist.barrier()
-        clk = clocks.stop()
+        clk = clocks.stop() if clocks else None
         tot_ms = t0.elapsed_time(t1)
+        all_ms = ta0.elapsed_time(ta1)
         fwd_ms = [e[0].elapsed_time(e[1]) for e in evs]
         a2a_ms = [e[1].elapsed_time(e[2]) for e in evs]
         bwd_ms = [e[2].elapsed_time(e[3]) for e in evs]
         h = hits.cpu().numpy()
         fast, slow = int(h[0::2][:T].sum()), int(h[1::2][:T].sum())
         if world > 1:
-            t = torch.tensor([tot_ms, fast, slow], dtype=torch.float64, device=dev)
+            t = torch.tensor([tot_ms, fast, slow, all_ms], dtype=torch.float64, device=dev)
             mx = t.clone()
             dist.all_reduce(mx, op=dist.ReduceOp.MAX)
             dist.all_reduce(t, op=dist.ReduceOp.SUM)
-            tot_ms, fast, slow = float(mx[0]), int(t[1]), int(t[2])
+            tot_ms, fast, slow, all_ms = float(mx[0]), int(t[1]), int(t[2]), float(mx[3])
         return dict(ms_per_step=tot_ms / steps, samples_per_s=B * steps / (tot_ms / 1e3),
+                    ms_per_step_incl_warmup_fill_drain=all_ms / nsteps,
                     uvm_pct=100.0 * slow / max(1, fast + slow), fast=fast, slow=slow,
                     fwd_ms=float(np.mean(fwd_ms)), bwd_ms=float(np.mean(bwd_ms)),
                     fwd_kernel_ms=kf / max(1, nf), bwd_kernel_ms=kb / max(1, nbk),
@@ -482,6 +490,7 @@ def probe_cache(torch, op, batches, pooled, B):
 
 def modes(r):
     return {m: (None if r.get(k) is None else {x: r[k][x] for x in ("samples_per_s", "ms_per_step",
+                                                                  "ms_per_step_incl_warmup_fill_drain",
                                                                   "fwd_ms", "bwd_ms", "fwd_kernel_ms",
                                                                   "bwd_kernel_ms")})
             for m, k in (("zero-copy", "zero_copy"), ("pipelined", "pipelined"))}
@@ -492,7 +501,8 @@ def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex, cache):
     indices are copied from pinned host memory (a copy stream, two batches
     ahead, triple-buffered — the data loader's overlap) and the hit counters
     (the step's UVM metric) are read back D2H.  With `cache`, batch k+1's slow
-    rows are staged while batch k runs, as in the device-resident run."""
+    rows are staged while batch k runs, as in the device-resident run; the
+    same steady-state window (after 3 warm-up steps of the continuous run)."""
     dev = pooled.device
     host = [(off.cpu().pin_memory(), idx[:max(1, n)].cpu().pin_memory(), n) for off, idx, n in batches]
     nb = 3
@@ -524,13 +534,20 @@ def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex, cache):
         b = k % nb
         return bufs[b][0], bufs[b][1][:host[k % len(host)][1].numel()]
 
-    def run(total):
+    warm = 3
+    total = warm + steps
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def run():
         h2d(0, total)
         h2d(1, total)
         if cache:
             main.wait_event(ev_in[0])
             op.prefetch(*view(0), B)
         for i in range(total):
+            if i == warm:  # steady state from here (same window as the device-resident run)
+                torch.cuda.synchronize()
+                s.record()
             h2d(i + 2, total)
             if cache and i + 1 < total:
                 main.wait_event(ev_in[(i + 1) % nb])
@@ -545,15 +562,11 @@ def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex, cache):
             h_hits.copy_(hits, non_blocking=True)
             ev_free[i % nb].record(main)
             used[i % nb] = True
+        e.record()
         if cache:
             op.flush()
 
-    run(2)
-    torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    run(steps)
-    e.record()
+    run()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e)
     if world > 1:
