@@ -176,6 +176,20 @@ typedef struct rs_system_spec {
 } rs_system_spec;
 
 /* include/shardplan/remap.hpp:27-39 (RemapTable) */
+/* SPRM remap files (include/shardplan/remap.hpp:60-63, core/src/remap.cpp:118-176),
+ * byte-compatible with the reference's write_remap / read_remap.  entries /
+ * out live at `location` (device reads stream through pinned memory in
+ * chunks, the file read overlapping the DMA).  rs_remap_read_header sizes the
+ * buffer; rs_remap_read fills it and returns the reference's
+ * slow_rows_allocated (count of negative entries).  Errors: IoError (open /
+ * write), ParseError (short, bad magic/version, hash_size out of range,
+ * truncated) — the reference's types and messages. */
+int rs_remap_write(rs_context* ctx, const char* path, uint32_t table_id, uint64_t hash_size,
+                   uint64_t hbm_rows, const int32_t* entries, int location);
+int rs_remap_read_header(const char* path, uint32_t* table_id, uint64_t* hash_size, uint64_t* hbm_rows);
+int rs_remap_read(rs_context* ctx, const char* path, int32_t* out, int location, uint64_t capacity,
+                  uint64_t* slow_rows_allocated);
+
 typedef struct rs_remap_view {
   uint32_t table_id;
   uint64_t hash_size;

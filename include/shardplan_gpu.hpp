@@ -184,6 +184,32 @@ inline std::pair<Tier, uint64_t> translate(const RemapTable& remap, uint64_t ori
   return {Tier::kSlow, static_cast<uint64_t>(-(int64_t)v - 1)};
 }
 
+/// include/shardplan/remap.hpp:62 — SPRM file, byte-identical to the reference's writer.
+inline void write_remap(const RemapTable& remap, const std::string& path) {
+  if (remap.entries.size() != remap.hash_size)
+    throw InvalidArgument(strfmt("write_remap: table %u has %zu entries for hash_size %llu",
+                                 remap.table_id, remap.entries.size(),
+                                 (unsigned long long)remap.hash_size));
+  check(rs_remap_write(nullptr, path.c_str(), remap.table_id, remap.hash_size, remap.hbm_rows,
+                       remap.entries.empty() ? nullptr : remap.entries.data(), RS_MEM_HOST));
+}
+
+/// include/shardplan/remap.hpp:63 — reference errors (IoError / ParseError) preserved.
+inline RemapTable read_remap(const std::string& path) {
+  RemapTable r;
+  uint32_t tid = 0;
+  uint64_t H = 0, hbm = 0;
+  check(rs_remap_read_header(path.c_str(), &tid, &H, &hbm));
+  r.table_id = tid;
+  r.hash_size = H;
+  r.hbm_rows = hbm;
+  r.entries.resize(H);
+  int32_t dummy = 0;
+  check(rs_remap_read(nullptr, path.c_str(), H ? r.entries.data() : &dummy, RS_MEM_HOST, H,
+                      &r.slow_rows_allocated));
+  return r;
+}
+
 /// include/shardplan/simulator.hpp:45-47 — tier counts on the GPU.
 inline SimReport simulate(const Trace& trace, const ShardingPlan& plan,
                           const std::vector<RemapTable>& remaps, const SystemSpec& system,

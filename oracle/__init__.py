@@ -408,6 +408,21 @@ class _RefLib:
             C_.c_int(int(omit_unaccessed)), _ptr(ent), C_.byref(slow)))
         return ent[:spec.hash_size], int(slow.value)
 
+    def write_remap(self, path, table_id, hash_size, hbm_rows, entries):
+        e = np.ascontiguousarray(entries, np.int32)
+        self._chk(self.lib.refc_write_remap(str(path).encode(), C_.c_uint32(table_id),
+                                            C_.c_uint64(hash_size), C_.c_uint64(hbm_rows),
+                                            _ptr(e if e.size else np.zeros(1, np.int32))))
+
+    def read_remap(self, path, capacity=1 << 26):
+        tid, H, hbm, slow = C_.c_uint32(), C_.c_uint64(), C_.c_uint64(), C_.c_uint64()
+        ent = np.empty(max(1, capacity), np.int32)
+        self._chk(self.lib.refc_read_remap(str(path).encode(), C_.byref(tid), C_.byref(H),
+                                           C_.byref(hbm), _ptr(ent), C_.c_uint64(capacity),
+                                           C_.byref(slow)))
+        return dict(table_id=int(tid.value), hash_size=int(H.value), hbm_rows=int(hbm.value),
+                    entries=ent[:int(H.value)].copy(), slow_rows_allocated=int(slow.value))
+
     def plan(self, tr, stats_h, kind, system, cost_kind=0, step_count=100,
              time_limit=float("inf")):
         """kind: 'milp' | 'greedy' | 'ldm'; cost_kind 0 size, 1 lookup, 2 size-lookup."""

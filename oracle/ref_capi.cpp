@@ -335,6 +335,31 @@ int refc_build_remap(void* stats, uint32_t j, uint32_t table_id,
   });
 }
 
+// ---------------------------------------------------------------- SPRM files
+int refc_write_remap(const char* path, uint32_t table_id, uint64_t hash_size, uint64_t hbm_rows,
+                     const int32_t* entries) {
+  return guarded([&] {
+    RemapTable r;
+    r.table_id = table_id;
+    r.hash_size = hash_size;
+    r.hbm_rows = hbm_rows;
+    r.entries.assign(entries, entries + hash_size);
+    write_remap(r, path);
+  });
+}
+
+int refc_read_remap(const char* path, uint32_t* table_id, uint64_t* hash_size, uint64_t* hbm_rows,
+                    int32_t* entries, uint64_t capacity, uint64_t* slow_rows_allocated) {
+  return guarded([&] {
+    RemapTable r = read_remap(path);
+    *table_id = r.table_id;
+    *hash_size = r.hash_size;
+    *hbm_rows = r.hbm_rows;
+    *slow_rows_allocated = r.slow_rows_allocated;
+    if (r.entries.size() <= capacity) std::memcpy(entries, r.entries.data(), r.entries.size() * 4);
+  });
+}
+
 // ---------------------------------------------------------------- simulate
 int refc_simulate(void* trace, uint32_t n_entries, const uint32_t* e_table,
                   const uint32_t* e_gpu, const uint64_t* e_hbm_rows,

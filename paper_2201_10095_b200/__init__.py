@@ -17,7 +17,7 @@ from .types import (FeatureGenSpec, FeatureStats, InfeasibleError, InvalidArgume
                     TIER_SLOW)
 from .profiler import (build_icdf, count_distinct_raw, hash_ids, hash_utilization, hash_value,
                        profile, profile_raw)
-from .remap import build_remap, translate
+from .remap import build_remap, read_remap, translate, write_remap
 from .simulator import simulate
 from .embedding import TieredEmbeddingBag
 from .runtime import Context, default_context
@@ -27,6 +27,6 @@ __all__ = [
     "ParseError", "PlanEntry", "RemapTable", "ShardingPlan", "ShardplanError", "SimReport",
     "SystemSpec", "TableIndexError", "TableSpec", "Trace", "WorkloadSpec", "TIER_FAST",
     "TIER_SLOW", "build_icdf", "count_distinct_raw", "hash_ids", "hash_utilization", "hash_value", "profile",
-    "profile_raw", "build_remap", "translate", "simulate", "TieredEmbeddingBag", "Context",
+    "profile_raw", "build_remap", "translate", "write_remap", "read_remap", "simulate", "TieredEmbeddingBag", "Context",
     "default_context",
 ]

@@ -27,6 +27,9 @@ void emb_enable_cache(rs_emb*, uint32_t);
 void emb_prefetch(rs_emb*, uint64_t, const uint32_t*, const uint32_t*);
 void emb_flush(rs_emb*);
 void emb_memory(const rs_emb*, uint64_t*, uint64_t*);
+void remap_write(rs_context*, const char*, uint32_t, uint64_t, uint64_t, const int32_t*, int);
+void remap_read_header(const char*, uint32_t*, uint64_t*, uint64_t*);
+void remap_read(rs_context*, const char*, int32_t*, int, uint64_t, uint64_t*);
 void emb_kernel_times(rs_emb*, double*, uint64_t*, double*, uint64_t*, int);
 void profile_view(const rs_profile*, uint32_t, rs_feature_stats*);
 uint32_t profile_tables(const rs_profile*);
@@ -299,6 +302,35 @@ int rs_radix_sort_pairs(rs_context* c, uint32_t* keys, uint32_t* vals, uint64_t 
     if (end_bit < 0 || end_bit > 32) throw rs::InvalidArgument("radix_sort: end_bit in [0, 32]");
     rs::Scratch scr = c->scratch(rs::radix_sort_scratch_bytes(n) + (4 << 20));
     rs::radix_sort_pairs(keys, vals, n, end_bit, scr, c->stream);
+  });
+}
+
+int rs_remap_write(rs_context* c, const char* path, uint32_t table_id, uint64_t H, uint64_t hbm_rows,
+                   const int32_t* entries, int loc) {
+  return guarded([&] {
+    need(path, "path");
+    if (H) need(entries, "entries");
+    if (loc == RS_MEM_DEVICE) need(c, "ctx");
+    rs::remap_write(c, path, table_id, H, hbm_rows, entries, loc);
+  });
+}
+
+int rs_remap_read_header(const char* path, uint32_t* table_id, uint64_t* H, uint64_t* hbm_rows) {
+  return guarded([&] {
+    need(path, "path");
+    need(table_id, "table_id");
+    need(H, "hash_size");
+    need(hbm_rows, "hbm_rows");
+    rs::remap_read_header(path, table_id, H, hbm_rows);
+  });
+}
+
+int rs_remap_read(rs_context* c, const char* path, int32_t* out, int loc, uint64_t capacity, uint64_t* slow) {
+  return guarded([&] {
+    need(path, "path");
+    need(out, "out");
+    if (loc == RS_MEM_DEVICE) need(c, "ctx");
+    rs::remap_read(c, path, out, loc, capacity, slow);
   });
 }
 

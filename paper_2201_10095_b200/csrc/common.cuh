@@ -20,6 +20,12 @@ struct Error : std::runtime_error {
 struct InvalidArgument : Error {
   explicit InvalidArgument(const std::string& m) : Error(-1, m) {}
 };
+struct ParseError : Error {
+  explicit ParseError(const std::string& m) : Error(-2, m) {}
+};
+struct IoError : Error {
+  explicit IoError(const std::string& m) : Error(-4, m) {}
+};
 struct OutOfRange : Error {
   explicit OutOfRange(const std::string& m) : Error(-5, m) {}
 };

@@ -121,3 +121,136 @@ void build_remap(rs_context* ctx, uint32_t table_id, uint64_t H, uint64_t hbm_ro
 }
 
 }  // namespace rs
+
+// ------------------------------------------------------------------ SPRM files
+// The reference's binary remap format (core/src/remap.cpp:118-176): "SPRM",
+// version 1, table_id u64, hash_size u64, hbm_rows u64 (little endian), then
+// hash_size int32 entries (little endian — the in-memory layout on the GPU's
+// hosts).  Reading streams the entries through a pinned buffer straight into
+// device memory in chunks (DMA overlapping the file read); the slow-row count
+// the reference recomputes on load is a device reduction.
+#include <cstdio>
+#include <cstring>
+
+namespace rs {
+namespace remap {
+
+constexpr size_t kSprmHeader = 29;  // RemapTable::kHeaderBytes
+
+__global__ void count_negative(const int32_t* __restrict__ e, uint64_t n, unsigned long long* __restrict__ out) {
+  uint64_t c = 0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    c += e[i] < 0;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
+
+}  // namespace remap
+
+static void put_u64(unsigned char* p, uint64_t v) {
+  for (int i = 0; i < 8; ++i) p[i] = (v >> (8 * i)) & 0xFF;
+}
+static uint64_t get_u64(const unsigned char* p) {
+  uint64_t v = 0;
+  for (int i = 0; i < 8; ++i) v |= uint64_t(p[i]) << (8 * i);
+  return v;
+}
+
+void remap_write(rs_context* ctx, const char* path, uint32_t table_id, uint64_t H, uint64_t hbm_rows,
+                 const int32_t* entries, int location) {
+  FILE* f = std::fopen(path, "wb");
+  if (!f) throw IoError(std::string("cannot open for writing: ") + path);
+  unsigned char header[remap::kSprmHeader];
+  std::memcpy(header, "SPRM", 4);
+  header[4] = 1;
+  put_u64(header + 5, table_id);
+  put_u64(header + 13, H);
+  put_u64(header + 21, hbm_rows);
+  bool ok = std::fwrite(header, 1, sizeof header, f) == sizeof header;
+  if (location == RS_MEM_DEVICE) {
+    constexpr size_t kChunk = size_t(16) << 20;  // entries per DMA chunk
+    int32_t* hb = ctx->pinned_buf<int32_t>(std::min<uint64_t>(H, kChunk));
+    for (uint64_t i = 0; ok && i < H; i += kChunk) {
+      const size_t n = size_t(std::min<uint64_t>(kChunk, H - i));
+      RS_CUDA(cudaMemcpyAsync(hb, entries + i, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+      ok = std::fwrite(hb, 4, n, f) == n;
+    }
+  } else if (H) {
+    ok = ok && std::fwrite(entries, 4, H, f) == H;
+  }
+  if (std::fclose(f) != 0 || !ok) throw IoError(std::string("write failed: ") + path);
+}
+
+// Header only (table_id, hash_size, hbm_rows) — sizes the caller's buffer.
+void remap_read_header(const char* path, uint32_t* table_id, uint64_t* H, uint64_t* hbm_rows) {
+  FILE* f = std::fopen(path, "rb");
+  if (!f) throw IoError(std::string("cannot open: ") + path);
+  unsigned char header[remap::kSprmHeader];
+  const bool got = std::fread(header, 1, sizeof header, f) == sizeof header;
+  std::fclose(f);
+  if (!got) throw ParseError(std::string("remap file too short: ") + path);
+  if (std::memcmp(header, "SPRM", 4) != 0 || header[4] != 1)
+    throw ParseError(std::string("bad remap magic or version: ") + path);
+  *table_id = uint32_t(get_u64(header + 5));
+  *H = get_u64(header + 13);
+  *hbm_rows = get_u64(header + 21);
+  if (*H > 0x7FFFFFFFULL) throw ParseError(std::string("remap hash_size out of range: ") + path);
+}
+
+void remap_read(rs_context* ctx, const char* path, int32_t* out, int location, uint64_t capacity,
+                uint64_t* slow_rows_allocated) {
+  uint32_t tid;
+  uint64_t H, hbm;
+  remap_read_header(path, &tid, &H, &hbm);
+  if (H > capacity) throw InvalidArgument("read_remap: output buffer smaller than hash_size");
+  FILE* f = std::fopen(path, "rb");
+  if (!f) throw IoError(std::string("cannot open: ") + path);
+  std::fseek(f, long(remap::kSprmHeader), SEEK_SET);
+  uint64_t slow = 0;
+  bool ok = true;
+  if (location == RS_MEM_DEVICE) {
+    cudaStream_t st = ctx->stream;
+    // double-buffered: read chunk k+1 from the file while chunk k is on the bus
+    constexpr size_t kChunk = size_t(8) << 20;
+    int32_t* hb = ctx->pinned_buf<int32_t>(2 * std::min<uint64_t>(std::max<uint64_t>(H, 1), kChunk));
+    const size_t cap = size_t(std::min<uint64_t>(std::max<uint64_t>(H, 1), kChunk));
+    cudaEvent_t done[2];
+    RS_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+    RS_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+    int k = 0;
+    for (uint64_t i = 0; ok && i < H; i += cap, k ^= 1) {
+      const size_t n = size_t(std::min<uint64_t>(cap, H - i));
+      if (i >= 2 * cap) RS_CUDA(cudaEventSynchronize(done[k]));
+      ok = std::fread(hb + k * cap, 4, n, f) == n;
+      if (ok) {
+        RS_CUDA(cudaMemcpyAsync(out + i, hb + k * cap, n * 4, cudaMemcpyHostToDevice, st));
+        RS_CUDA(cudaEventRecord(done[k], st));
+      }
+    }
+    Scratch scr = ctx->scratch(4096);
+    auto* d_slow = scr.take<unsigned long long>(1);
+    RS_CUDA(cudaMemsetAsync(d_slow, 0, 8, st));
+    if (ok && H) {
+      const unsigned g = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((H + 255) / 256, uint64_t(sm_count()) * 8)));
+      remap::count_negative<<<g, 256, 0, st>>>(out, H, d_slow);
+      RS_COUNT(1);
+      RS_LAUNCH_CHECK();
+    }
+    unsigned long long hs = 0;
+    RS_CUDA(cudaMemcpyAsync(&hs, d_slow, 8, cudaMemcpyDeviceToHost, st));
+    ctx->sync();
+    cudaEventDestroy(done[0]);
+    cudaEventDestroy(done[1]);
+    slow = hs;
+  } else {
+    ok = std::fread(out, 4, H, f) == H;
+    for (uint64_t i = 0; ok && i < H; ++i) slow += out[i] < 0;
+  }
+  std::fclose(f);
+  if (!ok) throw ParseError(std::string("remap file truncated: ") + path);
+  if (slow_rows_allocated) *slow_rows_allocated = slow;
+}
+
+}  // namespace rs

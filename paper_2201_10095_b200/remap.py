@@ -60,3 +60,48 @@ def translate(remap: RemapTable, original_index: int):
                               f"{remap.table_id}")
     v = int(remap.entries[original_index])
     return (TIER_FAST, v) if v >= 0 else (TIER_SLOW, -v - 1)
+
+
+def write_remap(remap: RemapTable, path, ctx=None) -> None:
+    """include/shardplan/remap.hpp:62 — SPRM binary file, byte-identical to the
+    reference's write_remap.  Entries may be a numpy array or an int32 cuda
+    tensor (streamed out through pinned memory)."""
+    if len(remap.entries) != remap.hash_size:
+        raise InvalidArgument(f"write_remap: table {remap.table_id} has {len(remap.entries)} "
+                              f"entries for hash_size {remap.hash_size}")
+    dev = is_device(remap.entries)
+    if dev:
+        ctx = ctx or default_context()
+        ent, loc, h = remap.entries, _lib.RS_MEM_DEVICE, ctx.h
+    else:
+        ent = np.ascontiguousarray(remap.entries, np.int32)
+        loc, h = _lib.RS_MEM_HOST, None
+    _lib.check(_lib.lib().rs_remap_write(h, str(path).encode(), C.c_uint32(remap.table_id),
+                                         C.c_uint64(remap.hash_size), C.c_uint64(remap.hbm_rows),
+                                         ptr(ent) if remap.hash_size else None, loc))
+
+
+def read_remap(path, device: bool = False, ctx=None) -> RemapTable:
+    """include/shardplan/remap.hpp:63 — reads an SPRM file (the reference's
+    errors: IoError, ParseError).  ``device``: entries land in an int32 cuda
+    tensor, streamed through pinned memory; slow_rows_allocated is counted on
+    the GPU."""
+    tid, H, hbm = C.c_uint32(), C.c_uint64(), C.c_uint64()
+    _lib.check(_lib.lib().rs_remap_read_header(str(path).encode(), C.byref(tid), C.byref(H),
+                                               C.byref(hbm)))
+    n = int(H.value)
+    slow = C.c_uint64()
+    if device:
+        import torch
+
+        ctx = ctx or default_context()
+        out = torch.empty(max(1, n), dtype=torch.int32, device=f"cuda:{ctx.device}")
+        _lib.check(_lib.lib().rs_remap_read(ctx.h, str(path).encode(), ptr(out), _lib.RS_MEM_DEVICE,
+                                            C.c_uint64(out.numel()), C.byref(slow)))
+        ent = out[:n]
+    else:
+        ent = np.empty(max(1, n), np.int32)
+        _lib.check(_lib.lib().rs_remap_read(None, str(path).encode(), ptr(ent), _lib.RS_MEM_HOST,
+                                            C.c_uint64(ent.size), C.byref(slow)))
+        ent = ent[:n]
+    return RemapTable(int(tid.value), n, int(hbm.value), int(slow.value), ent)

@@ -151,6 +151,16 @@ int main() {
       gpu_r.push_back(gpu::build_remap(plan.entries[j], stats[j], tabs[j]));
       for (uint64_t i = 0; i < tabs[j].hash_size; i += 97)
         CHECK(gpu::translate(gpu_r[j], i) == translate(ref_r[j], i));
+      // SPRM files: each side reads what the other wrote (remap.cpp:118-176)
+      const std::string pa = "/tmp/rs_dropin_a.sprm", pb = "/tmp/rs_dropin_b.sprm";
+      write_remap(ref_r[j], pa);
+      gpu::write_remap(gpu_r[j], pb);
+      auto ra = gpu::read_remap(pa);
+      auto rb = read_remap(pb);
+      CHECK(ra.entries == rb.entries && ra.table_id == rb.table_id && ra.hbm_rows == rb.hbm_rows &&
+            ra.hash_size == rb.hash_size && ra.slow_rows_allocated == rb.slow_rows_allocated);
+      std::remove(pa.c_str());
+      std::remove(pb.c_str());
     }
     for (uint64_t B : {256ULL, 1000ULL, 20000ULL}) {
       auto a = simulate(t, plan, ref_r, sys, B);
@@ -169,6 +179,14 @@ int main() {
       CHECK(eq);
     }
     CHECK(throws<InvalidArgument>([&] { gpu::simulate(t, plan, gpu_r, sys, 1 << 30); }));
+  }
+  CHECK(throws<IoError>([] { gpu::read_remap("/nonexistent/x.sprm"); }));
+  {
+    FILE* f = std::fopen("/tmp/rs_dropin_bad.sprm", "wb");
+    std::fwrite("SPRX", 1, 4, f);
+    std::fclose(f);
+    CHECK(throws<ParseError>([] { gpu::read_remap("/tmp/rs_dropin_bad.sprm"); }));
+    std::remove("/tmp/rs_dropin_bad.sprm");
   }
   // TieredEmbeddingBag (the §8b operator) through the C++ shim: forward is
   // the in-order fp32 sum of each bag's rows (bit-exact vs a host loop over
