@@ -137,7 +137,7 @@ struct WorkMap {
 
 // ---------------------------------------------------------------- segment list
 // WRITE = false: counts[wi] = segment heads in window wi.  WRITE = true: one
-// descriptor {start, key, table, 0} per head at sbase[wi] + rank (sbase =
+// descriptor {start, key, table, end} per head at sbase[wi] + rank (sbase =
 // exclusive scan of counts), so each class's segments are contiguous and in
 // position order.
 template <bool WRITE>
@@ -164,13 +164,33 @@ __global__ void __launch_bounds__(256) bwd_seg_scan_kernel(BwdArgs a, WorkMap m,
       if (lane == 0) counts[wi] = __popc(heads);
       continue;
     }
-    if (head) segs[sbase[wi] + __popc(heads & lanemask_lt())] = make_uint4(p0 + lane, key, t, 0u);
+    // .w = the segment's end: the next head in this window, the table's end
+    // when this is its last window, else written by the next window's first
+    // head — or by the table's last window when no head follows (descriptor
+    // sbase[wi] - 1 is then this one: windows of a table are consecutive work
+    // items and a table's first position is always a head).
+    if (heads == 0) {
+      if (lane == 0 && p0 + uint32_t(kChunk) >= te) reinterpret_cast<uint32_t*>(segs + sbase[wi] - 1)[3] = te;
+      continue;
+    }
+    if (!head) continue;
+    const uint32_t idx = sbase[wi] + __popc(heads & lanemask_lt());
+    uint4* sd = segs + idx;
+    const unsigned later = heads & ~(lanemask_lt() | (1u << lane));
+    *reinterpret_cast<uint2*>(sd) = make_uint2(p0 + lane, key);
+    if (later) {
+      reinterpret_cast<uint32_t*>(sd)[3] = p0 + uint32_t(__ffs(later) - 1);
+    } else if (p0 + uint32_t(kChunk) >= te) {
+      reinterpret_cast<uint32_t*>(sd)[3] = te;
+    }
+    reinterpret_cast<uint32_t*>(sd)[2] = t;
+    if (k > 0 && (heads & lanemask_lt()) == 0) reinterpret_cast<uint32_t*>(segs + idx - 1)[3] = p0 + lane;
   }
 }
 
 // ---------------------------------------------------------------- short segments
-// Segments [sbase[w_lo], sbase[w_hi]) of one lane class.  A segment ends at
-// the next descriptor's start (same table) or at its table's end.  Segments
+// Segments [sbase[w_lo], sbase[w_hi]) of one lane class ({start, key, table,
+// end} descriptors from the scan).  Segments
 // of <= 32 positions are summed in position order and their row updated;
 // longer ones go to the long list (a slot each, with their group count).
 template <int G, int VPL, int UNR, int MINB>
@@ -183,21 +203,34 @@ bwd_seg_kernel(BwdArgs a, const uint4* __restrict__ segs, const uint32_t* __rest
   const int grp = lane / G, lg = lane % G;
   const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
   const uint64_t s_lo = sbase[w_lo], s_hi = sbase[w_hi];
+  const uint32_t npos = a.tpos[a.T];
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   const bool ada = a.opt == RS_OPT_ROWWISE_ADAGRAD;
-  uint32_t cur_t = 0xFFFFFFFFu, t_end = 0;
-  TableDev td{};
-  for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; s_lo + w * BPW < s_hi; w += nwarps) {
+  const uint4 kNone = make_uint4(0u, 0u, kNoKey, 0u);
+  // Software pipeline over the grid-stride iterations: the next iteration's
+  // descriptor is loaded at the top of this one and its first G sample ids
+  // before this segment's update, so an iteration's dependent chain is
+  // grad rows -> update (the row and its state are in flight from the top).
+  // The table's fields are re-read per segment (L1 hits) instead of being
+  // held live across iterations.
+  uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  uint4 d = kNone;
+  uint32_t smp0 = 0;
+  {
     const uint64_t si = s_lo + w * BPW + grp;
-    const bool valid = si < s_hi;
-    const uint4 d = valid ? segs[si] : make_uint4(0u, 0u, 0xFFFFFFFFu, 0u);
-    const uint4 dn = si + 1 < s_hi ? segs[si + 1] : make_uint4(0u, 0u, 0xFFFFFFFFu, 0u);
-    if (valid && d.z != cur_t) {
-      cur_t = d.z;
-      td = a.tables[cur_t];
-      t_end = a.tpos[cur_t + 1];
+    if (si < s_hi) {
+      d = segs[si];
+      smp0 = a.vals[min(d.x + uint32_t(lg), npos - 1)];
     }
-    const uint32_t len = valid ? (dn.z == d.z ? dn.x : t_end) - d.x : 0u;
+  }
+  for (; s_lo + w * BPW < s_hi; w += nwarps) {
+    const bool valid = d.z != kNoKey;
+    uint4 d2 = kNone;
+    {
+      const uint64_t si = s_lo + (w + nwarps) * BPW + grp;
+      if (si < s_hi) d2 = segs[si];
+    }
+    const uint32_t len = valid ? d.w - d.x : 0u;
     if (len > uint32_t(kChunk)) {
       if (lg == 0) {
         const unsigned slot = atomicAdd(n_long, 1u);
@@ -206,8 +239,11 @@ bwd_seg_kernel(BwdArgs a, const uint4* __restrict__ segs, const uint32_t* __rest
         long_np[slot] = np;
         long_ng[slot] = (np + kGroupPieces - 1) / kGroupPieces;
       }
+      smp0 = d2.z != kNoKey ? a.vals[min(d2.x + uint32_t(lg), npos - 1)] : 0u;
+      d = d2;
       continue;
     }
+    const TableDev& td = a.tables[valid ? d.z : 0u];
     const uint32_t V = td.dim >> 2;
     // the row and its state first: the slot key addresses them directly
     float4 w4[VPL];
@@ -223,18 +259,19 @@ bwd_seg_kernel(BwdArgs a, const uint4* __restrict__ segs, const uint32_t* __rest
       }
       if (ada) m_old = *mom_ptr(td, e);
     }
+    const float* gcol = a.grad + td.col;
     float4 acc[VPL];
 #pragma unroll
     for (int vv = 0; vv < VPL; ++vv) acc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (uint32_t base = 0; base < len; base += G) {
       const uint32_t nn = min(uint32_t(G), len - base);
-      const uint32_t smp = uint32_t(lg) < nn ? a.vals[d.x + base + lg] : 0u;
+      const uint32_t smp = base == 0 ? smp0 : (uint32_t(lg) < nn ? a.vals[d.x + base + lg] : 0u);
       for (uint32_t j = 0; j < nn; j += UNR) {
         float4 g[UNR][VPL];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
           const uint32_t bu = __shfl_sync(gmask, smp, int(j) + u, G);
-          const float4* gr = reinterpret_cast<const float4*>(a.grad + uint64_t(bu) * a.stride + td.col);
+          const float4* gr = reinterpret_cast<const float4*>(gcol + uint64_t(bu) * a.stride);
 #pragma unroll
           for (int vv = 0; vv < VPL; ++vv) {
             const uint32_t vec = lg + vv * G;
@@ -249,7 +286,9 @@ bwd_seg_kernel(BwdArgs a, const uint4* __restrict__ segs, const uint32_t* __rest
           }
       }
     }
+    smp0 = d2.z != kNoKey ? a.vals[min(d2.x + uint32_t(lg), npos - 1)] : 0u;
     if (valid) update_row<G, VPL>(a, td, e, acc, w4, m_old, gmask, lg);
+    d = d2;
   }
 }
 
