@@ -430,6 +430,7 @@ struct rs_emb {
   uint32_t* gbase = nullptr;    // [long_cap + 1] exclusive scan of long_ng
   unsigned* n_long = nullptr;
   float* ppart = nullptr;       // [pieces][dmax] piece sums of long segments
+  uint4* pdesc = nullptr;       // [pieces] {start, count, table} of each piece
   float* gpart = nullptr;       // [groups][dmax] group sums of long segments
   uint32_t* d_meta = nullptr;
   uint32_t* h_meta = nullptr;
@@ -468,7 +469,7 @@ struct rs_emb {
     if (keys) cudaFree(keys);
     if (vals) cudaFree(vals);
     for (void* p : {(void*)scount, (void*)sbase, (void*)segs, (void*)longs, (void*)long_np, (void*)long_ng,
-                    (void*)pbase, (void*)gbase, (void*)n_long, (void*)ppart, (void*)gpart})
+                    (void*)pbase, (void*)gbase, (void*)n_long, (void*)ppart, (void*)pdesc, (void*)gpart})
       if (p) cudaFree(p);
     if (d_meta) cudaFree(d_meta);
     if (h_meta) cudaFreeHost(h_meta);
@@ -622,6 +623,7 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
     const size_t max_pieces = L / emb::kChunk + e->long_cap + 1;
     const size_t max_groups = L / (emb::kChunk * emb::kGroupPieces) + e->long_cap + 1;
     RS_CUDA(cudaMalloc(&e->ppart, max_pieces * e->dmax * 4));
+    RS_CUDA(cudaMalloc(&e->pdesc, max_pieces * sizeof(uint4)));
     RS_CUDA(cudaMalloc(&e->gpart, max_groups * e->dmax * 4));
     e->sort_scratch_bytes = radix_sort_scratch_bytes(L, T) + (4 << 20);
     e->tiles_cap = L / kSortTile + T + 2;
@@ -1016,11 +1018,12 @@ template <int VPL>
 static void launch_long(rs_emb* e, const emb::BwdArgs& a) {
   const unsigned g = unsigned(sm_count()) * 8;
   cudaStream_t st = e->ctx->stream;
-  emb::bwd_lpiece_kernel<16, 2 * VPL><<<g, emb::kBwdThreads, 0, st>>>(a, e->longs, e->n_long, e->pbase, e->ppart);
+  emb::bwd_piece_desc_kernel<<<g, emb::kBwdThreads, 0, st>>>(e->longs, e->n_long, e->pbase, e->pdesc);
+  emb::bwd_lpiece_kernel<16, 2 * VPL><<<g, emb::kBwdThreads, 0, st>>>(a, e->pdesc, e->n_long, e->pbase, e->ppart);
   emb::bwd_group_kernel<VPL><<<g, emb::kBwdThreads, 0, st>>>(a, e->longs, e->n_long, e->pbase, e->gbase,
                                                              e->ppart, e->gpart);
   emb::bwd_long_kernel<VPL><<<g, emb::kBwdThreads, 0, st>>>(a, e->longs, e->n_long, e->gbase, e->gpart);
-  RS_COUNT(3);
+  RS_COUNT(4);
 }
 
 void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx, const float* grad,

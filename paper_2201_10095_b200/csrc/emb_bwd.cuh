@@ -296,10 +296,31 @@ bwd_seg_kernel(BwdArgs a, const uint4* __restrict__ segs, const uint32_t* __rest
 // pbase / gbase = exclusive scans of long_np / long_ng over the long slots
 // (unused slots hold 0 and sort after every used one).
 //
+// Warp per long segment: one {start, count, table} descriptor per 32-position
+// piece at pdesc[pbase[li] + k], so the piece kernel needs no search.
+__global__ void __launch_bounds__(kBwdThreads) bwd_piece_desc_kernel(const uint4* __restrict__ longs,
+                                                                    const unsigned* __restrict__ n_long,
+                                                                    const uint32_t* __restrict__ pbase,
+                                                                    uint4* __restrict__ pdesc) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nl = *n_long;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t li = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; li < nl; li += nwarps) {
+    const uint4 L = longs[li];  // {start, len, key, table}
+    const uint32_t base = pbase[li], np = (L.y + kChunk - 1) / kChunk, end = L.x + L.y;
+    for (uint32_t k = lane; k < np; k += 32) {
+      const uint32_t pb = L.x + k * kChunk;
+      pdesc[base + k] = make_uint4(pb, min(uint32_t(kChunk), end - pb), L.w, 0u);
+    }
+  }
+}
+
 // Warp per piece (32 positions) of a long segment: summed in position order
-// from +0.0f (UNR grad rows in flight), stored to ppart[piece].
+// from +0.0f (UNR grad rows in flight), stored to ppart[piece].  Pipelined
+// like bwd_seg_kernel: the next piece's descriptor and sample ids are in
+// flight while this piece's grad rows are summed.
 template <int G, int VPL>
-__global__ void __launch_bounds__(kBwdThreads) bwd_lpiece_kernel(BwdArgs a, const uint4* __restrict__ longs,
+__global__ void __launch_bounds__(kBwdThreads) bwd_lpiece_kernel(BwdArgs a, const uint4* __restrict__ pdesc,
                                                                 const unsigned* __restrict__ n_long,
                                                                 const uint32_t* __restrict__ pbase,
                                                                 float* __restrict__ ppart) {
@@ -315,26 +336,32 @@ __global__ void __launch_bounds__(kBwdThreads) bwd_lpiece_kernel(BwdArgs a, cons
   if (nl == 0) return;
   const uint32_t npieces = pbase[nl];
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w * BPW < npieces; w += nwarps) {
+  uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  uint4 P = make_uint4(0u, 0u, 0u, 0u);
+  uint32_t s0 = 0, s1 = 0;  // the piece's sample ids (positions lg, lg + G)
+  if (w * BPW + grp < npieces) {
+    P = pdesc[w * BPW + grp];
+    s0 = uint32_t(lg) < P.y ? a.vals[P.x + lg] : 0u;
+    if (G < kChunk) s1 = uint32_t(lg) + G < P.y ? a.vals[P.x + G + lg] : 0u;
+  }
+  for (; w * BPW < npieces; w += nwarps) {
     const uint64_t pi = w * BPW + grp;
     const bool valid = pi < npieces;
-    uint32_t V = 0, np = 0, pb = 0;
-    const float* gcol = a.grad;
-    if (valid) {
-      const uint32_t li = upper_index(pbase, nl, pi);
-      const uint4 L = longs[li];  // {start, len, key, table}
-      const TableDev& td = a.tables[L.w];
-      V = td.dim >> 2;
-      pb = L.x + uint32_t(pi - pbase[li]) * kChunk;
-      np = min(L.x + L.y, pb + kChunk) - pb;
-      gcol = a.grad + td.col;
-    }
+    const uint64_t pn = pi + nwarps * BPW;
+    const uint4 Pn = pn < npieces ? pdesc[pn] : make_uint4(0u, 0u, 0u, 0u);
+    const uint32_t np = valid ? P.y : 0u;
+    const TableDev& td = a.tables[P.z];
+    const uint32_t V = td.dim >> 2;
+    const float* gcol = a.grad + td.col;
     float4 pc[VPL];
 #pragma unroll
     for (int vv = 0; vv < VPL; ++vv) pc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (uint32_t base = 0; base < np; base += G) {
+#pragma unroll
+    for (int half = 0; half < kChunk / G; ++half) {
+      const uint32_t base = uint32_t(half) * G;
+      if (base >= np) break;
       const uint32_t nn = min(uint32_t(G), np - base);
-      const uint32_t smp = uint32_t(lg) < nn ? a.vals[pb + base + lg] : 0u;
+      const uint32_t smp = half == 0 ? s0 : s1;
       for (uint32_t j = 0; j < nn; j += UNR) {
         float4 g[UNR][VPL];
 #pragma unroll
@@ -355,7 +382,10 @@ __global__ void __launch_bounds__(kBwdThreads) bwd_lpiece_kernel(BwdArgs a, cons
           }
       }
     }
+    s0 = uint32_t(lg) < Pn.y ? a.vals[Pn.x + lg] : 0u;
+    if (G < kChunk) s1 = uint32_t(lg) + G < Pn.y ? a.vals[Pn.x + G + lg] : 0u;
     if (valid) store_vec<G, VPL>(ppart + uint64_t(pi) * a.dmax, V, lg, pc);
+    P = Pn;
   }
 }
 
