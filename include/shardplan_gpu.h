@@ -190,6 +190,32 @@ int rs_remap_read_header(const char* path, uint32_t* table_id, uint64_t* hash_si
 int rs_remap_read(rs_context* ctx, const char* path, int32_t* out, int location, uint64_t capacity,
                   uint64_t* slow_rows_allocated);
 
+/* ------------------------------------------------------------- trace files */
+/* core/src/trace_io.cpp:75-158  read_trace(path) — text, or gzip for ".gz"
+ * paths (core/src/line_io.cpp).  Parsed on the GPU in chunks of
+ * `chunk_bytes` (0 = 256 MiB); the result stays in device memory, owned by
+ * the handle.  Errors as the reference, with its messages: IoError (cannot
+ * open / read failed), ParseError ("line N: ..."), InvalidArgument (unknown
+ * table, sample or id out of range, unsorted records, duplicate table,
+ * TableSpec validation). */
+typedef struct rs_trace_file rs_trace_file;
+int rs_trace_read(rs_context* ctx, const char* path, uint64_t chunk_bytes, rs_trace_file** out);
+/* The loaded trace as an rs_trace (tables on the host, record and id arrays on
+ * the device, location RS_MEM_DEVICE) — valid until rs_trace_file_destroy;
+ * pass it straight to rs_profile_run / rs_simulate. */
+int rs_trace_file_view(const rs_trace_file* f, rs_trace* view);
+/* Copies the record and id arrays into caller buffers (`location`), sized
+ * num_records / num_ids from the view; NULL skips an array. */
+int rs_trace_file_export(rs_context* ctx, const rs_trace_file* f, uint64_t* rec_sample,
+                         uint32_t* rec_table, uint64_t* rec_offset, uint32_t* rec_len,
+                         uint32_t* ids, int location);
+int rs_trace_file_destroy(rs_trace_file* f);
+/* core/src/trace_io.cpp:48-72  write_trace(trace, path, comments): the record
+ * lines are formatted on the GPU, byte-identical to the reference writer
+ * (gzip through zlib for ".gz").  `trace` must carry hashed ids. */
+int rs_trace_write(rs_context* ctx, const rs_trace* trace, const char* path,
+                   const char* const* comments, uint32_t n_comments);
+
 typedef struct rs_remap_view {
   uint32_t table_id;
   uint64_t hash_size;

@@ -328,6 +328,30 @@ class _RefLib:
             _ptr(rl), C_.c_uint64(ii.size), _ptr(ii), C_.byref(h)))
         return RefTrace(list(tables), num_samples, rs, rt, ro, rl, ii, None, None, h)
 
+    def read_trace(self, path):
+        """core/src/trace_io.cpp:75-158 (unmodified reference)."""
+        h = _P()
+        self._chk(self.lib.refc_read_trace(str(path).encode(), C_.byref(h)))
+        J, ns = C_.c_uint32(), C_.c_uint64()
+        self.lib.refc_trace_meta(h, C_.byref(J), C_.byref(ns), None, None, None, None, None)
+        J = int(J.value)
+        tid, card, hs = np.empty(J, np.uint32), np.empty(J, np.uint64), np.empty(J, np.uint64)
+        dim, eb = np.empty(J, np.uint32), np.empty(J, np.uint32)
+        if J:
+            self.lib.refc_trace_meta(h, C_.byref(C_.c_uint32()), C_.byref(ns), _ptr(tid), _ptr(card),
+                                     _ptr(hs), _ptr(dim), _ptr(eb))
+        from types import SimpleNamespace
+
+        specs = [SimpleNamespace(table_id=int(tid[j]), cardinality=int(card[j]), hash_size=int(hs[j]),
+                                 dim=int(dim[j]), elem_bytes=int(eb[j])) for j in range(J)]
+        return self._materialise(h, specs, int(ns.value))
+
+    def write_trace(self, tr, path, comments=()):
+        """core/src/trace_io.cpp:48-72 (unmodified reference); tr: a RefTrace."""
+        cs = [str(c).encode() for c in comments]
+        arr = (C_.c_char_p * max(1, len(cs)))(*cs)
+        self._chk(self.lib.refc_write_trace(tr.handle, str(path).encode(), arr, C_.c_uint32(len(cs))))
+
     def free_trace(self, tr):
         if tr.handle is not None:
             self.lib.refc_trace_free(tr.handle)

@@ -22,6 +22,7 @@
 #include "shardplan/milp.hpp"
 #include "shardplan/profiler.hpp"
 #include "shardplan/remap.hpp"
+#include "shardplan/trace_io.hpp"
 #include "shardplan/simulator.hpp"
 #include "shardplan/workload.hpp"
 #include "shardplan/zipf.hpp"
@@ -218,6 +219,43 @@ int refc_trace_copy(void* h, uint64_t* rec_sample, uint32_t* rec_table,
 }
 
 void refc_trace_free(void* h) { delete static_cast<TraceBox*>(h); }
+
+// core/src/trace_io.cpp:48-158
+int refc_read_trace(const char* path, void** out) {
+  return guarded([&] {
+    auto* box = new TraceBox;
+    try {
+      box->trace = read_trace(path);
+    } catch (...) {
+      delete box;
+      throw;
+    }
+    *out = box;
+  });
+}
+
+int refc_write_trace(void* h, const char* path, const char* const* comments, uint32_t n) {
+  return guarded([&] {
+    std::vector<std::string> c(comments, comments + n);
+    write_trace(static_cast<TraceBox*>(h)->trace, path, c);
+  });
+}
+
+int refc_trace_meta(void* h, uint32_t* J, uint64_t* num_samples, uint32_t* table_id, uint64_t* card,
+                    uint64_t* hash_size, uint32_t* dim, uint32_t* elem_bytes) {
+  const auto& t = static_cast<TraceBox*>(h)->trace;
+  *J = uint32_t(t.tables.size());
+  *num_samples = t.num_samples;
+  if (table_id)
+    for (size_t j = 0; j < t.tables.size(); ++j) {
+      table_id[j] = t.tables[j].table_id;
+      card[j] = t.tables[j].cardinality;
+      hash_size[j] = t.tables[j].hash_size;
+      dim[j] = t.tables[j].dim;
+      elem_bytes[j] = t.tables[j].elem_bytes;
+    }
+  return 0;
+}
 
 // ---------------------------------------------------------------- profile
 int refc_profile(void* trace, double rate, uint64_t seed, void** out) {

@@ -19,6 +19,7 @@ from .profiler import (build_icdf, count_distinct_raw, hash_ids, hash_utilizatio
                        profile, profile_raw)
 from .remap import build_remap, read_remap, translate, write_remap
 from .simulator import simulate
+from .trace_io import TraceFile, read_trace, write_trace
 from .embedding import TieredEmbeddingBag
 from .runtime import Context, default_context
 
@@ -27,6 +28,6 @@ __all__ = [
     "ParseError", "PlanEntry", "RemapTable", "ShardingPlan", "ShardplanError", "SimReport",
     "SystemSpec", "TableIndexError", "TableSpec", "Trace", "WorkloadSpec", "TIER_FAST",
     "TIER_SLOW", "build_icdf", "count_distinct_raw", "hash_ids", "hash_utilization", "hash_value", "profile",
-    "profile_raw", "build_remap", "translate", "write_remap", "read_remap", "simulate", "TieredEmbeddingBag", "Context",
+    "profile_raw", "build_remap", "translate", "write_remap", "read_remap", "read_trace", "write_trace", "TraceFile", "simulate", "TieredEmbeddingBag", "Context",
     "default_context",
 ]

@@ -112,6 +112,11 @@ _SIGS = {
     "rs_emb_memory": ([P, P, P], i32),
     "rs_emb_kernel_times": ([P, P, P, P, P, i32], i32),
     "rs_remap_write": ([P, C.c_char_p, u32, u64, u64, P, i32], i32),
+    "rs_trace_read": ([P, C.c_char_p, u64, P], i32),
+    "rs_trace_file_view": ([P, P], i32),
+    "rs_trace_file_export": ([P, P, P, P, P, P, P, i32], i32),
+    "rs_trace_file_destroy": ([P], i32),
+    "rs_trace_write": ([P, P, C.c_char_p, P, u32], i32),
     "rs_remap_read_header": ([C.c_char_p, P, P, P], i32),
     "rs_remap_read": ([P, C.c_char_p, P, i32, u64, P], i32),
     "rs_radix_sort_pairs": ([P, P, P, u64, i32], i32),

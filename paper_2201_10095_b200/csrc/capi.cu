@@ -5,6 +5,7 @@
 
 #include "../../include/shardplan_gpu.h"
 #include "context.cuh"
+#include "trace_file.cuh"
 
 struct rs_profile;
 struct rs_emb;
@@ -30,6 +31,8 @@ void emb_memory(const rs_emb*, uint64_t*, uint64_t*);
 void remap_write(rs_context*, const char*, uint32_t, uint64_t, uint64_t, const int32_t*, int);
 void remap_read_header(const char*, uint32_t*, uint64_t*, uint64_t*);
 void remap_read(rs_context*, const char*, int32_t*, int, uint64_t, uint64_t*);
+rs_trace_file* trace_read(rs_context*, const char*, uint64_t);
+void trace_write(rs_context*, const rs_trace*, const char*, const char* const*, uint32_t, uint64_t);
 void emb_kernel_times(rs_emb*, double*, uint64_t*, double*, uint64_t*, int);
 void profile_view(const rs_profile*, uint32_t, rs_feature_stats*);
 uint32_t profile_tables(const rs_profile*);
@@ -338,6 +341,69 @@ int rs_emb_kernel_times(rs_emb* e, double* fwd_ms, uint64_t* n_fwd, double* bwd_
   return guarded([&] {
     need(e, "emb");
     rs::emb_kernel_times(e, fwd_ms, n_fwd, bwd_ms, n_bwd, reset);
+  });
+}
+
+int rs_trace_read(rs_context* c, const char* path, uint64_t chunk_bytes, rs_trace_file** out) {
+  return guarded([&] {
+    need(c, "ctx");
+    need(path, "path");
+    need(out, "out");
+    *out = rs::trace_read(c, path, chunk_bytes);
+  });
+}
+
+int rs_trace_file_view(const rs_trace_file* f, rs_trace* v) {
+  return guarded([&] {
+    need(f, "trace_file");
+    need(v, "view");
+    *v = rs_trace{};
+    v->num_tables = uint32_t(f->tables.size());
+    v->tables = f->tables.data();
+    v->num_samples = f->num_samples;
+    v->num_records = f->nrec;
+    v->rec_sample = f->rec_sample;
+    v->rec_table = f->rec_table;
+    v->rec_offset = f->rec_offset;
+    v->rec_len = f->rec_len;
+    v->num_ids = f->nids;
+    v->ids = f->ids;
+    v->raw_ids = nullptr;
+    v->location = RS_MEM_DEVICE;
+  });
+}
+
+int rs_trace_file_export(rs_context* c, const rs_trace_file* f, uint64_t* rs_, uint32_t* rt, uint64_t* ro,
+                         uint32_t* rl, uint32_t* ids, int loc) {
+  return guarded([&] {
+    need(c, "ctx");
+    need(f, "trace_file");
+    const cudaMemcpyKind k = loc == RS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      if (dst && bytes) RS_CUDA(cudaMemcpyAsync(dst, src, bytes, k, c->stream));
+    };
+    cp(rs_, f->rec_sample, f->nrec * 8);
+    cp(rt, f->rec_table, f->nrec * 4);
+    cp(ro, f->rec_offset, f->nrec * 8);
+    cp(rl, f->rec_len, f->nrec * 4);
+    cp(ids, f->ids, f->nids * 4);
+    c->sync();
+  });
+}
+
+int rs_trace_file_destroy(rs_trace_file* f) {
+  return guarded([&] { delete f; });
+}
+
+int rs_trace_write(rs_context* c, const rs_trace* tr, const char* path, const char* const* comments,
+                   uint32_t n_comments) {
+  return guarded([&] {
+    need(c, "ctx");
+    need(tr, "trace");
+    need(path, "path");
+    if (n_comments) need(comments, "comments");
+    if (tr->num_tables) need(tr->tables, "tables");
+    rs::trace_write(c, tr, path, comments, n_comments, 0);
   });
 }
 
