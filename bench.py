@@ -56,6 +56,8 @@ def parse():
     p.add_argument("--profile-ids", type=float, default=1e9,
                    help="HP1 sweep size (BASELINE configs[4]); 0 disables")
     p.add_argument("--cpu-profile-ids", type=float, default=5e7)
+    p.add_argument("--trace-ids", type=float, default=2e8,
+                   help="trace-file write/read size (SURVEY §8f row 3, tools/trace_bench.py); 0 disables")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-prefetch", action="store_true",
                    help="headline in zero-copy mode only (no slow-row staging pipeline)")
@@ -671,6 +673,19 @@ def main():
     sweep = None
     if rank == 0 and world == 1 and args.profile_ids > 0:
         sweep = run_profile_sweep(args, torch, ctx, hbm_peak)
+    trace_io = None
+    if rank == 0 and world == 1 and args.trace_ids > 0:
+        import importlib.util
+        import tempfile
+        from types import SimpleNamespace
+
+        spec = importlib.util.spec_from_file_location("trace_bench", os.path.join(ROOT, "tools", "trace_bench.py"))
+        tb = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(tb)
+        with tempfile.TemporaryDirectory() as d:
+            trace_io = tb.measure(SimpleNamespace(ids=args.trace_ids, ref_ids=2e6, dir=d, gz=False, reps=3,
+                                                  chunk_mb=0))
+        torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -731,6 +746,7 @@ def main():
             "profile": {"ids": pn, "seconds_incl_host": prof_s, "ids_per_s": pn / prof_s,
                         "first_call_s": prof_cold_s},
             "profiler_sweep": sweep,
+            "trace_io": trace_io,
             "bw_uvm_h2d_gbs": bw_uvm / 1e9,
         }
         print(json.dumps(line), flush=True)

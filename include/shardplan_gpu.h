@@ -193,7 +193,7 @@ int rs_remap_read(rs_context* ctx, const char* path, int32_t* out, int location,
 /* ------------------------------------------------------------- trace files */
 /* core/src/trace_io.cpp:75-158  read_trace(path) — text, or gzip for ".gz"
  * paths (core/src/line_io.cpp).  Parsed on the GPU in chunks of
- * `chunk_bytes` (0 = 256 MiB); the result stays in device memory, owned by
+ * `chunk_bytes` (0 = 64 MiB); the result stays in device memory, owned by
  * the handle.  Errors as the reference, with its messages: IoError (cannot
  * open / read failed), ParseError ("line N: ..."), InvalidArgument (unknown
  * table, sample or id out of range, unsorted records, duplicate table,

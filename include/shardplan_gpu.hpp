@@ -13,6 +13,7 @@
 // the reference's own: shardplan::Trace, FeatureStats, PlanEntry, ...).
 #pragma once
 
+#include <cstdio>
 #include <memory>
 #include <span>
 #include <stdexcept>
@@ -31,7 +32,14 @@ namespace shardplan::gpu {
   const std::string m = rs_last_error();
   switch (status) {
     case RS_ERR_INVALID_ARGUMENT: throw InvalidArgument(m);
-    case RS_ERR_PARSE: throw ParseError(m);
+    case RS_ERR_PARSE: {
+      // "line N: what" -> ParseError(what, N): same what(), and line() as the reference
+      unsigned long long ln = 0;
+      int used = 0;
+      if (std::sscanf(m.c_str(), "line %llu: %n", &ln, &used) == 1 && used > 0 && ln > 0)
+        throw ParseError(m.substr(size_t(used)), size_t(ln));
+      throw ParseError(m);
+    }
     case RS_ERR_INFEASIBLE: throw InfeasibleError(m);
     case RS_ERR_IO: throw IoError(m);
     case RS_ERR_OUT_OF_RANGE: throw std::out_of_range(m);
@@ -208,6 +216,57 @@ inline RemapTable read_remap(const std::string& path) {
   check(rs_remap_read(nullptr, path.c_str(), H ? r.entries.data() : &dummy, RS_MEM_HOST, H,
                       &r.slow_rows_allocated));
   return r;
+}
+
+/// A trace file loaded on the GPU (rs_trace_file): the records and ids stay in
+/// device memory; view() is an rs_trace for rs_profile_run / rs_simulate.
+class TraceFile {
+ public:
+  explicit TraceFile(const std::string& path, uint64_t chunk_bytes = 0) {
+    check(rs_trace_read(Context::instance().get(), path.c_str(), chunk_bytes, &f_));
+  }
+  ~TraceFile() { rs_trace_file_destroy(f_); }
+  TraceFile(const TraceFile&) = delete;
+  TraceFile& operator=(const TraceFile&) = delete;
+  rs_trace view() const {
+    rs_trace v{};
+    check(rs_trace_file_view(f_, &v));
+    return v;
+  }
+  /// The reference's value type (records and ids copied to the host).
+  Trace to_host() const {
+    const rs_trace v = view();
+    Trace t;
+    for (uint32_t j = 0; j < v.num_tables; ++j) {
+      const rs_table_spec& s = v.tables[j];
+      t.tables.push_back(TableSpec{s.table_id, s.cardinality, s.hash_size, s.dim, s.elem_bytes});
+    }
+    t.num_samples = v.num_samples;
+    std::vector<uint64_t> smp(v.num_records), off(v.num_records);
+    std::vector<uint32_t> tab(v.num_records), len(v.num_records);
+    t.ids.resize(v.num_ids);
+    check(rs_trace_file_export(Context::instance().get(), f_, smp.data(), tab.data(), off.data(), len.data(),
+                               t.ids.data(), RS_MEM_HOST));
+    t.records.resize(v.num_records);
+    for (size_t r = 0; r < t.records.size(); ++r) t.records[r] = Trace::Record{smp[r], tab[r], off[r], len[r]};
+    return t;
+  }
+
+ private:
+  rs_trace_file* f_ = nullptr;
+};
+
+/// include/shardplan/trace_io.hpp:35 — parsed on the GPU, same errors.
+inline Trace read_trace(const std::string& path) { return TraceFile(path).to_host(); }
+
+/// include/shardplan/trace_io.hpp:32-33 — byte-identical to the reference writer.
+inline void write_trace(const Trace& trace, const std::string& path,
+                        const std::vector<std::string>& comments = {}) {
+  detail::TraceSoA soa(trace);
+  std::vector<const char*> cs;
+  for (const auto& c : comments) cs.push_back(c.c_str());
+  check(rs_trace_write(Context::instance().get(), &soa.view, path.c_str(), cs.empty() ? nullptr : cs.data(),
+                       static_cast<uint32_t>(cs.size())));
 }
 
 /// include/shardplan/simulator.hpp:45-47 — tier counts on the GPU.

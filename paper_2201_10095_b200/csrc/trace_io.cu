@@ -27,10 +27,13 @@
 #include <zlib.h>
 
 #include <algorithm>
+#include <chrono>
+#include <future>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <fcntl.h>
+#include <sys/stat.h>
 #include <map>
 #include <string>
 #include <string_view>
@@ -455,6 +458,7 @@ struct Source {
   int fd = -1;
   gzFile gz = nullptr;
   uint64_t off = 0;
+  uint64_t size = 0;  // plain files: bytes on disk (sizes the outputs)
   bool eof = false;
   explicit Source(const std::string& p) : path(p) {
     const bool is_gz = p.size() > 3 && p.compare(p.size() - 3, 3, ".gz") == 0;
@@ -465,6 +469,8 @@ struct Source {
     } else {
       fd = ::open(p.c_str(), O_RDONLY);
       if (fd < 0) throw IoError("cannot open: " + p);
+      struct stat sb {};
+      if (::fstat(fd, &sb) == 0 && sb.st_size > 0) size = uint64_t(sb.st_size);
     }
   }
   ~Source() {
@@ -553,18 +559,26 @@ rs_trace_file* trace_read(rs_context* ctx, const char* path, uint64_t chunk_byte
   cudaStream_t st = ctx->stream;
   Source src(path);
   auto tf = std::make_unique<rs_trace_file>();
-  if (chunk_bytes == 0) chunk_bytes = size_t(256) << 20;
+  if (chunk_bytes == 0) chunk_bytes = size_t(64) << 20;
   chunk_bytes = std::max<uint64_t>(chunk_bytes, 4096);
-  // pinned chunk (+1 for a final '\n'); grows when one line outgrows it
-  size_t hcap = 0;
+  static const bool dbg = getenv("RS_TRACE_DEBUG") != nullptr;
+  double t_read = 0, t_nl = 0, t_p1 = 0, t_tl = 0, t_p2 = 0;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto secs = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+  // two pinned chunks (+1 for a final '\n'): the next one is read while the
+  // current one is parsed; both grow when one line outgrows a chunk
+  size_t hcap = 0, ocap = 0;
   char* hbuf = static_cast<char*>(ctx->host_pool->take(chunk_bytes + 1, &hcap));
+  char* obuf = static_cast<char*>(ctx->host_pool->take(chunk_bytes + 1, &ocap));
   struct Give {
     rs_context* c;
     char*& p;
     size_t& cap;
     ~Give() { c->host_pool->give(p, cap); }
-  } give{ctx, hbuf, hcap};
+  } give{ctx, hbuf, hcap}, give2{ctx, obuf, ocap};
+  auto t00 = now();
   size_t have = src.read(hbuf, hcap - 1);
+  t_read += secs(t00, now());
 
   // ---- header line (core/src/trace_io.cpp:75-89)
   if (have == 0) parse_error("empty trace file", 1);
@@ -613,22 +627,20 @@ rs_trace_file* trace_read(rs_context* ctx, const char* path, uint64_t chunk_byte
     uint64_t map_cap = 0;
     char* buf = nullptr;
     uint64_t buf_cap = 0;
+    uint32_t* lend = nullptr;
+    size_t lend_cap = 0;
+    char* blk = nullptr;
+    size_t blk_cap = 0;
     uint32_t* recline = nullptr;
     uint64_t recline_cap = 0;
     unsigned long long* err = nullptr;
     uint32_t* nt = nullptr;
     ~Work() {
-      for (void* p : {(void*)mid, (void*)mhs, (void*)mline, (void*)buf, (void*)recline, (void*)err, (void*)nt})
+      for (void* p : {(void*)mid, (void*)mhs, (void*)mline, (void*)buf, (void*)recline, (void*)err, (void*)nt,
+                      (void*)lend, (void*)blk})
         if (p) cudaFree(p);
     }
   } w;
-  struct FreeAll {
-    std::vector<void*> v;
-    ~FreeAll() {
-      for (void* p : v)
-        if (p) cudaFree(p);
-    }
-  };
   RS_CUDA(cudaMalloc(&w.err, 8));
   RS_CUDA(cudaMalloc(&w.nt, 4));
   unsigned long long* d_err = w.err;
@@ -641,13 +653,17 @@ rs_trace_file* trace_read(rs_context* ctx, const char* path, uint64_t chunk_byte
     const bool last = src.eof || have < hcap - 1;
     if (!last) {
       const char* p = static_cast<const char*>(memrchr(hbuf + start, '\n', have - start));
-      if (!p) {  // one line longer than the chunk: grow and read more
+      if (!p) {  // one line longer than the chunk: grow both and read more
         size_t ncap = 0;
         char* nb = static_cast<char*>(ctx->host_pool->take(hcap * 2, &ncap));
         std::memcpy(nb, hbuf + start, have - start);
         ctx->host_pool->give(hbuf, hcap);
         hbuf = nb;
         hcap = ncap;
+        ctx->host_pool->give(obuf, ocap);
+        obuf = nullptr;
+        ocap = 0;
+        obuf = static_cast<char*>(ctx->host_pool->take(hcap, &ocap));
         have -= start;
         start = 0;
         have += src.read(hbuf + have, hcap - 1 - have);
@@ -659,8 +675,21 @@ rs_trace_file* trace_read(rs_context* ctx, const char* path, uint64_t chunk_byte
       cut = have;
     }
     const uint64_t n = cut - start;
+    // the next chunk (this one's partial last line + fresh bytes) is read
+    // into the other buffer while this one is parsed
+    std::future<size_t> next;
+    if (!last) {
+      char* ob = obuf;
+      const size_t oc = ocap;
+      const char* tail = hbuf + cut;
+      const size_t rest = have - cut;
+      next = std::async(std::launch::async, [&src, ob, oc, tail, rest] {
+        std::memmove(ob, tail, rest);
+        return rest + src.read(ob + rest, oc - 1 - rest);
+      });
+    }
     if (n > 0) {
-      FreeAll fa;
+      auto tc0 = now();
       if (n > w.buf_cap) {
         if (w.buf) RS_CUDA(cudaFree(w.buf));
         w.buf = nullptr;
@@ -679,19 +708,29 @@ rs_trace_file* trace_read(rs_context* ctx, const char* path, uint64_t chunk_byte
       RS_CUDA(cudaMemcpyAsync(h_small, tbase + ntiles, 4, cudaMemcpyDeviceToHost, st));
       ctx->sync();
       const uint32_t nlines = *reinterpret_cast<uint32_t*>(h_small);
-      uint32_t* lend = nullptr;
-      RS_CUDA(cudaMalloc(&lend, size_t(nlines) * 4 + 4));
-      fa.v.push_back(lend);
+      auto tc1 = now();
+      t_nl += secs(tc0, tc1);
+      if (size_t(nlines) + 1 > w.lend_cap) {
+        if (w.lend) RS_CUDA(cudaFree(w.lend));
+        w.lend = nullptr;
+        w.lend_cap = size_t(nlines) + 1 + (size_t(nlines) >> 2);
+        RS_CUDA(cudaMalloc(&w.lend, w.lend_cap * 4));
+      }
+      uint32_t* lend = w.lend;
       nl_write_kernel<<<grid_for(ntiles, 1), 256, 0, st>>>(d_buf, n, tbase, lend);
       RS_COUNT(2);
       // pass 1
       Pass1Out o{};
       const size_t nl1 = size_t(nlines) + 1;
-      char* blk = nullptr;
       const uint32_t t_cap = 1u << 20;
       const size_t bytes = nl1 * (1 + 4 * 6 + 8) + size_t(t_cap) * 4 + 8 * 256;
-      RS_CUDA(cudaMalloc(&blk, bytes));
-      fa.v.push_back(blk);
+      if (bytes > w.blk_cap) {
+        if (w.blk) RS_CUDA(cudaFree(w.blk));
+        w.blk = nullptr;
+        w.blk_cap = bytes + bytes / 4;
+        RS_CUDA(cudaMalloc(&w.blk, w.blk_cap));
+      }
+      char* blk = w.blk;
       size_t at = 0;
       auto carve = [&](size_t b) {
         char* p = blk + at;
@@ -730,6 +769,8 @@ rs_trace_file* trace_read(rs_context* ctx, const char* path, uint64_t chunk_byte
       unsigned long long err_line = h_small[1];
       const uint32_t nT = reinterpret_cast<uint32_t*>(h_small + 2)[0];
       if (nT > t_cap) throw Error(-9, "read_trace: too many table lines in one chunk");
+      auto tc2 = now();
+      t_p1 += secs(tc1, tc2);
       // T lines on the host, in line order (only those before the first error)
       std::vector<uint32_t> tl(nT);
       std::vector<uint32_t> tb(nT * 2);
@@ -780,16 +821,24 @@ rs_trace_file* trace_read(rs_context* ctx, const char* path, uint64_t chunk_byte
           ctx->sync();  // the host vectors are reused by the next chunk
         }
       }
-      // pass 2 + record order
-      if (tf->nrec + nR > tf->rec_cap) {
+      auto tc3 = now();
+      t_tl += secs(tc2, tc3);
+      // pass 2 + record order; the first chunk sizes the outputs for the file
+      uint64_t want_rec = tf->nrec + nR, want_ids = tf->nids + nI;
+      if (tf->nrec == 0 && src.size && n) {
+        const double scale = double(src.size) / double(n) * 1.02;
+        want_rec = std::max<uint64_t>(want_rec, uint64_t(double(nR) * scale) + 1024);
+        want_ids = std::max<uint64_t>(want_ids, uint64_t(double(nI) * scale) + 4096);
+      }
+      if (want_rec > tf->rec_cap) {
         uint64_t c = tf->rec_cap;
-        grow(tf->rec_sample, c, tf->nrec, tf->nrec + nR, st);
+        grow(tf->rec_sample, c, tf->nrec, want_rec, st);
         c = tf->rec_cap;
-        grow(tf->rec_table, c, tf->nrec, tf->nrec + nR, st);
+        grow(tf->rec_table, c, tf->nrec, want_rec, st);
         c = tf->rec_cap;
-        grow(tf->rec_offset, c, tf->nrec, tf->nrec + nR, st);
+        grow(tf->rec_offset, c, tf->nrec, want_rec, st);
         c = tf->rec_cap;
-        grow(tf->rec_len, c, tf->nrec, tf->nrec + nR, st);
+        grow(tf->rec_len, c, tf->nrec, want_rec, st);
         tf->rec_cap = c;
       }
       if (nR > w.recline_cap) {
@@ -798,7 +847,7 @@ rs_trace_file* trace_read(rs_context* ctx, const char* path, uint64_t chunk_byte
         w.recline_cap = std::max<uint64_t>(nR, 1024);
         RS_CUDA(cudaMalloc(&w.recline, w.recline_cap * 4));
       }
-      grow(tf->ids, tf->ids_cap, tf->nids, tf->nids + nI, st);
+      grow(tf->ids, tf->ids_cap, tf->nids, want_ids, st);
       if (nlines && nR) {
         Pass2Args a{o.kind, rscan, iscan, o.nids, o.smp, o.tab, o.idpos, tf->nrec, tf->nids, tf->num_samples,
                     tf->rec_sample, tf->rec_table, tf->rec_offset, tf->rec_len, w.recline, tf->ids, d_err};
@@ -837,16 +886,20 @@ rs_trace_file* trace_read(rs_context* ctx, const char* path, uint64_t chunk_byte
       }
       tf->nrec += nR;
       tf->nids += nI;
+      t_p2 += secs(tc3, now());
       lbase += nlines;
     }
     if (last) break;
-    // carry the partial line to the front and refill
-    const size_t rest = have - cut;
-    std::memmove(hbuf, hbuf + cut, rest);
-    have = rest;
+    auto tw = now();
+    have = next.get();
+    t_read += secs(tw, now());
+    std::swap(hbuf, obuf);
+    std::swap(hcap, ocap);
     start = 0;
-    have += src.read(hbuf + have, hcap - 1 - have);
   }
+  if (dbg)
+    std::fprintf(stderr, "read_trace: read-wait %.3f s, newlines %.3f, pass1 %.3f, T lines %.3f, pass2 %.3f\n",
+                 t_read, t_nl, t_p1, t_tl, t_p2);
   if (tf->tables.size() != expect_tables)
     parse_error(strfmt("header announced %zu tables, found %zu", size_t(expect_tables), tf->tables.size()), 0);
   return tf.release();

@@ -10,6 +10,8 @@
 
 #include "shardplan/baselines.hpp"
 #include "shardplan/milp.hpp"
+#include "shardplan/trace_io.hpp"
+#include "shardplan/workload.hpp"
 #include "shardplan_gpu.hpp"
 
 #include <cuda_runtime.h>
@@ -181,6 +183,35 @@ int main() {
     CHECK(throws<InvalidArgument>([&] { gpu::simulate(t, plan, gpu_r, sys, 1 << 30); }));
   }
   CHECK(throws<IoError>([] { gpu::read_remap("/nonexistent/x.sprm"); }));
+  // trace files (core/src/trace_io.cpp): each side reads what the other wrote
+  for (const char* ext : {".trace", ".trace.gz"}) {
+    Trace t = generate_trace(specs, 3000, 21);
+    const std::string pa = std::string("/tmp/rs_dropin_a") + ext, pb = std::string("/tmp/rs_dropin_b") + ext;
+    write_trace(t, pa, {"ref"});
+    gpu::write_trace(t, pb, {"ref"});
+    Trace a = gpu::read_trace(pa), b = read_trace(pb);
+    bool eq = a.num_samples == b.num_samples && a.ids == b.ids && a.records.size() == b.records.size() &&
+              a.tables.size() == b.tables.size();
+    for (size_t r = 0; eq && r < a.records.size(); ++r)
+      eq = a.records[r].sample == b.records[r].sample && a.records[r].table == b.records[r].table &&
+           a.records[r].offset == b.records[r].offset && a.records[r].len == b.records[r].len;
+    CHECK(eq && a.ids == t.ids);
+    std::remove(pa.c_str());
+    std::remove(pb.c_str());
+  }
+  {
+    FILE* f = std::fopen("/tmp/rs_dropin_bad.trace", "wb");
+    std::fputs("#shardplan-trace v1 tables=1 samples=10\nT 0 100 100 4 4\nR zero 0 1\n", f);
+    std::fclose(f);
+    bool line3 = false;
+    try {
+      gpu::read_trace("/tmp/rs_dropin_bad.trace");
+    } catch (const ParseError& e) {
+      line3 = e.line() == 3 && std::string(e.what()) == "line 3: bad sample_id: 'zero'";
+    }
+    CHECK(line3);
+    std::remove("/tmp/rs_dropin_bad.trace");
+  }
   {
     FILE* f = std::fopen("/tmp/rs_dropin_bad.sprm", "wb");
     std::fwrite("SPRX", 1, 4, f);
