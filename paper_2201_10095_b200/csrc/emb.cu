@@ -101,6 +101,40 @@ __device__ __forceinline__ void flush_hits(unsigned long long* hits, uint32_t t,
   }
 }
 
+// Pipelined-bag helpers of forward_kernel: the bag's table and CSR offsets,
+// its first G indices, their (checked) remap entries.
+__device__ __forceinline__ void fwd_bag_offsets(const uint32_t* __restrict__ cls_tables,
+                                                const uint32_t* __restrict__ offsets, uint64_t B, uint64_t wpt,
+                                                int BPW, int grp, uint64_t ww, uint32_t& t, uint32_t& s,
+                                                uint32_t& e) {
+  t = cls_tables[ww / wpt];
+  const uint64_t bb = (ww % wpt) * BPW + grp;
+  s = e = 0;
+  if (bb < B) {
+    s = offsets[uint64_t(t) * B + bb];
+    e = offsets[uint64_t(t) * B + bb + 1];
+  }
+}
+__device__ __forceinline__ uint32_t fwd_bag_index(const uint32_t* __restrict__ indices, int lg, uint32_t s,
+                                                  uint32_t e) {
+  return uint32_t(lg) < e - s ? ld_stream_u32(indices + s + lg) : 0u;
+}
+__device__ __forceinline__ int32_t fwd_bag_entry(const TableDev* __restrict__ tables, unsigned* err, int lg,
+                                                 uint32_t t, uint32_t s, uint32_t e, uint32_t idx) {
+  if (uint32_t(lg) >= e - s) return 0;
+  const TableDev& tn = tables[t];
+  if (idx >= tn.hash_size) {  // reported by the next backward / rs_emb_check
+    atomicOr(err, 1u);
+    idx = 0;
+  }
+  return tn.remap[idx];
+}
+
+// Software-pipelined over the warp's grid-stride bags: the next bag's
+// offsets are loaded at the top of this one, its first G indices once this
+// bag's first row loads are in flight, and their remap entries once those
+// rows have arrived — so a bag's dependent chain is its row loads, not
+// offsets -> index -> remap -> rows.
 template <int G, int VPL, int UNR, int MINB>
 __global__ void __launch_bounds__(kFwdThreads, MINB)
 forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__ cls_tables,
@@ -117,23 +151,32 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
   const uint64_t total_w = wpt * ntab;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   uint32_t cur_t = 0xFFFFFFFFu, fast = 0, tot = 0;
-  TableDev td{};
-  for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < total_w; w += nwarps) {
-    const uint32_t t = cls_tables[w / wpt];
+  // the pipelined bag: table, offsets, first G indices (checked) and entries
+  uint32_t nt = 0, ns = 0, ne = 0, nidx = 0;
+  int32_t nent = 0;
+  uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (w < total_w) {
+    fwd_bag_offsets(cls_tables, offsets, B, wpt, BPW, grp, w, nt, ns, ne);
+    nidx = fwd_bag_index(indices, lg, ns, ne);
+    nent = fwd_bag_entry(tables, err, lg, nt, ns, ne, nidx);
+  }
+  for (; w < total_w; w += nwarps) {
+    const uint32_t t = nt, s = ns, e = ne;
+    const int32_t ent0 = nent;
+    const uint64_t w2 = w + nwarps;
+    const bool more = w2 < total_w;
+    if (more) fwd_bag_offsets(cls_tables, offsets, B, wpt, BPW, grp, w2, nt, ns, ne);
+    bool pf = !more;  // next bag's index/entry issued?
     if (t != cur_t) {
       if (hits && cur_t != 0xFFFFFFFFu) flush_hits(hits, cur_t, fast, tot);
       fast = tot = 0;
       cur_t = t;
-      td = tables[t];
     }
+    // the table's fields are re-read per bag (L1 hits) rather than held live
+    const TableDev& td = tables[t];
     const uint32_t V = td.dim >> 2;
     const uint64_t b = (w % wpt) * BPW + grp;
     const bool valid = b < B;
-    uint32_t s = 0, e = 0;
-    if (valid) {
-      s = offsets[uint64_t(t) * B + b];
-      e = offsets[uint64_t(t) * B + b + 1];
-    }
     float4 acc[VPL];
 #pragma unroll
     for (int vv = 0; vv < VPL; ++vv) acc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -143,15 +186,19 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
       int32_t ent = 0;
       if (uint32_t(lg) < n) {
         const uint32_t l = base + lg;
-        uint32_t idx = ld_stream_u32(indices + l);
-        if (idx >= td.hash_size) {  // reported by the next backward / rs_emb_check
-          atomicOr(err, 1u);
-          idx = 0;
+        if (base == s) {
+          ent = ent0;
+        } else {
+          uint32_t idx = ld_stream_u32(indices + l);
+          if (idx >= td.hash_size) {
+            atomicOr(err, 1u);
+            idx = 0;
+          }
+          ent = td.remap[idx];
         }
-        ent = td.remap[idx];
         fast += ent >= 0;
         // the backward's sort keys, while the remap entry is in hand
-        // (key = table key base + storage slot, value = sample)
+        // (key = storage slot within the table, value = sample)
         if (keys) {
           if (l < max_keys) {
             keys[l] = slot_of_entry(td, ent);
@@ -173,6 +220,7 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
             v[u][vv] = (j + u < n && vec < V) ? ld_nc_f4(row + vec) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
+        if (!pf) nidx = fwd_bag_index(indices, lg, ns, ne);  // behind this bag's first rows
 #pragma unroll
         for (int u = 0; u < kFwdUnroll; ++u) {
           if (j + u < n) {
@@ -185,7 +233,15 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
             }
           }
         }
+        if (!pf) {
+          nent = fwd_bag_entry(tables, err, lg, nt, ns, ne, nidx);
+          pf = true;
+        }
       }
+    }
+    if (!pf) {  // an empty bag: fetch the next one's head directly
+      nidx = fwd_bag_index(indices, lg, ns, ne);
+      nent = fwd_bag_entry(tables, err, lg, nt, ns, ne, nidx);
     }
     if (valid) {
       float4* o = reinterpret_cast<float4*>(out + b * stride + td.col);
