@@ -390,7 +390,6 @@ struct rs_emb {
   uint32_t key_bits = 0;  // max over tables of the slot-key width
   // segmented sort tiles (per table): pos[ntiles+1] | cidx[ntiles] | cstride[ntiles]
   uint32_t* d_tiles = nullptr;
-  uint32_t* h_tiles = nullptr;
   size_t tiles_cap = 0;
   int bwd_vpl = 1;
   // backward buffers
@@ -491,6 +490,13 @@ struct rs_emb {
   uint32_t* d_meta = nullptr;
   uint32_t* h_meta = nullptr;
   size_t meta_words = 0;
+  // device backward plan (bwd_plan_kernel): class-major table order, class
+  // boundaries, class window bounds, sort tile count; the error word's copy
+  uint32_t* d_order = nullptr;
+  uint32_t* d_cpos = nullptr;
+  uint32_t* d_cw = nullptr;
+  uint32_t* d_nt = nullptr;
+  cudaEvent_t ev_err = nullptr;
   unsigned* d_err = nullptr;
   char* sort_scratch = nullptr;
   size_t sort_scratch_bytes = 0;
@@ -521,7 +527,6 @@ struct rs_emb {
     for (auto& c : classes)
       if (c.d_list) cudaFree(c.d_list);
     if (d_tiles) cudaFree(d_tiles);
-    if (h_tiles) cudaFreeHost(h_tiles);
     if (keys) cudaFree(keys);
     if (vals) cudaFree(vals);
     for (void* p : {(void*)scount, (void*)sbase, (void*)segs, (void*)longs, (void*)long_np, (void*)long_ng,
@@ -529,6 +534,9 @@ struct rs_emb {
       if (p) cudaFree(p);
     if (d_meta) cudaFree(d_meta);
     if (h_meta) cudaFreeHost(h_meta);
+    for (void* p : {(void*)d_order, (void*)d_cpos, (void*)d_cw, (void*)d_nt})
+      if (p) cudaFree(p);
+    if (ev_err) cudaEventDestroy(ev_err);
     if (d_err) cudaFree(d_err);
     if (sort_scratch) cudaFree(sort_scratch);
     if (side) {
@@ -657,6 +665,21 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
       RS_CUDA(cudaMemcpyAsync(c.d_list, c.tables.data(), 4 * c.tables.size(), cudaMemcpyHostToDevice, st));
     }
     {
+      std::vector<uint32_t> order, cpos{0};
+      for (auto& c : e->classes) {
+        order.insert(order.end(), c.tables.begin(), c.tables.end());
+        cpos.push_back(uint32_t(order.size()));
+      }
+      RS_CUDA(cudaMalloc(&e->d_order, 4 * std::max<size_t>(1, order.size())));
+      RS_CUDA(cudaMalloc(&e->d_cpos, 4 * cpos.size()));
+      RS_CUDA(cudaMalloc(&e->d_cw, 4 * cpos.size()));
+      RS_CUDA(cudaMalloc(&e->d_nt, 4));
+      if (!order.empty())
+        RS_CUDA(cudaMemcpy(e->d_order, order.data(), 4 * order.size(), cudaMemcpyHostToDevice));
+      RS_CUDA(cudaMemcpy(e->d_cpos, cpos.data(), 4 * cpos.size(), cudaMemcpyHostToDevice));
+      RS_CUDA(cudaEventCreateWithFlags(&e->ev_err, cudaEventDisableTiming));
+    }
+    {
       int v = 1;
       while (v * 32 * 4 < int(e->dmax)) v <<= 1;
       e->bwd_vpl = v;
@@ -684,7 +707,6 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
     e->sort_scratch_bytes = radix_sort_scratch_bytes(L, T) + (4 << 20);
     e->tiles_cap = L / kSortTile + T + 2;
     RS_CUDA(cudaMalloc(&e->d_tiles, 3 * e->tiles_cap * 4));
-    RS_CUDA(cudaHostAlloc(&e->h_tiles, 3 * e->tiles_cap * 4, cudaHostAllocDefault));
     RS_CUDA(cudaMalloc(&e->sort_scratch, e->sort_scratch_bytes));
     // per-backward metadata: tpos[T+1] | wstart[T+1] | wtab[T] (class-major
     // window work map)
@@ -769,9 +791,17 @@ void emb_enable_cache(rs_emb* e, uint32_t nslots) {
     RS_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
   RS_CUDA(cudaStreamSynchronize(st));
   // host threads: one gather pool (in) and one scatter pool (out) sharing the cores
-  const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
-  e->pool = std::make_unique<rs::ThreadPool>(std::min(16u, hw));
-  e->out_pool = std::make_unique<rs::ThreadPool>(std::min(8u, hw / 2));
+  // host threads for the row gathers / write-back scatters: half / a quarter
+  // of the cores (the caller's thread, the CUDA driver and both task queues
+  // need the rest; oversubscribing shows up as staging stalls)
+  const unsigned hw = std::max(4u, std::thread::hardware_concurrency());
+  auto env_threads = [](const char* name, unsigned dflt) {
+    const char* v = getenv(name);
+    const int n = v ? atoi(v) : 0;
+    return n > 0 ? unsigned(n) : dflt;
+  };
+  e->pool = std::make_unique<rs::ThreadPool>(env_threads("RS_GATHER_THREADS", std::min(16u, hw / 2)));
+  e->out_pool = std::make_unique<rs::ThreadPool>(env_threads("RS_SCATTER_THREADS", std::min(8u, hw / 4)));
   e->worker = std::make_unique<rs::TaskQueue>();
   e->out_worker = std::make_unique<rs::TaskQueue>();
   e->nslots = nslots;
@@ -1054,18 +1084,20 @@ void emb_kernel_times(rs_emb* e, double* fwd_ms, uint64_t* n_fwd, double* bwd_ms
 
 // Short-segment bag pass for one lane class over its window range [wlo, whi).
 template <int G, int VPL, int UNR, int MINB>
-static void launch_segs_v(rs_emb* e, const emb::BwdArgs& a, uint32_t wlo, uint32_t whi) {
-  const uint64_t est = uint64_t(whi - wlo) * 8 / (uint64_t(emb::kBwdWarps) * (32 / G)) + 1;
+static void launch_segs_v(rs_emb* e, const emb::BwdArgs& a, uint32_t ci, uint64_t max_windows) {
+  // the class's window range is on the device (bwd_plan_kernel): persistent
+  // grid, capped by the class's largest possible window count
+  const uint64_t est = max_windows * 8 / (uint64_t(emb::kBwdWarps) * (32 / G)) + 1;
   const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(est, uint64_t(sm_count()) * MINB)));
   emb::bwd_seg_kernel<G, VPL, UNR, MINB><<<grid, emb::kBwdThreads, 0, e->ctx->stream>>>(
-      a, e->segs, e->sbase, wlo, whi, e->longs, e->long_np, e->long_ng, e->n_long);
+      a, e->segs, e->sbase, e->d_cw, ci, e->longs, e->long_np, e->long_ng, e->n_long);
   RS_COUNT(1);
 }
 
 template <int G, int VPL>
-static void launch_segs(rs_emb* e, const emb::BwdArgs& a, uint32_t wlo, uint32_t whi) {
-  if constexpr (VPL == 1) launch_segs_v<G, 1, 4, 4>(e, a, wlo, whi);
-  else launch_segs_v<G, VPL, (VPL == 2 ? 2 : 1), 2>(e, a, wlo, whi);
+static void launch_segs(rs_emb* e, const emb::BwdArgs& a, uint32_t ci, uint64_t max_windows) {
+  if constexpr (VPL == 1) launch_segs_v<G, 1, 4, 4>(e, a, ci, max_windows);
+  else launch_segs_v<G, VPL, (VPL == 2 ? 2 : 1), 2>(e, a, ci, max_windows);
 }
 
 // Long segments: groups of 64 pieces, then one warp per segment (full warps,
@@ -1106,45 +1138,15 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
   } release{e};
   cudaStream_t st = e->ctx->stream;
   const uint32_t T = e->T;
-  uint32_t* tpos = e->h_meta;  // offsets[t*B], t = 0..T
   uint32_t* herr = e->h_meta + e->meta_words - 1;
-  RS_CUDA(cudaMemcpy2DAsync(tpos, 4, off, size_t(B) * 4, 4, T + 1, cudaMemcpyDeviceToHost, st));
-  RS_CUDA(cudaMemcpyAsync(herr, e->d_err, 4, cudaMemcpyDeviceToHost, st));
-  RS_CUDA(cudaStreamSynchronize(st));
-  if (*herr) {
-    RS_CUDA(cudaMemsetAsync(e->d_err, 0, 4, st));
-    e->keys_off = nullptr;
-    if (*herr & 1u) throw InvalidArgument("emb: an index is outside its table's hash_size");
-    throw InvalidArgument("emb: more lookups than max_lookups");
-  }
   // keys from the forward of this very batch?  (the sort below consumes them)
   const bool have_keys = e->keys_off == off && e->keys_idx == idx && e->keys_B == B;
   e->keys_off = nullptr;
-  const uint32_t L = tpos[T];
-  if (tpos[0] != 0) throw InvalidArgument("emb_backward: offsets must start at 0");
-  if (L > e->max_lookups) throw InvalidArgument("emb_backward: more lookups than max_lookups");
-  if (L == 0) return;
-  for (uint32_t t = 0; t < T; ++t)
-    if (tpos[t + 1] < tpos[t]) throw InvalidArgument("emb_backward: offsets must be non-decreasing");
-  // class-major window work map: table t has ceil(L_t / 32) windows
-  uint32_t* wstart = tpos + T + 1;
-  uint32_t* wtab = wstart + T + 1;
-  std::vector<uint64_t> class_chunks;
-  {
-    uint32_t acc = 0, i = 0;
-    for (const auto& c : e->classes) {
-      const uint32_t c0 = acc;
-      for (uint32_t t : c.tables) {
-        wstart[i] = acc;
-        wtab[i] = t;
-        acc += (tpos[t + 1] - tpos[t] + emb::kChunk - 1) / emb::kChunk;
-        ++i;
-      }
-      class_chunks.push_back(acc - c0);
-    }
-    wstart[T] = acc;
-  }
-  RS_CUDA(cudaMemcpyAsync(e->d_meta, e->h_meta, e->meta_words * 4, cudaMemcpyHostToDevice, st));
+  // Everything is enqueued before the host looks at anything: the plan
+  // (validation, work map, sort tiles) is computed on the device from the
+  // offsets, so the GPU runs the backward straight after the forward.  The
+  // host then waits only for the plan's error word and raises afterwards
+  // (an empty plan makes every later kernel a no-op).
   e->t_bwd.begin(st);
   if (!have_keys) {
     const uint64_t nb = uint64_t(e->T) * B;
@@ -1152,69 +1154,61 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
     emb::keygen_kernel<<<g, 256, 0, st>>>(e->d_tables, e->T, B, off, idx, e->keys, e->vals, e->d_err);
     RS_COUNT(1);
   }
+  uint32_t* d_tpos = e->d_meta;
+  uint32_t* d_wstart = e->d_meta + T + 1;
+  uint32_t* d_wtab = e->d_meta + 2 * (T + 1);
+  const uint32_t tcap = uint32_t(e->tiles_cap);
+  {
+    emb::BwdPlan pl{off, B, T, e->d_order, e->d_cpos, uint32_t(e->classes.size()), e->max_lookups,
+                    d_tpos, d_wstart, d_wtab, e->d_cw, e->d_tiles, tcap, e->d_nt, e->d_err};
+    emb::bwd_plan_kernel<<<1, 1024, 0, st>>>(pl);
+    RS_COUNT(1);
+    RS_CUDA(cudaMemcpyAsync(herr, e->d_err, 4, cudaMemcpyDeviceToHost, st));
+    RS_CUDA(cudaEventRecord(e->ev_err, st));
+  }
+  const uint64_t Lmax = e->max_lookups;
   Scratch scr;
   scr.base = e->sort_scratch;
   scr.cap = e->sort_scratch_bytes;
+  uint32_t* skeys = e->keys;
+  uint32_t* svals = e->vals;
   {
     // segmented sort: each table's CSR range sorted on its own (slot keys)
-    uint32_t* pos = e->h_tiles;
-    uint32_t nt = 0;
-    std::vector<uint32_t> cidx, cstr;
-    cidx.reserve(e->tiles_cap);
-    cstr.reserve(e->tiles_cap);
-    for (uint32_t t = 0; t < T; ++t) {
-      const uint32_t lt = tpos[t + 1] - tpos[t];
-      const uint32_t ntt = (lt + kSortTile - 1) / kSortTile;
-      for (uint32_t j = 0; j < ntt; ++j) {
-        pos[nt + j] = tpos[t] + j * kSortTile;
-        cidx.push_back(uint32_t(kRadix) * nt + j);
-        cstr.push_back(ntt);
-      }
-      nt += ntt;
-    }
-    pos[nt] = L;
-    memcpy(pos + nt + 1, cidx.data(), nt * 4);
-    memcpy(pos + 2 * nt + 1, cstr.data(), nt * 4);
-    RS_CUDA(cudaMemcpyAsync(e->d_tiles, e->h_tiles, (3 * size_t(nt) + 1) * 4, cudaMemcpyHostToDevice, st));
     TileMap tm;
     tm.pos = e->d_tiles;
-    tm.cidx = e->d_tiles + nt + 1;
-    tm.cstride = e->d_tiles + 2 * nt + 1;
-    radix_sort_pairs(e->keys, e->vals, L, int(e->key_bits), scr, st, tm, nt);
+    tm.cidx = e->d_tiles + tcap;
+    tm.cstride = e->d_tiles + 2 * size_t(tcap);
+    tm.ntd = e->d_nt;
+    radix_sort_pairs(e->keys, e->vals, Lmax, int(e->key_bits), scr, st, tm, tcap - 1, &skeys, &svals);
   }
-  emb::BwdArgs a{e->cur_tables, T, e->d_meta, e->keys, e->vals, grad, e->total_dim, e->dmax, lr, e->eps, e->opt};
+  emb::BwdArgs a{e->cur_tables, T, d_tpos, skeys, svals, grad, e->total_dim, e->dmax, lr, e->eps, e->opt};
   // segment list: count heads per window, scan, write descriptors
-  const uint32_t W = wstart[T];
-  const size_t woff = size_t(wstart - e->h_meta);
-  emb::WorkMap wm{e->d_meta + woff, e->d_meta + woff + T + 1, T};
-  const unsigned gs = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((uint64_t(W) + 7) / 8, uint64_t(sm_count()) * 16)));
+  const uint64_t Wmax = (Lmax + emb::kChunk - 1) / emb::kChunk + T;
+  emb::WorkMap wm{d_wstart, d_wtab, T};
+  const unsigned gs = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((Wmax + 7) / 8, uint64_t(sm_count()) * 16)));
   emb::bwd_seg_scan_kernel<false><<<gs, 256, 0, st>>>(a, wm, e->scount, nullptr, nullptr);
-  exclusive_scan<uint32_t>(ArrayIn<uint32_t>{e->scount}, W, e->sbase, e->sbase + W, scr, st);
+  exclusive_scan<uint32_t>(ArrayIn<uint32_t>{e->scount}, Wmax, e->sbase, e->sbase + Wmax, scr, st);
   emb::bwd_seg_scan_kernel<true><<<gs, 256, 0, st>>>(a, wm, nullptr, e->sbase, e->segs);
   RS_COUNT(2);
   // short segments per lane class (long ones are listed)
   RS_CUDA(cudaMemsetAsync(e->n_long, 0, 4, st));
   RS_CUDA(cudaMemsetAsync(e->long_np, 0, (e->long_cap + 1) * 4, st));
   RS_CUDA(cudaMemsetAsync(e->long_ng, 0, (e->long_cap + 1) * 4, st));
-  uint32_t wlo = 0;
   for (size_t ci = 0; ci < e->classes.size(); ++ci) {
     const auto& c = e->classes[ci];
-    const uint32_t whi = wlo + uint32_t(class_chunks[ci]);
-    if (whi > wlo) {
-      switch (c.G * 100 + c.VPL) {
-        case 101: launch_segs<1, 1>(e, a, wlo, whi); break;
-        case 201: launch_segs<2, 1>(e, a, wlo, whi); break;
-        case 401: launch_segs<4, 1>(e, a, wlo, whi); break;
-        case 801: launch_segs<8, 1>(e, a, wlo, whi); break;
-        case 1601: launch_segs<16, 1>(e, a, wlo, whi); break;
-        case 3201: launch_segs<32, 1>(e, a, wlo, whi); break;
-        case 3202: launch_segs<32, 2>(e, a, wlo, whi); break;
-        case 3204: launch_segs<32, 4>(e, a, wlo, whi); break;
-        case 3208: launch_segs<32, 8>(e, a, wlo, whi); break;
-        default: throw Error(-9, "emb_backward: unsupported lane class");
-      }
+    const uint64_t mw = Wmax;
+    switch (c.G * 100 + c.VPL) {
+      case 101: launch_segs<1, 1>(e, a, uint32_t(ci), mw); break;
+      case 201: launch_segs<2, 1>(e, a, uint32_t(ci), mw); break;
+      case 401: launch_segs<4, 1>(e, a, uint32_t(ci), mw); break;
+      case 801: launch_segs<8, 1>(e, a, uint32_t(ci), mw); break;
+      case 1601: launch_segs<16, 1>(e, a, uint32_t(ci), mw); break;
+      case 3201: launch_segs<32, 1>(e, a, uint32_t(ci), mw); break;
+      case 3202: launch_segs<32, 2>(e, a, uint32_t(ci), mw); break;
+      case 3204: launch_segs<32, 4>(e, a, uint32_t(ci), mw); break;
+      case 3208: launch_segs<32, 8>(e, a, uint32_t(ci), mw); break;
+      default: throw Error(-9, "emb_backward: unsupported lane class");
     }
-    wlo = whi;
   }
   // long segments: group offsets, group sums, final sums + updates
   exclusive_scan<uint32_t>(ArrayIn<uint32_t>{e->long_np}, e->long_cap, e->pbase, e->pbase + e->long_cap, scr, st);
@@ -1228,6 +1222,16 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
   }
   e->t_bwd.end(st);
   RS_LAUNCH_CHECK();
+  // the plan's verdict (the GPU is already past it or running the backward)
+  RS_CUDA(cudaEventSynchronize(e->ev_err));
+  if (const unsigned bad = *herr) {
+    RS_CUDA(cudaMemsetAsync(e->d_err, 0, 4, st));
+    if (bad & 1u) throw InvalidArgument("emb: an index is outside its table's hash_size");
+    if (bad & 2u) throw InvalidArgument("emb: more lookups than max_lookups");
+    if (bad & 4u) throw InvalidArgument("emb_backward: offsets must start at 0");
+    if (bad & 8u) throw InvalidArgument("emb_backward: more lookups than max_lookups");
+    throw InvalidArgument("emb_backward: offsets must be non-decreasing");
+  }
 }
 
 void emb_read_rows(rs_emb* e, uint32_t t, const uint32_t* rows, uint64_t n, float* out, float* mom) {

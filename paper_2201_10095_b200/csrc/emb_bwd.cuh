@@ -135,6 +135,124 @@ struct WorkMap {
   uint32_t nt;
 };
 
+// ---------------------------------------------------------------- plan
+// Block-wide exclusive scan of one value per thread (blockDim.x = 1024).
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* sm, uint32_t& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) sm[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    const uint32_t x = lane < int(blockDim.x >> 5) ? sm[lane] : 0u;
+    uint32_t xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) xi += y;
+    }
+    sm[lane] = xi - x;
+    if (lane == 31) sm[32] = xi;
+  }
+  __syncthreads();
+  const uint32_t r = sm[wid] + inc - v;
+  total = sm[32];
+  __syncthreads();
+  return r;
+}
+
+struct BwdPlan {
+  const uint32_t* off;    // the batch's table-major CSR offsets [T*B + 1]
+  uint64_t B;
+  uint32_t T;
+  const uint32_t* order;  // [T] tables in class-major order
+  const uint32_t* cpos;   // [ncls + 1] class boundaries in `order`
+  uint32_t ncls;
+  uint64_t max_lookups;
+  uint32_t* tpos;         // [T + 1] sorted-position start of each table
+  uint32_t* wstart;       // [T + 1] first window of order[i]
+  uint32_t* wtab;         // [T]
+  uint32_t* cw;           // [ncls + 1] first window of each class
+  uint32_t* tiles;        // sort tiles: pos | cidx | cstride, each `tcap` words
+  uint32_t tcap;
+  uint32_t* nt;           // sort tile count
+  unsigned* err;          // forward bits 1, 2; here 4 (off[0] != 0), 8 (> max_lookups), 16 (decreasing)
+};
+
+// One CTA of 1024 threads: everything the backward used to read back to the
+// host — validation, the class-major window work map and the segmented sort's
+// tile map — computed where the offsets are.  On any error (the forward's
+// included) the plan is empty, so every later kernel of the backward does
+// nothing and the host raises after the fact.
+__global__ void __launch_bounds__(1024) bwd_plan_kernel(BwdPlan p) {
+  __shared__ uint32_t sm[33];
+  __shared__ unsigned s_err;
+  const uint32_t T = p.T;
+  if (threadIdx.x == 0) s_err = 0;
+  __syncthreads();
+  for (uint32_t t = threadIdx.x; t <= T; t += blockDim.x) p.tpos[t] = p.off[uint64_t(t) * p.B];
+  __syncthreads();
+  unsigned bad = 0;
+  for (uint32_t t = threadIdx.x; t < T; t += blockDim.x)
+    if (p.tpos[t + 1] < p.tpos[t]) bad |= 16u;
+  if (threadIdx.x == 0) {
+    if (p.tpos[0] != 0) bad |= 4u;
+    if (p.tpos[T] > p.max_lookups) bad |= 8u;
+  }
+  if (bad) atomicOr(&s_err, bad);
+  __syncthreads();
+  if (s_err) {
+    if (threadIdx.x == 0) atomicOr(p.err, s_err);
+  }
+  __syncthreads();
+  const bool empty = *reinterpret_cast<volatile unsigned*>(p.err) != 0;
+  __syncthreads();
+  // windows of 32 sorted positions per table, class-major
+  uint32_t carry = 0;
+  for (uint32_t i0 = 0; i0 < T; i0 += blockDim.x) {
+    const uint32_t i = i0 + threadIdx.x;
+    uint32_t nw = 0, t = 0;
+    if (i < T) {
+      t = p.order[i];
+      nw = empty ? 0u : (p.tpos[t + 1] - p.tpos[t] + kChunk - 1) / kChunk;
+    }
+    uint32_t tot;
+    const uint32_t x = block_excl_scan(nw, sm, tot);
+    if (i < T) {
+      p.wstart[i] = carry + x;
+      p.wtab[i] = t;
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0) p.wstart[T] = carry;
+  __syncthreads();
+  for (uint32_t c = threadIdx.x; c <= p.ncls; c += blockDim.x) p.cw[c] = p.wstart[p.cpos[c]];
+  // sort tiles (table order): ceil(L_t / kSortTile) per table
+  uint32_t tb = 0;
+  for (uint32_t t0 = 0; t0 < T; t0 += blockDim.x) {
+    const uint32_t t = t0 + threadIdx.x;
+    uint32_t ntt = 0;
+    if (t < T && !empty) ntt = (p.tpos[t + 1] - p.tpos[t] + kSortTile - 1) / kSortTile;
+    uint32_t tot;
+    const uint32_t x = block_excl_scan(ntt, sm, tot);
+    for (uint32_t j = 0; j < ntt; ++j) {
+      const uint32_t k = tb + x + j;
+      p.tiles[k] = p.tpos[t] + j * kSortTile;
+      p.tiles[p.tcap + k] = uint32_t(kRadix) * (tb + x) + j;
+      p.tiles[2 * p.tcap + k] = ntt;
+    }
+    tb += tot;
+  }
+  if (threadIdx.x == 0) {
+    p.tiles[tb] = empty ? 0u : p.tpos[T];
+    *p.nt = tb;
+  }
+}
+
 // ---------------------------------------------------------------- segment list
 // WRITE = false: counts[wi] = segment heads in window wi.  WRITE = true: one
 // descriptor {start, key, table, end} per head at sbase[wi] + rank (sbase =
@@ -196,8 +314,9 @@ __global__ void __launch_bounds__(256) bwd_seg_scan_kernel(BwdArgs a, WorkMap m,
 template <int G, int VPL, int UNR, int MINB>
 __global__ void __launch_bounds__(kBwdThreads, MINB)
 bwd_seg_kernel(BwdArgs a, const uint4* __restrict__ segs, const uint32_t* __restrict__ sbase,
-               uint32_t w_lo, uint32_t w_hi, uint4* __restrict__ longs, uint32_t* __restrict__ long_np,
-               uint32_t* __restrict__ long_ng, unsigned* __restrict__ n_long) {
+               const uint32_t* __restrict__ cw, uint32_t ci, uint4* __restrict__ longs,
+               uint32_t* __restrict__ long_np, uint32_t* __restrict__ long_ng, unsigned* __restrict__ n_long) {
+  const uint32_t w_lo = cw[ci], w_hi = cw[ci + 1];  // the class's windows (bwd_plan_kernel)
   constexpr int BPW = 32 / G;
   const int lane = threadIdx.x & 31;
   const int grp = lane / G, lg = lane % G;

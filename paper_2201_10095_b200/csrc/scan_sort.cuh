@@ -208,6 +208,8 @@ struct TileMap {
   const uint32_t* pos = nullptr;
   const uint32_t* cidx = nullptr;
   const uint32_t* cstride = nullptr;
+  const uint32_t* ntd = nullptr;  // device tile count (the grid is a capacity)
+  __device__ __forceinline__ bool idle(unsigned b) const { return ntd && b >= *ntd; }
   __device__ __forceinline__ size_t begin(unsigned b) const { return pos ? pos[b] : size_t(b) * kSortTile; }
   __device__ __forceinline__ size_t end(unsigned b, size_t n) const {
     return pos ? pos[b + 1] : min(n, size_t(b + 1) * kSortTile);
@@ -222,6 +224,7 @@ static __global__ void __launch_bounds__(kSortThreads)
 radix_upsweep(const uint32_t* __restrict__ keys, size_t n, int shift, int nbits,
               uint32_t* __restrict__ counts, unsigned ntiles, TileMap tm) {
   __shared__ uint32_t wc[kSortWarps][kRadix];
+  if (tm.idle(blockIdx.x)) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int i = lane; i < kRadix; i += 32) wc[w][i] = 0;
   __syncwarp();
@@ -255,6 +258,7 @@ radix_downsweep(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict
                 unsigned ntiles, uint32_t* __restrict__ keys_out,
                 uint32_t* __restrict__ vals_out, TileMap tm) {
   __shared__ uint32_t wc[kSortWarps][kRadix];
+  if (tm.idle(blockIdx.x)) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int i = lane; i < kRadix; i += 32) wc[w][i] = 0;
   __syncwarp();
@@ -333,8 +337,14 @@ inline size_t radix_sort_scratch_bytes(size_t n, size_t extra_tiles = 0) {
 // ends in (keys, vals) — ping-pong buffers come from scratch.  n < 2^32.
 // (A one-kernel-per-pass decoupled look-back variant measured slower on B200
 // RM1: 3.00 vs 2.93 ms backward.)
+// With tm.ntd the tile count lives on the device (seg_tiles is the grid
+// capacity, n an upper bound).  With keys_res/vals_res the result stays where
+// the last pass wrote it (no copy back; it may be in scr) and they receive it.
 inline void radix_sort_pairs(uint32_t* keys, uint32_t* vals, size_t n, int end_bit,
-                             Scratch& scr, cudaStream_t st, TileMap tm = TileMap{}, unsigned seg_tiles = 0) {
+                             Scratch& scr, cudaStream_t st, TileMap tm = TileMap{}, unsigned seg_tiles = 0,
+                             uint32_t** keys_res = nullptr, uint32_t** vals_res = nullptr) {
+  if (keys_res) *keys_res = keys;
+  if (vals_res) *vals_res = vals;
   if (n <= 1 || end_bit <= 0) return;
   if (n >= (size_t(1) << 32)) throw Error(-1, "radix_sort_pairs: n >= 2^32");
   const unsigned ntiles = tm.pos ? seg_tiles : unsigned((n + kSortTile - 1) / kSortTile);
@@ -361,6 +371,11 @@ inline void radix_sort_pairs(uint32_t* keys, uint32_t* vals, size_t n, int end_b
     RS_LAUNCH_CHECK();
     std::swap(ki, ko);
     std::swap(vi, vo);
+  }
+  if (keys_res) {
+    *keys_res = ki;
+    if (vals_res) *vals_res = vi;
+    return;  // the result may live in scr: keep it reserved
   }
   if (ki != keys) {
     RS_CUDA(cudaMemcpyAsync(keys, ki, n * 4, cudaMemcpyDeviceToDevice, st));
