@@ -61,6 +61,8 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-prefetch", action="store_true",
                    help="headline in zero-copy mode only (no slow-row staging pipeline)")
+    p.add_argument("--prefetch-depth", type=int, default=2, choices=[1, 2],
+                   help="batches staged ahead (2: batch i+2's claim is queued behind forward i)")
     return p.parse_args()
 
 
@@ -292,17 +294,24 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
         slow_u = max(slow_u, u)
     nvtx = os.environ.get("BENCH_NVTX") == "1"
 
+    D = args.prefetch_depth
+
     def step(i, cache, ev=None):
         if nvtx:
             torch.cuda.nvtx.range_push("bench_step")
         off, idx, n = batches[i % len(batches)] if T else (None, None, 0)
-        if cache and i + 1 < cache:  # stage batch i+1's slow rows while batch i runs
+        if D == 1 and cache and i + 1 < cache:  # stage batch i+1's slow rows while batch i runs
             nb = batches[(i + 1) % len(batches)]
             op.prefetch(nb[0], nb[1], B)
         if ev:
             ev[0].record()
         if T:
             op.forward(off, idx, B, out=pooled, hits=hits)
+        if D == 2 and cache and i + 2 < cache:
+            # batch i+2: its claim queues behind this forward, so its host
+            # gather has this backward and the whole next step to finish
+            nb = batches[(i + 2) % len(batches)]
+            op.prefetch(nb[0], nb[1], B)
         if ev:
             ev[1].record()
         g = pooled
@@ -332,7 +341,8 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
         clocks, L0 = None, 0
         ta0.record()
         if cache and T:
-            op.prefetch(batches[0][0], batches[0][1], B)
+            for k in range(min(D, nsteps)):
+                op.prefetch(batches[k % len(batches)][0], batches[k % len(batches)][1], B)
         for i in range(nsteps):
             if i == warmup:
                 torch.cuda.synchronize()
@@ -412,7 +422,7 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
             and rep.total_accesses == int(hh.sum()))
     if do_e2e and T:
         res["e2e"] = run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex,
-                             res["mode"] == "pipelined")
+                             res["mode"] == "pipelined", args.prefetch_depth)
     if op:
         op.close()
     del remaps, batches
@@ -498,7 +508,7 @@ def modes(r):
             for m, k in (("zero-copy", "zero_copy"), ("pipelined", "pipelined"))}
 
 
-def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex, cache):
+def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex, cache, depth=2):
     """Same step through the public API with host inputs: every step's offsets +
     indices are copied from pinned host memory (a copy stream, two batches
     ahead, triple-buffered — the data loader's overlap) and the hit counters
@@ -507,7 +517,8 @@ def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex, cache):
     same steady-state window (after 3 warm-up steps of the continuous run)."""
     dev = pooled.device
     host = [(off.cpu().pin_memory(), idx[:max(1, n)].cpu().pin_memory(), n) for off, idx, n in batches]
-    nb = 3
+    nb = depth + 2  # in use: step i, the staged batches up to i + depth, the copy in flight
+    ahead = depth + 1
     bufs = [(torch.empty_like(batches[0][0]),
              torch.empty(max(b[1].numel() for b in batches), dtype=torch.int32, device=dev))
             for _ in range(nb)]
@@ -541,22 +552,26 @@ def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex, cache):
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     def run():
-        h2d(0, total)
-        h2d(1, total)
+        for k in range(ahead):
+            h2d(k, total)
         if cache:
-            main.wait_event(ev_in[0])
-            op.prefetch(*view(0), B)
+            for k in range(min(depth, total)):
+                main.wait_event(ev_in[k % nb])
+                op.prefetch(*view(k), B)
         for i in range(total):
             if i == warm:  # steady state from here (same window as the device-resident run)
                 torch.cuda.synchronize()
                 s.record()
-            h2d(i + 2, total)
-            if cache and i + 1 < total:
+            h2d(i + ahead, total)
+            if cache and depth == 1 and i + 1 < total:
                 main.wait_event(ev_in[(i + 1) % nb])
                 op.prefetch(*view(i + 1), B)
             main.wait_event(ev_in[i % nb])
             d_off, d_idx = view(i)
             op.forward(d_off, d_idx, B, out=pooled, hits=hits)
+            if cache and depth == 2 and i + 2 < total:
+                main.wait_event(ev_in[(i + 2) % nb])  # copied a step ago
+                op.prefetch(*view(i + 2), B)
             g = pooled
             if ex is not None:
                 g = ex.to_tables(ex.to_owners(pooled))

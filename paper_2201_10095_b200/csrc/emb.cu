@@ -27,6 +27,8 @@
 #include <numeric>
 #include <tuple>
 
+#include <sys/mman.h>
+
 #include "../../include/shardplan_gpu.h"
 #include "context.cuh"
 #include "host_worker.hpp"
@@ -377,6 +379,9 @@ struct rs_emb {
   size_t fast_bytes = 0;
   char* host_pool = nullptr;
   char* host_pool_dev = nullptr;
+  bool host_mapped = false;  // mmap + THP + cudaHostRegister (else cudaHostAlloc)
+  void* host_map_base = nullptr;
+  size_t host_map_bytes = 0;
   size_t host_bytes = 0;
   int32_t* remap_pool = nullptr;
   size_t remap_bytes = 0;
@@ -522,7 +527,14 @@ struct rs_emb {
       if (ev) cudaEventDestroy(ev);
     if (d_tables) cudaFree(d_tables);
     if (fast_pool) cudaFree(fast_pool);
-    if (host_pool) cudaFreeHost(host_pool);
+    if (host_pool) {
+      if (host_mapped) {
+        cudaHostUnregister(host_pool);
+        munmap(host_map_base, host_map_bytes);
+      } else {
+        cudaFreeHost(host_pool);
+      }
+    }
     if (remap_pool) cudaFree(remap_pool);
     for (auto& c : classes)
       if (c.d_list) cudaFree(c.d_list);
@@ -555,6 +567,35 @@ struct rs_emb {
 namespace rs {
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// The pinned host tier.  Random row gathers/scatters over tens of GB miss the
+// TLB on every row with 4 KiB pages, so the tier is an anonymous mapping
+// advised for transparent huge pages (2 MiB) and then pinned and mapped with
+// cudaHostRegister; cudaHostAlloc is the fallback (RS_HOST_THP=0 forces it).
+static void alloc_host_tier(rs_emb* e) {
+  const char* env = getenv("RS_HOST_THP");
+  const bool thp = !(env && env[0] == '0');
+  constexpr size_t kHuge = size_t(2) << 20;
+  if (thp) {
+    const size_t bytes = (e->host_bytes + kHuge - 1) / kHuge * kHuge;
+    const size_t map = bytes + kHuge;
+    void* base = mmap(nullptr, map, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+    if (base != MAP_FAILED) {
+      char* p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(base) + kHuge - 1) & ~uintptr_t(kHuge - 1));
+      madvise(p, bytes, MADV_HUGEPAGE);
+      if (cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable) == cudaSuccess) {
+        e->host_pool = p;
+        e->host_mapped = true;
+        e->host_map_base = base;
+        e->host_map_bytes = map;
+        return;
+      }
+      cudaGetLastError();
+      munmap(base, map);
+    }
+  }
+  RS_CUDA(cudaHostAlloc(&e->host_pool, e->host_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+}
 
 rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64_t max_batch,
                    uint64_t max_lookups, int opt, float eps) {
@@ -606,7 +647,7 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
     e->host_bytes = std::max<size_t>(hb, 256);
     e->remap_bytes = rb;
     RS_CUDA(cudaMalloc(&e->fast_pool, e->fast_bytes));
-    RS_CUDA(cudaHostAlloc(&e->host_pool, e->host_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    alloc_host_tier(e);
     RS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->host_pool_dev), e->host_pool, 0));
     RS_CUDA(cudaMalloc(&e->remap_pool, std::max<size_t>(rb, 256)));
     RS_CUDA(cudaMalloc(&e->d_err, 16));
