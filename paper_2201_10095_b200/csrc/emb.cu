@@ -119,11 +119,11 @@ __device__ __forceinline__ void fwd_bag_offsets(const uint32_t* __restrict__ cls
 }
 __device__ __forceinline__ uint32_t fwd_bag_index(const uint32_t* __restrict__ indices, int lg, uint32_t s,
                                                   uint32_t e) {
-  return uint32_t(lg) < e - s ? ld_stream_u32(indices + s + lg) : 0u;
+  return s < e && uint32_t(lg) < e - s ? ld_stream_u32(indices + s + lg) : 0u;
 }
 __device__ __forceinline__ int32_t fwd_bag_entry(const TableDev* __restrict__ tables, unsigned* err, int lg,
                                                  uint32_t t, uint32_t s, uint32_t e, uint32_t idx) {
-  if (uint32_t(lg) >= e - s) return 0;
+  if (s >= e || uint32_t(lg) >= e - s) return 0;
   const TableDev& tn = tables[t];
   if (idx >= tn.hash_size) {  // reported by the next backward / rs_emb_check
     atomicOr(err, 1u);
@@ -182,7 +182,10 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
     float4 acc[VPL];
 #pragma unroll
     for (int vv = 0; vv < VPL; ++vv) acc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (lg == 0) tot += e - s;
+    if (lg == 0) {
+      if (e > s) tot += e - s;
+      else if (e < s) atomicOr(err, 16u);  // decreasing offsets: the next backward raises
+    }
     for (uint32_t base = s; base < e; base += G) {
       const uint32_t n = min(uint32_t(G), e - base);
       int32_t ent = 0;
@@ -266,6 +269,7 @@ __global__ void __launch_bounds__(256)
 keygen_kernel(const TableDev* __restrict__ tables, uint32_t T, uint64_t B,
               const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ indices,
               uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, unsigned* __restrict__ err) {
+  if (*reinterpret_cast<volatile unsigned*>(err)) return;  // offsets rejected by bwd_plan_kernel
   const int lane = threadIdx.x & 31;
   const uint64_t nbags = uint64_t(T) * B;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
@@ -275,7 +279,9 @@ keygen_kernel(const TableDev* __restrict__ tables, uint32_t T, uint64_t B,
     uint64_t H = 0;
     if (g < nbags) {
       s = offsets[g];
-      len = offsets[g + 1] - s;
+      const uint32_t e = offsets[g + 1];
+      if (e < s) atomicOr(err, 16u);  // a decreasing bag: the gate empties the plan
+      len = e > s ? e - s : 0u;
       t = uint32_t(g / B);
       H = tables[t].hash_size;
     }
@@ -1189,12 +1195,6 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
   // host then waits only for the plan's error word and raises afterwards
   // (an empty plan makes every later kernel a no-op).
   e->t_bwd.begin(st);
-  if (!have_keys) {
-    const uint64_t nb = uint64_t(e->T) * B;
-    unsigned g = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((nb / 32 + 7) / 8, uint64_t(sm_count()) * 16)));
-    emb::keygen_kernel<<<g, 256, 0, st>>>(e->d_tables, e->T, B, off, idx, e->keys, e->vals, e->d_err);
-    RS_COUNT(1);
-  }
   uint32_t* d_tpos = e->d_meta;
   uint32_t* d_wstart = e->d_meta + T + 1;
   uint32_t* d_wtab = e->d_meta + 2 * (T + 1);
@@ -1204,6 +1204,13 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
                     d_tpos, d_wstart, d_wtab, e->d_cw, e->d_tiles, tcap, e->d_nt, e->d_err};
     emb::bwd_plan_kernel<<<1, 1024, 0, st>>>(pl);
     RS_COUNT(1);
+    if (!have_keys) {  // a batch the last forward did not see: keys from the (validated) offsets
+      const uint64_t nb = uint64_t(e->T) * B;
+      unsigned g = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((nb / 32 + 7) / 8, uint64_t(sm_count()) * 16)));
+      emb::keygen_kernel<<<g, 256, 0, st>>>(e->d_tables, e->T, B, off, idx, e->keys, e->vals, e->d_err);
+      emb::bwd_plan_gate_kernel<<<1, 256, 0, st>>>(pl);  // an index error empties the plan too
+      RS_COUNT(2);
+    }
     RS_CUDA(cudaMemcpyAsync(herr, e->d_err, 4, cudaMemcpyDeviceToHost, st));
     RS_CUDA(cudaEventRecord(e->ev_err, st));
   }
@@ -1267,11 +1274,12 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
   RS_CUDA(cudaEventSynchronize(e->ev_err));
   if (const unsigned bad = *herr) {
     RS_CUDA(cudaMemsetAsync(e->d_err, 0, 4, st));
-    if (bad & 1u) throw InvalidArgument("emb: an index is outside its table's hash_size");
-    if (bad & 2u) throw InvalidArgument("emb: more lookups than max_lookups");
+    // the offsets first (an index read through bad offsets is meaningless)
     if (bad & 4u) throw InvalidArgument("emb_backward: offsets must start at 0");
     if (bad & 8u) throw InvalidArgument("emb_backward: more lookups than max_lookups");
-    throw InvalidArgument("emb_backward: offsets must be non-decreasing");
+    if (bad & 16u) throw InvalidArgument("emb_backward: offsets must be non-decreasing");
+    if (bad & 2u) throw InvalidArgument("emb: more lookups than max_lookups");
+    throw InvalidArgument("emb: an index is outside its table's hash_size");
   }
 }
 

@@ -253,6 +253,17 @@ __global__ void __launch_bounds__(1024) bwd_plan_kernel(BwdPlan p) {
   }
 }
 
+// After a stand-alone keygen: an index error it found empties the plan.
+__global__ void bwd_plan_gate_kernel(BwdPlan p) {
+  if (*reinterpret_cast<volatile unsigned*>(p.err) == 0) return;
+  for (uint32_t c = threadIdx.x; c <= p.ncls; c += blockDim.x) p.cw[c] = 0;
+  if (threadIdx.x == 0) {
+    p.wstart[p.T] = 0;
+    p.tiles[0] = 0;
+    *p.nt = 0;
+  }
+}
+
 // ---------------------------------------------------------------- segment list
 // WRITE = false: counts[wi] = segment heads in window wi.  WRITE = true: one
 // descriptor {start, key, table, end} per head at sbase[wi] + rank (sbase =

@@ -258,7 +258,14 @@ __global__ void __launch_bounds__(256) pass2_kernel(Lines L, TableMap tm, Pass2A
   const int lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < L.nlines; i += nwarps) {
-    if (a.kind[i] != kR) continue;
+    const uint8_t kind = a.kind[i];
+    if (kind != kR) {
+      // a failed line keeps its record slot: point the slot at the line, so an
+      // order check against its (unwritten) record blames this line, never a
+      // stale one
+      if (kind == kBad && lane == 0) a.recline[a.rscan[i]] = uint32_t(i);
+      continue;
+    }
     const uint64_t ln = L.lbase + i;
     uint32_t s, e;
     bounds(L, uint32_t(i), s, e);

@@ -248,6 +248,55 @@ def test_out_of_range_index_is_reported(cuda_ctx, coracle):
     op.close()
 
 
+def test_backward_rejects_bad_batches_without_touching_weights(cuda_ctx, coracle):
+    """The backward validates its batch on the device (bwd_plan_kernel) and
+    raises the documented InvalidArgument; an empty plan means no row moves.
+    A batch the last forward did not see goes through the stand-alone keygen,
+    whose index errors empty the plan too."""
+    import torch
+
+    rng = np.random.default_rng(21)
+    specs, remaps, offsets, idx, d_off, d_idx, _ = _setup(coracle, [16, 32], [100, 60], [0.5, 0.3], 16, 6, rng)
+    op = sp.TieredEmbeddingBag(specs, remaps, 16, max(1, idx.size), "rowwise_adagrad", ctx=cuda_ctx)
+    op.init_weights(SEED, SCALE)
+    rows = [np.arange(s.hash_size, dtype=np.uint32) for s in specs]
+
+    def snapshot():
+        torch.cuda.synchronize()
+        return [op.read_rows(t, r) for t, r in enumerate(rows)]
+
+    def same(a, b):
+        return all(np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1]) for x, y in zip(a, b))
+
+    y = op.forward(d_off, d_idx, 16)
+    before = snapshot()
+    bad_start = d_off.clone()
+    bad_start[0] = 1
+    bad_order = d_off.clone()
+    k = int(np.nonzero(np.diff(offsets) > 0)[0][0]) + 1  # an offset that can be lowered
+    bad_order[k] = int(offsets[k - 1]) - 1 if offsets[k - 1] > 0 else int(offsets[k + 1]) + 5
+    bad_bound = d_off.clone()
+    bad_bound[16] = int(offsets[32]) + 1  # table 1 starts after table 2
+    too_many = d_off.clone()
+    too_many[-1] = idx.size + 1
+    bad_idx = d_idx.clone()
+    bad_idx[0] = 100  # == hash_size of table 0
+    cases = [(bad_start, d_idx, "offsets must start at 0"),
+             (bad_order, d_idx, "non-decreasing"),
+             (bad_bound, d_idx, "non-decreasing"),
+             (too_many, d_idx, "more lookups than max_lookups"),
+             (d_off.clone(), bad_idx, "outside its table's hash_size")]
+    for o, i, msg in cases:
+        with pytest.raises(sp.InvalidArgument, match=msg):
+            op.backward(o, i, y, 16, 0.1)
+        assert same(snapshot(), before), msg
+    # the operator is clean afterwards
+    y = op.forward(d_off, d_idx, 16)
+    op.backward(d_off, d_idx, y, 16, 0.1)
+    assert not same(snapshot(), before)
+    op.close()
+
+
 @pytest.mark.parametrize("opt", ["sgd", "rowwise_adagrad"])
 def test_backward_tree_edges(cuda_ctx, coracle, opt):
     """Segment lengths on every edge of the reduction tree (oracle.h): 1, 31,
