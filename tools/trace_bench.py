@@ -60,7 +60,7 @@ def measure(a):
            "write_s": t_write, "write_ids_per_s": n / t_write,
            "read_s": t_read, "read_ids_per_s": n / t_read, "read_text_gbs": size / t_read / 1e9}
     os.remove(path)
-    if oracle.ref_available():
+    if oracle.ref_available() and a.ref_ids > 0:
         # prefix of the same trace for the single-threaded reference
         m = int(a.ref_ids // per * len(specs) * 0.9)
         m = max(1, min(R, m))
