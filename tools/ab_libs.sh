@@ -1,7 +1,10 @@
-# A/B of library builds: bash tools/ab_libs.sh [reps] — "old" = paper_2201_10095_b200/libshardplan_gpu_old.so
-reps=${1:-3}
+# A/B of library builds over repeated bench runs:
+#   bash tools/ab_libs.sh REPS NAME...   (NAME "cur" = the in-tree library,
+#   otherwise paper_2201_10095_b200/libshardplan_gpu_NAME.so)
+reps=${1:-3}; shift
+names=${@:-old cur}
 for rep in $(seq $reps); do
-for v in old cur; do
+for v in $names; do
   if [ $v = cur ]; then L=""; else L="RS_LIB_PATH=$PWD/paper_2201_10095_b200/libshardplan_gpu_$v.so"; fi
   env $L timeout -s KILL 300 python bench.py --no-cpu --profile-ids 0 --trace-ids 0 --no-greedy > gpurun_out/ab_$v.log 2>&1
   tail -1 gpurun_out/ab_$v.log | python -c "
