@@ -61,6 +61,10 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-prefetch", action="store_true",
                    help="headline in zero-copy mode only (no slow-row staging pipeline)")
+    p.add_argument("--plan-gpus", type=int, default=0,
+                   help="plan for M GPUs but run one of their shards here (with --as-rank; "
+                        "one process, no all-to-all) — e.g. RM2 at 8 GPUs, rank 0's tables")
+    p.add_argument("--as-rank", type=int, default=0)
     p.add_argument("--prefetch-depth", type=int, default=2, choices=[1, 2],
                    help="batches staged ahead (2: batch i+2's claim is queued behind forward i)")
     return p.parse_args()
@@ -413,7 +417,12 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
         hits.zero_()
         op.forward(off, idx, B, out=pooled, hits=hits)
         tr = wl.kjt_to_trace(lspecs, off, idx, n, B, 0, ctx=ctx)
-        rep = sp.simulate(tr, sp.ShardingPlan("x", 1, [plan.entries[j] for j in local]), remaps,
+        import copy
+
+        ents = [copy.copy(plan.entries[j]) for j in local]
+        for e in ents:  # this GPU's shard as a one-GPU system
+            e.gpu = 0
+        rep = sp.simulate(tr, sp.ShardingPlan("x", 1, ents), remaps,
                           sp.SystemSpec(1, B, system.cap_hbm_bytes, system.cap_dram_bytes,
                                         system.bw_hbm, system.bw_uvm), B, ctx=ctx)
         hh = hits.cpu().numpy()
@@ -626,7 +635,12 @@ def main():
     B = args.batch
     hbm_peak, peak_kind = measured_peaks()
     bw_uvm = h2d_bandwidth(torch, dev)
-    system = wl.system_for(specs, world, B, hbm_peak * 1e9, bw_uvm, args.hbm_fraction)
+    emulate = args.plan_gpus > 1 and world == 1
+    M = args.plan_gpus if emulate else world
+    prank = args.as_rank if emulate else rank
+    if emulate and prank >= M:
+        raise SystemExit("--as-rank outside [0, --plan-gpus)")
+    system = wl.system_for(specs, M, B, hbm_peak * 1e9, bw_uvm, args.hbm_fraction)
     tables = [w.table for w in specs]
 
     # ---- HP1: profile the training data on the GPU (whole-sample rate 1.0)
@@ -676,12 +690,49 @@ def main():
         del strace, sidx, soff
         torch.cuda.empty_cache()
 
+    if emulate and prank < 0:
+        # every shard of the M-GPU plans, one after the other on this GPU: the
+        # plan's step time is its slowest shard's (the all-to-all is not run)
+        shards = []
+        for q in range(M):
+            rq = run_plan(args, torch, dist, q, world, dev, ctx, specs, stats, prof, rec, system,
+                          args.steps, args.warmup, False, B)
+            gq = run_plan(args, torch, dist, q, world, dev, ctx, specs, stats, prof, gre, system,
+                          args.greedy_steps, 1, False, B)
+            shards.append({"rank": q,
+                           "tables": sum(1 for e in rec.entries if e.gpu == q),
+                           "greedy_tables": sum(1 for e in gre.entries if e.gpu == q),
+                           "recshard": {k: rq[k] for k in ("samples_per_s", "ms_per_step", "uvm_pct", "fast",
+                                                           "slow", "mode")},
+                           "greedy": {k: gq[k] for k in ("samples_per_s", "ms_per_step", "uvm_pct", "fast",
+                                                         "slow", "mode")}})
+            torch.cuda.empty_cache()
+        prof.close()
+
+        def system_of(key):
+            ms = max(x[key]["ms_per_step"] for x in shards)
+            slow = sum(x[key]["slow"] for x in shards)
+            tot = slow + sum(x[key]["fast"] for x in shards)
+            return {"samples_per_s": B / (ms / 1e3), "ms_per_step_slowest_shard": ms,
+                    "uvm_access_pct": 100.0 * slow / max(1, tot)}
+
+        rs_, gs_ = system_of("recshard"), system_of("greedy")
+        print(json.dumps({
+            "metric": "EMB fwd+bwd samples/s of an M-GPU plan, every shard run on this GPU in turn "
+                      "(slowest shard sets the step; no all-to-all)",
+            "config": {"workload": f"{args.config}-like", "tables": len(specs), "global_batch": B,
+                       "plan_gpus": M, "fast_tier_cap": f"{args.hbm_fraction:.0%} of table bytes",
+                       "optimizer": args.optimizer},
+            "recshard": rs_, "greedy": gs_, "recshard_vs_greedy": rs_["samples_per_s"] / gs_["samples_per_s"],
+            "simulated_uvm_pct": sim_uvm, "planner_s": plan_s, "shards": shards}), flush=True)
+        return
+
     first = gre if args.only == "greedy" else rec
-    r = run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, first, system,
+    r = run_plan(args, torch, dist, prank, world, dev, ctx, specs, stats, prof, first, system,
                  args.steps, args.warmup, True, B)
     g = None
     if not args.no_greedy and args.only is None:
-        g = run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, gre, system,
+        g = run_plan(args, torch, dist, prank, world, dev, ctx, specs, stats, prof, gre, system,
                      args.greedy_steps, 1, False, B)
     prof.close()
 
@@ -726,7 +777,9 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (GPU Zipf generator, random-init weights)",
             "config": {"workload": f"{args.config}-like", "tables": len(specs), "global_batch": B,
-                       "optimizer": args.optimizer, "parallelism": f"table-wise mp{world}",
+                       "optimizer": args.optimizer,
+                       "parallelism": (f"one shard (rank {prank}) of a table-wise mp{M} plan, "
+                                       "no all-to-all" if emulate else f"table-wise mp{world}"),
                        "fast_tier_cap": "40% of table bytes", "l2": "256 MiB flush between steps"
                        if not args.no_flush else f"{args.nbatches} distinct batches cycled"},
             "uvm_access_pct": r["uvm_pct"],

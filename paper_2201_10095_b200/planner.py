@@ -291,9 +291,21 @@ def recshard_plan(specs, stats, system, step_count=100, iters=200):
     load = [0.0] * M
     bytes_on = [0] * M
     assign = [0] * len(specs)
+    # a GPU can only take a table if its slow tier can hold what its fast tier
+    # cannot: the fast tier holds profiled rows only (the curves end at the
+    # distinct rows seen), so never-seen rows always count against DRAM
+    acc_on = [0] * M
+    acc = [int(c.bytes[-1]) for c in curves]
+
+    def fits(m, j):
+        b = bytes_on[m] + specs[j].bytes()
+        return b - min(system.cap_hbm_bytes, acc_on[m] + acc[j]) <= system.cap_dram_bytes
+
     for j in order:
-        g = min(range(M), key=lambda m: (load[m], bytes_on[m], m))
+        ok = [m for m in range(M) if fits(m, j)]
+        g = min(ok or range(M), key=lambda m: (load[m], bytes_on[m], m))
         assign[j] = g
+        acc_on[g] += acc[j]
         load[g] += curves[j].cost[-1]
         bytes_on[g] += specs[j].bytes()
 
