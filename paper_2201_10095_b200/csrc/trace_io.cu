@@ -1007,17 +1007,21 @@ __global__ void __launch_bounds__(256) fmt_write_kernel(RecArrays a, uint64_t r0
 }
 
 // The reference's LineWriter (core/src/line_io.cpp:31-86): plain or gzip.
+// Plain files are written with positioned writes, large spans split over a
+// few threads (page-cache copies are memory-bound, one thread reaches a
+// fraction of the host's bandwidth).
 struct Sink {
   std::string path;
-  FILE* plain = nullptr;
+  int fd = -1;
+  uint64_t off = 0;
   gzFile gz = nullptr;
   explicit Sink(const std::string& p) : path(p) {
     if (p.size() > 3 && p.compare(p.size() - 3, 3, ".gz") == 0) {
       gz = gzopen(p.c_str(), "wb");
       if (!gz) throw IoError("cannot open for writing: " + p);
     } else {
-      plain = std::fopen(p.c_str(), "wb");
-      if (!plain) throw IoError("cannot open for writing: " + p);
+      fd = ::open(p.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
+      if (fd < 0) throw IoError("cannot open for writing: " + p);
     }
   }
   void write(const char* b, size_t n) {
@@ -1028,9 +1032,31 @@ struct Sink {
         b += k;
         n -= k;
       }
-    } else if (n && std::fwrite(b, 1, n, plain) != n) {
-      throw IoError("write failed: " + path);
+      return;
     }
+    if (!n) return;
+    constexpr size_t kPiece = size_t(16) << 20;
+    const int nth = int(std::min<size_t>(8, std::max<size_t>(1, n / kPiece)));
+    std::vector<int> bad(size_t(nth), 0);
+    auto work = [&](int k) {
+      const size_t a = n * size_t(k) / size_t(nth), e = n * size_t(k + 1) / size_t(nth);
+      size_t done = 0;
+      while (a + done < e) {
+        const ssize_t r = ::pwrite(fd, b + a + done, e - a - done, off_t(off + a + done));
+        if (r <= 0) {
+          bad[size_t(k)] = 1;
+          return;
+        }
+        done += size_t(r);
+      }
+    };
+    std::vector<std::thread> th;
+    for (int k = 1; k < nth; ++k) th.emplace_back(work, k);
+    work(0);
+    for (auto& t : th) t.join();
+    for (int x : bad)
+      if (x) throw IoError("write failed: " + path);
+    off += n;
   }
   void close() {
     if (gz) {
@@ -1038,15 +1064,15 @@ struct Sink {
       gz = nullptr;
       if (rc != Z_OK) throw IoError("gzip close failed: " + path);
     }
-    if (plain) {
-      FILE* f = plain;
-      plain = nullptr;
-      if (std::fclose(f) != 0) throw IoError("close failed: " + path);
+    if (fd >= 0) {
+      const int f = fd;
+      fd = -1;
+      if (::close(f) != 0) throw IoError("close failed: " + path);
     }
   }
   ~Sink() {
     if (gz) gzclose(gz);
-    if (plain) std::fclose(plain);
+    if (fd >= 0) ::close(fd);
   }
 };
 
@@ -1089,7 +1115,7 @@ void trace_write(rs_context* ctx, const rs_trace* tr, const char* path, const ch
                 static_cast<const uint64_t*>(to_dev(tr->rec_offset, R * 8)),
                 static_cast<const uint32_t*>(to_dev(tr->rec_len, R * 4)),
                 static_cast<const uint32_t*>(to_dev(tr->ids, tr->num_ids * 4)), tr->num_ids};
-    if (batch_records == 0) batch_records = uint64_t(4) << 20;
+    if (batch_records == 0) batch_records = uint64_t(1) << 20;
     const uint64_t nb = std::min<uint64_t>(batch_records, R);
     uint64_t* lens = nullptr;
     uint64_t* pos = nullptr;
@@ -1103,20 +1129,26 @@ void trace_write(rs_context* ctx, const rs_trace* tr, const char* path, const ch
     RS_CUDA(cudaMemsetAsync(err, 0, 4, st));
     char* text = nullptr;
     uint64_t text_cap = 0;
-    size_t hcap = 0;
-    char* hb = nullptr;
+    // two pinned text buffers: batch k+1 is formatted and copied out while
+    // batch k is written
+    size_t hcap[2] = {0, 0};
+    char* hb[2] = {nullptr, nullptr};
+    std::future<void> writing;
     struct Bufs {
       rs_context* c;
       char*& t;
-      char*& h;
-      size_t& hc;
+      char** h;
+      size_t* hc;
+      std::future<void>& w;
       ~Bufs() {
+        if (w.valid()) w.wait();
         if (t) cudaFree(t);
-        c->host_pool->give(h, hc);
+        for (int k = 0; k < 2; ++k) c->host_pool->give(h[k], hc[k]);
       }
-    } bufs{ctx, text, hb, hcap};
+    } bufs{ctx, text, hb, hcap, writing};
     uint64_t* h_small = ctx->pinned_buf<uint64_t>(2);
-    for (uint64_t r0 = 0; r0 < R; r0 += nb) {
+    int cur = 0;
+    for (uint64_t r0 = 0; r0 < R; r0 += nb, cur ^= 1) {
       const uint64_t n = std::min<uint64_t>(nb, R - r0);
       const unsigned g = grid_for(n * 32, 256);
       fmt_len_kernel<<<g, 256, 0, st>>>(a, r0, n, lens, err);
@@ -1134,19 +1166,22 @@ void trace_write(rs_context* ctx, const rs_trace* tr, const char* path, const ch
         text_cap = bytes + bytes / 4;
         RS_CUDA(cudaMalloc(&text, text_cap));
       }
-      if (bytes > hcap) {
-        ctx->host_pool->give(hb, hcap);
-        hb = nullptr;
-        hcap = 0;
-        hb = static_cast<char*>(ctx->host_pool->take(bytes + bytes / 4, &hcap));
+      if (bytes > hcap[cur]) {
+        ctx->host_pool->give(hb[cur], hcap[cur]);
+        hb[cur] = nullptr;
+        hcap[cur] = 0;
+        hb[cur] = static_cast<char*>(ctx->host_pool->take(bytes + bytes / 4, &hcap[cur]));
       }
       fmt_write_kernel<<<g, 256, 0, st>>>(a, r0, n, pos, text);
       RS_COUNT(2);
       RS_LAUNCH_CHECK();
-      RS_CUDA(cudaMemcpyAsync(hb, text, bytes, cudaMemcpyDeviceToHost, st));
+      RS_CUDA(cudaMemcpyAsync(hb[cur], text, bytes, cudaMemcpyDeviceToHost, st));
       ctx->sync();
-      out.write(hb, bytes);
+      if (writing.valid()) writing.get();  // the previous batch is on disk (errors surface here)
+      char* buf = hb[cur];
+      writing = std::async(std::launch::async, [&out, buf, bytes] { out.write(buf, bytes); });
     }
+    if (writing.valid()) writing.get();
   }
   out.close();
 }
