@@ -786,15 +786,17 @@ void emb_enable_cache(rs_emb* e, uint32_t nslots) {
   RS_CUDA(cudaMalloc(&e->slot_tab, uint64_t(nslots) * 4));
   RS_CUDA(cudaMalloc(&e->slot_row, uint64_t(nslots) * 4));
   RS_CUDA(cudaMalloc(&e->free_stack, uint64_t(nslots) * 4));
-  RS_CUDA(cudaMalloc(&e->copy_list, bc * 4));
-  RS_CUDA(cudaMalloc(&e->copy_tab, bc * 4));
-  RS_CUDA(cudaMalloc(&e->copy_row, bc * 4));
+  // copy lists double-buffered by generation parity: with two batches staged
+  // ahead, the claim for g+2 runs while g+1's lists may still be read
+  RS_CUDA(cudaMalloc(&e->copy_list, 2 * bc * 4));
+  RS_CUDA(cudaMalloc(&e->copy_tab, 2 * bc * 4));
+  RS_CUDA(cudaMalloc(&e->copy_row, 2 * bc * 4));
   RS_CUDA(cudaMalloc(&e->wb_tab, bc * 4));
   RS_CUDA(cudaMalloc(&e->wb_row, bc * 4));
   RS_CUDA(cudaMalloc(&e->d_bin, bc * stride * 4));
   RS_CUDA(cudaMalloc(&e->d_bout, bc * stride * 4));
   RS_CUDA(cudaMalloc(&e->free_top, 4));
-  RS_CUDA(cudaMalloc(&e->ncopy, 4));
+  RS_CUDA(cudaMalloc(&e->ncopy, 2 * 4));
   RS_CUDA(cudaMalloc(&e->n_wb, 4));
   RS_CUDA(cudaMalloc(&e->cache_err, 4));
   RS_CUDA(cudaHostAlloc(&e->h_bin, bc * stride * 4, cudaHostAllocDefault));
@@ -884,13 +886,15 @@ static void stage_in_task(rs_emb* e, uint64_t g, uint64_t out_before) {
   RS_CUDA(cudaStreamSynchronize(s));  // the previous DMA out of h_bin is done
   RS_CUDA(cudaEventSynchronize(e->ev_claim[g & 3]));
   const double t1 = dbg ? now_us() : 0;
-  RS_CUDA(cudaMemcpyAsync(e->h_cnt, e->ncopy, 4, cudaMemcpyDeviceToHost, s));
+  const uint64_t cs = (g & 1) * e->bcap;  // this generation's copy-list set
+  unsigned* ncopy = e->ncopy + (g & 1);
+  RS_CUDA(cudaMemcpyAsync(e->h_cnt, ncopy, 4, cudaMemcpyDeviceToHost, s));
   RS_CUDA(cudaStreamSynchronize(s));
   const uint64_t n = std::min<uint64_t>(e->h_cnt[0], e->bcap);
   const uint64_t stride = e->dmax;
   if (n) {
-    RS_CUDA(cudaMemcpyAsync(e->h_ctab, e->copy_tab, n * 4, cudaMemcpyDeviceToHost, s));
-    RS_CUDA(cudaMemcpyAsync(e->h_crow, e->copy_row, n * 4, cudaMemcpyDeviceToHost, s));
+    RS_CUDA(cudaMemcpyAsync(e->h_ctab, e->copy_tab + cs, n * 4, cudaMemcpyDeviceToHost, s));
+    RS_CUDA(cudaMemcpyAsync(e->h_crow, e->copy_row + cs, n * 4, cudaMemcpyDeviceToHost, s));
     RS_CUDA(cudaStreamSynchronize(s));
     const double t2 = dbg ? now_us() : 0;
     // gather chunk c on the CPU while chunk c-1 is on the bus
@@ -911,7 +915,7 @@ static void stage_in_task(rs_emb* e, uint64_t g, uint64_t out_before) {
       fprintf(stderr, "stage_in g=%llu n=%llu t=%.0f wait=%.0fus lists=%.0fus gather+enqueue=%.0fus (%u threads)\n",
               (unsigned long long)g, (unsigned long long)n, t0, t1 - t0, t2 - t1, t3 - t2, e->pool->size());
     const unsigned grid = unsigned(std::min<uint64_t>((n + 7) / 8, uint64_t(sm_count()) * 4));
-    emb::uvm_scatter_in_kernel<<<grid, 256, 0, s>>>(e->d_tables_c, e->copy_list, e->copy_tab, e->ncopy, e->bcap,
+    emb::uvm_scatter_in_kernel<<<grid, 256, 0, s>>>(e->d_tables_c, e->copy_list + cs, e->copy_tab + cs, ncopy, e->bcap,
                                                    e->d_bin, e->staging, stride);
     RS_COUNT(1);
     RS_LAUNCH_CHECK();
@@ -1001,14 +1005,15 @@ void emb_prefetch(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
   RS_CUDA(cudaEventRecord(e->ev_main, e->ctx->stream));
   cudaStream_t st = e->claim_stream;
   RS_CUDA(cudaStreamWaitEvent(st, e->ev_main, 0));
-  RS_CUDA(cudaMemsetAsync(e->ncopy, 0, 4, st));
+  const uint64_t cs = (g & 1) * e->bcap;
+  RS_CUDA(cudaMemsetAsync(e->ncopy + (g & 1), 0, 4, st));
   if (e->nslow_tabs) {
     const uint64_t work = uint64_t(e->nslow_tabs) * ((B + 31) / 32);
     emb::uvm_claim_kernel<<<unsigned(std::max<uint64_t>(1, std::min<uint64_t>((work + 7) / 8, uint64_t(sm_count()) * 8))),
                             256, 0, st>>>(
         e->d_tables_c, e->d_slow_tabs, e->nslow_tabs, B, off, idx, 1u << (g & 3), e->slot_gen,
-        e->slot_tab, e->slot_row, e->free_stack, e->free_top, e->copy_list, e->copy_tab, e->copy_row, e->bcap,
-        e->ncopy, e->cache_err);
+        e->slot_tab, e->slot_row, e->free_stack, e->free_top, e->copy_list + cs, e->copy_tab + cs,
+        e->copy_row + cs, e->bcap, e->ncopy + (g & 1), e->cache_err);
     RS_COUNT(1);
     RS_LAUNCH_CHECK();
   }

@@ -139,9 +139,9 @@ def test_backward_deterministic(cuda_ctx, coracle):
         assert np.array_equal(ma.view(np.uint32), mb.view(np.uint32))
 
 
-def _train(cuda_ctx, coracle, cached, steps=5, nslots=4096):
-    """Fwd+bwd over distinct batches; with `cached`, batch k+1 is prefetched
-    (slow rows staged in HBM) while batch k runs."""
+def _train(cuda_ctx, coracle, cached, steps=5, nslots=4096, depth=1):
+    """Fwd+bwd over distinct batches; with `cached`, batch k+depth is
+    prefetched (slow rows staged in HBM) while batch k runs."""
     import torch
 
     dims, Hs, frac, B, ml = ([64, 128, 32], [300, 500, 2000], [0.3, 0.1, 0.5], 128, 12)
@@ -161,13 +161,14 @@ def _train(cuda_ctx, coracle, cached, steps=5, nslots=4096):
     op.init_weights(SEED, SCALE)
     if cached:
         op.enable_uvm_cache(nslots)
-        op.prefetch(batches[0][0], batches[0][1], B)
+        for k in range(min(depth, steps)):
+            op.prefetch(batches[k][0], batches[k][1], B)
     outs = []
     for k in range(steps):
         off, idx, _ = batches[k]
         y = op.forward(off, idx, B)
-        if cached and k + 1 < steps:
-            op.prefetch(batches[k + 1][0], batches[k + 1][1], B)
+        if cached and k + depth < steps:
+            op.prefetch(batches[k + depth][0], batches[k + depth][1], B)
         outs.append(y.clone())
         op.backward(off, idx, y * 0.5 + 0.01, B, 0.05)
     torch.cuda.synchronize()
@@ -188,6 +189,20 @@ def test_uvm_cache_bit_identical_to_zero_copy(cuda_ctx, coracle):
         for (wa, ma), (wb, mb) in zip(rows, ref_rows):
             assert np.array_equal(wa.view(np.uint32), wb.view(np.uint32))
             assert np.array_equal(ma.view(np.uint32), mb.view(np.uint32))
+
+
+@pytest.mark.parametrize("nslots", [4096, 2600])
+def test_uvm_cache_two_batches_ahead_bit_identical(cuda_ctx, coracle, nslots):
+    """Staging two batches ahead (the bench's pipeline: four generations live —
+    one awaiting eviction, the current one, two staged) gives exactly the
+    zero-copy results."""
+    ref_out, ref_rows = _train(cuda_ctx, coracle, cached=False, steps=7)
+    out, rows = _train(cuda_ctx, coracle, cached=True, steps=7, nslots=nslots, depth=2)
+    for a, b in zip(out, ref_out):
+        assert torch_equal(a, b)
+    for (wa, ma), (wb, mb) in zip(rows, ref_rows):
+        assert np.array_equal(wa.view(np.uint32), wb.view(np.uint32))
+        assert np.array_equal(ma.view(np.uint32), mb.view(np.uint32))
 
 
 def torch_equal(a, b):
