@@ -27,6 +27,7 @@
 #include <zlib.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <future>
 #include <cstdarg>
@@ -1009,31 +1010,32 @@ __global__ void __launch_bounds__(256) fmt_write_kernel(RecArrays a, uint64_t r0
 // The reference's LineWriter (core/src/line_io.cpp:31-86): plain or gzip.
 // Plain files are written with positioned writes, large spans split over a
 // few threads (page-cache copies are memory-bound, one thread reaches a
-// fraction of the host's bandwidth).
+// fraction of the host's bandwidth).  ".gz" files are one gzip member whose
+// deflate stream is compressed in 1 MiB blocks on all threads (each block
+// primed with the 32 KiB before it, joined with sync flushes; the CRC-32 by
+// crc32_combine) — what any zlib reader, the reference's gzread included,
+// reads back as one stream.  zlib's default level, as the reference's
+// gzopen(path, "wb"); the compressed bytes differ from a one-thread stream,
+// the text they hold does not.
 struct Sink {
   std::string path;
   int fd = -1;
   uint64_t off = 0;
-  gzFile gz = nullptr;
+  bool gz = false;
+  uint32_t crc = 0;
+  uint64_t isize = 0;
+  std::string tail;  // the last 32 KiB written (the next block's dictionary)
   explicit Sink(const std::string& p) : path(p) {
-    if (p.size() > 3 && p.compare(p.size() - 3, 3, ".gz") == 0) {
-      gz = gzopen(p.c_str(), "wb");
-      if (!gz) throw IoError("cannot open for writing: " + p);
-    } else {
-      fd = ::open(p.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
-      if (fd < 0) throw IoError("cannot open for writing: " + p);
+    gz = p.size() > 3 && p.compare(p.size() - 3, 3, ".gz") == 0;
+    fd = ::open(p.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
+    if (fd < 0) throw IoError("cannot open for writing: " + p);
+    if (gz) {
+      const unsigned char hdr[10] = {0x1f, 0x8b, 8, 0, 0, 0, 0, 0, 0, 3};  // deflate, no name/mtime, unix
+      raw(reinterpret_cast<const char*>(hdr), sizeof hdr);
+      crc = uint32_t(crc32(0L, Z_NULL, 0));
     }
   }
-  void write(const char* b, size_t n) {
-    if (gz) {
-      while (n) {
-        const unsigned k = unsigned(std::min<size_t>(n, size_t(1) << 30));
-        if (gzwrite(gz, b, k) != int(k)) throw IoError("gzip write failed: " + path);
-        b += k;
-        n -= k;
-      }
-      return;
-    }
+  void raw(const char* b, size_t n) {
     if (!n) return;
     constexpr size_t kPiece = size_t(16) << 20;
     const int nth = int(std::min<size_t>(8, std::max<size_t>(1, n / kPiece)));
@@ -1055,23 +1057,98 @@ struct Sink {
     work(0);
     for (auto& t : th) t.join();
     for (int x : bad)
-      if (x) throw IoError("write failed: " + path);
+      if (x) throw IoError(std::string(gz ? "gzip write failed: " : "write failed: ") + path);
     off += n;
   }
-  void close() {
-    if (gz) {
-      const int rc = gzclose(gz);
-      gz = nullptr;
-      if (rc != Z_OK) throw IoError("gzip close failed: " + path);
+  // One raw-deflate block: `dict` primes the window, Z_SYNC_FLUSH (or
+  // Z_FINISH for the stream's end) closes it on a byte boundary.
+  static std::string deflate_block(const char* b, size_t n, const char* dict, size_t nd, int flush) {
+    z_stream z{};
+    if (deflateInit2(&z, Z_DEFAULT_COMPRESSION, Z_DEFLATED, -15, 8, Z_DEFAULT_STRATEGY) != Z_OK)
+      throw IoError("gzip write failed: deflateInit2");
+    if (nd) deflateSetDictionary(&z, reinterpret_cast<const Bytef*>(dict), uInt(nd));
+    std::string out(deflateBound(&z, uLong(n)) + 64, '\0');
+    z.next_in = reinterpret_cast<Bytef*>(const_cast<char*>(b));
+    z.avail_in = uInt(n);
+    z.next_out = reinterpret_cast<Bytef*>(out.data());
+    z.avail_out = uInt(out.size());
+    const int rc = deflate(&z, flush);
+    const size_t used = out.size() - z.avail_out;
+    deflateEnd(&z);
+    if (rc == Z_STREAM_ERROR || z.avail_in != 0) throw IoError("gzip write failed: deflate");
+    out.resize(used);
+    return out;
+  }
+  void write(const char* b, size_t n) {
+    if (!gz) return raw(b, n);
+    if (!n) return;
+    constexpr size_t kBlock = size_t(1) << 20, kDict = size_t(32) << 10;
+    const size_t nb = (n + kBlock - 1) / kBlock;
+    std::vector<std::string> outs(nb);
+    std::vector<uint32_t> crcs(nb);
+    std::atomic<size_t> next{0};
+    std::atomic<int> failed{0};
+    auto work = [&] {
+      for (size_t i; (i = next.fetch_add(1)) < nb;) {
+        try {
+          const size_t a = i * kBlock, e = std::min(n, a + kBlock);
+          const char* dict = nullptr;
+          size_t nd = 0;
+          if (a >= kDict) {
+            dict = b + a - kDict;
+            nd = kDict;
+          } else if (a > 0 || !tail.empty()) {  // the window spans the previous call
+            std::string& d = outs[i];  // scratch: replaced by the block below
+            d = tail.substr(tail.size() - std::min(tail.size(), kDict - a)) + std::string(b, a);
+            std::string block = deflate_block(b + a, e - a, d.data(), d.size(), Z_SYNC_FLUSH);
+            crcs[i] = uint32_t(crc32(0L, reinterpret_cast<const Bytef*>(b + a), uInt(e - a)));
+            outs[i] = std::move(block);
+            continue;
+          }
+          outs[i] = deflate_block(b + a, e - a, dict, nd, Z_SYNC_FLUSH);
+          crcs[i] = uint32_t(crc32(0L, reinterpret_cast<const Bytef*>(b + a), uInt(e - a)));
+        } catch (...) {
+          failed = 1;
+        }
+      }
+    };
+    const unsigned nth = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), unsigned(nb)));
+    std::vector<std::thread> th;
+    for (unsigned k = 1; k < nth; ++k) th.emplace_back(work);
+    work();
+    for (auto& t : th) t.join();
+    if (failed) throw IoError("gzip write failed: " + path);
+    std::string all;
+    for (size_t i = 0; i < nb; ++i) {
+      const size_t len = std::min(n, (i + 1) * kBlock) - i * kBlock;
+      crc = uint32_t(crc32_combine(crc, crcs[i], z_off_t(len)));
+      all += outs[i];
     }
-    if (fd >= 0) {
-      const int f = fd;
-      fd = -1;
-      if (::close(f) != 0) throw IoError("close failed: " + path);
+    isize += n;
+    raw(all.data(), all.size());
+    if (n >= kDict) {
+      tail.assign(b + n - kDict, kDict);
+    } else {
+      tail += std::string(b, n);
+      if (tail.size() > kDict) tail.erase(0, tail.size() - kDict);
     }
   }
+  void close() {
+    if (fd < 0) return;
+    if (gz) {
+      // the stream's final (empty) block, then CRC-32 and ISIZE, little-endian
+      std::string fin = deflate_block("", 0, nullptr, 0, Z_FINISH);
+      unsigned char tr[8];
+      for (int k = 0; k < 4; ++k) tr[k] = (crc >> (8 * k)) & 0xFF;
+      for (int k = 0; k < 4; ++k) tr[4 + k] = (uint32_t(isize) >> (8 * k)) & 0xFF;
+      fin.append(reinterpret_cast<const char*>(tr), 8);
+      raw(fin.data(), fin.size());
+    }
+    const int f = fd;
+    fd = -1;
+    if (::close(f) != 0) throw IoError(std::string(gz ? "gzip close failed: " : "close failed: ") + path);
+  }
   ~Sink() {
-    if (gz) gzclose(gz);
     if (fd >= 0) ::close(fd);
   }
 };
