@@ -489,6 +489,40 @@ def run_profile_sweep(args, torch, ctx, hbm_peak):
     return out
 
 
+def run_profile_sweep_sharded(args, torch, dist, ctx, world, rank):
+    """HP1 on N GPUs: the same ~args.profile_ids-id cfg1 trace on
+    every rank, each rank profiling its tables' records (sharded.subtrace; no
+    id exchange), the FeatureStats all-gathered.  Timed as the max over ranks
+    of (sub-trace + profile + gather); weak in ids per table, strong in total."""
+    import paper_2201_10095_b200 as sp
+    from paper_2201_10095_b200 import workload as wl
+    from paper_2201_10095_b200.sharded import profile_sharded
+
+    specs = wl.cfg1_specs()
+    per_sample = sum(w.gen.mean_pooling for w in specs)
+    S = int(args.profile_ids // per_sample)
+    gen = wl.BatchGenerator(specs, S, WORKLOAD_SEED + 1)
+    off, idx, n = gen.batch(0)
+    tr = wl.kjt_to_trace(specs, off, idx, n, S, 0, ctx=ctx)
+    prof = lambda t, r, s: sp.profile(t, r, s, ctx=ctx)  # noqa: E731
+    profile_sharded(tr, 1.0, PROFILE_SEED, profile_fn=prof)  # warm-up
+    times = []
+    for _ in range(3):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        profile_sharded(tr, 1.0, PROFILE_SEED, profile_fn=prof)
+        torch.cuda.synchronize()
+        t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{ctx.device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        times.append(float(t[0]))
+    secs = float(np.median(times))
+    del tr, idx, off
+    torch.cuda.empty_cache()
+    return {"workload": "cfg1 tables, rate 1.0, tables split over ranks", "ids": int(n), "n_gpus": world,
+            "seconds": secs, "ids_per_s": n / secs}
+
+
 def probe_cache(torch, op, batches, pooled, B):
     """Diagnostics: each stage of the staged pipeline timed alone (synchronised)."""
     def wall(f):
@@ -737,8 +771,10 @@ def main():
     prof.close()
 
     sweep = None
-    if rank == 0 and world == 1 and args.profile_ids > 0:
+    if world == 1 and args.profile_ids > 0:
         sweep = run_profile_sweep(args, torch, ctx, hbm_peak)
+    elif world > 1 and args.profile_ids > 0:
+        sweep = run_profile_sweep_sharded(args, torch, dist, ctx, world, rank)
     trace_io = None
     if rank == 0 and world == 1 and args.trace_ids > 0:
         import importlib.util

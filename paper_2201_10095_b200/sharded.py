@@ -117,3 +117,80 @@ class ShardedEmbeddingBag:
         g = self.ex.to_tables(grad_owned)
         if self.op:
             self.op.backward(offsets, indices, g.contiguous(), self.B, lr)
+
+
+# ---------------------------------------------------------------- HP1 across GPUs
+def profile_split(tables, world: int):
+    """Tables -> ranks for a sharded profile: longest-processing-
+    time on hash sizes (the per-table counter footprint), ties by table order.
+    Returns one list of table positions per rank."""
+    load = [0] * world
+    out = [[] for _ in range(world)]
+    for j in sorted(range(len(tables)), key=lambda j: (-int(tables[j].hash_size), j)):
+        r = min(range(world), key=lambda m: (load[m], m))
+        out[r].append(j)
+        load[r] += int(tables[j].hash_size)
+    return [sorted(x) for x in out]
+
+
+def subtrace(trace, positions):
+    """The records (and their ids, re-packed contiguously) of the tables at
+    `positions`; num_samples unchanged.  Profile statistics of a table depend
+    only on its own records and the sample ids (selection is per sample,
+    core/src/profiler.cpp:68-76), so they are identical on the sub-trace."""
+    from .types import Trace
+
+    tabs = [trace.tables[j] for j in positions]
+    ids = trace.ids if trace.ids is not None else trace.raw_ids
+    if hasattr(trace.rec_table, "is_cuda"):
+        import torch
+
+        want = torch.tensor([int(t.table_id) for t in tabs], dtype=torch.int64, device=trace.rec_table.device)
+        keep = torch.isin(trace.rec_table.long() & 0xFFFFFFFF, want)
+        rl = trace.rec_len[keep]
+        lens = rl.long()
+        offs = torch.cumsum(lens, 0) - lens
+        n = int(lens.sum().item()) if lens.numel() else 0
+        src = trace.rec_offset[keep].long()
+        gather = (src.repeat_interleave(lens) + torch.arange(n, device=lens.device)
+                  - offs.repeat_interleave(lens))
+        new_ids = ids[gather].contiguous()
+        rs, rt, ro = trace.rec_sample[keep].contiguous(), trace.rec_table[keep].contiguous(), offs.contiguous()
+        rl = rl.contiguous()
+    else:
+        want = np.array([int(t.table_id) for t in tabs], np.uint32)
+        keep = np.isin(np.asarray(trace.rec_table, np.uint32), want)
+        rl = np.asarray(trace.rec_len, np.uint32)[keep]
+        lens = rl.astype(np.int64)
+        offs = (np.cumsum(lens) - lens).astype(np.uint64)
+        src = np.asarray(trace.rec_offset, np.uint64)[keep].astype(np.int64)
+        gather = np.repeat(src - offs.astype(np.int64), lens) + np.arange(int(lens.sum()), dtype=np.int64)
+        new_ids = np.asarray(ids)[gather]
+        rs, rt, ro = np.asarray(trace.rec_sample, np.uint64)[keep], np.asarray(trace.rec_table, np.uint32)[keep], offs
+    if trace.ids is not None:
+        return Trace(tabs, trace.num_samples, rs, rt, ro, rl, ids=new_ids)
+    return Trace(tabs, trace.num_samples, rs, rt, ro, rl, raw_ids=new_ids)
+
+
+def profile_sharded(trace, sample_rate: float, seed: int, group=None, profile_fn=None):
+    """profile() with the tables split over the ranks of `group` (no exchange
+    of ids: each rank profiles its tables' records; the FeatureStats are then
+    all-gathered).  Every rank returns the full list, in trace table order —
+    equal to profile() of the whole trace.  `profile_fn(trace, rate, seed)`
+    defaults to the GPU profile()."""
+    import torch.distributed as dist
+
+    if profile_fn is None:
+        from .profiler import profile as profile_fn
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    split = profile_split(trace.tables, world)
+    mine = split[rank]
+    got = profile_fn(subtrace(trace, mine), sample_rate, seed) if mine else []
+    parts = [None] * world
+    dist.all_gather_object(parts, (mine, list(got)), group=group)
+    out = [None] * len(trace.tables)
+    for pos, stats in parts:
+        for j, st in zip(pos, stats):
+            out[j] = st
+    return out

@@ -205,3 +205,30 @@ def test_profile_partitioned_vs_oracle(cuda_ctx, coracle):
                            lens[order], hashed, 1.0, 0)
     assert_stats_equal(got, want)
     del oracle
+
+
+def test_profile_by_table_shards_equals_whole(cuda_ctx):
+    """HP1 across GPUs: each rank profiles the records of its
+    tables (sharded.subtrace, device arrays) — the shards' FeatureStats,
+    reassembled, equal the whole-trace profile bit for bit.  The ranks run one
+    after the other here (one GPU)."""
+    import torch
+
+    from paper_2201_10095_b200 import workload as wl
+    from paper_2201_10095_b200.sharded import profile_split, subtrace
+
+    specs = wl.rm_specs("rm1", 20260809, J=7, hash_scale=0.01)
+    gen = wl.BatchGenerator(specs, 20000, 77)
+    off, idx, n = gen.batch(0)
+    tr = wl.kjt_to_trace(specs, off, idx, n, 20000, 0, ctx=cuda_ctx)
+    # the reference layout: records sorted by (sample, table)
+    order = torch.argsort((tr.rec_sample << 32) | (tr.rec_table.long() & 0xFFFFFFFF), stable=True)
+    tr = Trace(tr.tables, tr.num_samples, tr.rec_sample[order].contiguous(), tr.rec_table[order].contiguous(),
+               tr.rec_offset[order].contiguous(), tr.rec_len[order].contiguous(), ids=tr.ids)
+    whole = sp.profile(tr, 0.7, 3, ctx=cuda_ctx)
+    for world in (2, 3):
+        got = [None] * len(specs)
+        for pos in profile_split(tr.tables, world):
+            for j, st in zip(pos, sp.profile(subtrace(tr, pos), 0.7, 3, ctx=cuda_ctx)):
+                got[j] = st
+        assert_stats_equal(got, [vars(s) for s in whole])

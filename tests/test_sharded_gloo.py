@@ -80,3 +80,91 @@ def test_exchange_world2_gloo(B):
     assert sorted(r[0] for r in res) == [0, 1]
     assert all(r[1] for r in res), "pooled rows did not reach their sample owners intact"
     assert all(r[2] for r in res), "gradients did not return to the table owners intact"
+
+
+# ---------------------------------------------------------------- HP1 by table
+def _small_trace(seed=3):
+    from paper_2201_10095_b200.types import TableSpec, Trace
+
+    rng = np.random.default_rng(seed)
+    tables = [TableSpec(j * 5 + 2, 1000, int(h), 8, 4) for j, h in enumerate([300, 2000, 50, 999, 4096])]
+    S, J = 400, len(tables)
+    lens = rng.integers(0, 6, S * J).astype(np.uint32)
+    keep = lens > 0
+    rec_sample = np.repeat(np.arange(S, dtype=np.uint64), J)[keep]
+    rec_table = np.tile(np.array([t.table_id for t in tables], np.uint32), S)[keep]
+    lens = lens[keep]
+    rec_offset = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.uint64)
+    hs = {t.table_id: t.hash_size for t in tables}
+    ids = np.concatenate([rng.integers(0, hs[int(t)], int(n)) for t, n in zip(rec_table, lens)]).astype(np.uint32)
+    return Trace(tables, S, rec_sample, rec_table, rec_offset, lens, ids=ids)
+
+
+def _cpu_profile(tr, rate, seed):
+    import oracle
+
+    return oracle.C().profile(tr.tables, tr.num_samples, tr.rec_sample, tr.rec_table, tr.rec_offset,
+                              tr.rec_len, tr.ids, rate, seed)
+
+
+def _profile_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2201_10095_b200.sharded import profile_sharded
+
+        tr = _small_trace()
+        got = profile_sharded(tr, 0.6, 11, profile_fn=_cpu_profile)
+        want = _cpu_profile(tr, 0.6, 11)
+        ok = len(got) == len(want) and all(
+            g["table_id"] == w["table_id"] and g["total_accesses"] == w["total_accesses"]
+            and g["distinct_rows_accessed"] == w["distinct_rows_accessed"]
+            and float(g["coverage"]) == float(w["coverage"])
+            and np.array_equal(np.asarray(g["rows_by_rank"]), np.asarray(w["rows_by_rank"]))
+            and np.array_equal(np.asarray(g["icdf_steps"]), np.asarray(w["icdf_steps"]))
+            and np.array_equal(np.asarray(g["access_cdf"]).view(np.uint64), np.asarray(w["access_cdf"]).view(np.uint64))
+            for g, w in zip(got, want))
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_profile_split_balances_counters():
+    from paper_2201_10095_b200.sharded import profile_split
+
+    tabs = _small_trace().tables
+    for world in (1, 2, 3, 7):
+        parts = profile_split(tabs, world)
+        assert sorted(sum(parts, [])) == list(range(len(tabs)))
+    assert profile_split(tabs, 2) == [[4], [0, 1, 2, 3]]  # LPT on hash sizes: 4096 vs 2000+999+300+50
+
+
+def test_subtrace_keeps_each_tables_profile():
+    """A table's statistics on the sub-trace of its shard equal those on the
+    whole trace (selection is per sample)."""
+    from paper_2201_10095_b200.sharded import profile_split, subtrace
+
+    tr = _small_trace()
+    want = _cpu_profile(tr, 0.6, 11)
+    for pos in profile_split(tr.tables, 3):
+        got = _cpu_profile(subtrace(tr, pos), 0.6, 11)
+        for j, g in zip(pos, got):
+            w = want[j]
+            assert g["table_id"] == w["table_id"]
+            assert np.array_equal(np.asarray(g["rows_by_rank"]), np.asarray(w["rows_by_rank"]))
+            assert float(g["coverage"]) == float(w["coverage"]) and float(g["avg_pooling"]) == float(w["avg_pooling"])
+
+
+def test_profile_sharded_world2_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_profile_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r[0] for r in res) == [0, 1]
+    assert all(r[1] for r in res), "sharded profile differs from the whole-trace profile"
