@@ -56,13 +56,16 @@ enum : uint8_t { kSkip = 0, kT = 1, kR = 2, kBad = 3 };
 
 // std::from_chars<uint64_t> over the whole token: non-empty, digits only, no
 // overflow (core/src/trace_io.cpp:25-32).
+// x*10 + c overflows u64 iff x > 1844674407370955161 or (x == that and c > 5)
+// — a compare with constants instead of a 64-bit division per digit.
 __device__ __forceinline__ bool parse_u64(const char* p, const char* e, uint64_t* v) {
   if (p == e) return false;
+  constexpr uint64_t kLim = 1844674407370955161ull;  // (2^64 - 1) / 10
   uint64_t x = 0;
   for (; p < e; ++p) {
     const unsigned c = unsigned((unsigned char)*p) - unsigned('0');
     if (c > 9u) return false;
-    if (x > (~0ull - c) / 10ull) return false;
+    if (x >= kLim && (x > kLim || c > 5u)) return false;
     x = x * 10ull + c;
   }
   *v = x;
