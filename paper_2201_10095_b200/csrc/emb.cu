@@ -508,6 +508,8 @@ struct rs_emb {
   uint32_t* d_cw = nullptr;
   uint32_t* d_nt = nullptr;
   cudaEvent_t ev_err = nullptr;
+  cudaStream_t fwd_side = nullptr;  // every other forward lane class
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   unsigned* d_err = nullptr;
   char* sort_scratch = nullptr;
   size_t sort_scratch_bytes = 0;
@@ -555,6 +557,12 @@ struct rs_emb {
     for (void* p : {(void*)d_order, (void*)d_cpos, (void*)d_cw, (void*)d_nt})
       if (p) cudaFree(p);
     if (ev_err) cudaEventDestroy(ev_err);
+    for (cudaEvent_t ev : {ev_fork, ev_join})
+      if (ev) cudaEventDestroy(ev);
+    if (fwd_side) {
+      cudaStreamSynchronize(fwd_side);
+      cudaStreamDestroy(fwd_side);
+    }
     if (d_err) cudaFree(d_err);
     if (sort_scratch) cudaFree(sort_scratch);
     if (side) {
@@ -725,6 +733,9 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
         RS_CUDA(cudaMemcpy(e->d_order, order.data(), 4 * order.size(), cudaMemcpyHostToDevice));
       RS_CUDA(cudaMemcpy(e->d_cpos, cpos.data(), 4 * cpos.size(), cudaMemcpyHostToDevice));
       RS_CUDA(cudaEventCreateWithFlags(&e->ev_err, cudaEventDisableTiming));
+      RS_CUDA(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
+      RS_CUDA(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
+      RS_CUDA(cudaStreamCreateWithFlags(&e->fwd_side, cudaStreamNonBlocking));
     }
     {
       int v = 1;
@@ -1077,7 +1088,7 @@ void emb_init_weights(rs_emb* e, uint64_t seed, float scale) {
 
 template <int G, int VPL>
 static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint32_t* off,
-                       const uint32_t* idx, float* out, unsigned long long* hits) {
+                       const uint32_t* idx, float* out, unsigned long long* hits, cudaStream_t st) {
   constexpr int BPW = 32 / G;
   const uint64_t warps = (B + BPW - 1) / BPW * c.tables.size();
   const uint64_t blocks = (warps * 32 + emb::kFwdThreads - 1) / emb::kFwdThreads;
@@ -1085,7 +1096,7 @@ static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint
   auto args = std::make_tuple(e->cur_tables, c.d_list, uint32_t(c.tables.size()), B, off, idx, out,
                               e->total_dim, hits, e->keys, e->vals, uint64_t(e->max_lookups), e->d_err);
   auto go = [&](auto kern) {
-    std::apply([&](auto... a) { kern<<<grid, emb::kFwdThreads, 0, e->ctx->stream>>>(a...); }, args);
+    std::apply([&](auto... a) { kern<<<grid, emb::kFwdThreads, 0, st>>>(a...); }, args);
   };
   // (unroll, min blocks/SM): measured on B200 RM1 all-HBM — (4, 6) 1.15 ms,
   // (2, 8) 1.14, (4, 8) 1.17, (6, 6) 1.22, (8, 6) 1.55, (8, 1) 1.85
@@ -1103,19 +1114,33 @@ void emb_forward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx
   e->keys_idx = idx;
   e->keys_B = B;
   auto* h = reinterpret_cast<unsigned long long*>(hits);
-  for (const auto& c : e->classes) {
+  // lane classes write disjoint columns, keys and hit counters: every other
+  // class runs on a forked stream so one launch's tail overlaps the next
+  cudaStream_t main = e->ctx->stream;
+  const bool fork = e->classes.size() > 1;
+  if (fork) {
+    RS_CUDA(cudaEventRecord(e->ev_fork, main));
+    RS_CUDA(cudaStreamWaitEvent(e->fwd_side, e->ev_fork, 0));
+  }
+  for (size_t ci = 0; ci < e->classes.size(); ++ci) {
+    const auto& c = e->classes[ci];
+    cudaStream_t st = (ci & 1) ? e->fwd_side : main;
     switch (c.G * 100 + c.VPL) {
-      case 101: launch_fwd<1, 1>(e, c, B, off, idx, out, h); break;
-      case 201: launch_fwd<2, 1>(e, c, B, off, idx, out, h); break;
-      case 401: launch_fwd<4, 1>(e, c, B, off, idx, out, h); break;
-      case 801: launch_fwd<8, 1>(e, c, B, off, idx, out, h); break;
-      case 1601: launch_fwd<16, 1>(e, c, B, off, idx, out, h); break;
-      case 3201: launch_fwd<32, 1>(e, c, B, off, idx, out, h); break;
-      case 3202: launch_fwd<32, 2>(e, c, B, off, idx, out, h); break;
-      case 3204: launch_fwd<32, 4>(e, c, B, off, idx, out, h); break;
-      case 3208: launch_fwd<32, 8>(e, c, B, off, idx, out, h); break;
+      case 101: launch_fwd<1, 1>(e, c, B, off, idx, out, h, st); break;
+      case 201: launch_fwd<2, 1>(e, c, B, off, idx, out, h, st); break;
+      case 401: launch_fwd<4, 1>(e, c, B, off, idx, out, h, st); break;
+      case 801: launch_fwd<8, 1>(e, c, B, off, idx, out, h, st); break;
+      case 1601: launch_fwd<16, 1>(e, c, B, off, idx, out, h, st); break;
+      case 3201: launch_fwd<32, 1>(e, c, B, off, idx, out, h, st); break;
+      case 3202: launch_fwd<32, 2>(e, c, B, off, idx, out, h, st); break;
+      case 3204: launch_fwd<32, 4>(e, c, B, off, idx, out, h, st); break;
+      case 3208: launch_fwd<32, 8>(e, c, B, off, idx, out, h, st); break;
       default: throw Error(-9, "emb_forward: unsupported lane class");
     }
+  }
+  if (fork) {
+    RS_CUDA(cudaEventRecord(e->ev_join, e->fwd_side));
+    RS_CUDA(cudaStreamWaitEvent(main, e->ev_join, 0));
   }
   RS_LAUNCH_CHECK();
   e->t_fwd.end(e->ctx->stream);
