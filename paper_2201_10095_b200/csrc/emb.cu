@@ -1161,20 +1161,20 @@ void emb_kernel_times(rs_emb* e, double* fwd_ms, uint64_t* n_fwd, double* bwd_ms
 
 // Short-segment bag pass for one lane class over its window range [wlo, whi).
 template <int G, int VPL, int UNR, int MINB>
-static void launch_segs_v(rs_emb* e, const emb::BwdArgs& a, uint32_t ci, uint64_t max_windows) {
+static void launch_segs_v(rs_emb* e, const emb::BwdArgs& a, uint32_t ci, uint64_t max_windows, cudaStream_t st) {
   // the class's window range is on the device (bwd_plan_kernel): persistent
   // grid, capped by the class's largest possible window count
   const uint64_t est = max_windows * 8 / (uint64_t(emb::kBwdWarps) * (32 / G)) + 1;
   const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(est, uint64_t(sm_count()) * MINB)));
-  emb::bwd_seg_kernel<G, VPL, UNR, MINB><<<grid, emb::kBwdThreads, 0, e->ctx->stream>>>(
+  emb::bwd_seg_kernel<G, VPL, UNR, MINB><<<grid, emb::kBwdThreads, 0, st>>>(
       a, e->segs, e->sbase, e->d_cw, ci, e->longs, e->long_np, e->long_ng, e->n_long);
   RS_COUNT(1);
 }
 
 template <int G, int VPL>
-static void launch_segs(rs_emb* e, const emb::BwdArgs& a, uint32_t ci, uint64_t max_windows) {
-  if constexpr (VPL == 1) launch_segs_v<G, 1, 4, 4>(e, a, ci, max_windows);
-  else launch_segs_v<G, VPL, (VPL == 2 ? 2 : 1), 2>(e, a, ci, max_windows);
+static void launch_segs(rs_emb* e, const emb::BwdArgs& a, uint32_t ci, uint64_t max_windows, cudaStream_t st) {
+  if constexpr (VPL == 1) launch_segs_v<G, 1, 4, 4>(e, a, ci, max_windows, st);
+  else launch_segs_v<G, VPL, (VPL == 2 ? 2 : 1), 2>(e, a, ci, max_windows, st);
 }
 
 // Long segments: groups of 64 pieces, then one warp per segment (full warps,
@@ -1272,21 +1272,33 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
   RS_CUDA(cudaMemsetAsync(e->n_long, 0, 4, st));
   RS_CUDA(cudaMemsetAsync(e->long_np, 0, (e->long_cap + 1) * 4, st));
   RS_CUDA(cudaMemsetAsync(e->long_ng, 0, (e->long_cap + 1) * 4, st));
+  // classes update disjoint rows (the long list is an atomic append): every
+  // other class on the forked stream, as in the forward
+  const bool fork = e->classes.size() > 1;
+  if (fork) {
+    RS_CUDA(cudaEventRecord(e->ev_fork, st));
+    RS_CUDA(cudaStreamWaitEvent(e->fwd_side, e->ev_fork, 0));
+  }
   for (size_t ci = 0; ci < e->classes.size(); ++ci) {
     const auto& c = e->classes[ci];
     const uint64_t mw = Wmax;
+    cudaStream_t cs = (ci & 1) ? e->fwd_side : st;
     switch (c.G * 100 + c.VPL) {
-      case 101: launch_segs<1, 1>(e, a, uint32_t(ci), mw); break;
-      case 201: launch_segs<2, 1>(e, a, uint32_t(ci), mw); break;
-      case 401: launch_segs<4, 1>(e, a, uint32_t(ci), mw); break;
-      case 801: launch_segs<8, 1>(e, a, uint32_t(ci), mw); break;
-      case 1601: launch_segs<16, 1>(e, a, uint32_t(ci), mw); break;
-      case 3201: launch_segs<32, 1>(e, a, uint32_t(ci), mw); break;
-      case 3202: launch_segs<32, 2>(e, a, uint32_t(ci), mw); break;
-      case 3204: launch_segs<32, 4>(e, a, uint32_t(ci), mw); break;
-      case 3208: launch_segs<32, 8>(e, a, uint32_t(ci), mw); break;
+      case 101: launch_segs<1, 1>(e, a, uint32_t(ci), mw, cs); break;
+      case 201: launch_segs<2, 1>(e, a, uint32_t(ci), mw, cs); break;
+      case 401: launch_segs<4, 1>(e, a, uint32_t(ci), mw, cs); break;
+      case 801: launch_segs<8, 1>(e, a, uint32_t(ci), mw, cs); break;
+      case 1601: launch_segs<16, 1>(e, a, uint32_t(ci), mw, cs); break;
+      case 3201: launch_segs<32, 1>(e, a, uint32_t(ci), mw, cs); break;
+      case 3202: launch_segs<32, 2>(e, a, uint32_t(ci), mw, cs); break;
+      case 3204: launch_segs<32, 4>(e, a, uint32_t(ci), mw, cs); break;
+      case 3208: launch_segs<32, 8>(e, a, uint32_t(ci), mw, cs); break;
       default: throw Error(-9, "emb_backward: unsupported lane class");
     }
+  }
+  if (fork) {
+    RS_CUDA(cudaEventRecord(e->ev_join, e->fwd_side));
+    RS_CUDA(cudaStreamWaitEvent(st, e->ev_join, 0));
   }
   // long segments: group offsets, group sums, final sums + updates
   exclusive_scan<uint32_t>(ArrayIn<uint32_t>{e->long_np}, e->long_cap, e->pbase, e->pbase + e->long_cap, scr, st);
