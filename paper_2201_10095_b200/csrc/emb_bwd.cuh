@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(kBwdThreads) bwd_piece_desc_kernel(const uint4
 // like bwd_seg_kernel: the next piece's descriptor and sample ids are in
 // flight while this piece's grad rows are summed.
 template <int G, int VPL>
-__global__ void __launch_bounds__(kBwdThreads) bwd_lpiece_kernel(BwdArgs a, const uint4* __restrict__ pdesc,
+__global__ void __launch_bounds__(kBwdThreads, 3) bwd_lpiece_kernel(BwdArgs a, const uint4* __restrict__ pdesc,
                                                                 const unsigned* __restrict__ n_long,
                                                                 const uint32_t* __restrict__ pbase,
                                                                 float* __restrict__ ppart) {
@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(kBwdThreads) bwd_lpiece_kernel(BwdArgs a, cons
   // per lane, a dim-64 row 1) — the sums are elementwise, so the lane layout
   // does not change any result
   constexpr int BPW = 32 / G;
-  constexpr int UNR = 8;
+  constexpr int UNR = 4;  // 4 rows in flight at 3 CTAs/SM beat 8 at 2 (A/B: bwd -0.1-0.2 ms)
   const int lane = threadIdx.x & 31;
   const int grp = lane / G, lg = lane % G;
   const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
