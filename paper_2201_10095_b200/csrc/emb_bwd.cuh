@@ -239,11 +239,19 @@ __global__ void __launch_bounds__(1024) bwd_plan_kernel(BwdPlan p) {
     if (t < T && !empty) ntt = (p.tpos[t + 1] - p.tpos[t] + kSortTile - 1) / kSortTile;
     uint32_t tot;
     const uint32_t x = block_excl_scan(ntt, sm, tot);
-    for (uint32_t j = 0; j < ntt; ++j) {
-      const uint32_t k = tb + x + j;
-      p.tiles[k] = p.tpos[t] + j * kSortTile;
-      p.tiles[p.tcap + k] = uint32_t(kRadix) * (tb + x) + j;
-      p.tiles[2 * p.tcap + k] = ntt;
+    // the warp writes its 32 tables' tiles one table at a time, lanes over tiles
+    const int lane = threadIdx.x & 31;
+    for (int i = 0; i < 32; ++i) {
+      const uint32_t ti = __shfl_sync(0xffffffffu, t, i);
+      const uint32_t ni = __shfl_sync(0xffffffffu, ntt, i);
+      const uint32_t bi = tb + __shfl_sync(0xffffffffu, x, i);
+      if (ni == 0) continue;
+      const uint32_t start = p.tpos[ti];
+      for (uint32_t j = lane; j < ni; j += 32) {
+        p.tiles[bi + j] = start + j * kSortTile;
+        p.tiles[p.tcap + bi + j] = uint32_t(kRadix) * bi + j;
+        p.tiles[2 * p.tcap + bi + j] = ni;
+      }
     }
     tb += tot;
   }
