@@ -284,8 +284,15 @@ __global__ void __launch_bounds__(256) bwd_seg_scan_kernel(BwdArgs a, WorkMap m,
   const int lane = threadIdx.x & 31;
   const uint64_t nwork = m.wstart[m.nt];
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t wi = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; wi < nwork; wi += nwarps) {
-    const uint32_t i = upper_index(m.wstart, m.nt, wi);
+  // each warp walks a contiguous run of windows: one table search per run,
+  // then the table index only moves forward (and the keys it reads are
+  // consecutive)
+  const uint64_t per = (nwork + nwarps - 1) / nwarps;
+  const uint64_t w0 = ((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * per;
+  const uint64_t w1 = min(nwork, w0 + per);
+  uint32_t i = w0 < w1 ? upper_index(m.wstart, m.nt, w0) : 0u;
+  for (uint64_t wi = w0; wi < w1; ++wi) {
+    while (m.wstart[i + 1] <= wi) ++i;  // (tables without windows are skipped)
     const uint32_t t = m.wtab[i];
     const uint32_t k = uint32_t(wi - m.wstart[i]);
     const uint32_t tb = a.tpos[t], te = a.tpos[t + 1];
