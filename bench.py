@@ -469,6 +469,15 @@ def run_profile_sweep(args, torch, ctx, hbm_peak):
     out = {"workload": "cfg1 tables, rate 1.0", "ids": int(n), "records": R,
            "seconds": secs, "ids_per_s": n / secs, "algorithmic_gbs": alg / secs / 1e9,
            "frac_of_hbm": alg / secs / 1e9 / hbm_peak}
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    try:  # DRAM bytes of one such call from the committed ncu launch list
+        tb = json.load(open(tp)).get("cfg1_profile_1e9", {}).get("dram_bytes")
+        if tb:
+            tb = tb * n / 1e9
+            out["traffic"] = {"dram_bytes": tb, "gbs": tb / secs / 1e9, "frac_of_hbm": tb / secs / 1e9 / hbm_peak,
+                              "bound": "per-id instructions + shared-memory atomics (partition and count passes)"}
+    except Exception:
+        pass
     if oracle.ref_available():
         m = min(R, int(args.cpu_profile_ids // 20))
         sub = (tr.rec_sample[:m].cpu().numpy().view(np.uint64), tr.rec_table[:m].cpu().numpy().view(np.uint32),
