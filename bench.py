@@ -142,72 +142,136 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------- reference arm
-def cpu_emb_baseline(specs, B, seconds, threads, optimizer):
-    """The oracle port (oracle/oracle.c EmbeddingBag fwd+bwd — the reference has
-    no EmbeddingBag) on a bounded sample of the workload: every 12th
-    table at full hash size, one batch of B samples generated with the same
-    generator, repeated for ~`seconds`; samples/s scaled to the whole step by
-    lookup count.  Host threads: `threads` (tables in parallel)."""
-    import torch
+METRIC = "EMB fwd+bwd samples/s (RecShard plan; greedy-size plan alongside); UVM access %"
 
-    import oracle
-    from paper_2201_10095_b200 import workload as wl
 
-    sub = specs[::12] if len(specs) > 12 else specs
-    c = oracle.C()
-    gen = wl.BatchGenerator(sub, B, WORKLOAD_SEED)
-    off_d, idx_d, n = gen.batch(10_000)
-    off = off_d.cpu().numpy().view(np.uint32).astype(np.uint64)
-    idx = idx_d[:n].cpu().numpy().view(np.uint32).copy()
-    dims = [w.table.dim for w in sub]
-    Hs = [w.table.hash_size for w in sub]
-    W = [c.init_table(INIT_SEED, w.table.table_id, w.table.hash_size, w.table.dim, 0.1) for w in sub]
-    mom = [np.zeros(h, np.float32) for h in Hs] if optimizer != "sgd" else None
-    opt = 0 if optimizer == "sgd" else 1
+def line_config(args, n_tables, parallelism):
+    """The `config` object both arms print (the driver pairs the lines by metric)."""
+    return {"workload": f"{args.config}-like", "tables": n_tables, "global_batch": args.batch,
+            "optimizer": args.optimizer, "parallelism": parallelism,
+            "fast_tier_cap": f"{args.hbm_fraction:.0%} of table bytes",
+            "l2": "256 MiB flush between steps" if not args.no_flush
+            else f"{args.nbatches} distinct batches cycled"}
+
+
+class RefEmbWorkload:
+    """The CPU reference side of the EMB step, built WITHOUT the GPU library:
+    a bounded table sample (every `every`-th table, full hash sizes) whose
+    training batch comes from the unmodified reference generator
+    (shardplan::generate_trace, core/src/workload.cpp:198-217, via oracle/_ref)
+    regrouped into table-major CSR, and whose tables are initialised ONCE
+    (oracle.c or_init_table, the same weights the GPU operator starts from).
+    `step()` is one fwd + (grad = pooled) + bwd with the row-wise update over
+    the sample on `threads` host threads (oracle.c — the reference has no
+    EmbeddingBag); samples/s are scaled to the whole workload by
+    expected lookups."""
+
+    def __init__(self, specs, B, optimizer, threads, every=12):
+        from concurrent.futures import ThreadPoolExecutor
+
+        import oracle
+        from paper_2201_10095_b200 import workload as wl  # pure Python (no .so)
+
+        self.sub = specs[::every] if len(specs) > every else list(specs)
+        self.B, self.threads, self.optimizer = B, threads, optimizer
+        R = oracle.Ref()
+        t0 = time.perf_counter()
+        tr = R.generate_trace([(w.table, (w.gen.zipf_exponent, w.gen.mean_pooling, w.gen.coverage,
+                                          w.gen.pooling_law)) for w in self.sub], B, WORKLOAD_SEED)
+        self.gen_s = time.perf_counter() - t0
+        self.offsets, self.indices = oracle.trace_to_csr(tr, [w.table.table_id for w in self.sub], B)
+        n = int(self.offsets[-1])
+        R.free_trace(tr)
+        self.n = n
+        c = oracle.C()
+        self.dims = [w.table.dim for w in self.sub]
+        self.Hs = [w.table.hash_size for w in self.sub]
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(max_workers=threads) as ex:
+            self.W = list(ex.map(lambda w: c.init_table(INIT_SEED, w.table.table_id, w.table.hash_size,
+                                                        w.table.dim, 0.1), self.sub))
+        self.init_s = time.perf_counter() - t0
+        self.mom = [np.zeros(h, np.float32) for h in self.Hs] if optimizer != "sgd" else None
+        self.full_lookups = wl.expected_lookups(specs, B)
+        self.n_specs = len(specs)
+
+    def step(self):
+        import oracle
+
+        oracle.emb_step_cpu(self.B, self.dims, self.Hs, self.offsets, self.indices, self.W, self.mom,
+                            0 if self.optimizer == "sgd" else 1, LR, 1e-8, self.threads)
+
+    def samples_per_s(self, step_s):
+        return self.B / (step_s * self.full_lookups / self.n)
+
+    def sample_text(self, reps, secs):
+        return (f"oracle/oracle.c fwd+bwd ({self.optimizer}) on {len(self.sub)} of {self.n_specs} "
+                f"tables (every 12th, full hash sizes; weights initialised once), 1 batch of {self.B} "
+                f"samples = {self.n} lookups from the unmodified reference generate_trace; {reps} steps "
+                f"in {secs:.1f}s, scaled to the full step by expected lookups ({self.full_lookups:.3g})")
+
+
+def cpu_emb_baseline(specs, B, seconds, threads, optimizer, work=None):
+    """cpu_baseline of our arm: RefEmbWorkload stepped for ~`seconds`."""
+    w = work or RefEmbWorkload(specs, B, optimizer, threads)
+    w.step()  # warm
     reps, t0 = 0, time.perf_counter()
     while True:
-        oracle.emb_step_cpu(B, dims, Hs, off, idx, W, mom, opt, LR, 1e-8, threads)
+        w.step()
         reps += 1
         el = time.perf_counter() - t0
         if el >= seconds:
             break
-    full_lookups = wl.expected_lookups(specs, B)
-    sample_lookups = float(n)
-    step_s = (el / reps) * (full_lookups / sample_lookups)
-    del torch
-    return dict(value=B / step_s, unit="samples/s", cores=threads, kind="port",
-                sample=(f"oracle/oracle.c fwd+bwd ({optimizer}), {len(sub)} of {len(specs)} tables "
-                        f"(every 12th, full hash sizes), 1 batch of {B} samples = {n} lookups, "
-                        f"{reps} reps in {el:.1f}s; scaled to the full step by expected lookups "
-                        f"({full_lookups:.3g})"))
+    return dict(value=w.samples_per_s(el / reps), unit="samples/s", cores=threads, kind="port",
+                sample=w.sample_text(reps, el))
+
+
+def loaded_native_libs():
+    """Shared objects of this repo mapped into the process (evidence of which
+    native code ran)."""
+    out = set()
+    try:
+        with open("/proc/self/maps") as f:
+            for ln in f:
+                p = ln.split()[-1]
+                if p.endswith(".so") and p.startswith(ROOT):
+                    out.add(os.path.relpath(p, ROOT))
+    except OSError:
+        pass
+    return sorted(out)
 
 
 def run_reference(args, rank, world):
+    """`--impl reference`: the CPU implementation of the path on this host's
+    cores (rank 0 only; other ranks exit without work).  Never loads
+    libshardplan_gpu.so: inputs come from the unmodified reference generator."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
     specs = specs_for(args.config)
-    import torch  # noqa: F401  (the generator needs the GPU for input synthesis only)
-
-    per = max(1.0, args.cpu_seconds / max(1, args.steps))
-    vals = []
+    work = RefEmbWorkload(specs, args.batch, args.optimizer, threads)
     for _ in range(args.warmup):
-        cpu_emb_baseline(specs, args.batch, 0.0, threads, args.optimizer)
+        work.step()
+    times = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        vals.append(cpu_emb_baseline(specs, args.batch, per, threads, args.optimizer))
+        s = time.perf_counter()
+        work.step()
+        times.append(time.perf_counter() - s)
     el = time.perf_counter() - t0
-    v = float(np.median([x["value"] for x in vals]))
-    line = {"impl": "reference", "metric": "EMB fwd+bwd samples/s", "value": v,
+    v = work.samples_per_s(float(np.sum(times)) / len(times))
+    M = world
+    line = {"impl": "reference", "metric": METRIC, "value": v,
             "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * args.batch / v, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config}-like", "global_batch": args.batch},
+            "config": line_config(args, len(specs), f"table-wise mp{M}"),
             "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads, "kind": "port",
-                             "sample": vals[0]["sample"]},
+                             "sample": work.sample_text(args.steps, el)},
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
-            "wall_s": el}
+            "setup_s": {"reference_generate_trace": work.gen_s, "init_tables": work.init_s},
+            "native_libs_loaded": loaded_native_libs()}
     print(json.dumps(line), flush=True)
 
 
@@ -647,11 +711,32 @@ def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex, cache, 
             "mode": "pipelined" if cache else "zero-copy"}
 
 
+def free_port():
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `bench.py --gpus N` launched directly: spawn the N ranks the way the
+        # driver does (torchrun, one process per GPU, rendezvous on 127.0.0.1)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE {world}; running {world} ranks",
+              file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
     import torch
 
     dist = None
@@ -660,12 +745,6 @@ def main():
 
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    if args.impl == "reference":
-        run_reference(args, rank, world)
-        if dist:
-            dist.barrier()
-            dist.destroy_process_group()
-        return
 
     import paper_2201_10095_b200 as sp
     from paper_2201_10095_b200 import planner
@@ -816,17 +895,14 @@ def main():
             except Exception:
                 traffic = None
         line = {
-            "metric": "EMB fwd+bwd samples/s (RecShard plan; greedy-size plan alongside); UVM access %",
+            "metric": METRIC,
             "value": r["samples_per_s"], "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (GPU Zipf generator, random-init weights)",
-            "config": {"workload": f"{args.config}-like", "tables": len(specs), "global_batch": B,
-                       "optimizer": args.optimizer,
-                       "parallelism": (f"one shard (rank {prank}) of a table-wise mp{M} plan, "
-                                       "no all-to-all" if emulate else f"table-wise mp{world}"),
-                       "fast_tier_cap": "40% of table bytes", "l2": "256 MiB flush between steps"
-                       if not args.no_flush else f"{args.nbatches} distinct batches cycled"},
+            "config": line_config(args, len(specs),
+                                  f"one shard (rank {prank}) of a table-wise mp{M} plan, no all-to-all"
+                                  if emulate else f"table-wise mp{world}"),
             "uvm_access_pct": r["uvm_pct"],
             "plan": first.strategy, "planner_s": plan_s,
             "simulated_uvm_pct": sim_uvm,

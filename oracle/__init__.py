@@ -502,6 +502,27 @@ class _RefLib:
         return rep
 
 
+def trace_to_csr(tr, table_ids, B, sample_base=0):
+    """A reference Trace (records sorted by (sample, table), inc/workload.hpp:41-58)
+    regrouped as the operator's table-major CSR batch: offsets u64[T*B+1]
+    (bag (t, b) = samples sample_base + b), indices u32 in per-table sample order."""
+    T = len(table_ids)
+    tid = np.asarray(table_ids, np.uint32)
+    tix = np.searchsorted(tid, tr.rec_table)
+    s = tr.rec_sample.astype(np.int64) - sample_base
+    keep = (s >= 0) & (s < B)
+    tix, s = tix[keep], s[keep]
+    st, ln = tr.rec_offset[keep].astype(np.int64), tr.rec_len[keep].astype(np.int64)
+    lens = np.zeros((T, B), np.uint64)
+    lens[tix, s] = ln
+    offsets = np.concatenate([[0], np.cumsum(lens.ravel())]).astype(np.uint64)
+    order = np.lexsort((s, tix))
+    st, ln = st[order], ln[order]
+    n = int(ln.sum())
+    pos = np.repeat(st - np.concatenate([[0], np.cumsum(ln)[:-1]]), ln) + np.arange(n)
+    return offsets, np.ascontiguousarray(tr.ids[pos], np.uint32)
+
+
 def emb_step_cpu(B, dims, hash_sizes, offsets, indices, weights, momentum, opt, lr, eps,
                  threads):
     """One oracle fwd + (grad = pooled) + bwd over all tables, tables spread over

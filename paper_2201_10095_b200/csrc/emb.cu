@@ -66,10 +66,17 @@ __device__ __forceinline__ float* row_ptr_host(const TableDev& td, int32_t e) {
 }
 // Row of remap entry e as the hot paths see it: slow rows come from their HBM
 // staging slot when the batch was prefetched (uvm_cache.cuh).
+// A slow row without a slot (a claim that ran out of slots: slot_of stays
+// kNoSlot, 0xFFFFFFFF) is read/written in the host tier instead, so a failed
+// claim can never send the kernels outside the staging buffer; the failure
+// itself is reported before the batch runs (begin_step).
 __device__ __forceinline__ float* row_ptr(const TableDev& td, int32_t e) {
   if (e >= 0) return td.fast + uint64_t(e) * td.dim;
   const uint64_t s = uint64_t(-int64_t(e) - 1);
-  if (td.slot_of) return td.staging + uint64_t(td.slot_of[s]) * td.stage_stride;
+  if (td.slot_of) {
+    const uint32_t sl = td.slot_of[s];
+    if (sl < 0xFFFFFFFEu) return td.staging + uint64_t(sl) * td.stage_stride;
+  }
   return td.slow + s * td.dim;
 }
 __device__ __forceinline__ float* mom_ptr(const TableDev& td, int32_t e) {
@@ -440,6 +447,7 @@ struct rs_emb {
   cudaStream_t side_out = nullptr;
   cudaStream_t claim_stream = nullptr;
   uint64_t gather_seq[4] = {0, 0, 0, 0}, wb_seq = 0;
+  unsigned gen_err[4] = {0, 0, 0, 0};  // cache_err seen by generation g's stage-in (host)
 
   TableDev* d_tables_c = nullptr;
   uint32_t* d_slow_tabs = nullptr;  // tables with slow rows
@@ -867,12 +875,18 @@ void emb_enable_cache(rs_emb* e, uint32_t nslots) {
   e->nslots = nslots;
 }
 
-static void check_cache_error(rs_emb* e) {
+static const char* kCacheErrMsg =
+    "emb: slow-row cache out of slots; enable it with more slots "
+    "(>= 4x the unique slow rows of a batch: up to four generations are live)";
+
+// Reads and clears the device error word of the claim kernels.
+static unsigned take_cache_error(rs_emb* e) {
   unsigned err = 0;
-  RS_CUDA(cudaMemcpy(&err, e->cache_err, 4, cudaMemcpyDeviceToHost));
-  if (err)
-    throw InvalidArgument("emb: slow-row cache out of slots; enable it with more slots "
-                          "(>= 2x the unique slow rows of a batch)");
+  RS_CUDA(cudaMemcpyAsync(&e->h_cnt[3], e->cache_err, 4, cudaMemcpyDeviceToHost, e->ctx->stream));
+  RS_CUDA(cudaStreamSynchronize(e->ctx->stream));
+  err = e->h_cnt[3];
+  if (err) RS_CUDA(cudaMemsetAsync(e->cache_err, 0, 4, e->ctx->stream));
+  return err;
 }
 
 // Host row of (table t, slow row r) in the pinned host tier.
@@ -900,7 +914,9 @@ static void stage_in_task(rs_emb* e, uint64_t g, uint64_t out_before) {
   const uint64_t cs = (g & 1) * e->bcap;  // this generation's copy-list set
   unsigned* ncopy = e->ncopy + (g & 1);
   RS_CUDA(cudaMemcpyAsync(e->h_cnt, ncopy, 4, cudaMemcpyDeviceToHost, s));
+  RS_CUDA(cudaMemcpyAsync(e->h_cnt + 2, e->cache_err, 4, cudaMemcpyDeviceToHost, s));
   RS_CUDA(cudaStreamSynchronize(s));
+  e->gen_err[g & 3] = e->h_cnt[2];  // read by begin_step before generation g runs
   const uint64_t n = std::min<uint64_t>(e->h_cnt[0], e->bcap);
   const uint64_t stride = e->dmax;
   if (n) {
@@ -1047,10 +1063,12 @@ void emb_flush(rs_emb* e) {
   e->out_worker->drain();
   e->done_gen = -1;
   RS_CUDA(cudaStreamSynchronize(e->ctx->stream));
-  check_cache_error(e);
   e->pending.clear();
   e->cur_gen = -1;
   e->staged_dirty = false;
+  for (unsigned& x : e->gen_err) x = 0;
+  // the cache is empty and consistent again; a failed claim is still reported
+  if (take_cache_error(e)) throw InvalidArgument(kCacheErrMsg);
 }
 
 // Picks the tables for a forward: the oldest prefetched batch (staged rows)
@@ -1066,6 +1084,14 @@ static void begin_step(rs_emb* e) {
     e->pending.erase(e->pending.begin());
     e->cur_gen = int64_t(g);
     e->worker->wait(e->gather_seq[g & 3]);  // its copies are enqueued
+    if (e->gen_err[g & 3]) {
+      // some of this batch's slow rows got no slot: refuse to run it (a later
+      // staged batch could otherwise re-read a row this one updates in the
+      // host tier); flush() empties the cache and clears the error
+      e->cur_gen = -1;
+      e->pending.insert(e->pending.begin(), g);
+      throw InvalidArgument(kCacheErrMsg);
+    }
     RS_CUDA(cudaStreamWaitEvent(e->ctx->stream, e->ev_gather[g & 3], 0));
     e->cur_tables = e->d_tables_c;
   } else {

@@ -949,6 +949,8 @@ struct RankDevice {
   uint64_t* icdf;     // J * 101
   uint64_t* tstart;   // J + 1
   size_t n;
+  uint32_t split = 0;  // > 0: the (table, count) key does not fit 32 bits; rank
+                       // at most `split` tables per call instead (nothing ranked)
 };
 
 inline int bits_for(uint64_t v) {  // bits needed to represent values 0..v
@@ -981,10 +983,13 @@ inline RankDevice rank_group(rs_context* ctx, Scratch& scr, const uint32_t* d_co
   const size_t nd = h2[1];
   const int cbits = std::max(1, bits_for(maxc));
   const int tbits = bits_for(J > 0 ? J - 1 : 0);
-  if (cbits + tbits > 32)
-    throw Error(-9, "rank: table/count key exceeds 32 bits; split the table group");
-
   RankDevice out{};
+  if (cbits + tbits > 32) {
+    // rows counted >= 2^(32 - tbits) times: fewer tables per key space
+    out.split = cbits >= 32 ? 1u : (1u << (32 - cbits));
+    return out;
+  }
+
   out.n = nd;
   out.rows = scr.take<uint32_t>(nd + 1);
   out.cdf = scr.take<double>(nd + 1);
@@ -1192,21 +1197,47 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
         if (h_err & kErrRowRange)
           throw InvalidArgument("profile: hashed id outside its table's hash_size");
       }
-      RankDevice rk = rank_group(ctx, scr, d_cnt, base_g, Jg, d_acc + t_lo);
-      std::vector<uint64_t> tstart(Jg + 1);
-      const size_t at = res->nd;
-      res->grow(rk.n, st);
-      RS_CUDA(cudaMemcpyAsync(tstart.data(), rk.tstart, (Jg + 1) * 8, cudaMemcpyDeviceToHost, st));
-      RS_CUDA(cudaMemcpyAsync(res->icdf.data() + size_t(t_lo) * 101, rk.icdf,
-                              size_t(Jg) * 101 * 8, cudaMemcpyDeviceToHost, st));
-      if (rk.n) {
-        RS_CUDA(cudaMemcpyAsync(res->rows + at, rk.rows, rk.n * 4, cudaMemcpyDeviceToHost, st));
-        RS_CUDA(cudaMemcpyAsync(res->cdf + at, rk.cdf, rk.n * 8, cudaMemcpyDeviceToHost, st));
-        RS_CUDA(cudaMemcpyAsync(res->d_rows + at, rk.rows, rk.n * 4, cudaMemcpyDeviceToDevice, st));
+      // K2 over the group; a group whose hottest row needs more count bits
+      // than the packed (table, count) key leaves is ranked in table ranges
+      uint32_t step = Jg;
+      for (uint32_t a = 0; a < Jg;) {
+        const uint32_t b = std::min(Jg, a + step);
+        std::vector<uint64_t> base_r(base_g.begin() + a, base_g.begin() + b + 1);
+        for (auto& x : base_r) x -= base_g[a];
+        const size_t mark_r = scr.used;
+        RankDevice rk = rank_group(ctx, scr, d_cnt + base_g[a], base_r, b - a, d_acc + t_lo + a);
+        if (rk.split) {
+          scr.used = mark_r;
+          step = std::min(step, rk.split);
+          if (b - a <= step) throw Error(-9, "rank: table range split did not shrink the key");
+          continue;
+        }
+        const uint32_t r_lo = t_lo + a, Jr = b - a;
+        std::vector<uint64_t> tstart(Jr + 1);
+        const size_t at = res->nd;
+        res->grow(rk.n, st);
+        RS_CUDA(cudaMemcpyAsync(tstart.data(), rk.tstart, (Jr + 1) * 8, cudaMemcpyDeviceToHost, st));
+        RS_CUDA(cudaMemcpyAsync(res->icdf.data() + size_t(r_lo) * 101, rk.icdf,
+                                size_t(Jr) * 101 * 8, cudaMemcpyDeviceToHost, st));
+        if (rk.n) {
+          RS_CUDA(cudaMemcpyAsync(res->rows + at, rk.rows, rk.n * 4, cudaMemcpyDeviceToHost, st));
+          RS_CUDA(cudaMemcpyAsync(res->cdf + at, rk.cdf, rk.n * 8, cudaMemcpyDeviceToHost, st));
+          RS_CUDA(cudaMemcpyAsync(res->d_rows + at, rk.rows, rk.n * 4, cudaMemcpyDeviceToDevice, st));
+        }
+        res->nd = at + rk.n;
+        ctx->sync();
+        for (uint32_t j = r_lo; j < r_lo + Jr; ++j) res->distinct[j] = tstart[j - r_lo + 1] - tstart[j - r_lo];
+        scr.used = mark_r;
+        a = b;
       }
-      res->nd = at + rk.n;
-      ctx->sync();
-      for (uint32_t j = t_lo; j < t_hi; ++j) res->distinct[j] = tstart[j - t_lo + 1] - tstart[j - t_lo];
+      if (g > 0) {
+        // later groups (sum of hash sizes >= 2^31) can find out-of-range rows too
+        auto* hb = ctx->pinned_buf<unsigned>(1);
+        RS_CUDA(cudaMemcpyAsync(hb, d_err, 4, cudaMemcpyDeviceToHost, st));
+        ctx->sync();
+        if (hb[0] & kErrRowRange)
+          throw InvalidArgument("profile: hashed id outside its table's hash_size");
+      }
       scr.used = mark;
     }
     // assemble (tables are group-contiguous, so concatenation keeps order)

@@ -32,6 +32,7 @@ namespace emb {
 
 constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
 constexpr uint32_t kClaim = 0xFFFFFFFEu;
+constexpr uint32_t kDeadRow = 0xFFFFFFFFu;  // slot_row of a slot whose copy-list entry overflowed
 
 // Claim / mark the staging slots of one batch's slow rows.  New slots are
 // queued in copy_list for the copy kernel.  Only tables with slow rows are
@@ -81,11 +82,17 @@ uvm_claim_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict
           copy_list[k] = slot;
           copy_tab[k] = t;
           copy_row[k] = s;
+          __threadfence();
+          atomicExch(p, slot);
         } else {
+          // no room to copy the row in: the slot is never filled, so the row
+          // keeps no slot (row_ptr falls back to the host tier) and the slot
+          // is freed by the next eviction without a write-back
+          slot_row[slot] = kDeadRow;
           atomicOr(err, 2u);
+          __threadfence();
+          atomicExch(p, kNoSlot);
         }
-        __threadfence();
-        atomicExch(p, slot);
       } else if (old != kClaim) {
         atomicOr(&slot_gen[old], gen_bit);
       }
@@ -129,7 +136,13 @@ uvm_evict_kernel(const TableDev* __restrict__ tables, uint32_t nslots, uint32_t 
     const bool mine = (g & gen_bit) != 0;
     const bool kept = mine && (g & keep) != 0;
     if (kept) slot_gen[my] = g & ~gen_bit;
-    unsigned evict = __ballot_sync(0xffffffffu, mine && !kept);
+    // a slot whose row was never copied in (kDeadRow) is freed without a write-back
+    const bool dead = mine && !kept && slot_row[my] == kDeadRow;
+    if (dead) {
+      slot_gen[my] = 0;
+      free_stack[atomicAdd(free_top, 1)] = my;
+    }
+    unsigned evict = __ballot_sync(0xffffffffu, mine && !kept && !dead);
     unsigned k0 = 0;
     if (lane == 0 && evict) k0 = atomicAdd(n_wb, unsigned(__popc(evict)));
     k0 = __shfl_sync(0xffffffffu, k0, 0);

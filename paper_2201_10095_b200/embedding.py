@@ -83,7 +83,7 @@ class TieredEmbeddingBag:
 
     def enable_uvm_cache(self, nslots: int):
         """HBM staging of slow-tier rows with side-stream prefetch/write-back
-        (csrc/uvm_cache.cuh); nslots >= 2x the unique slow rows of a batch."""
+        (csrc/uvm_cache.cuh); nslots >= 4x the unique slow rows of a batch (up to four generations are live)."""
         _lib.check(_lib.lib().rs_emb_enable_uvm_cache(self.h, C.c_uint32(nslots)))
 
     def prefetch(self, offsets, indices, batch: int):

@@ -212,11 +212,15 @@ def torch_equal(a, b):
 
 
 def test_uvm_cache_errors(cuda_ctx, coracle):
+    """Out of staging slots: the batch is refused BEFORE its forward runs (no
+    kernel touches an unfilled slot), flush() empties the cache and clears the
+    error, and the operator then runs zero-copy with the oracle's results."""
     import torch
 
     rng = np.random.default_rng(5)
-    specs, remaps, offsets, idx, d_off, d_idx, _ = _setup(coracle, [64], [1000], [0.0], 64, 10, rng)
+    specs, remaps, offsets, idx, d_off, d_idx, Ws = _setup(coracle, [64], [1000], [0.0], 64, 10, rng)
     op = sp.TieredEmbeddingBag(specs, remaps, 64, idx.size, "sgd", ctx=cuda_ctx)
+    op.init_weights(SEED, SCALE)
     with pytest.raises(sp.InvalidArgument):  # prefetch needs the cache
         op.prefetch(d_off, d_idx, 64)
     op.enable_uvm_cache(4)  # far fewer slots than slow rows in the batch
@@ -224,8 +228,14 @@ def test_uvm_cache_errors(cuda_ctx, coracle):
     op.prefetch(d_off, d_idx, 64)  # the next batch and the one after: two live
     with pytest.raises(sp.InvalidArgument):  # a third would be two batches ahead
         op.prefetch(d_off, d_idx, 64)
-    with pytest.raises(sp.InvalidArgument):  # out of slots is reported
+    with pytest.raises(sp.InvalidArgument):  # out of slots: refused before the forward
+        op.forward(d_off, d_idx, 64)
+    with pytest.raises(sp.InvalidArgument):  # flush reports it once, then the cache is clean
         op.flush()
+    op.flush()
+    y = op.forward(d_off, d_idx, 64)  # zero-copy again
+    want = coracle.emb_forward(64, [64], offsets.astype(np.uint64), idx, Ws)
+    assert np.array_equal(y.cpu().numpy(), want)
     torch.cuda.synchronize()
     op.close()
 

@@ -229,3 +229,75 @@ def test_emb_backward_sgd_oracle_matches_autograd(coracle):
     coracle.emb_backward(B, dims, offsets, idx, grad, Wc, None, 0, 0.05, 1e-8)
     for a, b in zip(Wc, ref):
         np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6)
+
+
+# --------------------------------------------------------------- fp64 EmbeddingBag oracle
+def test_emb64_forward_matches_torch_embedding_bag(coracle):
+    """oracle/emb64.py (the independent fp64 oracle of the operator) against
+    torch.nn.functional.embedding_bag(mode="sum") in float64."""
+    torch = pytest.importorskip("torch")
+    from oracle import emb64
+
+    rng = np.random.default_rng(11)
+    dims, H, B = [8, 64, 4], [300, 41, 7], 97
+    Ws = [coracle.init_table(5, t, H[t], d, 0.3) for t, d in enumerate(dims)]
+    lens = rng.integers(0, 9, len(dims) * B)
+    lens[rng.random(lens.size) < 0.1] = 0
+    offsets = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    idx = np.concatenate([rng.integers(0, H[i // B], l) for i, l in enumerate(lens)]).astype(np.uint32)
+    got, gabs = emb64.forward(B, dims, offsets, idx, Ws)
+    col = 0
+    for t, d in enumerate(dims):
+        o = offsets[t * B:(t + 1) * B + 1].astype(np.int64)
+        ref = torch.nn.functional.embedding_bag(
+            torch.from_numpy(idx[o[0]:o[-1]].astype(np.int64)), torch.from_numpy(Ws[t]).double(),
+            torch.from_numpy(o[:-1] - o[0]), mode="sum")
+        np.testing.assert_allclose(got[:, col:col + d], ref.numpy(), rtol=1e-13, atol=1e-15)
+        assert (gabs[:, col:col + d] >= np.abs(got[:, col:col + d]) - 1e-15).all()
+        col += d
+    # the C oracle's fp32 forward is inside the fp64 oracle's bound
+    emb64.check(coracle.emb_forward(B, dims, offsets, idx, Ws), got, emb64.RTOL * gabs + 1e-30, "fwd")
+
+
+@pytest.mark.parametrize("opt", ["sgd", "rowwise_adagrad"])
+def test_emb64_update_matches_autograd_and_adagrad_definition(coracle, opt):
+    """fp64 row gradients = autograd of sum(pooled * grad) (float64); the
+    row-wise update is FBGEMM's (exact row-wise Adagrad: one state per row,
+    mean of squared gradient); the fp32 C oracle (the kernels' reduction
+    tree) lands inside the fp64 bound."""
+    torch = pytest.importorskip("torch")
+    from oracle import emb64
+
+    rng = np.random.default_rng(12)
+    dims, H, B = [16, 8], [60, 25], 120
+    lens = rng.integers(0, 7, len(dims) * B)
+    offsets = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    idx = np.concatenate([np.minimum(rng.zipf(1.3, l) - 1, H[i // B] - 1)
+                          for i, l in enumerate(lens)]).astype(np.uint32)
+    Ws = [coracle.init_table(8, t, H[t], d, 0.5) for t, d in enumerate(dims)]
+    grad = rng.standard_normal((B, sum(dims))).astype(np.float32)
+    lr, eps = 0.3, 1e-8
+    mom = [np.full(h, 0.25, np.float32) for h in H]
+    Wc, Mc = [w.copy() for w in Ws], [m.copy() for m in mom]
+    coracle.emb_backward(B, dims, offsets, idx, grad, Wc, Mc if opt != "sgd" else None,
+                         0 if opt == "sgd" else 1, lr, eps)
+    col = 0
+    for t, d in enumerate(dims):
+        w = torch.tensor(Ws[t], dtype=torch.float64, requires_grad=True)
+        o = offsets[t * B:(t + 1) * B + 1].astype(np.int64)
+        y = torch.nn.functional.embedding_bag(torch.from_numpy(idx[o[0]:o[-1]].astype(np.int64)), w,
+                                              torch.from_numpy(o[:-1] - o[0]), mode="sum")
+        (y * torch.from_numpy(grad[:, col:col + d]).double()).sum().backward()
+        rows, g, ga = emb64.row_grads(B, dims, offsets, idx, grad, t)
+        np.testing.assert_allclose(g, w.grad.numpy()[rows], rtol=1e-13, atol=1e-14)
+        wn, mn, wb, mb = emb64.update(Ws[t][rows], mom[t][rows], g, ga, opt, lr, eps)
+        if opt == "sgd":
+            np.testing.assert_allclose(wn, (w - lr * w.grad).detach().numpy()[rows], rtol=1e-13)
+        else:
+            gg = w.grad.numpy()[rows]
+            m1 = mom[t][rows].astype(np.float64) + (gg * gg).mean(axis=1)
+            np.testing.assert_allclose(mn, m1, rtol=1e-13)
+            np.testing.assert_allclose(wn, Ws[t][rows] - lr * gg / (np.sqrt(m1) + eps)[:, None], rtol=1e-12)
+            emb64.check(Mc[t][rows], mn, mb, "momentum")
+        emb64.check(Wc[t][rows], wn, wb, "weights")
+        col += d
