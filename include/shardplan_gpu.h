@@ -245,6 +245,51 @@ int rs_simulate(rs_context* ctx, const rs_trace* trace, uint32_t num_entries,
                 const rs_remap_view* remaps, const rs_system_spec* system,
                 uint64_t batch_size, rs_sim_report* out);
 
+/* ------------------------------------------------------------- planner (host)
+ * The sharder's cost model and placements (tiny host
+ * work, no GPU): bit-identical plans to the reference's, faster.  Tables are
+ * (TableSpec, FeatureStats) pairs aligned by index — a MilpInstance
+ * (include/shardplan/plan.hpp:37-47) — and `entries` receives one
+ * rs_plan_entry per table in the same order, gpu_cost num_gpus doubles.
+ * Errors: RS_ERR_INVALID_ARGUMENT / RS_ERR_INFEASIBLE with the reference's
+ * messages; the message is rs_plan_last_error(). */
+typedef struct rs_plan_table {
+  rs_table_spec spec;
+  double coverage;              /* FeatureStats.coverage */
+  double avg_pooling;           /* FeatureStats.avg_pooling */
+  const uint64_t* icdf_steps;   /* FeatureStats.icdf_steps, 101 entries */
+} rs_plan_table;
+
+typedef struct rs_plan_summary {
+  double objective;     /* ShardingPlan.objective (max_m gpu_cost) */
+  double lower_bound;   /* ShardingPlan.lower_bound */
+  int proved_optimal;   /* ShardingPlan.proved_optimal */
+} rs_plan_summary;
+
+#define RS_COST_SIZE 0         /* CostKind::kSize          hash_size * dim */
+#define RS_COST_LOOKUP 1       /* CostKind::kLookup        avg_pool * dim */
+#define RS_COST_SIZE_LOOKUP 2  /* CostKind::kSizeAndLookup avg_pool * dim * log10(hash_size) */
+
+const char* rs_plan_last_error(void);
+/* core/src/baselines.cpp:44-67  table_fixed_cost(spec, stats, kind);
+ * avg_pooling may be NULL for RS_COST_SIZE (stats == nullptr). */
+int rs_table_fixed_cost(const rs_table_spec* spec, const double* avg_pooling, int kind, double* out);
+/* core/src/baselines.cpp:136-203  greedy_shard(costs, specs, stats, system) */
+int rs_plan_greedy(uint32_t num_tables, const rs_plan_table* tables, const double* costs,
+                   const rs_system_spec* system, rs_plan_entry* entries, double* gpu_cost,
+                   rs_plan_summary* summary);
+/* core/src/baselines.cpp:205-292  ldm_shard(costs, specs, stats, system) */
+int rs_plan_ldm(uint32_t num_tables, const rs_plan_table* tables, const double* costs,
+                const rs_system_spec* system, rs_plan_entry* entries, double* gpu_cost,
+                rs_plan_summary* summary);
+/* core/src/milp_solve.cpp:633-709  solve(build_instance(stats, specs, system,
+ * ablation, step_count), time_limit_seconds) — INFINITY for the default
+ * budget.  `threads` (0 = all cores) evaluate the local search's candidate
+ * moves; the plan does not depend on it. */
+int rs_plan_solve(uint32_t num_tables, const rs_plan_table* tables, const rs_system_spec* system,
+                  uint32_t step_count, int use_pooling, int use_coverage, double time_limit_seconds,
+                  uint32_t threads, rs_plan_entry* entries, double* gpu_cost, rs_plan_summary* summary);
+
 /* ------------------------------------------------------------- EmbeddingBag
  * The tiered operator that serves a plan (no reference implementation: the
  * paper used FBGEMM; semantics PAPER.md:275 and :605-607).
