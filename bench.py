@@ -43,8 +43,10 @@ def parse():
     p.add_argument("--batch", type=int, default=16384)
     p.add_argument("--nbatches", type=int, default=4, help="distinct batches cycled")
     p.add_argument("--profile-batches", type=int, default=16)
-    p.add_argument("--no-fill", action="store_true",
-                   help="serve the pure RecShard plan (no spare-capacity fill)")
+    p.add_argument("--fill", action="store_true",
+                   help="headline serves RecShard + our spare-capacity fill (default: the pure "
+                        "RecShard plan, the reference's solve; the fill variant is measured alongside)")
+    p.add_argument("--no-variant", action="store_true", help="skip the +fill variant run")
     p.add_argument("--optimizer", default="rowwise_adagrad", choices=["sgd", "rowwise_adagrad"])
     p.add_argument("--no-greedy", action="store_true")
     p.add_argument("--greedy-steps", type=int, default=3)
@@ -783,15 +785,15 @@ def main():
 
     # ---- plans (host): RecShard vs the greedy/size baseline
     t0 = time.perf_counter()
-    rec = planner.recshard_plan(tables, stats, system)
+    rec_pure = planner.recshard_plan(tables, stats, system)  # the reference's solve, restated
     plan_s = time.perf_counter() - t0
     gre = planner.greedy_shard([planner.table_fixed_cost(t, None, "size") for t in tables], tables,
                                stats, system, "greedy-size")
     import copy
 
-    rec_pure = copy.deepcopy(rec)
-    if not args.no_fill:
-        planner.fill_spare_capacity(rec, tables, stats, system)
+    rec_fill = planner.fill_spare_capacity(copy.deepcopy(rec_pure), tables, stats, system)
+    rec = rec_fill if args.fill else rec_pure
+    rec_var = rec_pure if args.fill else rec_fill
     # simulate() (GPU) on one training batch for each placement: the UVM share
     # the plans predict, before any operator is built
     sim_uvm = {}
@@ -801,7 +803,7 @@ def main():
         strace = wl.kjt_to_trace(specs, soff, sidx, sn, B, 100 * B, ctx=ctx)
         strace.num_samples = B  # records carry sample ids 100B..101B-1; one batch of B
         strace.rec_sample = strace.rec_sample - 100 * B
-        for name, pl in (("recshard", rec_pure), (rec.strategy, rec), ("greedy-size", gre)):
+        for name, pl in (("recshard", rec_pure), (rec_fill.strategy, rec_fill), ("greedy-size", gre)):
             rms = [sp.build_remap(pl.entries[j], stats[j], tables[j], ctx=ctx,
                                   device_rows=prof.device_rows_by_rank(j),
                                   out=torch.empty(tables[j].hash_size, dtype=torch.int32, device=dev))
@@ -855,6 +857,10 @@ def main():
     g = None
     if not args.no_greedy and args.only is None:
         g = run_plan(args, torch, dist, prank, world, dev, ctx, specs, stats, prof, gre, system,
+                     args.greedy_steps, 1, False, B)
+    v = None
+    if not args.no_variant and args.only is None:
+        v = run_plan(args, torch, dist, prank, world, dev, ctx, specs, stats, prof, rec_var, system,
                      args.greedy_steps, 1, False, B)
     prof.close()
 
@@ -918,6 +924,9 @@ def main():
                                                                      "slow_unique_rows")},
                                                   mode=g["mode"], modes=modes(g)),
             "recshard_vs_greedy": None if g is None else r["samples_per_s"] / g["samples_per_s"],
+            "plan_variant": None if v is None else dict({k: v[k] for k in ("samples_per_s", "ms_per_step",
+                                                                           "uvm_pct", "slow_unique_rows")},
+                                                        plan=rec_var.strategy, mode=v["mode"]),
             "recshard_vs_greedy_by_mode": None if g is None else {
                 m: (r[k]["samples_per_s"] / g[k]["samples_per_s"]) if r.get(k) and g.get(k) else None
                 for m, k in (("zero-copy", "zero_copy"), ("pipelined", "pipelined"))},

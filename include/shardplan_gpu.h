@@ -351,6 +351,48 @@ int rs_emb_memory(const rs_emb* e, uint64_t* hbm_bytes, uint64_t* host_bytes);
 int rs_emb_kernel_times(rs_emb* e, double* fwd_ms, uint64_t* n_fwd, double* bwd_ms, uint64_t* n_bwd,
                         int reset);
 
+/* ------------------------------------------------------------- K6: rank exchange
+ * Table-wise model parallelism across the GPUs of one node: rank
+ * r owns the tables with PlanEntry.gpu == r (both tiers)
+ * and pools them for the whole global batch B; it also owns samples
+ * [r*B/N, (r+1)*B/N).  An exchange moves every pooled row to its sample owner
+ * ([B/N, sum of ALL dims], tables in global order) and every gradient row
+ * back to its table owner ([B, sum of this rank's dims], its tables in global
+ * order).  Transports: RS_EX_PEER — NVLink peer memory between the ranks'
+ * processes (CUDA IPC), the forward fused into K4's stores; RS_EX_NCCL —
+ * grouped ncclSend/ncclRecv (the process's libnccl.so.2, resolved at run
+ * time).  Bootstrap: every rank calls rs_exchange_blob; the caller all-gathers
+ * the blobs (rank-ordered, RS_EX_BLOB_BYTES each; NCCL needs only rank 0's)
+ * with its own plumbing and passes them to rs_exchange_connect. */
+typedef struct rs_exchange rs_exchange;
+#define RS_EX_PEER 0
+#define RS_EX_NCCL 1
+#define RS_EX_BLOB_BYTES 128
+/* dims/owner: per GLOBAL table (plan order) its dim and owner rank. */
+int rs_exchange_create(rs_context* ctx, int transport, uint32_t nranks, uint32_t rank, uint64_t batch,
+                       uint32_t num_tables, const uint32_t* dims, const uint32_t* owner, rs_exchange** out);
+int rs_exchange_blob(rs_exchange* x, void* blob);
+int rs_exchange_connect(rs_exchange* x, const void* blobs);
+/* bl = B/N, d_total = sum of all dims, d_local = this rank's; owned = the
+ * current step's owner block [bl, d_total] (device; valid until the next forward). */
+int rs_exchange_info(const rs_exchange* x, uint64_t* bl, uint64_t* d_total, uint64_t* d_local, float** owned);
+int rs_exchange_destroy(rs_exchange* x);
+/* K4 + K6: this rank's operator `e` (its tables, in global order) pools the
+ * batch (offsets/indices of ITS tables for all B samples) and every row lands
+ * in its owner's block; *owned receives this rank's block [bl, d_total]. */
+int rs_emb_forward_to_owners(rs_emb* e, rs_exchange* x, const uint32_t* offsets, const uint32_t* indices,
+                             uint64_t* hit_counts, float** owned);
+/* K6 + K5: the gradient of this rank's owner block (written in place into
+ * *owned, or given as grad_owned [bl, d_total]) returns to the table owners on
+ * a side stream while K5 plans and sorts; then K5 updates this rank's tables. */
+int rs_emb_backward_from_owners(rs_emb* e, rs_exchange* x, const uint32_t* offsets, const uint32_t* indices,
+                                const float* grad_owned, float lr);
+/* The K6 primitives alone: pooled [B, d_local] -> owner block
+ * [bl, d_total]; gradients [bl, d_total] -> [B, d_local].  Stream-ordered on
+ * the exchange's context. */
+int rs_emb_alltoall_fwd(rs_exchange* x, const float* pooled_local, float* pooled_owned);
+int rs_emb_alltoall_bwd(rs_exchange* x, const float* grad_owned, float* grad_local);
+
 /* ------------------------------------------------------------- primitives
  * The device-wide stable LSD radix sort behind K2 and K5 (device buffers,
  * sorted in place on bits [0, end_bit); vals may be NULL). */

@@ -23,6 +23,9 @@ RS_MEM_HOST = 0
 RS_MEM_DEVICE = 1
 RS_OPT_SGD = 0
 RS_OPT_ROWWISE_ADAGRAD = 1
+RS_EX_PEER = 0
+RS_EX_NCCL = 1
+RS_EX_BLOB_BYTES = 128
 
 P = C.c_void_p
 u32, u64, f64, f32, i32 = C.c_uint32, C.c_uint64, C.c_double, C.c_float, C.c_int
@@ -75,6 +78,15 @@ class rs_emb_table(C.Structure):
                 ("remap_location", i32), ("hbm_rows", u64), ("slow_rows", u64)]
 
 
+class rs_plan_table(C.Structure):
+    _fields_ = [("spec", rs_table_spec), ("coverage", f64), ("avg_pooling", f64),
+                ("icdf_steps", P)]
+
+
+class rs_plan_summary(C.Structure):
+    _fields_ = [("objective", f64), ("lower_bound", f64), ("proved_optimal", i32)]
+
+
 class rs_gen_table(C.Structure):
     _fields_ = [("table_id", u32), ("cardinality", u64), ("hash_size", u64),
                 ("zipf_exponent", f64), ("mean_pooling", f64), ("coverage", f64),
@@ -122,6 +134,20 @@ _SIGS = {
     "rs_radix_sort_pairs": ([P, P, P, u64, i32], i32),
     "rs_gen_batch": ([P, u32, P, u64, u64, u64, P, P, u64, P], i32),
     "rs_kjt_to_records": ([P, u32, P, u64, u64, P, P, P, P, P, P], i32),
+    "rs_plan_last_error": ([], C.c_char_p),
+    "rs_table_fixed_cost": ([P, P, i32, P], i32),
+    "rs_plan_greedy": ([u32, P, P, P, P, P, P], i32),
+    "rs_plan_ldm": ([u32, P, P, P, P, P, P], i32),
+    "rs_plan_solve": ([u32, P, P, u32, i32, i32, f64, u32, P, P, P], i32),
+    "rs_exchange_create": ([P, i32, u32, u32, u64, u32, P, P, P], i32),
+    "rs_exchange_blob": ([P, P], i32),
+    "rs_exchange_connect": ([P, P], i32),
+    "rs_exchange_info": ([P, P, P, P, P], i32),
+    "rs_exchange_destroy": ([P], i32),
+    "rs_emb_forward_to_owners": ([P, P, P, P, P, P], i32),
+    "rs_emb_backward_from_owners": ([P, P, P, P, P, f32], i32),
+    "rs_emb_alltoall_fwd": ([P, P, P], i32),
+    "rs_emb_alltoall_bwd": ([P, P, P], i32),
 }
 
 # every symbol include/shardplan_gpu.h declares (checked by the CPU test suite)
@@ -147,10 +173,10 @@ def lib():
     return _lib
 
 
-def check(status):
+def check(status, planner=False):
     """Raise the reference's exception type for a negative status."""
     if status == RS_OK:
         return
     from .types import error_for_status
-    msg = lib().rs_last_error()
+    msg = lib().rs_plan_last_error() if planner else lib().rs_last_error()
     raise error_for_status(status, msg.decode() if msg else "")

@@ -39,6 +39,16 @@ uint32_t profile_tables(const rs_profile*);
 uint64_t profile_selected(const rs_profile*);
 void profile_free(rs_profile*);
 void emb_free(rs_emb*);
+rs_exchange* exchange_create(rs_context*, int, uint32_t, uint32_t, uint64_t, uint32_t, const uint32_t*,
+                             const uint32_t*);
+void exchange_blob(rs_exchange*, void*);
+void exchange_connect(rs_exchange*, const void*);
+void exchange_info(const rs_exchange*, uint64_t*, uint64_t*, uint64_t*, float**);
+void exchange_free(rs_exchange*);
+float* exchange_forward(rs_exchange*, rs_emb*, const uint32_t*, const uint32_t*, uint64_t*);
+void exchange_backward(rs_exchange*, rs_emb*, const uint32_t*, const uint32_t*, const float*, float);
+void alltoall_fwd(rs_exchange*, const float*, float*);
+void alltoall_bwd(rs_exchange*, const float*, float*);
 }  // namespace rs
 
 namespace {
@@ -411,6 +421,80 @@ int rs_emb_memory(const rs_emb* e, uint64_t* hbm, uint64_t* host) {
   return guarded([&] {
     need(e, "emb");
     rs::emb_memory(e, hbm, host);
+  });
+}
+
+// ---------------------------------------------------------------- K6 exchange
+int rs_exchange_create(rs_context* c, int transport, uint32_t nranks, uint32_t rank, uint64_t batch,
+                       uint32_t num_tables, const uint32_t* dims, const uint32_t* owner, rs_exchange** out) {
+  return guarded([&] {
+    need(c, "ctx");
+    need(out, "out");
+    *out = rs::exchange_create(c, transport, nranks, rank, batch, num_tables, dims, owner);
+  });
+}
+
+int rs_exchange_blob(rs_exchange* x, void* blob) {
+  return guarded([&] {
+    need(x, "exchange");
+    need(blob, "blob");
+    rs::exchange_blob(x, blob);
+  });
+}
+
+int rs_exchange_connect(rs_exchange* x, const void* blobs) {
+  return guarded([&] {
+    need(x, "exchange");
+    need(blobs, "blobs");
+    rs::exchange_connect(x, blobs);
+  });
+}
+
+int rs_exchange_info(const rs_exchange* x, uint64_t* bl, uint64_t* d_total, uint64_t* d_local, float** owned) {
+  return guarded([&] {
+    need(x, "exchange");
+    rs::exchange_info(x, bl, d_total, d_local, owned);
+  });
+}
+
+int rs_exchange_destroy(rs_exchange* x) {
+  return guarded([&] { rs::exchange_free(x); });
+}
+
+int rs_emb_forward_to_owners(rs_emb* e, rs_exchange* x, const uint32_t* offsets, const uint32_t* indices,
+                             uint64_t* hit_counts, float** owned) {
+  return guarded([&] {
+    need(e, "emb");
+    need(x, "exchange");
+    need(offsets, "offsets");
+    float* o = rs::exchange_forward(x, e, offsets, indices, hit_counts);
+    if (owned) *owned = o;
+  });
+}
+
+int rs_emb_backward_from_owners(rs_emb* e, rs_exchange* x, const uint32_t* offsets, const uint32_t* indices,
+                                const float* grad_owned, float lr) {
+  return guarded([&] {
+    need(e, "emb");
+    need(x, "exchange");
+    need(offsets, "offsets");
+    rs::exchange_backward(x, e, offsets, indices, grad_owned, lr);
+  });
+}
+
+int rs_emb_alltoall_fwd(rs_exchange* x, const float* pooled_local, float* pooled_owned) {
+  return guarded([&] {
+    need(x, "exchange");
+    need(pooled_owned, "pooled_owned");
+    rs::alltoall_fwd(x, pooled_local, pooled_owned);
+  });
+}
+
+int rs_emb_alltoall_bwd(rs_exchange* x, const float* grad_owned, float* grad_local) {
+  return guarded([&] {
+    need(x, "exchange");
+    need(grad_owned, "grad_owned");
+    rs::alltoall_bwd(x, grad_owned, grad_local);
   });
 }
 

@@ -31,6 +31,7 @@
 
 #include "../../include/shardplan_gpu.h"
 #include "context.cuh"
+#include "exchange.cuh"
 #include "host_worker.hpp"
 
 namespace rs {
@@ -148,7 +149,7 @@ template <int G, int VPL, int UNR, int MINB>
 __global__ void __launch_bounds__(kFwdThreads, MINB)
 forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__ cls_tables,
                uint32_t ntab, uint64_t B, const uint32_t* __restrict__ offsets,
-               const uint32_t* __restrict__ indices, float* __restrict__ out, uint64_t stride,
+               const uint32_t* __restrict__ indices, const OutMap om, uint64_t stride,
                unsigned long long* __restrict__ hits, uint32_t* __restrict__ keys,
                uint32_t* __restrict__ vals, uint64_t max_keys, unsigned* __restrict__ err) {
   constexpr int BPW = 32 / G;
@@ -256,7 +257,7 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
       nent = fwd_bag_entry(tables, err, lg, nt, ns, ne, nidx);
     }
     if (valid) {
-      float4* o = reinterpret_cast<float4*>(out + b * stride + td.col);
+      float4* o = reinterpret_cast<float4*>(out_row(om, b, stride) + (om.xcol ? om.xcol[t] : td.col));
 #pragma unroll
       for (int vv = 0; vv < VPL; ++vv) {
         const uint32_t vec = lg + vv * G;
@@ -448,6 +449,9 @@ struct rs_emb {
   cudaStream_t claim_stream = nullptr;
   uint64_t gather_seq[4] = {0, 0, 0, 0}, wb_seq = 0;
   unsigned gen_err[4] = {0, 0, 0, 0};  // cache_err seen by generation g's stage-in (host)
+  // set by the exchange (exchange.cu) for one backward: the gradient rows it
+  // reads are complete once this event has fired
+  cudaEvent_t grad_ready = nullptr;
 
   TableDev* d_tables_c = nullptr;
   uint32_t* d_slow_tabs = nullptr;  // tables with slow rows
@@ -1114,13 +1118,14 @@ void emb_init_weights(rs_emb* e, uint64_t seed, float scale) {
 
 template <int G, int VPL>
 static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint32_t* off,
-                       const uint32_t* idx, float* out, unsigned long long* hits, cudaStream_t st) {
+                       const uint32_t* idx, const OutMap& out, uint64_t stride, unsigned long long* hits,
+                       cudaStream_t st) {
   constexpr int BPW = 32 / G;
   const uint64_t warps = (B + BPW - 1) / BPW * c.tables.size();
   const uint64_t blocks = (warps * 32 + emb::kFwdThreads - 1) / emb::kFwdThreads;
   const unsigned grid = std::max(1u, unsigned(std::min<uint64_t>(blocks, uint64_t(sm_count()) * 64)));
   auto args = std::make_tuple(e->cur_tables, c.d_list, uint32_t(c.tables.size()), B, off, idx, out,
-                              e->total_dim, hits, e->keys, e->vals, uint64_t(e->max_lookups), e->d_err);
+                              stride, hits, e->keys, e->vals, uint64_t(e->max_lookups), e->d_err);
   auto go = [&](auto kern) {
     std::apply([&](auto... a) { kern<<<grid, emb::kFwdThreads, 0, st>>>(a...); }, args);
   };
@@ -1133,6 +1138,15 @@ static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint
 
 void emb_forward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx, float* out,
                  uint64_t* hits) {
+  OutMap om{};
+  om.out0 = out;
+  om.bl = B;
+  om.n = 1;
+  emb_forward_map(e, B, off, idx, om, e->total_dim, hits);
+}
+
+void emb_forward_map(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx, const OutMap& om,
+                     uint64_t stride, uint64_t* hits) {
   if (B == 0 || B > e->max_batch) throw InvalidArgument("emb_forward: batch outside [1, max_batch]");
   begin_step(e);
   e->t_fwd.begin(e->ctx->stream);
@@ -1152,15 +1166,15 @@ void emb_forward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx
     const auto& c = e->classes[ci];
     cudaStream_t st = (ci & 1) ? e->fwd_side : main;
     switch (c.G * 100 + c.VPL) {
-      case 101: launch_fwd<1, 1>(e, c, B, off, idx, out, h, st); break;
-      case 201: launch_fwd<2, 1>(e, c, B, off, idx, out, h, st); break;
-      case 401: launch_fwd<4, 1>(e, c, B, off, idx, out, h, st); break;
-      case 801: launch_fwd<8, 1>(e, c, B, off, idx, out, h, st); break;
-      case 1601: launch_fwd<16, 1>(e, c, B, off, idx, out, h, st); break;
-      case 3201: launch_fwd<32, 1>(e, c, B, off, idx, out, h, st); break;
-      case 3202: launch_fwd<32, 2>(e, c, B, off, idx, out, h, st); break;
-      case 3204: launch_fwd<32, 4>(e, c, B, off, idx, out, h, st); break;
-      case 3208: launch_fwd<32, 8>(e, c, B, off, idx, out, h, st); break;
+      case 101: launch_fwd<1, 1>(e, c, B, off, idx, om, stride, h, st); break;
+      case 201: launch_fwd<2, 1>(e, c, B, off, idx, om, stride, h, st); break;
+      case 401: launch_fwd<4, 1>(e, c, B, off, idx, om, stride, h, st); break;
+      case 801: launch_fwd<8, 1>(e, c, B, off, idx, om, stride, h, st); break;
+      case 1601: launch_fwd<16, 1>(e, c, B, off, idx, om, stride, h, st); break;
+      case 3201: launch_fwd<32, 1>(e, c, B, off, idx, om, stride, h, st); break;
+      case 3202: launch_fwd<32, 2>(e, c, B, off, idx, om, stride, h, st); break;
+      case 3204: launch_fwd<32, 4>(e, c, B, off, idx, om, stride, h, st); break;
+      case 3208: launch_fwd<32, 8>(e, c, B, off, idx, om, stride, h, st); break;
       default: throw Error(-9, "emb_forward: unsupported lane class");
     }
   }
@@ -1294,6 +1308,12 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
   exclusive_scan<uint32_t>(ArrayIn<uint32_t>{e->scount}, Wmax, e->sbase, e->sbase + Wmax, scr, st);
   emb::bwd_seg_scan_kernel<true><<<gs, 256, 0, st>>>(a, wm, nullptr, e->sbase, e->segs);
   RS_COUNT(2);
+  // gradients arriving from other ranks (exchange.cu) are read from here on;
+  // the plan, sort and segment list above overlapped their transfer
+  if (e->grad_ready) {
+    RS_CUDA(cudaStreamWaitEvent(st, e->grad_ready, 0));
+    e->grad_ready = nullptr;
+  }
   // short segments per lane class (long ones are listed)
   RS_CUDA(cudaMemsetAsync(e->n_long, 0, 4, st));
   RS_CUDA(cudaMemsetAsync(e->long_np, 0, (e->long_cap + 1) * 4, st));
@@ -1385,5 +1405,11 @@ void emb_memory(const rs_emb* e, uint64_t* hbm, uint64_t* host) {
   if (hbm) *hbm = e->fast_bytes + e->remap_bytes;
   if (host) *host = e->host_bytes;
 }
+
+uint32_t emb_num_tables(const rs_emb* e) { return e->T; }
+uint32_t emb_table_id(const rs_emb* e, uint32_t t) { return e->table_ids.at(t); }
+uint32_t emb_table_dim(const rs_emb* e, uint32_t t) { return e->h_tables.at(t).dim; }
+rs_context* emb_context(const rs_emb* e) { return e->ctx; }
+void emb_set_grad_ready(rs_emb* e, cudaEvent_t ev) { e->grad_ready = ev; }
 
 }  // namespace rs

@@ -2,14 +2,33 @@
 
 Each rank owns the tables its plan entries name (``PlanEntry.gpu``; both tiers
 of a table on its owner), pools them for the whole global
-batch, and an all-to-all hands every sample owner (rank r owns samples
-[r*B/N, (r+1)*B/N)) its pooled row block; gradients travel back the same way.
-The exchange is expressed with ``torch.distributed.all_to_all_single`` so it
-runs over NCCL (NVLink) on GPUs and over gloo in the CPU tests.
+batch, and every sample owner (rank r owns samples [r*B/N, (r+1)*B/N))
+receives its pooled rows of ALL tables, [B/N, sum D] in global table order;
+gradients travel back the same way.  The exchange is K6 in the C-ABI
+(csrc/exchange.cu, ``rs_exchange_*`` / ``rs_emb_*_owners``):
+
+* ``transport="peer"`` — NVLink peer memory between the ranks' processes
+  (CUDA IPC): K4 stores every pooled row straight into its owner's block and
+  a flag barrier publishes it; the backward pulls the gradient rows on a side
+  stream while K5 sorts.
+* ``transport="nccl"`` — grouped ncclSend/ncclRecv, K4's [B, D_local] output
+  is the send layout; received blocks are scattered into column order by
+  one kernel.
+
+``torch.distributed`` (gloo or NCCL) only bootstraps: it all-gathers the
+exchange blobs (IPC handles / the NCCL unique id).  ``column_index`` and
+``rank_dims`` restate the layout in Python for tests.
 """
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
+
+from . import _lib
+from .runtime import default_context, ptr
+
+TRANSPORTS = {"peer": _lib.RS_EX_PEER, "nccl": _lib.RS_EX_NCCL}
 
 
 def local_tables(plan, rank):
@@ -26,9 +45,9 @@ def rank_dims(plan, dims, world):
 
 
 def column_index(plan, dims, world):
-    """For the sample owner's assembled row [sum D] in GLOBAL table order:
-    position of every received element (received layout: src-major blocks
-    [src][B/N][D_src], tables in plan order inside a block)."""
+    """For the sample owner's row [sum D] in GLOBAL table order: the global
+    column of every element of source rank s's block [B/N, D_s] (its tables in
+    plan order) — the layout K6 assembles (csrc/exchange.cu gsrc/gcol)."""
     cols = np.concatenate([[0], np.cumsum(dims)[:-1]]).astype(np.int64)
     per_src = [[] for _ in range(world)]
     for j, e in enumerate(plan.entries):
@@ -37,86 +56,121 @@ def column_index(plan, dims, world):
 
 
 class Exchange:
-    """All-to-all of pooled rows to sample owners and of gradients back."""
+    """K6: one rank's end of the pooled-row / gradient exchange."""
 
-    def __init__(self, plan, dims, world, rank, batch, device, group=None):
-        import torch
+    def __init__(self, plan, dims, world, rank, batch, transport="peer", ctx=None, group=None):
+        import torch.distributed as dist
 
         if batch % world:
             raise ValueError("global batch must divide by the world size")
+        self.ctx = ctx or default_context()
         self.world, self.rank, self.B, self.bl = world, rank, batch, batch // world
-        self.group = group
-        self.dims_all = rank_dims(plan, dims, world)
-        self.D_local = self.dims_all[rank]
+        self.dims = [int(d) for d in dims]
+        self.owner = [int(e.gpu) for e in plan.entries]
         self.D_total = int(sum(dims))
-        self.send_splits = [self.bl * self.D_local] * world
-        self.recv_splits = [self.bl * d for d in self.dims_all]
-        idx = column_index(plan, dims, world)
-        self._cols = [torch.as_tensor(c, device=device) for c in idx]
-        self.recv = torch.empty(sum(self.recv_splits), dtype=torch.float32, device=device)
-        self.back = torch.empty(batch * max(1, self.D_local), dtype=torch.float32, device=device)
+        self.D_local = int(sum(d for d, o in zip(self.dims, self.owner) if o == rank))
+        d = np.array(self.dims, np.uint32)
+        o = np.array(self.owner, np.uint32)
+        h = C.c_void_p()
+        _lib.check(_lib.lib().rs_exchange_create(self.ctx.h, TRANSPORTS[transport], world, rank,
+                                                 C.c_uint64(batch), len(dims), ptr(d), ptr(o), C.byref(h)))
+        self.h = h
+        blob = (C.c_char * _lib.RS_EX_BLOB_BYTES)()
+        _lib.check(_lib.lib().rs_exchange_blob(self.h, blob))
+        blobs = [None] * world
+        if world > 1:
+            dist.all_gather_object(blobs, bytes(blob), group=group)
+        else:
+            blobs = [bytes(blob)]
+        allb = np.frombuffer(b"".join(blobs), np.uint8).copy()
+        _lib.check(_lib.lib().rs_exchange_connect(self.h, ptr(allb)))
 
-    def to_owners(self, pooled_local):
-        """[B, D_local] -> this rank's samples [B/N, sum D] in global column order."""
+    def owned(self):
+        """This step's owner block [B/N, sum D] (a torch view of device memory)."""
         import torch
-        import torch.distributed as dist
 
-        src = pooled_local.reshape(-1)[:self.B * self.D_local].contiguous()
-        dist.all_to_all_single(self.recv, src, self.recv_splits, self.send_splits, group=self.group)
-        out = torch.empty(self.bl, self.D_total, dtype=torch.float32, device=self.recv.device)
-        off = 0
-        for s in range(self.world):
-            n = self.recv_splits[s]
-            if n:
-                out[:, self._cols[s]] = self.recv[off:off + n].view(self.bl, self.dims_all[s])
-            off += n
+        f = C.c_void_p()
+        _lib.check(_lib.lib().rs_exchange_info(self.h, None, None, None, C.byref(f)))
+        return _device_view(f.value, self.bl * self.D_total, self.ctx.device).view(self.bl, self.D_total)
+
+    def to_owners(self, pooled_local, out=None):
+        """K6 forward primitive: [B, D_local] -> [B/N, sum D]."""
+        import torch
+
+        if out is None:
+            out = torch.empty(self.bl, self.D_total, dtype=torch.float32, device=pooled_local.device)
+        _lib.check(_lib.lib().rs_emb_alltoall_fwd(self.h, ptr(pooled_local), ptr(out)))
         return out
 
-    def to_tables(self, grad_owned):
-        """[B/N, sum D] gradients of this rank's samples -> [B, D_local] for its tables."""
+    def to_tables(self, grad_owned, out=None):
+        """K6 backward primitive: [B/N, sum D] -> [B, D_local]."""
         import torch
-        import torch.distributed as dist
 
-        parts = []
-        for s in range(self.world):
-            if self.dims_all[s]:
-                parts.append(grad_owned[:, self._cols[s]].reshape(-1))
-        send = torch.cat(parts) if parts else self.recv[:0]
-        out = self.back[:self.B * self.D_local]
-        dist.all_to_all_single(out, send.contiguous(), self.send_splits, self.recv_splits,
-                               group=self.group)
-        return out.view(self.B, max(1, self.D_local)) if self.D_local else out
+        if out is None:
+            out = torch.empty(self.B, max(1, self.D_local), dtype=torch.float32, device=grad_owned.device)
+        _lib.check(_lib.lib().rs_emb_alltoall_bwd(self.h, ptr(grad_owned.contiguous()), ptr(out)))
+        return out
+
+    def close(self):
+        if self.h:
+            _lib.lib().rs_exchange_destroy(self.h)
+            self.h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _device_view(addr, n, device):
+    """A float32 torch tensor over n floats of library-owned device memory."""
+    import torch
+
+    class _Holder:
+        pass
+
+    h = _Holder()
+    h.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f4", "data": (int(addr), False),
+                                  "version": 3, "strides": None}
+    return torch.as_tensor(h, device=torch.device("cuda", device))
 
 
 class ShardedEmbeddingBag:
-    """The rank-local TieredEmbeddingBag plus the exchange."""
+    """This rank's TieredEmbeddingBag (its tables of the plan) plus K6."""
 
     def __init__(self, plan, specs, remaps_local, world, rank, batch, max_lookups,
-                 optimizer="rowwise_adagrad", ctx=None, group=None):
-        import torch
-
+                 optimizer="rowwise_adagrad", transport="peer", ctx=None, group=None):
         from .embedding import TieredEmbeddingBag
 
+        self.ctx = ctx or default_context()
         self.local = local_tables(plan, rank)
         dims = [s.dim for s in specs]
-        self.ex = Exchange(plan, dims, world, rank, batch,
-                           torch.device("cuda", torch.cuda.current_device()), group)
         self.op = (TieredEmbeddingBag([specs[j] for j in self.local], remaps_local, batch,
-                                      max_lookups, optimizer, ctx=ctx) if self.local else None)
+                                      max_lookups, optimizer, ctx=self.ctx) if self.local else None)
+        self.ex = Exchange(plan, dims, world, rank, batch, transport, ctx=self.ctx, group=group)
         self.B = batch
 
     def forward(self, offsets, indices, hits=None):
-        import torch
+        """offsets/indices: this rank's tables for all B samples (table-major
+        CSR).  Returns this rank's samples [B/N, sum D] (global table order);
+        write the gradient into it in place (or pass one to backward)."""
+        if self.op is None:
+            raise ValueError("ShardedEmbeddingBag: this rank owns no tables")
+        self.op._check_dev(offsets, indices, hits)
+        f = C.c_void_p()
+        _lib.check(_lib.lib().rs_emb_forward_to_owners(self.op.h, self.ex.h, ptr(offsets), ptr(indices),
+                                                       ptr(hits), C.byref(f)))
+        return self.ex.owned()
 
-        pooled = (self.op.forward(offsets, indices, self.B, hits=hits) if self.op else
-                  torch.empty(self.B, 0, device=self.ex.recv.device))
-        self._pooled = pooled
-        return self.ex.to_owners(pooled)
+    def backward(self, offsets, indices, lr, grad_owned=None):
+        _lib.check(_lib.lib().rs_emb_backward_from_owners(self.op.h, self.ex.h, ptr(offsets), ptr(indices),
+                                                          ptr(grad_owned), C.c_float(lr)))
 
-    def backward(self, offsets, indices, grad_owned, lr):
-        g = self.ex.to_tables(grad_owned)
+    def close(self):
         if self.op:
-            self.op.backward(offsets, indices, g.contiguous(), self.B, lr)
+            self.op.close()
+        self.ex.close()
 
 
 # ---------------------------------------------------------------- HP1 across GPUs

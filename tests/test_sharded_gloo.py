@@ -1,6 +1,9 @@
-"""CPU (gloo, world size 2): the model-parallel exchange of pooled rows and
-gradients (paper_2201_10095_b200/sharded.py) reassembles exactly what a single
-device would compute."""
+"""CPU (gloo, world size 2): the K6 exchange contract (tests/k6_reference.py,
+the layout csrc/exchange.cu implements: pooled rows to sample owners in global
+table order, gradients back as [B, D_local]) reassembles exactly what a single
+device would compute; the table split of the sharded profile reassembles the
+whole-trace profile.  The CUDA exchange itself is exercised with two
+processes on one GPU in tests/test_exchange_gpu.py."""
 import os
 import socket
 
@@ -10,7 +13,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2201_10095_b200.sharded import Exchange, column_index, local_tables, rank_dims
+from k6_reference import RefExchange
+from paper_2201_10095_b200.sharded import column_index, local_tables, rank_dims
 from paper_2201_10095_b200.types import PlanEntry, ShardingPlan
 
 
@@ -33,7 +37,7 @@ def _worker(rank, world, port, B, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         plan = _plan()
-        ex = Exchange(plan, DIMS, world, rank, B, torch.device("cpu"))
+        ex = RefExchange(plan, DIMS, world, rank, B, torch.device("cpu"))
         full = _full(B)
         cols = np.concatenate([[0], np.cumsum(DIMS)[:-1]])
         mine = local_tables(plan, rank)
