@@ -43,10 +43,11 @@ def parse():
     p.add_argument("--batch", type=int, default=16384)
     p.add_argument("--nbatches", type=int, default=4, help="distinct batches cycled")
     p.add_argument("--profile-batches", type=int, default=16)
-    p.add_argument("--fill", action="store_true",
-                   help="headline serves RecShard + our spare-capacity fill (default: the pure "
-                        "RecShard plan, the reference's solve; the fill variant is measured alongside)")
-    p.add_argument("--no-variant", action="store_true", help="skip the +fill variant run")
+    p.add_argument("--pure", action="store_true",
+                   help="headline serves the pure RecShard plan (the reference's solve, whose "
+                        "1%%-of-accesses ICDF steps leave HBM unused); default: that plan + the "
+                        "row-granular spare-capacity fill. The other one is measured alongside")
+    p.add_argument("--no-variant", action="store_true", help="skip the alternate-plan run")
     p.add_argument("--optimizer", default="rowwise_adagrad", choices=["sgd", "rowwise_adagrad"])
     p.add_argument("--no-greedy", action="store_true")
     p.add_argument("--greedy-steps", type=int, default=3)
@@ -555,13 +556,36 @@ def run_profile_sweep(args, torch, ctx, hbm_peak):
                                    w.table.dim, w.table.elem_bytes) for w in specs],
                       int(sub[0].max()) + 1, *sub, ids_h)
         cs = Rf.time_profile(rt, 1.0, PROFILE_SEED)
+        # parity on the same prefix: GPU profile() vs the reference's, every
+        # FeatureStats field bit-exact (doubles compared as raw bits)
+        want = Rf.profile(rt, 1.0, PROFILE_SEED)
         Rf.free_trace(rt)
+        ptr = sp.Trace([w.table for w in specs], int(sub[0].max()) + 1, *sub, ids=ids_h)
+        got = sp.profile(ptr, 1.0, PROFILE_SEED, ctx=ctx)
         out["cpu_reference"] = {"ids_per_s": last / cs, "cores": 1, "kind": "reference",
                                 "sample": f"first {m} records ({last} ids) of the same trace, "
-                                          "unmodified shardplan::profile (single-threaded)"}
+                                          "unmodified shardplan::profile (single-threaded)",
+                                "bit_exact": stats_equal(got, want)}
     del tr, idx, off
     torch.cuda.empty_cache()
     return out
+
+
+def stats_equal(got, want):
+    """GPU FeatureStats list == the reference's (oracle.Ref dicts), bit for bit."""
+    if len(got) != len(want):
+        return False
+    for g, w in zip(got, want):
+        if (g.table_id != w["table_id"] or g.total_accesses != w["total_accesses"]
+                or g.distinct_rows_accessed != w["distinct_rows_accessed"]
+                or np.float64(g.coverage).view(np.uint64) != np.float64(w["coverage"]).view(np.uint64)
+                or np.float64(g.avg_pooling).view(np.uint64) != np.float64(w["avg_pooling"]).view(np.uint64)
+                or not np.array_equal(np.asarray(g.icdf_steps, np.uint64), w["icdf_steps"])
+                or not np.array_equal(np.asarray(g.rows_by_rank, np.uint32), w["rows_by_rank"])
+                or not np.array_equal(np.asarray(g.access_cdf, np.float64).view(np.uint64),
+                                      w["access_cdf"].view(np.uint64))):
+            return False
+    return True
 
 
 def run_profile_sweep_sharded(args, torch, dist, ctx, world, rank):
@@ -792,8 +816,8 @@ def main():
     import copy
 
     rec_fill = planner.fill_spare_capacity(copy.deepcopy(rec_pure), tables, stats, system)
-    rec = rec_fill if args.fill else rec_pure
-    rec_var = rec_pure if args.fill else rec_fill
+    rec = rec_pure if args.pure else rec_fill
+    rec_var = rec_fill if args.pure else rec_pure
     # simulate() (GPU) on one training batch for each placement: the UVM share
     # the plans predict, before any operator is built
     sim_uvm = {}
@@ -910,6 +934,11 @@ def main():
                                   f"one shard (rank {prank}) of a table-wise mp{M} plan, no all-to-all"
                                   if emulate else f"table-wise mp{world}"),
             "uvm_access_pct": r["uvm_pct"],
+            "parity": {
+                "profile_prefix_vs_reference": (sweep or {}).get("cpu_reference", {}).get("bit_exact"),
+                "uvm_counts_vs_simulate": r.get("uvm_matches_simulate"),
+                "tests": "tests/test_scale_gpu.py (cfg1 + RM1-slice fwd/bwd vs the fp64 oracle, full cfg1 "
+                         "profile vs the reference), tests/test_pipeline_gpu.py (bundled configs end to end)"},
             "plan": first.strategy, "planner_s": plan_s,
             "simulated_uvm_pct": sim_uvm,
             "uvm_matches_simulate": r.get("uvm_matches_simulate"),

@@ -294,7 +294,8 @@ int rs_plan_solve(uint32_t num_tables, const rs_plan_table* tables, const rs_sys
  * The tiered operator that serves a plan (no reference implementation: the
  * paper used FBGEMM; semantics PAPER.md:275 and :605-607).
  * Each table's rows live in the fast tier (HBM) or the slow tier (pinned
- * host memory read zero-copy over PCIe) as its remap says.  Weights are fp32.
+ * host memory read zero-copy over PCIe) as its remap says.  Rows are fp32 or
+ * fp16 (elem_bytes 2); pooling, gradients and the optimizer run in fp32.
  *
  * Batch format (table-major CSR, the reference Trace regrouped per table):
  *   offsets: u32[T*B + 1]; bag (t, b) = indices[offsets[t*B+b] .. offsets[t*B+b+1])
@@ -309,7 +310,13 @@ typedef struct rs_emb_table {
   const int32_t* remap;         /* hash_size entries, host or device */
   int remap_location;
   uint64_t hbm_rows;            /* fast-tier rows (remap >= 0) */
-  uint64_t slow_rows;           /* slow-tier rows to back (remap < 0) */
+  uint64_t slow_rows;           /* slow-tier rows to back (remap < 0): RemapTable.slow_rows_allocated */
+  uint32_t elem_bytes;          /* TableSpec.elem_bytes (inc/types.hpp:31): 4 = fp32 rows, 2 = fp16
+                                   rows (fp32 arithmetic, round-to-nearest-even stores); 0 means 4 */
+  int allow_unbacked;           /* 1: slow offsets >= slow_rows are rows an omit_unaccessed remap
+                                   (inc/remap.hpp:43-48) left without storage — they pool as zero
+                                   vectors and their gradients are dropped (rs_emb_unbacked counts
+                                   them); 0: such an entry is rejected at create */
 } rs_emb_table;
 
 int rs_emb_create(rs_context* ctx, uint32_t num_tables, const rs_emb_table* tables,
@@ -343,6 +350,9 @@ int rs_emb_flush(rs_emb* e);
 /* Reads rows by ORIGINAL id into host memory (parity checks). */
 int rs_emb_read_rows(rs_emb* e, uint32_t t, const uint32_t* rows, uint64_t n,
                      float* out, float* momentum_out);
+/* Lookups that hit unbacked rows since the last reset (per table, u64[T],
+ * host), and how many remap entries of each table are unbacked (may be NULL). */
+int rs_emb_unbacked(rs_emb* e, uint64_t* lookups, uint64_t* rows, int reset);
 /* Bytes of HBM / pinned host memory held by the tiers. */
 int rs_emb_memory(const rs_emb* e, uint64_t* hbm_bytes, uint64_t* host_bytes);
 /* Kernel-only time of the forward / backward kernel sequences since the last

@@ -320,7 +320,7 @@ inline std::vector<uint64_t> count_distinct_raw(const Trace& trace, const std::v
 
 /// The tiered EmbeddingBag serving a sharding plan (the paper ran
 /// FBGEMM): rows the remap sends to the fast tier live in HBM,
-/// the others in pinned host memory.  forward = sum-pool (an empty bag pools
+/// the others in pinned host memory (fp32 or fp16 rows, fp32 arithmetic).  forward = sum-pool (an empty bag pools
 /// to 0) with per-table fast/slow hit counts equal to
 /// simulate()'s accounting; backward = deterministic row-wise SGD or exact
 /// row-wise Adagrad.  Batches are table-major CSR in DEVICE memory
@@ -339,9 +339,13 @@ class TieredEmbeddingBag {
     for (size_t i = 0; i < specs.size(); ++i) {
       const auto& s = specs[i];
       const auto& r = remaps[i];
-      if (s.elem_bytes != 4) throw InvalidArgument("TieredEmbeddingBag: fp32 tables only (elem_bytes 4)");
+      // elem_bytes 2 or 4 (inc/types.hpp:50-52; validated by rs_emb_create);
+      // an omit_unaccessed remap (inc/remap.hpp:43-48) backs only its
+      // slow_rows_allocated prefix and the other slow rows pool as zeros
+      const uint64_t slow = s.hash_size - r.hbm_rows;
+      const int unbacked = r.slow_rows_allocated < slow ? 1 : 0;
       tabs.push_back({s.table_id, s.hash_size, s.dim, r.entries.data(), RS_MEM_HOST, r.hbm_rows,
-                      s.hash_size - r.hbm_rows});
+                      unbacked ? r.slow_rows_allocated : slow, s.elem_bytes, unbacked});
       total_dim_ += s.dim;
     }
     check(rs_emb_create(ctx_.get(), static_cast<uint32_t>(tabs.size()), tabs.data(), max_batch, max_lookups,

@@ -75,7 +75,8 @@ class rs_sim_report(C.Structure):
 
 class rs_emb_table(C.Structure):
     _fields_ = [("table_id", u32), ("hash_size", u64), ("dim", u32), ("remap", P),
-                ("remap_location", i32), ("hbm_rows", u64), ("slow_rows", u64)]
+                ("remap_location", i32), ("hbm_rows", u64), ("slow_rows", u64),
+                ("elem_bytes", u32), ("allow_unbacked", i32)]
 
 
 class rs_plan_table(C.Structure):
@@ -122,6 +123,7 @@ _SIGS = {
     "rs_emb_prefetch": ([P, u64, P, P], i32),
     "rs_emb_flush": ([P], i32),
     "rs_emb_memory": ([P, P, P], i32),
+    "rs_emb_unbacked": ([P, P, P, i32], i32),
     "rs_emb_kernel_times": ([P, P, P, P, P, i32], i32),
     "rs_remap_write": ([P, C.c_char_p, u32, u64, u64, P, i32], i32),
     "rs_trace_read": ([P, C.c_char_p, u64, P], i32),

@@ -20,6 +20,7 @@ void build_remap(rs_context*, uint32_t, uint64_t, uint64_t, const uint32_t*, uin
 void simulate(rs_context*, const rs_trace*, uint32_t, const rs_plan_entry*, uint32_t,
               const rs_remap_view*, const rs_system_spec*, uint64_t, rs_sim_report*);
 rs_emb* emb_create(rs_context*, uint32_t, const rs_emb_table*, uint64_t, uint64_t, int, float);
+void emb_unbacked(rs_emb*, uint64_t*, uint64_t*, int);
 void emb_init_weights(rs_emb*, uint64_t, float);
 void emb_forward(rs_emb*, uint64_t, const uint32_t*, const uint32_t*, float*, uint64_t*);
 void emb_backward(rs_emb*, uint64_t, const uint32_t*, const uint32_t*, const float*, float);
@@ -246,6 +247,13 @@ int rs_emb_create(rs_context* c, uint32_t T, const rs_emb_table* tabs, uint64_t 
 
 int rs_emb_destroy(rs_emb* e) {
   return guarded([&] { rs::emb_free(e); });
+}
+
+int rs_emb_unbacked(rs_emb* e, uint64_t* lookups, uint64_t* rows, int reset) {
+  return guarded([&] {
+    need(e, "emb");
+    rs::emb_unbacked(e, lookups, rows, reset);
+  });
 }
 
 int rs_emb_init_weights(rs_emb* e, uint64_t seed, float scale) {

@@ -1,6 +1,7 @@
 // Shared device helpers for the RecShard B200 hot paths (sm_100a only).
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -95,6 +96,12 @@ __device__ __forceinline__ float4 ld_nc_f4(const float4* p) {
   asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
                : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
                : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint2 ld_nc_u2(const uint2* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
   return r;
 }
 

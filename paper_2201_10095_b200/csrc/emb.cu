@@ -39,20 +39,24 @@ namespace emb {
 
 struct TableDev {
   const int32_t* remap;
-  float* fast;
-  float* slow;       // device view of pinned host memory
+  char* fast;        // [hbm_rows][rbytes]
+  char* slow;        // [slow_rows][rbytes], device view of pinned host memory
   float* mom_fast;
   float* mom_slow;
+  const char* zero;  // one zero row (>= rbytes): what an unbacked row reads as
   uint64_t hash_size;
   uint64_t col;      // column offset in pooled rows
   uint32_t dim;
+  uint32_t rbytes;   // dim * elem_bytes
+  uint32_t ebytes;   // 4 (fp32) or 2 (fp16 storage, fp32 arithmetic)
+  uint32_t nkeys;    // hbm_rows + slow_rows: the backward's key of every unbacked row
   uint64_t hbm_rows;
-  uint64_t slow_rows;
+  uint64_t slow_rows;  // BACKED slow rows; slow offsets past them are unbacked
   // HBM staging of slow-tier rows (uvm_cache.cuh); slot_of == nullptr means
   // slow rows are read/written zero-copy in host memory.
   uint32_t* slot_of;
-  float* staging;
-  uint64_t stage_stride;
+  char* staging;
+  uint64_t stage_stride;  // bytes per staging slot
 };
 
 __host__ __device__ inline int lanes_for(uint32_t dim) {
@@ -61,34 +65,90 @@ __host__ __device__ inline int lanes_for(uint32_t dim) {
   return int(L);
 }
 
-// Row of remap entry e in the host tier (no staging).
-__device__ __forceinline__ float* row_ptr_host(const TableDev& td, int32_t e) {
-  return e >= 0 ? td.fast + uint64_t(e) * td.dim : td.slow + uint64_t(-int64_t(e) - 1) * td.dim;
+// Storage element <-> fp32, four at a time (a lane's `vec`: elements
+// 4*vec .. 4*vec+3 of a row).  fp16 rows: 8-byte loads, exact widening,
+// round-to-nearest-even narrowing on store.
+template <class E>
+struct Elem;
+template <>
+struct Elem<float> {
+  static __device__ __forceinline__ float4 load_nc(const char* row, uint32_t vec) {
+    return ld_nc_f4(reinterpret_cast<const float4*>(row) + vec);
+  }
+  static __device__ __forceinline__ float4 load(const char* row, uint32_t vec) {
+    return reinterpret_cast<const float4*>(row)[vec];
+  }
+  static __device__ __forceinline__ void store(char* row, uint32_t vec, float4 v) {
+    reinterpret_cast<float4*>(row)[vec] = v;
+  }
+};
+template <>
+struct Elem<__half> {
+  static __device__ __forceinline__ float4 widen(uint2 u) {
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+  }
+  static __device__ __forceinline__ float4 load_nc(const char* row, uint32_t vec) {
+    return widen(ld_nc_u2(reinterpret_cast<const uint2*>(row) + vec));
+  }
+  static __device__ __forceinline__ float4 load(const char* row, uint32_t vec) {
+    return widen(reinterpret_cast<const uint2*>(row)[vec]);
+  }
+  static __device__ __forceinline__ void store(char* row, uint32_t vec, float4 v) {
+    const __half2 a = __floats2half2_rn(v.x, v.y), b = __floats2half2_rn(v.z, v.w);
+    uint2 u;
+    u.x = *reinterpret_cast<const uint32_t*>(&a);
+    u.y = *reinterpret_cast<const uint32_t*>(&b);
+    reinterpret_cast<uint2*>(row)[vec] = u;
+  }
+};
+// Runtime-typed access for the cold paths (init, read-back, long segments).
+__device__ __forceinline__ float4 load4(const TableDev& td, const char* row, uint32_t vec) {
+  return td.ebytes == 2 ? Elem<__half>::load(row, vec) : Elem<float>::load(row, vec);
+}
+__device__ __forceinline__ void store4(const TableDev& td, char* row, uint32_t vec, float4 v) {
+  if (td.ebytes == 2) Elem<__half>::store(row, vec, v);
+  else Elem<float>::store(row, vec, v);
+}
+
+// Slow offset of a (negative) remap entry.
+__device__ __forceinline__ uint64_t slow_off(int32_t e) { return uint64_t(-int64_t(e) - 1); }
+// Row of remap entry e in the host tier (no staging); unbacked rows read as zero.
+__device__ __forceinline__ const char* row_ptr_host(const TableDev& td, int32_t e) {
+  if (e >= 0) return td.fast + uint64_t(e) * td.rbytes;
+  const uint64_t s = slow_off(e);
+  return s < td.slow_rows ? td.slow + s * td.rbytes : td.zero;
 }
 // Row of remap entry e as the hot paths see it: slow rows come from their HBM
 // staging slot when the batch was prefetched (uvm_cache.cuh).
 // A slow row without a slot (a claim that ran out of slots: slot_of stays
 // kNoSlot, 0xFFFFFFFF) is read/written in the host tier instead, so a failed
 // claim can never send the kernels outside the staging buffer; the failure
-// itself is reported before the batch runs (begin_step).
-__device__ __forceinline__ float* row_ptr(const TableDev& td, int32_t e) {
-  if (e >= 0) return td.fast + uint64_t(e) * td.dim;
-  const uint64_t s = uint64_t(-int64_t(e) - 1);
+// itself is reported before the batch runs (begin_step).  A slow offset past
+// the backed rows (an omit_unaccessed remap, inc/remap.hpp:43-48) has no
+// storage: it reads as the zero row and is never written (its backward key
+// is the sentinel nkeys).
+__device__ __forceinline__ char* row_ptr(const TableDev& td, int32_t e) {
+  if (e >= 0) return td.fast + uint64_t(e) * td.rbytes;
+  const uint64_t s = slow_off(e);
+  if (s >= td.slow_rows) return const_cast<char*>(td.zero);
   if (td.slot_of) {
     const uint32_t sl = td.slot_of[s];
     if (sl < 0xFFFFFFFEu) return td.staging + uint64_t(sl) * td.stage_stride;
   }
-  return td.slow + s * td.dim;
+  return td.slow + s * td.rbytes;
 }
 __device__ __forceinline__ float* mom_ptr(const TableDev& td, int32_t e) {
-  return e >= 0 ? td.mom_fast + uint64_t(e) : td.mom_slow + uint64_t(-int64_t(e) - 1);
+  return e >= 0 ? td.mom_fast + uint64_t(e) : td.mom_slow + slow_off(e);
 }
 // Backward keys are storage slots within the table: key = e >= 0 ? e :
-// hbm_rows + (-e - 1), a bijection of the remap entries onto
-// [0, hbm_rows + slow_rows).  Tables keep their CSR position ranges (the
-// backward sorts each table's range on its own).
+// hbm_rows + (-e - 1), a bijection of the backed remap entries onto
+// [0, nkeys); every unbacked entry keys to nkeys (one segment per table that
+// the update skips).  Tables keep their CSR position ranges (the backward
+// sorts each table's range on its own).
 __device__ __forceinline__ uint32_t slot_of_entry(const TableDev& td, int32_t e) {
-  return e >= 0 ? uint32_t(e) : uint32_t(td.hbm_rows + uint64_t(-int64_t(e) - 1));
+  return e >= 0 ? uint32_t(e) : uint32_t(min(td.hbm_rows + slow_off(e), uint64_t(td.nkeys)));
 }
 __device__ __forceinline__ int32_t entry_of_key(const TableDev& td, uint32_t key) {
   const uint32_t s = key;
@@ -96,18 +156,26 @@ __device__ __forceinline__ int32_t entry_of_key(const TableDev& td, uint32_t key
 }
 
 constexpr int kFwdThreads = 256;
+#ifndef RS_FWD_MINB
+#define RS_FWD_MINB 6
+#endif
 
-// Flushes a warp's accumulated (fast, total) lookup counts for table t.
-__device__ __forceinline__ void flush_hits(unsigned long long* hits, uint32_t t, uint32_t fast,
-                                           uint32_t tot) {
+// Flushes a warp's accumulated (fast, total) lookup counts for table t (the
+// caller's simulate() accounting, may be null) and its unbacked-row lookups.
+__device__ __forceinline__ void flush_hits(unsigned long long* hits, unsigned long long* unbacked, uint32_t t,
+                                           uint32_t fast, uint32_t tot, uint32_t unb) {
 #pragma unroll
   for (int o2 = 16; o2; o2 >>= 1) {
     fast += __shfl_xor_sync(0xffffffffu, fast, o2);
     tot += __shfl_xor_sync(0xffffffffu, tot, o2);
+    unb += __shfl_xor_sync(0xffffffffu, unb, o2);
   }
-  if ((threadIdx.x & 31) == 0 && tot) {
-    atomicAdd(&hits[2 * uint64_t(t)], (unsigned long long)fast);
-    atomicAdd(&hits[2 * uint64_t(t) + 1], (unsigned long long)(tot - fast));
+  if ((threadIdx.x & 31) == 0) {
+    if (hits && tot) {
+      atomicAdd(&hits[2 * uint64_t(t)], (unsigned long long)fast);
+      atomicAdd(&hits[2 * uint64_t(t) + 1], (unsigned long long)(tot - fast));
+    }
+    if (unb) atomicAdd(&unbacked[t], (unsigned long long)unb);
   }
 }
 
@@ -145,13 +213,14 @@ __device__ __forceinline__ int32_t fwd_bag_entry(const TableDev* __restrict__ ta
 // bag's first row loads are in flight, and their remap entries once those
 // rows have arrived — so a bag's dependent chain is its row loads, not
 // offsets -> index -> remap -> rows.
-template <int G, int VPL, int UNR, int MINB>
+template <int G, int VPL, int UNR, int MINB, class E>
 __global__ void __launch_bounds__(kFwdThreads, MINB)
 forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__ cls_tables,
                uint32_t ntab, uint64_t B, const uint32_t* __restrict__ offsets,
                const uint32_t* __restrict__ indices, const OutMap om, uint64_t stride,
-               unsigned long long* __restrict__ hits, uint32_t* __restrict__ keys,
-               uint32_t* __restrict__ vals, uint64_t max_keys, unsigned* __restrict__ err) {
+               unsigned long long* __restrict__ hits, unsigned long long* __restrict__ unbacked,
+               uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t max_keys,
+               unsigned* __restrict__ err) {
   constexpr int BPW = 32 / G;
   constexpr int kFwdUnroll = UNR;
   const int lane = threadIdx.x & 31;
@@ -160,7 +229,7 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
   const uint64_t wpt = (B + BPW - 1) / BPW;
   const uint64_t total_w = wpt * ntab;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  uint32_t cur_t = 0xFFFFFFFFu, fast = 0, tot = 0;
+  uint32_t cur_t = 0xFFFFFFFFu, fast = 0, tot = 0, unb = 0;
   // the pipelined bag: table, offsets, first G indices (checked) and entries
   uint32_t nt = 0, ns = 0, ne = 0, nidx = 0;
   int32_t nent = 0;
@@ -178,8 +247,8 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
     if (more) fwd_bag_offsets(cls_tables, offsets, B, wpt, BPW, grp, w2, nt, ns, ne);
     bool pf = !more;  // next bag's index/entry issued?
     if (t != cur_t) {
-      if (hits && cur_t != 0xFFFFFFFFu) flush_hits(hits, cur_t, fast, tot);
-      fast = tot = 0;
+      if (cur_t != 0xFFFFFFFFu) flush_hits(hits, unbacked, cur_t, fast, tot, unb);
+      fast = tot = unb = 0;
       cur_t = t;
     }
     // the table's fields are re-read per bag (L1 hits) rather than held live
@@ -210,6 +279,7 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
           ent = td.remap[idx];
         }
         fast += ent >= 0;
+        unb += ent < 0 && slow_off(ent) >= td.slow_rows;
         // the backward's sort keys, while the remap entry is in hand
         // (key = storage slot within the table, value = sample)
         if (keys) {
@@ -226,11 +296,11 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
 #pragma unroll
         for (int u = 0; u < kFwdUnroll; ++u) {
           const int32_t eu = __shfl_sync(gmask, ent, int(j) + u, G);
-          const float4* row = reinterpret_cast<const float4*>(row_ptr(td, eu));
+          const char* row = row_ptr(td, eu);
 #pragma unroll
           for (int vv = 0; vv < VPL; ++vv) {
             const uint32_t vec = lg + vv * G;
-            v[u][vv] = (j + u < n && vec < V) ? ld_nc_f4(row + vec) : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[u][vv] = (j + u < n && vec < V) ? Elem<E>::load_nc(row, vec) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
         if (!pf) nidx = fwd_bag_index(indices, lg, ns, ne);  // behind this bag's first rows
@@ -265,7 +335,7 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
       }
     }
   }
-  if (hits && cur_t != 0xFFFFFFFFu) flush_hits(hits, cur_t, fast, tot);
+  if (cur_t != 0xFFFFFFFFu) flush_hits(hits, unbacked, cur_t, fast, tot, unb);
 }
 
 // ------------------------------------------------------------------ backward
@@ -329,6 +399,8 @@ namespace rs {
 namespace emb {
 
 // ------------------------------------------------------------------ init / read
+// Init values are drawn in fp32 (or_init_weight) and rounded to the storage
+// type; unbacked rows have no storage.
 __global__ void init_kernel(TableDev td, uint32_t table_id, uint64_t seed, float scale) {
   const uint32_t V = td.dim >> 2;
   const uint64_t n = td.hash_size * V;
@@ -336,6 +408,8 @@ __global__ void init_kernel(TableDev td, uint32_t table_id, uint64_t seed, float
        i += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t row = i / V;
     const uint32_t vec = uint32_t(i % V);
+    const int32_t e = td.remap[row];
+    if (e < 0 && slow_off(e) >= td.slow_rows) continue;
     const uint64_t ds = derive_stream(seed, table_id, row);
     float x[4];
 #pragma unroll
@@ -343,13 +417,12 @@ __global__ void init_kernel(TableDev td, uint32_t table_id, uint64_t seed, float
       const uint64_t u = mix64(ds + vec * 4 + k) >> 40;
       x[k] = __fmul_rn(__fsub_rn(__fmul_rn(float(u), 0x1.0p-24f), 0.5f), scale);
     }
-    const int32_t e = td.remap[row];
-    float4* w = reinterpret_cast<float4*>(row_ptr_host(td, e));
-    w[vec] = make_float4(x[0], x[1], x[2], x[3]);
+    store4(td, const_cast<char*>(row_ptr_host(td, e)), vec, make_float4(x[0], x[1], x[2], x[3]));
     if (vec == 0 && td.mom_fast) *mom_ptr(td, e) = 0.f;
   }
 }
 
+// Rows by original id, widened to fp32 (unbacked rows read as zero, momentum 0).
 __global__ void read_rows_kernel(TableDev td, const uint32_t* __restrict__ rows, uint64_t n,
                                  float* __restrict__ out, float* __restrict__ mom_out) {
   const uint32_t V = td.dim >> 2;
@@ -358,19 +431,30 @@ __global__ void read_rows_kernel(TableDev td, const uint32_t* __restrict__ rows,
     const uint64_t r = i / V;
     const uint32_t vec = uint32_t(i % V);
     const int32_t e = td.remap[rows[r]];
-    reinterpret_cast<float4*>(out + r * td.dim)[vec] =
-        reinterpret_cast<const float4*>(row_ptr_host(td, e))[vec];
-    if (mom_out && vec == 0) mom_out[r] = td.mom_fast ? *mom_ptr(td, e) : 0.f;
+    const bool backed = e >= 0 || slow_off(e) < td.slow_rows;
+    reinterpret_cast<float4*>(out + r * td.dim)[vec] = load4(td, row_ptr_host(td, e), vec);
+    if (mom_out && vec == 0) mom_out[r] = td.mom_fast && backed ? *mom_ptr(td, e) : 0.f;
   }
 }
 
+// Every remap entry must land inside its tier: fast entries below hbm_rows,
+// slow ones below slow_rows unless unbacked rows are allowed (then anything
+// past slow_rows is an unbacked row and counted).
 __global__ void check_remap_kernel(const int32_t* __restrict__ remap, uint64_t H, uint64_t hbm_rows,
-                                   uint64_t slow_rows, unsigned* __restrict__ err) {
+                                   uint64_t slow_rows, int allow_unbacked, unsigned* __restrict__ err,
+                                   unsigned long long* __restrict__ n_unbacked) {
+  uint32_t unb = 0;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < H;
        i += uint64_t(gridDim.x) * blockDim.x) {
     const int32_t e = remap[i];
-    if (e >= 0 ? uint64_t(e) >= hbm_rows : uint64_t(-int64_t(e) - 1) >= slow_rows) atomicOr(err, 1u);
+    if (e >= 0) {
+      if (uint64_t(e) >= hbm_rows) atomicOr(err, 1u);
+    } else if (slow_off(e) >= slow_rows) {
+      if (allow_unbacked) ++unb;
+      else atomicOr(err, 1u);
+    }
   }
+  if (unb) atomicAdd(n_unbacked, (unsigned long long)unb);
 }
 
 }  // namespace emb
@@ -389,6 +473,7 @@ struct rs_emb {
   TableDev* d_tables = nullptr;
   uint64_t total_dim = 0;
   uint32_t dmax = 0;
+  uint32_t rmax = 0;  // max row bytes (staging slot stride)
   char* fast_pool = nullptr;
   size_t fast_bytes = 0;
   char* host_pool = nullptr;
@@ -399,9 +484,14 @@ struct rs_emb {
   size_t host_bytes = 0;
   int32_t* remap_pool = nullptr;
   size_t remap_bytes = 0;
-  // forward classes: (G, VPL) -> table list
+  // unbacked rows (omit_unaccessed remaps): per-table lookup counters, the
+  // zero row they read, and how many remap entries each table leaves unbacked
+  unsigned long long* d_unbacked = nullptr;
+  char* zero_row = nullptr;
+  std::vector<uint64_t> unbacked_rows;
+  // forward classes: (G, VPL, element bytes) -> table list
   struct Class {
-    int G, VPL;
+    int G, VPL, EB;
     std::vector<uint32_t> tables;
     uint32_t* d_list = nullptr;
   };
@@ -421,7 +511,7 @@ struct rs_emb {
   uint64_t keys_B = 0;
   // HBM staging of slow rows (uvm_cache.cuh)
   uint32_t nslots = 0;
-  float* staging = nullptr;
+  char* staging = nullptr;
   uint32_t* slot_of = nullptr;  // sum(slow_rows)
   uint32_t* slot_gen = nullptr;
   uint32_t* slot_tab = nullptr;
@@ -435,7 +525,7 @@ struct rs_emb {
   uint32_t bcap = 0;
   uint32_t *copy_tab = nullptr, *copy_row = nullptr, *wb_tab = nullptr, *wb_row = nullptr;
   unsigned* n_wb = nullptr;
-  float *d_bin = nullptr, *d_bout = nullptr, *h_bin = nullptr, *h_bout = nullptr;
+  char *d_bin = nullptr, *d_bout = nullptr, *h_bin = nullptr, *h_bout = nullptr;
   uint32_t *h_ctab = nullptr, *h_crow = nullptr, *h_wtab = nullptr, *h_wrow = nullptr;
   unsigned* h_cnt = nullptr;
   cudaEvent_t ev_claim[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -576,6 +666,8 @@ struct rs_emb {
       cudaStreamDestroy(fwd_side);
     }
     if (d_err) cudaFree(d_err);
+    for (void* p : {(void*)d_unbacked, (void*)zero_row})
+      if (p) cudaFree(p);
     if (sort_scratch) cudaFree(sort_scratch);
     if (side) {
       cudaStreamSynchronize(side);
@@ -641,6 +733,7 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
     cudaStream_t st = ctx->stream;
     size_t fb = 0, hb = 0, rb = 0;
     std::vector<size_t> foff(T), hoff(T), roff(T), mfoff(T), mhoff(T);
+    std::vector<uint32_t> eb(T);
     for (uint32_t t = 0; t < T; ++t) {
       const rs_emb_table& x = tabs[t];
       if (x.dim == 0 || x.dim % 4 || x.dim > 1024)
@@ -648,15 +741,21 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
       if (x.hash_size == 0 || x.hash_size > 0x7FFFFFFFULL)
         throw InvalidArgument("emb: table " + std::to_string(x.table_id) + ": hash_size out of range");
       if (x.hbm_rows > x.hash_size) throw InvalidArgument("emb: hbm_rows exceeds hash_size");
+      if (x.hbm_rows + x.slow_rows > x.hash_size)
+        throw InvalidArgument("emb: table " + std::to_string(x.table_id) + ": hbm_rows + slow_rows exceeds hash_size");
       if (!x.remap) throw InvalidArgument("emb: table " + std::to_string(x.table_id) + " has no remap");
+      eb[t] = x.elem_bytes ? x.elem_bytes : 4u;
+      if (eb[t] != 2 && eb[t] != 4)  // inc/types.hpp:50-52
+        throw InvalidArgument("emb: table " + std::to_string(x.table_id) + ": elem_bytes must be 2 or 4");
       foff[t] = fb;
-      fb += align256(x.hbm_rows * x.dim * 4);
+      fb += align256(x.hbm_rows * x.dim * eb[t]);
       hoff[t] = hb;
-      hb += align256(x.slow_rows * x.dim * 4);
+      hb += align256(x.slow_rows * x.dim * eb[t]);
       roff[t] = rb;
       rb += align256(x.hash_size * 4);
       e->total_dim += x.dim;
       e->dmax = std::max(e->dmax, x.dim);
+      e->rmax = std::max(e->rmax, (x.dim * eb[t] + 15) / 16 * 16);
       e->table_ids.push_back(x.table_id);
     }
     // Adagrad state (4 B/row) of BOTH tiers lives in HBM: a slow-tier row's
@@ -677,6 +776,11 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
     RS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->host_pool_dev), e->host_pool, 0));
     RS_CUDA(cudaMalloc(&e->remap_pool, std::max<size_t>(rb, 256)));
     RS_CUDA(cudaMalloc(&e->d_err, 16));
+    RS_CUDA(cudaMalloc(&e->d_unbacked, 8 * size_t(T)));
+    RS_CUDA(cudaMemsetAsync(e->d_unbacked, 0, 8 * size_t(T), st));
+    RS_CUDA(cudaMalloc(&e->zero_row, 4096));
+    RS_CUDA(cudaMemsetAsync(e->zero_row, 0, 4096, st));
+    e->unbacked_rows.assign(T, 0);
     uint64_t col = 0;
     e->h_tables.resize(T);
     for (uint32_t t = 0; t < T; ++t) {
@@ -687,8 +791,12 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
                               x.remap_location == RS_MEM_DEVICE ? cudaMemcpyDeviceToDevice
                                                                 : cudaMemcpyHostToDevice,
                               st));
-      d.fast = reinterpret_cast<float*>(e->fast_pool + foff[t]);
-      d.slow = reinterpret_cast<float*>(e->host_pool_dev + hoff[t]);
+      d.fast = e->fast_pool + foff[t];
+      d.slow = e->host_pool_dev + hoff[t];
+      d.zero = e->zero_row;
+      d.ebytes = eb[t];
+      d.rbytes = x.dim * eb[t];
+      d.nkeys = uint32_t(x.hbm_rows + x.slow_rows);
       d.mom_fast = opt == RS_OPT_ROWWISE_ADAGRAD ? reinterpret_cast<float*>(e->fast_pool + mfoff[t]) : nullptr;
       d.mom_slow = opt == RS_OPT_ROWWISE_ADAGRAD ? reinterpret_cast<float*>(e->fast_pool + mhoff[t]) : nullptr;
       d.hash_size = x.hash_size;
@@ -698,19 +806,25 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
       d.slow_rows = x.slow_rows;
       col += x.dim;
       // every remap entry must land inside its tier's allocation
-      RS_CUDA(cudaMemsetAsync(e->d_err, 0, 4, st));
+      RS_CUDA(cudaMemsetAsync(e->d_err, 0, 16, st));
       unsigned g = unsigned(std::min<uint64_t>((x.hash_size + 255) / 256, uint64_t(sm_count()) * 8));
-      check_remap_kernel<<<std::max(1u, g), 256, 0, st>>>(d.remap, x.hash_size, x.hbm_rows, x.slow_rows, e->d_err);
-      unsigned herr = 0;
-      RS_CUDA(cudaMemcpyAsync(&herr, e->d_err, 4, cudaMemcpyDeviceToHost, st));
+      check_remap_kernel<<<std::max(1u, g), 256, 0, st>>>(d.remap, x.hash_size, x.hbm_rows, x.slow_rows,
+                                                          x.allow_unbacked, e->d_err,
+                                                          reinterpret_cast<unsigned long long*>(e->d_err + 2));
+      unsigned herr[4] = {0, 0, 0, 0};
+      RS_CUDA(cudaMemcpyAsync(herr, e->d_err, 16, cudaMemcpyDeviceToHost, st));
       RS_CUDA(cudaStreamSynchronize(st));
-      if (herr)
+      if (herr[0])
         throw InvalidArgument("emb: table " + std::to_string(x.table_id) +
                               ": remap entry outside the fast/slow tier sizes");
+      std::memcpy(&e->unbacked_rows[t], herr + 2, 8);
     }
     e->key_bits = 1;
-    for (const auto& d : e->h_tables)
-      while (e->key_bits < 32 && (uint64_t(1) << e->key_bits) < d.hbm_rows + d.slow_rows) ++e->key_bits;
+    // keys span [0, nkeys] (nkeys: the unbacked sentinel)
+    for (uint32_t t = 0; t < T; ++t) {
+      const uint64_t nk = uint64_t(e->h_tables[t].nkeys) + (e->unbacked_rows[t] ? 1 : 0);
+      while (e->key_bits < 32 && (uint64_t(1) << e->key_bits) < nk) ++e->key_bits;
+    }
     RS_CUDA(cudaMalloc(&e->d_tables, sizeof(TableDev) * T));
     RS_CUDA(cudaMemcpyAsync(e->d_tables, e->h_tables.data(), sizeof(TableDev) * T, cudaMemcpyHostToDevice, st));
     // forward classes
@@ -719,10 +833,11 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
       const int VPL = int((tabs[t].dim / 4 + G - 1) / G);
       int vp2 = 1;
       while (vp2 < VPL) vp2 <<= 1;
+      const int EB = int(eb[t]);
       auto it = std::find_if(e->classes.begin(), e->classes.end(),
-                             [&](const rs_emb::Class& c) { return c.G == G && c.VPL == vp2; });
+                             [&](const rs_emb::Class& c) { return c.G == G && c.VPL == vp2 && c.EB == EB; });
       if (it == e->classes.end()) {
-        e->classes.push_back({G, vp2, {}, nullptr});
+        e->classes.push_back({G, vp2, EB, {}, nullptr});
         it = e->classes.end() - 1;
       }
       it->tables.push_back(t);
@@ -799,11 +914,11 @@ void emb_enable_cache(rs_emb* e, uint32_t nslots) {
   cudaStream_t st = e->ctx->stream;
   uint64_t total_slow = 0;
   for (const auto& d : e->h_tables) total_slow += d.slow_rows;
-  const uint64_t stride = e->dmax;
+  const uint64_t stride = e->rmax;  // bytes per slot / bounce row
   // one generation's rows fit in half the slots (nslots >= 2x a batch's rows)
   e->bcap = nslots / 2 + 1;
   const uint64_t bc = e->bcap;
-  RS_CUDA(cudaMalloc(&e->staging, uint64_t(nslots) * stride * 4));
+  RS_CUDA(cudaMalloc(&e->staging, uint64_t(nslots) * stride));
   RS_CUDA(cudaMalloc(&e->slot_of, std::max<uint64_t>(total_slow, 1) * 4));
   RS_CUDA(cudaMalloc(&e->slot_gen, uint64_t(nslots) * 4));
   RS_CUDA(cudaMalloc(&e->slot_tab, uint64_t(nslots) * 4));
@@ -816,14 +931,14 @@ void emb_enable_cache(rs_emb* e, uint32_t nslots) {
   RS_CUDA(cudaMalloc(&e->copy_row, 2 * bc * 4));
   RS_CUDA(cudaMalloc(&e->wb_tab, bc * 4));
   RS_CUDA(cudaMalloc(&e->wb_row, bc * 4));
-  RS_CUDA(cudaMalloc(&e->d_bin, bc * stride * 4));
-  RS_CUDA(cudaMalloc(&e->d_bout, bc * stride * 4));
+  RS_CUDA(cudaMalloc(&e->d_bin, bc * stride));
+  RS_CUDA(cudaMalloc(&e->d_bout, bc * stride));
   RS_CUDA(cudaMalloc(&e->free_top, 4));
   RS_CUDA(cudaMalloc(&e->ncopy, 2 * 4));
   RS_CUDA(cudaMalloc(&e->n_wb, 4));
   RS_CUDA(cudaMalloc(&e->cache_err, 4));
-  RS_CUDA(cudaHostAlloc(&e->h_bin, bc * stride * 4, cudaHostAllocDefault));
-  RS_CUDA(cudaHostAlloc(&e->h_bout, bc * stride * 4, cudaHostAllocDefault));
+  RS_CUDA(cudaHostAlloc(&e->h_bin, bc * stride, cudaHostAllocDefault));
+  RS_CUDA(cudaHostAlloc(&e->h_bout, bc * stride, cudaHostAllocDefault));
   for (uint32_t** hp : {&e->h_ctab, &e->h_crow, &e->h_wtab, &e->h_wrow})
     RS_CUDA(cudaHostAlloc(hp, bc * 4, cudaHostAllocDefault));
   RS_CUDA(cudaHostAlloc(&e->h_cnt, 16, cudaHostAllocDefault));
@@ -894,10 +1009,9 @@ static unsigned take_cache_error(rs_emb* e) {
 }
 
 // Host row of (table t, slow row r) in the pinned host tier.
-static inline float* host_slow_row(rs_emb* e, uint32_t t, uint32_t r) {
+static inline char* host_slow_row(rs_emb* e, uint32_t t, uint32_t r) {
   const TableDev& d = e->h_tables[t];
-  return reinterpret_cast<float*>(e->host_pool + (reinterpret_cast<char*>(d.slow) - e->host_pool_dev)) +
-         uint64_t(r) * d.dim;
+  return e->host_pool + (d.slow - e->host_pool_dev) + uint64_t(r) * d.rbytes;
 }
 
 // Worker task: rows claimed for generation g (claim event ev_claim[g & 3])
@@ -922,7 +1036,7 @@ static void stage_in_task(rs_emb* e, uint64_t g, uint64_t out_before) {
   RS_CUDA(cudaStreamSynchronize(s));
   e->gen_err[g & 3] = e->h_cnt[2];  // read by begin_step before generation g runs
   const uint64_t n = std::min<uint64_t>(e->h_cnt[0], e->bcap);
-  const uint64_t stride = e->dmax;
+  const uint64_t stride = e->rmax;
   if (n) {
     RS_CUDA(cudaMemcpyAsync(e->h_ctab, e->copy_tab + cs, n * 4, cudaMemcpyDeviceToHost, s));
     RS_CUDA(cudaMemcpyAsync(e->h_crow, e->copy_row + cs, n * 4, cudaMemcpyDeviceToHost, s));
@@ -935,10 +1049,10 @@ static void stage_in_task(rs_emb* e, uint64_t g, uint64_t out_before) {
       e->pool->parallel_for(c1 - c0, [&](size_t b, size_t en) {
         for (size_t k = c0 + b; k < c0 + en; ++k) {
           const uint32_t t = e->h_ctab[k];
-          memcpy(e->h_bin + k * stride, host_slow_row(e, t, e->h_crow[k]), size_t(e->h_tables[t].dim) * 4);
+          memcpy(e->h_bin + k * stride, host_slow_row(e, t, e->h_crow[k]), e->h_tables[t].rbytes);
         }
       });
-      RS_CUDA(cudaMemcpyAsync(e->d_bin + c0 * stride, e->h_bin + c0 * stride, (c1 - c0) * stride * 4,
+      RS_CUDA(cudaMemcpyAsync(e->d_bin + c0 * stride, e->h_bin + c0 * stride, (c1 - c0) * stride,
                               cudaMemcpyHostToDevice, s));
     }
     const double t3 = dbg ? now_us() : 0;
@@ -966,16 +1080,16 @@ static void stage_out_task(rs_emb* e, cudaEvent_t evicted) {
   RS_CUDA(cudaStreamSynchronize(s));
   const uint64_t n = std::min<uint64_t>(e->h_cnt[1], e->bcap);
   if (!n) return;
-  const uint64_t stride = e->dmax;
+  const uint64_t stride = e->rmax;
   RS_CUDA(cudaMemcpyAsync(e->h_wtab, e->wb_tab, n * 4, cudaMemcpyDeviceToHost, s));
   RS_CUDA(cudaMemcpyAsync(e->h_wrow, e->wb_row, n * 4, cudaMemcpyDeviceToHost, s));
-  RS_CUDA(cudaMemcpyAsync(e->h_bout, e->d_bout, n * stride * 4, cudaMemcpyDeviceToHost, s));
+  RS_CUDA(cudaMemcpyAsync(e->h_bout, e->d_bout, n * stride, cudaMemcpyDeviceToHost, s));
   RS_CUDA(cudaStreamSynchronize(s));
   const double t2 = dbg ? now_us() : 0;
   e->out_pool->parallel_for(n, [&](size_t b, size_t en) {
     for (size_t k = b; k < en; ++k) {
       const uint32_t t = e->h_wtab[k];
-      memcpy(host_slow_row(e, t, e->h_wrow[k]), e->h_bout + k * stride, size_t(e->h_tables[t].dim) * 4);
+      memcpy(host_slow_row(e, t, e->h_wrow[k]), e->h_bout + k * stride, e->h_tables[t].rbytes);
     }
   });
   if (dbg)
@@ -992,7 +1106,7 @@ static void evict(rs_emb* e, uint32_t gen_bits, uint32_t keep) {
   RS_CUDA(cudaMemsetAsync(e->n_wb, 0, 4, st));
   const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((e->nslots + 255) / 256, uint64_t(sm_count()) * 8)));
   emb::uvm_evict_kernel<<<grid, 256, 0, st>>>(e->d_tables_c, e->nslots, gen_bits, keep, e->slot_gen, e->slot_tab,
-                                              e->slot_row, e->free_stack, e->free_top, e->staging, e->dmax,
+                                              e->slot_row, e->free_stack, e->free_top, e->staging, e->rmax,
                                               e->d_bout, e->wb_tab, e->wb_row, e->bcap, e->n_wb, e->cache_err);
   RS_COUNT(1);
   RS_LAUNCH_CHECK();
@@ -1116,7 +1230,7 @@ void emb_init_weights(rs_emb* e, uint64_t seed, float scale) {
   RS_LAUNCH_CHECK();
 }
 
-template <int G, int VPL>
+template <int G, int VPL, class E>
 static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint32_t* off,
                        const uint32_t* idx, const OutMap& out, uint64_t stride, unsigned long long* hits,
                        cudaStream_t st) {
@@ -1125,15 +1239,42 @@ static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint
   const uint64_t blocks = (warps * 32 + emb::kFwdThreads - 1) / emb::kFwdThreads;
   const unsigned grid = std::max(1u, unsigned(std::min<uint64_t>(blocks, uint64_t(sm_count()) * 64)));
   auto args = std::make_tuple(e->cur_tables, c.d_list, uint32_t(c.tables.size()), B, off, idx, out,
-                              stride, hits, e->keys, e->vals, uint64_t(e->max_lookups), e->d_err);
+                              stride, hits, e->d_unbacked, e->keys, e->vals, uint64_t(e->max_lookups), e->d_err);
   auto go = [&](auto kern) {
     std::apply([&](auto... a) { kern<<<grid, emb::kFwdThreads, 0, st>>>(a...); }, args);
   };
   // (unroll, min blocks/SM): measured on B200 RM1 all-HBM — (4, 6) 1.15 ms,
   // (2, 8) 1.14, (4, 8) 1.17, (6, 6) 1.22, (8, 6) 1.55, (8, 1) 1.85
-  if (VPL > 1) go(emb::forward_kernel<G, VPL, 8, 1>);
-  else go(emb::forward_kernel<G, VPL, 4, 6>);
+  if constexpr (VPL > 1) {
+    go(emb::forward_kernel<G, VPL, 8, 1, E>);
+  } else {
+    static const int minb = [] {  // A/B knob: RS_FWD_MINB=4 trades occupancy for no spills
+      const char* v = getenv("RS_FWD_MINB");
+      return v ? atoi(v) : RS_FWD_MINB;
+    }();
+    if (minb == 4) go(emb::forward_kernel<G, VPL, 4, 4, E>);
+    else go(emb::forward_kernel<G, VPL, 4, 6, E>);
+  }
   RS_COUNT(1);
+}
+
+// One launch per lane class, instantiated per (G, VPL) and storage type.
+template <class E>
+static void launch_fwd_class(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint32_t* off,
+                             const uint32_t* idx, const OutMap& om, uint64_t stride, unsigned long long* h,
+                             cudaStream_t st) {
+  switch (c.G * 100 + c.VPL) {
+    case 101: launch_fwd<1, 1, E>(e, c, B, off, idx, om, stride, h, st); break;
+    case 201: launch_fwd<2, 1, E>(e, c, B, off, idx, om, stride, h, st); break;
+    case 401: launch_fwd<4, 1, E>(e, c, B, off, idx, om, stride, h, st); break;
+    case 801: launch_fwd<8, 1, E>(e, c, B, off, idx, om, stride, h, st); break;
+    case 1601: launch_fwd<16, 1, E>(e, c, B, off, idx, om, stride, h, st); break;
+    case 3201: launch_fwd<32, 1, E>(e, c, B, off, idx, om, stride, h, st); break;
+    case 3202: launch_fwd<32, 2, E>(e, c, B, off, idx, om, stride, h, st); break;
+    case 3204: launch_fwd<32, 4, E>(e, c, B, off, idx, om, stride, h, st); break;
+    case 3208: launch_fwd<32, 8, E>(e, c, B, off, idx, om, stride, h, st); break;
+    default: throw Error(-9, "emb_forward: unsupported lane class");
+  }
 }
 
 void emb_forward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* idx, float* out,
@@ -1165,18 +1306,8 @@ void emb_forward_map(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t*
   for (size_t ci = 0; ci < e->classes.size(); ++ci) {
     const auto& c = e->classes[ci];
     cudaStream_t st = (ci & 1) ? e->fwd_side : main;
-    switch (c.G * 100 + c.VPL) {
-      case 101: launch_fwd<1, 1>(e, c, B, off, idx, om, stride, h, st); break;
-      case 201: launch_fwd<2, 1>(e, c, B, off, idx, om, stride, h, st); break;
-      case 401: launch_fwd<4, 1>(e, c, B, off, idx, om, stride, h, st); break;
-      case 801: launch_fwd<8, 1>(e, c, B, off, idx, om, stride, h, st); break;
-      case 1601: launch_fwd<16, 1>(e, c, B, off, idx, om, stride, h, st); break;
-      case 3201: launch_fwd<32, 1>(e, c, B, off, idx, om, stride, h, st); break;
-      case 3202: launch_fwd<32, 2>(e, c, B, off, idx, om, stride, h, st); break;
-      case 3204: launch_fwd<32, 4>(e, c, B, off, idx, om, stride, h, st); break;
-      case 3208: launch_fwd<32, 8>(e, c, B, off, idx, om, stride, h, st); break;
-      default: throw Error(-9, "emb_forward: unsupported lane class");
-    }
+    if (c.EB == 2) launch_fwd_class<__half>(e, c, B, off, idx, om, stride, h, st);
+    else launch_fwd_class<float>(e, c, B, off, idx, om, stride, h, st);
   }
   if (fork) {
     RS_CUDA(cudaEventRecord(e->ev_join, e->fwd_side));
@@ -1200,21 +1331,38 @@ void emb_kernel_times(rs_emb* e, double* fwd_ms, uint64_t* n_fwd, double* bwd_ms
 }
 
 // Short-segment bag pass for one lane class over its window range [wlo, whi).
-template <int G, int VPL, int UNR, int MINB>
+template <int G, int VPL, int UNR, int MINB, class E>
 static void launch_segs_v(rs_emb* e, const emb::BwdArgs& a, uint32_t ci, uint64_t max_windows, cudaStream_t st) {
   // the class's window range is on the device (bwd_plan_kernel): persistent
   // grid, capped by the class's largest possible window count
   const uint64_t est = max_windows * 8 / (uint64_t(emb::kBwdWarps) * (32 / G)) + 1;
   const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(est, uint64_t(sm_count()) * MINB)));
-  emb::bwd_seg_kernel<G, VPL, UNR, MINB><<<grid, emb::kBwdThreads, 0, st>>>(
+  emb::bwd_seg_kernel<G, VPL, UNR, MINB, E><<<grid, emb::kBwdThreads, 0, st>>>(
       a, e->segs, e->sbase, e->d_cw, ci, e->longs, e->long_np, e->long_ng, e->n_long);
   RS_COUNT(1);
 }
 
-template <int G, int VPL>
+template <int G, int VPL, class E>
 static void launch_segs(rs_emb* e, const emb::BwdArgs& a, uint32_t ci, uint64_t max_windows, cudaStream_t st) {
-  if constexpr (VPL == 1) launch_segs_v<G, 1, 4, 4>(e, a, ci, max_windows, st);
-  else launch_segs_v<G, VPL, (VPL == 2 ? 2 : 1), 2>(e, a, ci, max_windows, st);
+  if constexpr (VPL == 1) launch_segs_v<G, 1, 4, 4, E>(e, a, ci, max_windows, st);
+  else launch_segs_v<G, VPL, (VPL == 2 ? 2 : 1), 2, E>(e, a, ci, max_windows, st);
+}
+
+template <class E>
+static void launch_segs_class(rs_emb* e, const rs_emb::Class& c, const emb::BwdArgs& a, uint32_t ci, uint64_t mw,
+                              cudaStream_t cs) {
+  switch (c.G * 100 + c.VPL) {
+    case 101: launch_segs<1, 1, E>(e, a, ci, mw, cs); break;
+    case 201: launch_segs<2, 1, E>(e, a, ci, mw, cs); break;
+    case 401: launch_segs<4, 1, E>(e, a, ci, mw, cs); break;
+    case 801: launch_segs<8, 1, E>(e, a, ci, mw, cs); break;
+    case 1601: launch_segs<16, 1, E>(e, a, ci, mw, cs); break;
+    case 3201: launch_segs<32, 1, E>(e, a, ci, mw, cs); break;
+    case 3202: launch_segs<32, 2, E>(e, a, ci, mw, cs); break;
+    case 3204: launch_segs<32, 4, E>(e, a, ci, mw, cs); break;
+    case 3208: launch_segs<32, 8, E>(e, a, ci, mw, cs); break;
+    default: throw Error(-9, "emb_backward: unsupported lane class");
+  }
 }
 
 // Long segments: groups of 64 pieces, then one warp per segment (full warps,
@@ -1329,18 +1477,8 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
     const auto& c = e->classes[ci];
     const uint64_t mw = Wmax;
     cudaStream_t cs = (ci & 1) ? e->fwd_side : st;
-    switch (c.G * 100 + c.VPL) {
-      case 101: launch_segs<1, 1>(e, a, uint32_t(ci), mw, cs); break;
-      case 201: launch_segs<2, 1>(e, a, uint32_t(ci), mw, cs); break;
-      case 401: launch_segs<4, 1>(e, a, uint32_t(ci), mw, cs); break;
-      case 801: launch_segs<8, 1>(e, a, uint32_t(ci), mw, cs); break;
-      case 1601: launch_segs<16, 1>(e, a, uint32_t(ci), mw, cs); break;
-      case 3201: launch_segs<32, 1>(e, a, uint32_t(ci), mw, cs); break;
-      case 3202: launch_segs<32, 2>(e, a, uint32_t(ci), mw, cs); break;
-      case 3204: launch_segs<32, 4>(e, a, uint32_t(ci), mw, cs); break;
-      case 3208: launch_segs<32, 8>(e, a, uint32_t(ci), mw, cs); break;
-      default: throw Error(-9, "emb_backward: unsupported lane class");
-    }
+    if (c.EB == 2) launch_segs_class<__half>(e, c, a, uint32_t(ci), mw, cs);
+    else launch_segs_class<float>(e, c, a, uint32_t(ci), mw, cs);
   }
   if (fork) {
     RS_CUDA(cudaEventRecord(e->ev_join, e->fwd_side));
@@ -1399,6 +1537,16 @@ void emb_read_rows(rs_emb* e, uint32_t t, const uint32_t* rows, uint64_t n, floa
 void emb_free(rs_emb* e) {
   if (e) cudaStreamSynchronize(e->ctx->stream);
   delete e;
+}
+
+void emb_unbacked(rs_emb* e, uint64_t* lookups, uint64_t* rows, int reset) {
+  cudaStream_t st = e->ctx->stream;
+  if (lookups) {
+    RS_CUDA(cudaMemcpyAsync(lookups, e->d_unbacked, 8 * size_t(e->T), cudaMemcpyDeviceToHost, st));
+    RS_CUDA(cudaStreamSynchronize(st));
+  }
+  if (reset) RS_CUDA(cudaMemsetAsync(e->d_unbacked, 0, 8 * size_t(e->T), st));
+  if (rows) std::copy(e->unbacked_rows.begin(), e->unbacked_rows.end(), rows);
 }
 
 void emb_memory(const rs_emb* e, uint64_t* hbm, uint64_t* host) {

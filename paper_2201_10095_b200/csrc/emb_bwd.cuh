@@ -72,7 +72,7 @@ __device__ __forceinline__ uint32_t upper_index(const uint32_t* v, uint32_t n, u
 // Arithmetic order matches or_emb_backward: per-lane sum of squares in vec
 // order, xor butterfly over the G lanes (= lanes_for(dim) when G is; extra
 // lanes hold +0.0f, which leaves q >= 0 unchanged).
-template <int G, int VPL>
+template <int G, int VPL, class E>
 __device__ __forceinline__ void update_row(const BwdArgs& a, const TableDev& td, int32_t e,
                                            const float4 (&g)[VPL], const float4 (&w)[VPL],
                                            float m_old, unsigned gmask, int lg) {
@@ -95,7 +95,7 @@ __device__ __forceinline__ void update_row(const BwdArgs& a, const TableDev& td,
     if (lg == 0) *mom_ptr(td, e) = m;
     mult = __fdiv_rn(a.lr, __fadd_rn(__fsqrt_rn(m), a.eps));
   }
-  float4* wp = reinterpret_cast<float4*>(row_ptr(td, e));
+  char* wp = row_ptr(td, e);
 #pragma unroll
   for (int vv = 0; vv < VPL; ++vv) {
     const uint32_t vec = lg + vv * G;
@@ -105,7 +105,7 @@ __device__ __forceinline__ void update_row(const BwdArgs& a, const TableDev& td,
       x.y = __fsub_rn(x.y, __fmul_rn(mult, g[vv].y));
       x.z = __fsub_rn(x.z, __fmul_rn(mult, g[vv].z));
       x.w = __fsub_rn(x.w, __fmul_rn(mult, g[vv].w));
-      wp[vec] = x;
+      Elem<E>::store(wp, vec, x);
     }
   }
 }
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(256) bwd_seg_scan_kernel(BwdArgs a, WorkMap m,
 // end} descriptors from the scan).  Segments
 // of <= 32 positions are summed in position order and their row updated;
 // longer ones go to the long list (a slot each, with their group count).
-template <int G, int VPL, int UNR, int MINB>
+template <int G, int VPL, int UNR, int MINB, class E>
 __global__ void __launch_bounds__(kBwdThreads, MINB)
 bwd_seg_kernel(BwdArgs a, const uint4* __restrict__ segs, const uint32_t* __restrict__ sbase,
                const uint32_t* __restrict__ cw, uint32_t ci, uint4* __restrict__ longs,
@@ -394,13 +394,16 @@ bwd_seg_kernel(BwdArgs a, const uint4* __restrict__ segs, const uint32_t* __rest
     float4 w4[VPL];
     float m_old = 0.f;
     int32_t e = 0;
-    if (valid) {
+    // the unbacked sentinel (key nkeys) has no row: summed like any
+    // segment (keeps the warp's shuffles converged), never applied
+    const bool upd = valid && d.y < td.nkeys;
+    if (upd) {
       e = entry_of_key(td, d.y);
-      const float4* wr = reinterpret_cast<const float4*>(row_ptr(td, e));
+      const char* wr = row_ptr(td, e);
 #pragma unroll
       for (int vv = 0; vv < VPL; ++vv) {
         const uint32_t vec = lg + vv * G;
-        w4[vv] = vec < V ? wr[vec] : make_float4(0.f, 0.f, 0.f, 0.f);
+        w4[vv] = vec < V ? Elem<E>::load(wr, vec) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
       if (ada) m_old = *mom_ptr(td, e);
     }
@@ -432,7 +435,7 @@ bwd_seg_kernel(BwdArgs a, const uint4* __restrict__ segs, const uint32_t* __rest
       }
     }
     smp0 = d2.z != kNoKey ? a.vals[min(d2.x + uint32_t(lg), npos - 1)] : 0u;
-    if (valid) update_row<G, VPL>(a, td, e, acc, w4, m_old, gmask, lg);
+    if (upd) update_row<G, VPL, E>(a, td, e, acc, w4, m_old, gmask, lg);
     d = d2;
   }
 }
@@ -586,9 +589,17 @@ __global__ void __launch_bounds__(kBwdThreads) bwd_long_kernel(BwdArgs a, const 
     const uint4 L = longs[li];
     const TableDev& td = a.tables[L.w];
     const uint32_t V = td.dim >> 2;
+    if (L.z >= td.nkeys) continue;  // the unbacked sentinel: no row to update
     const int32_t e = entry_of_key(td, L.z);
     float4 w[VPL], acc[VPL], x[VPL];
-    load_vec<32, VPL>(row_ptr(td, e), V, lane, w);
+    {
+      const char* wr = row_ptr(td, e);
+#pragma unroll
+      for (int vv = 0; vv < VPL; ++vv) {
+        const uint32_t vec = lane + vv * 32;
+        w[vv] = vec < V ? load4(td, wr, vec) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
     const float m_old = a.opt == RS_OPT_ROWWISE_ADAGRAD ? *mom_ptr(td, e) : 0.f;
     const uint32_t g0 = gbase[li], g1 = gbase[li + 1];
     load_vec<32, VPL>(gpart + uint64_t(g0) * a.dmax, V, lane, acc);
@@ -597,7 +608,8 @@ __global__ void __launch_bounds__(kBwdThreads) bwd_long_kernel(BwdArgs a, const 
 #pragma unroll
       for (int vv = 0; vv < VPL; ++vv) add4(acc[vv], x[vv]);
     }
-    update_row<32, VPL>(a, td, e, acc, w, m_old, 0xffffffffu, lane);
+    if (td.ebytes == 2) update_row<32, VPL, __half>(a, td, e, acc, w, m_old, 0xffffffffu, lane);
+    else update_row<32, VPL, float>(a, td, e, acc, w, m_old, 0xffffffffu, lane);
   }
 }
 

@@ -433,6 +433,7 @@ float* exchange_forward(rs_exchange* x, rs_emb* e, const uint32_t* off, const ui
   if (x->kind == RS_EX_PEER) {
     if (!x->local.empty()) {
       OutMap om{};
+      om.out0 = mine;  // out_row's single-destination path (N == 1)
       om.peers = x->d_peer_blocks[x->parity];
       om.xcol = x->xcol;
       om.bl = x->bl;

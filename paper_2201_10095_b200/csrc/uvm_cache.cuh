@@ -34,6 +34,18 @@ constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
 constexpr uint32_t kClaim = 0xFFFFFFFEu;
 constexpr uint32_t kDeadRow = 0xFFFFFFFFu;  // slot_row of a slot whose copy-list entry overflowed
 
+// A warp copies one row of `bytes` (a multiple of 8: dim % 4 == 0 rows of
+// fp32 or fp16), 16 bytes per lane-access when the row allows it.
+__device__ __forceinline__ void copy_row_bytes(char* dst, const char* src, uint32_t bytes, int lane) {
+  if ((bytes & 15) == 0) {
+    for (uint32_t v = lane; v < bytes / 16; v += 32)
+      reinterpret_cast<float4*>(dst)[v] = reinterpret_cast<const float4*>(src)[v];
+  } else {
+    for (uint32_t v = lane; v < bytes / 8; v += 32)
+      reinterpret_cast<uint2*>(dst)[v] = reinterpret_cast<const uint2*>(src)[v];
+  }
+}
+
 // Claim / mark the staging slots of one batch's slow rows.  New slots are
 // queued in copy_list for the copy kernel.  Only tables with slow rows are
 // walked; a warp takes 32 consecutive bags of one table and flattens their
@@ -62,7 +74,8 @@ uvm_claim_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict
     for (uint32_t l = s0 + lane; l < s1; l += 32) {
       const int32_t e = td.remap[indices[l]];
       if (e >= 0) continue;
-      const uint32_t s = uint32_t(-int64_t(e) - 1);
+      const uint64_t s = slow_off(e);
+      if (s >= td.slow_rows) continue;  // unbacked: nothing to stage
       uint32_t* p = td.slot_of + s;
       const uint32_t old = atomicCAS(p, kNoSlot, kClaim);
       if (old == kNoSlot) {
@@ -75,13 +88,13 @@ uvm_claim_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict
         }
         const uint32_t slot = free_stack[top - 1];
         slot_tab[slot] = t;
-        slot_row[slot] = s;
+        slot_row[slot] = uint32_t(s);
         slot_gen[slot] = gen_bit;
         const unsigned k = atomicAdd(ncopy, 1u);
         if (k < cap) {
           copy_list[k] = slot;
           copy_tab[k] = t;
-          copy_row[k] = s;
+          copy_row[k] = uint32_t(s);
           __threadfence();
           atomicExch(p, slot);
         } else {
@@ -104,16 +117,12 @@ uvm_claim_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict
 __global__ void __launch_bounds__(256)
 uvm_scatter_in_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__ copy_list,
                       const uint32_t* __restrict__ copy_tab, const unsigned* __restrict__ ncopy, uint32_t cap,
-                      const float* __restrict__ bounce, float* __restrict__ staging, uint64_t stride) {
+                      const char* __restrict__ bounce, char* __restrict__ staging, uint64_t stride) {
   const int lane = threadIdx.x & 31;
   const uint64_t n = min(*ncopy, cap);
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t k = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; k < n; k += nwarps) {
-    const uint32_t V = tables[copy_tab[k]].dim >> 2;
-    const float4* src = reinterpret_cast<const float4*>(bounce + k * stride);
-    float4* dst = reinterpret_cast<float4*>(staging + uint64_t(copy_list[k]) * stride);
-    for (uint32_t v = lane; v < V; v += 32) dst[v] = src[v];
-  }
+  for (uint64_t k = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; k < n; k += nwarps)
+    copy_row_bytes(staging + uint64_t(copy_list[k]) * stride, bounce + k * stride, tables[copy_tab[k]].rbytes, lane);
 }
 
 // Release every slot of generation bit `gen_bit` that no batch in `keep`
@@ -124,8 +133,8 @@ __global__ void __launch_bounds__(256)
 uvm_evict_kernel(const TableDev* __restrict__ tables, uint32_t nslots, uint32_t gen_bit, uint32_t keep,
                  uint32_t* __restrict__ slot_gen, const uint32_t* __restrict__ slot_tab,
                  const uint32_t* __restrict__ slot_row, uint32_t* __restrict__ free_stack,
-                 int* __restrict__ free_top, const float* __restrict__ staging, uint64_t stride,
-                 float* __restrict__ bounce, uint32_t* __restrict__ wb_tab, uint32_t* __restrict__ wb_row,
+                 int* __restrict__ free_top, const char* __restrict__ staging, uint64_t stride,
+                 char* __restrict__ bounce, uint32_t* __restrict__ wb_tab, uint32_t* __restrict__ wb_row,
                  uint32_t cap, unsigned* __restrict__ n_wb, unsigned* __restrict__ err) {
   const int lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
@@ -154,9 +163,7 @@ uvm_evict_kernel(const TableDev* __restrict__ tables, uint32_t nslots, uint32_t 
       const TableDev& td = tables[t];
       const uint32_t s = slot_row[slot];
       if (k0 < cap) {
-        const float4* from = reinterpret_cast<const float4*>(staging + uint64_t(slot) * stride);
-        float4* to = reinterpret_cast<float4*>(bounce + uint64_t(k0) * stride);
-        for (uint32_t v = lane; v < (td.dim >> 2); v += 32) to[v] = from[v];
+        copy_row_bytes(bounce + uint64_t(k0) * stride, staging + uint64_t(slot) * stride, td.rbytes, lane);
         if (lane == 0) {
           wb_tab[k0] = t;
           wb_row[k0] = s;

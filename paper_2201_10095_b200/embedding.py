@@ -6,7 +6,10 @@ backward}``, whose forward accounting equals ``simulate()``
 (core/src/simulator.cpp:86).  Rows live in the fast tier (HBM) or the slow
 tier (pinned host memory read zero-copy over PCIe) as each table's remap
 says; forward is a sum-pool, backward a deterministic row-wise SGD or
-exact-row-wise-Adagrad update (csrc/emb.cu).
+exact-row-wise-Adagrad update (csrc/emb.cu).  Rows are fp32 or fp16
+(TableSpec.elem_bytes 2); arithmetic is fp32.  With an omit_unaccessed remap
+only the profiled slow rows have storage; the others pool as zeros and drop
+their gradients (counted by ``unbacked()``).
 """
 from __future__ import annotations
 
@@ -36,17 +39,26 @@ class TieredEmbeddingBag:
         self.hbm_rows = [int(r.hbm_rows) for r in remaps]
         tabs = (_lib.rs_emb_table * len(specs))()
         hold = []
+        self.unbacked_tables = 0
         for i, (s, r) in enumerate(zip(specs, remaps)):
-            if s.elem_bytes != 4:
-                raise InvalidArgument("TieredEmbeddingBag: fp32 tables only (elem_bytes 4)")
+            if s.elem_bytes not in (2, 4):  # inc/types.hpp:50-52
+                raise InvalidArgument(f"table {s.table_id}: elem_bytes must be 2 or 4")
+            # an omit_unaccessed remap (inc/remap.hpp:43-48) backs only its
+            # slow_rows_allocated prefix; the rest pool as zero rows
+            slow = int(s.hash_size - r.hbm_rows)
+            alloc = int(r.slow_rows_allocated)
+            unbacked = alloc < slow
+            if unbacked:
+                slow = alloc
+                self.unbacked_tables += 1
             if is_device(r.entries):
                 p, loc = ptr(r.entries), _lib.RS_MEM_DEVICE
             else:
                 a = np.ascontiguousarray(r.entries, np.int32)
                 hold.append(a)
                 p, loc = ptr(a), _lib.RS_MEM_HOST
-            tabs[i] = _lib.rs_emb_table(s.table_id, s.hash_size, s.dim, p, loc, r.hbm_rows,
-                                        s.hash_size - r.hbm_rows)
+            tabs[i] = _lib.rs_emb_table(s.table_id, s.hash_size, s.dim, p, loc, r.hbm_rows, slow,
+                                        s.elem_bytes, int(unbacked))
         h = C.c_void_p()
         _lib.check(_lib.lib().rs_emb_create(self.ctx.h, len(specs), tabs, C.c_uint64(max_batch),
                                             C.c_uint64(max_lookups), OPTIMIZERS[optimizer],
@@ -110,6 +122,16 @@ class TieredEmbeddingBag:
         _lib.check(_lib.lib().rs_emb_kernel_times(self.h, C.byref(f), C.byref(nf), C.byref(b),
                                                   C.byref(nb), int(reset)))
         return float(f.value), int(nf.value), float(b.value), int(nb.value)
+
+    def unbacked(self, reset: bool = False):
+        """(lookups, rows) per table: lookups of rows an omit_unaccessed remap
+        left without storage since the last reset (they pooled as zero rows),
+        and how many remap entries are unbacked."""
+        n = len(self.specs)
+        lk = np.zeros(n, np.uint64)
+        rw = np.zeros(n, np.uint64)
+        _lib.check(_lib.lib().rs_emb_unbacked(self.h, ptr(lk), ptr(rw), int(reset)))
+        return lk, rw
 
     def memory(self):
         a, b = C.c_uint64(), C.c_uint64()

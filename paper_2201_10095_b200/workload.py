@@ -65,7 +65,9 @@ def cfg1_specs():
 RM_SHAPES = {
     "rm1": dict(J=100, hlo=1e5, hhi=1e7, dims=(64, 128)),
     "rm2": dict(J=300, hlo=1e5, hhi=1e7, dims=(64, 128)),
-    "rm3": dict(J=512, hlo=1e5, hhi=1e8, dims=(256,)),
+    # fp16 rows (TableSpec.elem_bytes 2): 512 tables of up to 1e8 x 256 rows
+    # are ~3.8 TB even at 2 bytes — served with omit_unaccessed remaps
+    "rm3": dict(J=512, hlo=1e5, hhi=1e8, dims=(256,), elem_bytes=2),
 }
 
 
@@ -89,7 +91,8 @@ def rm_specs(name: str, seed: int = 20260809, J: int | None = None, hash_scale: 
         law = laws[j % 3]
         if law == 0:
             pool = float(max(1, round(pool)))
-        out.append(WorkloadSpec(TableSpec(j, card, H, D, 4), FeatureGenSpec(alpha, pool, cov, law)))
+        out.append(WorkloadSpec(TableSpec(j, card, H, D, shp.get("elem_bytes", 4)),
+                                FeatureGenSpec(alpha, pool, cov, law)))
     return out
 
 
