@@ -93,7 +93,11 @@ __device__ __forceinline__ uint64_t fast_mod(uint64_t x, uint64_t d, uint64_t m)
 // ---------------------------------------------------------------- memory
 __device__ __forceinline__ float4 ld_nc_f4(const float4* p) {
   float4 r;
+#ifdef RS_NC_NONVOLATILE
+  asm("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
+#else
   asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
+#endif
                : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
                : "l"(p));
   return r;

@@ -72,6 +72,12 @@ template <class E>
 struct Elem;
 template <>
 struct Elem<float> {
+  using Raw = float4;  // a lane's four stored elements, as loaded
+  static __device__ __forceinline__ Raw load_raw_nc(const char* row, uint32_t vec) {
+    return ld_nc_f4(reinterpret_cast<const float4*>(row) + vec);
+  }
+  static __device__ __forceinline__ float4 widen_raw(Raw r) { return r; }
+  static __device__ __forceinline__ Raw zero_raw() { return make_float4(0.f, 0.f, 0.f, 0.f); }
   static __device__ __forceinline__ float4 load_nc(const char* row, uint32_t vec) {
     return ld_nc_f4(reinterpret_cast<const float4*>(row) + vec);
   }
@@ -84,11 +90,17 @@ struct Elem<float> {
 };
 template <>
 struct Elem<__half> {
+  using Raw = uint2;
+  static __device__ __forceinline__ Raw load_raw_nc(const char* row, uint32_t vec) {
+    return ld_nc_u2(reinterpret_cast<const uint2*>(row) + vec);
+  }
+  static __device__ __forceinline__ Raw zero_raw() { return make_uint2(0u, 0u); }
   static __device__ __forceinline__ float4 widen(uint2 u) {
     const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
     const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
     return make_float4(a.x, a.y, b.x, b.y);
   }
+  static __device__ __forceinline__ float4 widen_raw(Raw r) { return widen(r); }
   static __device__ __forceinline__ float4 load_nc(const char* row, uint32_t vec) {
     return widen(ld_nc_u2(reinterpret_cast<const uint2*>(row) + vec));
   }
@@ -139,6 +151,18 @@ __device__ __forceinline__ char* row_ptr(const TableDev& td, int32_t e) {
   }
   return td.slow + s * td.rbytes;
 }
+// The fast tier's base and row size held in registers for a hot loop (the
+// compiler otherwise re-reads them from the table array for every row: stores
+// elsewhere in the loop may alias it); slow rows take row_ptr.
+struct RowBase {
+  char* fast;
+  uint32_t rbytes;
+};
+__device__ __forceinline__ RowBase row_base(const TableDev& td) { return RowBase{td.fast, td.rbytes}; }
+__device__ __forceinline__ char* row_ptr(const TableDev& td, const RowBase& rb, int32_t e) {
+  if (e >= 0) return rb.fast + uint64_t(uint32_t(e)) * rb.rbytes;
+  return row_ptr(td, e);
+}
 __device__ __forceinline__ float* mom_ptr(const TableDev& td, int32_t e) {
   return e >= 0 ? td.mom_fast + uint64_t(e) : td.mom_slow + slow_off(e);
 }
@@ -156,9 +180,6 @@ __device__ __forceinline__ int32_t entry_of_key(const TableDev& td, uint32_t key
 }
 
 constexpr int kFwdThreads = 256;
-#ifndef RS_FWD_MINB
-#define RS_FWD_MINB 6
-#endif
 
 // Flushes a warp's accumulated (fast, total) lookup counts for table t (the
 // caller's simulate() accounting, may be null) and its unbacked-row lookups.
@@ -179,20 +200,8 @@ __device__ __forceinline__ void flush_hits(unsigned long long* hits, unsigned lo
   }
 }
 
-// Pipelined-bag helpers of forward_kernel: the bag's table and CSR offsets,
-// its first G indices, their (checked) remap entries.
-__device__ __forceinline__ void fwd_bag_offsets(const uint32_t* __restrict__ cls_tables,
-                                                const uint32_t* __restrict__ offsets, uint64_t B, uint64_t wpt,
-                                                int BPW, int grp, uint64_t ww, uint32_t& t, uint32_t& s,
-                                                uint32_t& e) {
-  t = cls_tables[ww / wpt];
-  const uint64_t bb = (ww % wpt) * BPW + grp;
-  s = e = 0;
-  if (bb < B) {
-    s = offsets[uint64_t(t) * B + bb];
-    e = offsets[uint64_t(t) * B + bb + 1];
-  }
-}
+// Pipelined-bag helpers of forward_kernel: the bag's first G indices and
+// their (checked) remap entries.
 __device__ __forceinline__ uint32_t fwd_bag_index(const uint32_t* __restrict__ indices, int lg, uint32_t s,
                                                   uint32_t e) {
   return s < e && uint32_t(lg) < e - s ? ld_stream_u32(indices + s + lg) : 0u;
@@ -208,53 +217,97 @@ __device__ __forceinline__ int32_t fwd_bag_entry(const TableDev* __restrict__ ta
   return tn.remap[idx];
 }
 
-// Software-pipelined over the warp's grid-stride bags: the next bag's
+// K4: a G-lane group per bag (BPW = 32/G bags per warp-iteration, a
+// "bag-group"), software-pipelined over the warp's bags: the next bag's
 // offsets are loaded at the top of this one, its first G indices once this
 // bag's first row loads are in flight, and their remap entries once those
 // rows have arrived — so a bag's dependent chain is its row loads, not
 // offsets -> index -> remap -> rows.
+//
+// Scheduling: a warp claims `chunk` consecutive bag-groups (one atomic per
+// chunk, the next chunk claimed a chunk ahead) and walks them in order with
+// 32-bit incremental (table, bag) bookkeeping.  Small chunks keep the whole
+// GPU inside a narrow band of one table's bags, so the table's Zipf head
+// stays hot in L1/L2 (measured on B200, RM1: chunk 1 1.68 ms (counter
+// contention), 2 1.30, 4 1.44, 16 2.03, 64 4.68; the old grid-stride loop
+// 1.55 ms), and the per-table hit counters are flushed only when the table
+// changes.
 template <int G, int VPL, int UNR, int MINB, class E>
 __global__ void __launch_bounds__(kFwdThreads, MINB)
 forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__ cls_tables,
-               uint32_t ntab, uint64_t B, const uint32_t* __restrict__ offsets,
-               const uint32_t* __restrict__ indices, const OutMap om, uint64_t stride,
-               unsigned long long* __restrict__ hits, unsigned long long* __restrict__ unbacked,
-               uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t max_keys,
-               unsigned* __restrict__ err) {
+                uint32_t ntab, uint32_t B, const uint32_t* __restrict__ offsets,
+                const uint32_t* __restrict__ indices, const OutMap om, uint64_t stride,
+                unsigned long long* __restrict__ hits, unsigned long long* __restrict__ unbacked,
+                uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t max_keys,
+                unsigned* __restrict__ err, uint32_t* __restrict__ work, uint32_t chunk) {
   constexpr int BPW = 32 / G;
-  constexpr int kFwdUnroll = UNR;
   const int lane = threadIdx.x & 31;
   const int grp = lane / G, lg = lane % G;
   const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
-  const uint64_t wpt = (B + BPW - 1) / BPW;
-  const uint64_t total_w = wpt * ntab;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t wpt = (B + BPW - 1) / BPW;  // bag-groups per table
+  const uint32_t total_w = wpt * ntab;
+  auto grab = [&]() {
+    uint32_t c = 0;
+    if (lane == 0) c = atomicAdd(work, 1u);
+    return __shfl_sync(0xffffffffu, c, 0);
+  };
   uint32_t cur_t = 0xFFFFFFFFu, fast = 0, tot = 0, unb = 0;
-  // the pipelined bag: table, offsets, first G indices (checked) and entries
+  // cursor: w (linear bag-group), wend (its chunk's end), ti / k (table slot,
+  // bag-group within the table); cn: the chunk claimed ahead
+  uint32_t w = grab() * chunk;
+  if (w >= total_w) return;
+  uint32_t wend = min(total_w, w + chunk);
+  uint32_t ti = w / wpt, k = w - ti * wpt;
+  uint32_t cn = grab();
+  auto bag_offsets = [&](uint32_t ti_, uint32_t k_, uint32_t& t_, uint32_t& s_, uint32_t& e_) {
+    t_ = cls_tables[ti_];
+    const uint32_t bb = k_ * BPW + grp;
+    s_ = e_ = 0;
+    if (bb < B) {
+      const uint64_t o = uint64_t(t_) * B + bb;
+      s_ = offsets[o];
+      e_ = offsets[o + 1];
+    }
+  };
   uint32_t nt = 0, ns = 0, ne = 0, nidx = 0;
   int32_t nent = 0;
-  uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (w < total_w) {
-    fwd_bag_offsets(cls_tables, offsets, B, wpt, BPW, grp, w, nt, ns, ne);
-    nidx = fwd_bag_index(indices, lg, ns, ne);
-    nent = fwd_bag_entry(tables, err, lg, nt, ns, ne, nidx);
-  }
-  for (; w < total_w; w += nwarps) {
+  bag_offsets(ti, k, nt, ns, ne);
+  nidx = fwd_bag_index(indices, lg, ns, ne);
+  nent = fwd_bag_entry(tables, err, lg, nt, ns, ne, nidx);
+  while (true) {
     const uint32_t t = nt, s = ns, e = ne;
     const int32_t ent0 = nent;
-    const uint64_t w2 = w + nwarps;
-    const bool more = w2 < total_w;
-    if (more) fwd_bag_offsets(cls_tables, offsets, B, wpt, BPW, grp, w2, nt, ns, ne);
+    const uint32_t kb = k;
+    // advance the cursor to the next bag-group
+    bool more = true;
+    if (w + 1 < wend) {
+      ++w;
+      if (++k == wpt) {
+        k = 0;
+        ++ti;
+      }
+    } else {
+      w = cn * chunk;
+      if (w < total_w) {
+        wend = min(total_w, w + chunk);
+        ti = w / wpt;
+        k = w - ti * wpt;
+        cn = grab();
+      } else {
+        more = false;
+      }
+    }
+    if (more) bag_offsets(ti, k, nt, ns, ne);
     bool pf = !more;  // next bag's index/entry issued?
     if (t != cur_t) {
       if (cur_t != 0xFFFFFFFFu) flush_hits(hits, unbacked, cur_t, fast, tot, unb);
       fast = tot = unb = 0;
       cur_t = t;
     }
-    // the table's fields are re-read per bag (L1 hits) rather than held live
     const TableDev& td = tables[t];
     const uint32_t V = td.dim >> 2;
-    const uint64_t b = (w % wpt) * BPW + grp;
+    const RowBase rbase = row_base(td);
+    const uint32_t b = kb * BPW + grp;
     const bool valid = b < B;
     float4 acc[VPL];
 #pragma unroll
@@ -280,23 +333,21 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
         }
         fast += ent >= 0;
         unb += ent < 0 && slow_off(ent) >= td.slow_rows;
-        // the backward's sort keys, while the remap entry is in hand
-        // (key = storage slot within the table, value = sample)
         if (keys) {
           if (l < max_keys) {
             keys[l] = slot_of_entry(td, ent);
-            vals[l] = uint32_t(b);
+            vals[l] = b;
           } else {
             atomicOr(err, 2u);
           }
         }
       }
-      for (uint32_t j = 0; j < n; j += kFwdUnroll) {
-        float4 v[kFwdUnroll][VPL];
+      for (uint32_t j = 0; j < n; j += UNR) {
+        float4 v[UNR][VPL];
 #pragma unroll
-        for (int u = 0; u < kFwdUnroll; ++u) {
+        for (int u = 0; u < UNR; ++u) {
           const int32_t eu = __shfl_sync(gmask, ent, int(j) + u, G);
-          const char* row = row_ptr(td, eu);
+          const char* row = row_ptr(td, rbase, eu);
 #pragma unroll
           for (int vv = 0; vv < VPL; ++vv) {
             const uint32_t vec = lg + vv * G;
@@ -305,7 +356,7 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
         }
         if (!pf) nidx = fwd_bag_index(indices, lg, ns, ne);  // behind this bag's first rows
 #pragma unroll
-        for (int u = 0; u < kFwdUnroll; ++u) {
+        for (int u = 0; u < UNR; ++u) {
           if (j + u < n) {
 #pragma unroll
             for (int vv = 0; vv < VPL; ++vv) {
@@ -334,6 +385,7 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
         if (vec < V) o[vec] = acc[vv];
       }
     }
+    if (!more) break;
   }
   if (cur_t != 0xFFFFFFFFu) flush_hits(hits, unbacked, cur_t, fast, tot, unb);
 }
@@ -487,6 +539,7 @@ struct rs_emb {
   // unbacked rows (omit_unaccessed remaps): per-table lookup counters, the
   // zero row they read, and how many remap entries each table leaves unbacked
   unsigned long long* d_unbacked = nullptr;
+  uint32_t* d_work = nullptr;  // forward_kernel's chunk counters (one per lane class)
   char* zero_row = nullptr;
   std::vector<uint64_t> unbacked_rows;
   // forward classes: (G, VPL, element bytes) -> table list
@@ -666,7 +719,7 @@ struct rs_emb {
       cudaStreamDestroy(fwd_side);
     }
     if (d_err) cudaFree(d_err);
-    for (void* p : {(void*)d_unbacked, (void*)zero_row})
+    for (void* p : {(void*)d_unbacked, (void*)zero_row, (void*)d_work})
       if (p) cudaFree(p);
     if (sort_scratch) cudaFree(sort_scratch);
     if (side) {
@@ -777,6 +830,7 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
     RS_CUDA(cudaMalloc(&e->remap_pool, std::max<size_t>(rb, 256)));
     RS_CUDA(cudaMalloc(&e->d_err, 16));
     RS_CUDA(cudaMalloc(&e->d_unbacked, 8 * size_t(T)));
+    RS_CUDA(cudaMalloc(&e->d_work, 256));
     RS_CUDA(cudaMemsetAsync(e->d_unbacked, 0, 8 * size_t(T), st));
     RS_CUDA(cudaMalloc(&e->zero_row, 4096));
     RS_CUDA(cudaMemsetAsync(e->zero_row, 0, 4096, st));
@@ -1230,31 +1284,39 @@ void emb_init_weights(rs_emb* e, uint64_t seed, float scale) {
   RS_LAUNCH_CHECK();
 }
 
+static uint32_t fwd_chunk() {
+  static const uint32_t c = [] {
+    const char* v = getenv("RS_FWD_CHUNK");
+    return v ? uint32_t(std::max(1, atoi(v))) : 4u;
+  }();
+  return c;
+}
+
 template <int G, int VPL, class E>
 static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint32_t* off,
                        const uint32_t* idx, const OutMap& out, uint64_t stride, unsigned long long* hits,
                        cudaStream_t st) {
   constexpr int BPW = 32 / G;
-  const uint64_t warps = (B + BPW - 1) / BPW * c.tables.size();
-  const uint64_t blocks = (warps * 32 + emb::kFwdThreads - 1) / emb::kFwdThreads;
-  const unsigned grid = std::max(1u, unsigned(std::min<uint64_t>(blocks, uint64_t(sm_count()) * 64)));
-  auto args = std::make_tuple(e->cur_tables, c.d_list, uint32_t(c.tables.size()), B, off, idx, out,
-                              stride, hits, e->d_unbacked, e->keys, e->vals, uint64_t(e->max_lookups), e->d_err);
-  auto go = [&](auto kern) {
-    std::apply([&](auto... a) { kern<<<grid, emb::kFwdThreads, 0, st>>>(a...); }, args);
-  };
-  // (unroll, min blocks/SM): measured on B200 RM1 all-HBM — (4, 6) 1.15 ms,
-  // (2, 8) 1.14, (4, 8) 1.17, (6, 6) 1.22, (8, 6) 1.55, (8, 1) 1.85
-  if constexpr (VPL > 1) {
-    go(emb::forward_kernel<G, VPL, 8, 1, E>);
-  } else {
-    static const int minb = [] {  // A/B knob: RS_FWD_MINB=4 trades occupancy for no spills
-      const char* v = getenv("RS_FWD_MINB");
-      return v ? atoi(v) : RS_FWD_MINB;
-    }();
-    if (minb == 4) go(emb::forward_kernel<G, VPL, 4, 4, E>);
-    else go(emb::forward_kernel<G, VPL, 4, 6, E>);
-  }
+  const uint64_t warps = (B + BPW - 1) / BPW * c.tables.size();  // bag-groups
+  // persistent: one full wave; the class's own chunk counter (classes run
+  // on two streams)
+  uint32_t* work = e->d_work + (&c - e->classes.data());
+  const uint32_t chunk = fwd_chunk();
+  const uint64_t chunks = (warps + chunk - 1) / chunk;
+  if (warps >= (uint64_t(1) << 32)) throw InvalidArgument("emb_forward: batch too large for one launch");
+  constexpr int MINB = VPL > 1 ? 1 : 5;  // B200 RM1: (unroll 4, 5 CTAs/SM) 1.27 ms, 6: 1.33, 4: 1.82
+  auto kern = emb::forward_kernel<G, VPL, (VPL > 1 ? 8 : 4), MINB, E>;
+  static const int per_sm = [&] {
+    int n = 0;
+    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, emb::kFwdThreads, 0));
+    return std::max(1, n);
+  }();
+  const unsigned grid = unsigned(std::max<uint64_t>(
+      1, std::min<uint64_t>(uint64_t(sm_count()) * per_sm, (chunks * 32 + emb::kFwdThreads - 1) / emb::kFwdThreads)));
+  RS_CUDA(cudaMemsetAsync(work, 0, 4, st));
+  kern<<<grid, emb::kFwdThreads, 0, st>>>(
+      e->cur_tables, c.d_list, uint32_t(c.tables.size()), uint32_t(B), off, idx, out, stride, hits, e->d_unbacked,
+      e->keys, e->vals, uint64_t(e->max_lookups), e->d_err, work, chunk);
   RS_COUNT(1);
 }
 
