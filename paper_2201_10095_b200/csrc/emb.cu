@@ -1392,6 +1392,9 @@ void emb_kernel_times(rs_emb* e, double* fwd_ms, uint64_t* n_fwd, double* bwd_ms
   }
 }
 
+#ifndef RS_SEG_MINB
+#define RS_SEG_MINB 4
+#endif
 // Short-segment bag pass for one lane class over its window range [wlo, whi).
 template <int G, int VPL, int UNR, int MINB, class E>
 static void launch_segs_v(rs_emb* e, const emb::BwdArgs& a, uint32_t ci, uint64_t max_windows, cudaStream_t st) {
@@ -1406,7 +1409,7 @@ static void launch_segs_v(rs_emb* e, const emb::BwdArgs& a, uint32_t ci, uint64_
 
 template <int G, int VPL, class E>
 static void launch_segs(rs_emb* e, const emb::BwdArgs& a, uint32_t ci, uint64_t max_windows, cudaStream_t st) {
-  if constexpr (VPL == 1) launch_segs_v<G, 1, 4, 4, E>(e, a, ci, max_windows, st);
+  if constexpr (VPL == 1) launch_segs_v<G, 1, 4, RS_SEG_MINB, E>(e, a, ci, max_windows, st);
   else launch_segs_v<G, VPL, (VPL == 2 ? 2 : 1), 2, E>(e, a, ci, max_windows, st);
 }
 

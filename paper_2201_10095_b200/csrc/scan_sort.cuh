@@ -251,8 +251,11 @@ radix_upsweep(const uint32_t* __restrict__ keys, size_t n, int shift, int nbits,
 
 // Stable scatter: offsets[d * ntiles + tile] holds the global start of digit d
 // for this tile (exclusive scan of the digit-major count matrix).
+#ifndef RS_SORT_MINB
+#define RS_SORT_MINB 5
+#endif
 template <bool HAS_VALUES>
-static __global__ void __launch_bounds__(kSortThreads)
+static __global__ void __launch_bounds__(kSortThreads, RS_SORT_MINB)
 radix_downsweep(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                 size_t n, int shift, int nbits, const uint32_t* __restrict__ offsets,
                 unsigned ntiles, uint32_t* __restrict__ keys_out,
