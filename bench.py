@@ -529,7 +529,11 @@ def run_profile_sweep(args, torch, ctx, hbm_peak):
         t0 = time.perf_counter()
         p = sp.profiler.profile_handle(tr, 1.0, PROFILE_SEED, ctx=ctx)
         times.append(time.perf_counter() - t0)
+        # release this result before the next call, so its pinned host buffers
+        # return to the context's pool (a live result makes the next call pin
+        # fresh pages: ~25 ms per 100 MB, which is host allocation, not profiling)
         p.close()
+        del p
     secs = float(np.median(times))
     H = sum(w.table.hash_size for w in specs)
     alg = 4.0 * n + 24.0 * R + 8.0 * H  # id + record + (zero + read) per row

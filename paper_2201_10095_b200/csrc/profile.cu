@@ -12,6 +12,7 @@
 // CPU and GPU); the ICDF uses the reference's integer test
 // 100*prefix(k) >= i*total (core/src/profiler.cpp:38).
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <numeric>
 
@@ -364,11 +365,25 @@ rec_info_kernel(const uint64_t* __restrict__ rec_sample, const uint32_t* __restr
   }
 }
 
+constexpr uint32_t kPSmemTables = 512;  // per-table (base, H) held in shared memory up to this J
+
 struct PSmem {
   uint32_t woff[kPRecWin + 1];  // record offsets of the window (+ end sentinel)
   uint32_t winfo[kPRecWin];
   uint32_t r0, nrec;
+  uint32_t tbase[kPSmemTables];  // group-local counter base of table index t (< 2^31)
+  uint32_t thash[kPSmemTables];  // its hash size
 };
+
+// Loads the per-table (base, H) of the launch's tables into shared memory
+// (the expansion otherwise reads both from global memory for every id).
+__device__ __forceinline__ void load_table_params(const Tables& tp, PSmem& sm) {
+  if (tp.J > kPSmemTables) return;
+  for (uint32_t t = threadIdx.x; t < tp.J; t += blockDim.x) {
+    sm.tbase[t] = uint32_t(tp.base[t]);
+    sm.thash[t] = uint32_t(tp.hsize[t]);
+  }
+}
 
 // Expands tile [a, a + kPTile) of the id pool: fn(addr) for every selected id
 // of an in-group table.  *rcur: first record of the tile (advanced to the
@@ -448,10 +463,11 @@ __device__ __forceinline__ void expand_tile(uint64_t a, uint64_t N, uint64_t R, 
         while (k + 1 <= nwin && sm.woff[k + 1] <= q) ++k;
         const uint32_t t = sm.winfo[k];
         if (t != kSkip) {
-          const uint64_t H = tp.hsize[t];
+          const bool smt = tp.J <= kPSmemTables;
+          const uint64_t H = smt ? sm.thash[t] : tp.hsize[t];
           const uint64_t row = RAW ? fast_mod(mix64(rawv[u]), H, tp.magic[t]) : uint64_t(idv[u]);
           if (row >= H) atomicOr(err, kErrRowRange);
-          else fn(uint32_t(tp.base[t] + row), u);
+          else fn(uint32_t((smt ? sm.tbase[t] : tp.base[t]) + row), u);
         }
       }
     }
@@ -488,11 +504,12 @@ template <bool RAW, bool SCATTER>
 __global__ void __launch_bounds__(kPThreads)
 part_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restrict__ rinfo, uint64_t R, uint64_t N,
             const uint32_t* __restrict__ ids, const uint64_t* __restrict__ raw, Tables tp, uint32_t nb,
-            uint64_t ids_per_cta, uint32_t* __restrict__ mat, uint32_t* __restrict__ out,
+            uint64_t ids_per_cta, uint32_t* __restrict__ mat, uint16_t* __restrict__ out,
             unsigned* __restrict__ err, unsigned* __restrict__ bad) {
   __shared__ PSmem sm;
   extern __shared__ uint32_t cnt[];  // [nb] counts (P1) or cursors (P2) | P2: tile counts, offsets
   const uint32_t nct = gridDim.x;
+  load_table_params(tp, sm);
   for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x)
     cnt[i] = SCATTER ? mat[uint64_t(i) * nct + blockIdx.x] : 0u;
   const uint64_t a0 = uint64_t(blockIdx.x) * ids_per_cta;
@@ -549,7 +566,7 @@ part_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restrict__ rinf
     for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
       const uint32_t x = stage[i];
       const uint32_t b = x >> kP3Bits;
-      out[cnt[b] + (i - toff[b])] = x;
+      out[cnt[b] + (i - toff[b])] = uint16_t(x & ((1u << kP3Bits) - 1));  // bucket-local (the region is the bucket)
     }
     __syncthreads();
     for (uint32_t j = 0; j < per; ++j) {
@@ -582,7 +599,7 @@ __global__ void part_chunks_kernel(const uint32_t* __restrict__ bstart, uint32_t
 // position of bucket b (bstart[nb] = total), cbase = exclusive scan of the
 // chunk counts (cbase[nb] = total chunks).
 __global__ void __launch_bounds__(1024)
-part_hist_kernel(const uint32_t* __restrict__ addrs, const uint32_t* __restrict__ bstart,
+part_hist_kernel(const uint16_t* __restrict__ addrs, const uint32_t* __restrict__ bstart,
                  const uint32_t* __restrict__ cbase, uint32_t nb, uint32_t chunk,
                  uint32_t* __restrict__ counters, uint64_t ncounters) {
   extern __shared__ uint32_t h[];
@@ -601,19 +618,31 @@ part_hist_kernel(const uint32_t* __restrict__ addrs, const uint32_t* __restrict_
     __syncthreads();
     const uint32_t p0 = bstart[b] + c * chunk;
     const uint32_t p1 = min(bstart[b + 1], p0 + chunk);
-    // 8 address loads in flight per thread, then their atomics
+    // 8 address loads in flight per thread (two 16-bit bucket-local
+    // addresses per 32-bit load), then their atomics
     constexpr int U = 8;
-    for (uint32_t pb = p0; pb < p1; pb += U * blockDim.x) {
+    const uint32_t* a32 = reinterpret_cast<const uint32_t*>(addrs);
+    uint32_t q = p0;
+    if ((q & 1) && q < p1) {  // odd head: one 16-bit address
+      if (threadIdx.x == 0) atomicAdd(&h[addrs[q]], 1u);
+      ++q;
+    }
+    const uint32_t w0 = q >> 1, w1 = p1 >> 1;  // whole 32-bit words [w0, w1)
+    for (uint32_t pb = w0; pb < w1; pb += U * blockDim.x) {
       uint32_t x[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint32_t p = pb + u * blockDim.x + threadIdx.x;
-        x[u] = p < p1 ? __ldcs(addrs + p) : 0xFFFFFFFFu;
+        x[u] = p < w1 ? __ldcs(a32 + p) : 0xFFFFFFFFu;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (x[u] != 0xFFFFFFFFu) atomicAdd(&h[x[u] & (span - 1)], 1u);
+        if (pb + u * blockDim.x + threadIdx.x < w1) {
+          atomicAdd(&h[x[u] & 0xFFFFu], 1u);
+          atomicAdd(&h[x[u] >> 16], 1u);
+        }
     }
+    if ((p1 & 1) && p1 > q && threadIdx.x == 0) atomicAdd(&h[addrs[p1 - 1]], 1u);  // odd tail
     __syncthreads();
     const uint64_t cb = uint64_t(b) << kP3Bits;
     for (uint32_t i = threadIdx.x; i < span; i += blockDim.x)
@@ -912,7 +941,7 @@ inline bool part_histogram(rs_context* ctx, Scratch& scr, bool raw, const uint64
   exclusive_scan<uint32_t>(ArrayIn<uint32_t>{mat}, size_t(nb) * nct, mscan, mscan + size_t(nb) * nct, scr, st);
   uint32_t* bstart = scr.take<uint32_t>(nb + 1);
   part_bstart_kernel<<<(nb + 256) / 256, 256, 0, st>>>(mscan, nb, nct, mscan + size_t(nb) * nct, bstart);
-  uint32_t* addrs = scr.take<uint32_t>(N);
+  uint16_t* addrs = reinterpret_cast<uint16_t*>(scr.take<uint32_t>((N + 1) / 2));
   const size_t psm2 = 3 * psm;  // cursors | tile counts | tile offsets
   if (raw) {
     set_smem_attr(part_kernel<true, true>, psm2);
@@ -1034,6 +1063,17 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
       throw InvalidArgument("profile: table hash_size must be in [1, 2^31-1]");
   }
   cudaStream_t st = ctx->stream;
+  // RS_PROFILE_DEBUG=1: phase times on stderr (each phase synchronised)
+  static const bool dbg = getenv("RS_PROFILE_DEBUG") != nullptr;
+  auto t_0 = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (!dbg) return;
+    RS_CUDA(cudaStreamSynchronize(st));
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "profile %-12s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t_0).count());
+    t_0 = t;
+  };
+  phase("enter");
 
   // table-id lookup (sorted ids -> index), per-table hash params
   std::vector<uint32_t> order(J);
@@ -1079,6 +1119,7 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
                 Scratch::bytes_for(N, 4) + Scratch::bytes_for(kPMaxBuckets + 1, 4) * 3 +
                 scan_scratch_bytes(size_t(kPMaxBuckets) * sm_count() * 4, 4);
   Scratch scr = ctx->scratch(need);
+  phase("scratch");
 
   const uint64_t* d_rs = on_dev ? tr->rec_sample : stage(tr->rec_sample, R, false, scr, st);
   const uint32_t* d_rt = on_dev ? tr->rec_table : stage(tr->rec_table, R, false, scr, st);
@@ -1177,6 +1218,7 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
         else run(hash_hist<false, false>, 0, R, rsm, nullptr, nullptr);
       }
       RS_LAUNCH_CHECK();
+      phase("histogram");
       if (g == 0) {
         // errors, selection and per-table totals are known after the first group
         auto* hb = ctx->pinned_buf<uint64_t>(2 * size_t(J) + 2);
@@ -1224,8 +1266,10 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
           RS_CUDA(cudaMemcpyAsync(res->cdf + at, rk.cdf, rk.n * 8, cudaMemcpyDeviceToHost, st));
           RS_CUDA(cudaMemcpyAsync(res->d_rows + at, rk.rows, rk.n * 4, cudaMemcpyDeviceToDevice, st));
         }
+        phase("rank");
         res->nd = at + rk.n;
         ctx->sync();
+        phase("d2h");
         for (uint32_t j = r_lo; j < r_lo + Jr; ++j) res->distinct[j] = tstart[j - r_lo + 1] - tstart[j - r_lo];
         scr.used = mark_r;
         a = b;
@@ -1252,6 +1296,7 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
     }
     if (!res->d_rows) res->grow(0, st);
     ctx->sync();
+    phase("assemble");
   } catch (...) {
     delete res;
     throw;

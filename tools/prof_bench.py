@@ -42,6 +42,7 @@ def main():
         ts.append(time.perf_counter() - t0)
         torch.cuda.nvtx.range_pop()
         h.close()
+        del h  # its pinned result buffers go back to the pool before the next call
     ts.sort()
     print(json.dumps({"ids": int(n), "records": int(tr.rec_sample.numel()), "s": ts[len(ts) // 2],
                       "ids_per_s": n / ts[len(ts) // 2]}))
