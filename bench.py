@@ -62,6 +62,7 @@ def parse():
     p.add_argument("--trace-ids", type=float, default=2e8,
                    help="trace-file write/read size (SURVEY §8f row 3, tools/trace_bench.py); 0 disables")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-uniform", action="store_true", help="skip the uniform-row (alpha=0) forward control")
     p.add_argument("--no-prefetch", action="store_true",
                    help="headline in zero-copy mode only (no slow-row staging pipeline)")
     p.add_argument("--plan-gpus", type=int, default=0,
@@ -335,7 +336,7 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
         uq = 0
         for t, w in enumerate(lspecs):
             lt = int(o[(t + 1) * B] - o[t * B])
-            rb = 4 * w.table.dim
+            rb = w.table.elem_bytes * w.table.dim
             fb += lt * (rb + 8 + 8)  # row + index + remap entry; + key/value written for the backward
             u = np.unique(ih[o[t * B]:o[(t + 1) * B]]).size
             uq += u
@@ -506,6 +507,82 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
     return res
 
 
+def traffic_record():
+    """profiles/traffic.json (tools/make_traffic.py: ncu DRAM bytes per forward
+    / backward / profile call) with `_matches` = whether it was measured on
+    the library this run loaded (sha256), else None."""
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(tp):
+        return None
+    try:
+        tj = json.load(open(tp))
+        import hashlib
+
+        from paper_2201_10095_b200 import _lib
+
+        h = hashlib.sha256()
+        with open(_lib.LIB_PATH, "rb") as f:
+            for b in iter(lambda: f.read(1 << 20), b""):
+                h.update(b)
+        tj["_matches"] = tj.get("library_sha256") == h.hexdigest()
+        return tj
+    except Exception:
+        return None
+
+
+def run_uniform_control(args, torch, ctx, specs, B, hbm_peak, reps=10):
+    """The forward's L2-free control ("an alpha=0 uniform-row
+    control"): the same tables (all rows in HBM, identity remaps) and the same
+    bag structure as the headline batches, but every index drawn uniformly
+    from its table, so there is no Zipf head to reuse from L1/L2 and the
+    gather runs against DRAM.  Kernel-only time (CUDA events on the
+    operator's stream) over `reps` forwards, each after a 256 MiB L2 flush;
+    the same algorithmic bytes as the headline roofline."""
+    import paper_2201_10095_b200 as sp
+    from paper_2201_10095_b200 import workload as wl
+
+    dev = torch.device("cuda", ctx.device)
+    remaps = [sp.RemapTable(w.table.table_id, w.table.hash_size, w.table.hash_size, 0,
+                            torch.arange(w.table.hash_size, dtype=torch.int32, device=dev)) for w in specs]
+    gen = wl.BatchGenerator(specs, B, WORKLOAD_SEED)
+    off, idx, n = gen.batch(100)
+    o = off.cpu().numpy().view(np.uint32).astype(np.int64)
+    T = len(specs)
+    counts = torch.from_numpy(np.diff(o[::B][:T + 1]).astype(np.int64)).to(dev)
+    H = torch.tensor([w.table.hash_size for w in specs], dtype=torch.float64, device=dev)
+    hl = torch.repeat_interleave(H, counts)
+    g = torch.Generator(device=dev)
+    g.manual_seed(12345)
+    uidx = (torch.rand(int(n), generator=g, device=dev, dtype=torch.float64) * hl).to(torch.int64)
+    uidx = torch.minimum(uidx, (hl - 1).to(torch.int64)).to(torch.int32)
+    del hl
+    op = sp.TieredEmbeddingBag([w.table for w in specs], remaps, B, max(1, int(n)), args.optimizer, ctx=ctx)
+    op.init_weights(INIT_SEED, 0.1)
+    D = sum(w.table.dim for w in specs)
+    pooled = torch.empty(B, D, dtype=torch.float32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        op.forward(off, uidx, B, out=pooled)
+    torch.cuda.synchronize()
+    op.kernel_times(reset=True)
+    for _ in range(reps):
+        flush.zero_()
+        op.forward(off, uidx, B, out=pooled)
+    torch.cuda.synchronize()
+    fk, nf, _, _ = op.kernel_times(reset=True)
+    ms = fk / max(1, nf)
+    fb = 4 * (T * B + 1) + 4 * B * D
+    for t, w in enumerate(specs):
+        fb += int(o[(t + 1) * B] - o[t * B]) * (w.table.elem_bytes * w.table.dim + 16)
+    op.close()
+    del remaps, uidx, off, idx, pooled, flush
+    torch.cuda.empty_cache()
+    gbs = fb / (ms / 1e3) / 1e9
+    return {"workload": f"{args.config}-like tables, headline bag structure, uniform row ids, all rows in HBM",
+            "lookups": int(n), "kernel_ms": ms, "algorithmic_bytes": fb, "achieved": gbs, "peak": hbm_peak,
+            "unit": "GB/s", "frac": gbs / hbm_peak}
+
+
 def run_profile_sweep(args, torch, ctx, hbm_peak):
     """HP1 at scale (BASELINE configs[4]): profile() over ~args.profile_ids hashed
     ids on the cfg1 tables (8 x 1e6 rows, Zipf 1.05, pooling 20), timed end to
@@ -540,9 +617,8 @@ def run_profile_sweep(args, torch, ctx, hbm_peak):
     out = {"workload": "cfg1 tables, rate 1.0", "ids": int(n), "records": R,
            "seconds": secs, "ids_per_s": n / secs, "algorithmic_gbs": alg / secs / 1e9,
            "frac_of_hbm": alg / secs / 1e9 / hbm_peak}
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
     try:  # DRAM bytes of one such call from the committed ncu launch list
-        tb = json.load(open(tp)).get("cfg1_profile_1e9", {}).get("dram_bytes")
+        tb = (traffic_record() or {}).get("cfg1_profile_1e9", {}).get("dram_bytes")
         if tb:
             tb = tb * n / 1e9
             out["traffic"] = {"dram_bytes": tb, "gbs": tb / secs / 1e9, "frac_of_hbm": tb / secs / 1e9 / hbm_peak,
@@ -892,6 +968,11 @@ def main():
                      args.greedy_steps, 1, False, B)
     prof.close()
 
+    uniform = None
+    if rank == 0 and world == 1 and not args.no_uniform:
+        need = sum(w.table.hash_size * (w.table.dim * w.table.elem_bytes + 8) for w in specs)
+        if need < 0.8 * torch.cuda.mem_get_info(dev)[0]:
+            uniform = run_uniform_control(args, torch, ctx, specs, B, hbm_peak)
     sweep = None
     if world == 1 and args.profile_ids > 0:
         sweep = run_profile_sweep(args, torch, ctx, hbm_peak)
@@ -921,13 +1002,12 @@ def main():
         fk, bk = r["fwd_kernel_ms"], r["bwd_kernel_ms"]
         fwd_gbs = r["fwd_bytes"] / (fk / 1e3) / 1e9 if fk > 0 else 0.0
         bwd_gbs = r["bwd_bytes"] / (bk / 1e3) / 1e9 if bk > 0 else 0.0
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tp):
-            try:
-                traffic = json.load(open(tp)).get(args.config, {}).get("forward_dram_bytes")
-            except Exception:
-                traffic = None
+        traffic, traffic_src = None, None
+        tj = traffic_record()
+        if tj is not None:
+            traffic = tj.get(args.config, {}).get("forward_dram_bytes")
+            traffic_src = {k: tj.get(k) for k in ("commit", "date", "script", "library_sha256")}
+            traffic_src["library_matches"] = tj.get("_matches")
         line = {
             "metric": METRIC,
             "value": r["samples_per_s"], "unit": "samples/s", "n_gpus": world,
@@ -966,10 +1046,13 @@ def main():
             "roofline": {"bound": "hbm", "kernel": "emb forward (gather-pool, both lane-class launches)",
                          "achieved": fwd_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": fwd_gbs / hbm_peak, "peak_kind": peak_kind,
-                         "traffic": traffic, "algorithmic_bytes": r["fwd_bytes"],
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "dram_frac": (traffic / (fk / 1e3) / 1e9 / hbm_peak) if traffic and fk > 0 else None,
+                         "algorithmic_bytes": r["fwd_bytes"],
                          "kernel_ms": fk, "mode": r["mode"],
                          "backward": {"achieved": bwd_gbs, "frac": bwd_gbs / hbm_peak,
-                                      "algorithmic_bytes": r["bwd_bytes"], "kernel_ms": bk}},
+                                      "algorithmic_bytes": r["bwd_bytes"], "kernel_ms": bk},
+                         "uniform_control": uniform},
             "cpu_baseline": cpu,
             "e2e": r.get("e2e"),
             "gpu_launches": r["launches"],
