@@ -63,6 +63,9 @@ def parse():
                    help="trace-file write/read size (SURVEY §8f row 3, tools/trace_bench.py); 0 disables")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-uniform", action="store_true", help="skip the uniform-row (alpha=0) forward control")
+    p.add_argument("--omit-unaccessed", action="store_true",
+                   help="remaps with RemapOptions.omit_unaccessed (inc/remap.hpp:43-48): only profiled slow "
+                        "rows get host storage, never-profiled rows pool as zeros (default for rm3)")
     p.add_argument("--no-prefetch", action="store_true",
                    help="headline in zero-copy mode only (no slow-row staging pipeline)")
     p.add_argument("--plan-gpus", type=int, default=0,
@@ -71,7 +74,10 @@ def parse():
     p.add_argument("--as-rank", type=int, default=0)
     p.add_argument("--prefetch-depth", type=int, default=2, choices=[1, 2],
                    help="batches staged ahead (2: batch i+2's claim is queued behind forward i)")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.config == "rm3":
+        a.omit_unaccessed = True  # 3.9 TB of fp16 rows: only profiled rows can be backed
+    return a
 
 
 def measured_peaks():
@@ -155,7 +161,8 @@ def line_config(args, n_tables, parallelism):
             "optimizer": args.optimizer, "parallelism": parallelism,
             "fast_tier_cap": f"{args.hbm_fraction:.0%} of table bytes",
             "l2": "256 MiB flush between steps" if not args.no_flush
-            else f"{args.nbatches} distinct batches cycled"}
+            else f"{args.nbatches} distinct batches cycled",
+            **({"remaps": "omit_unaccessed"} if args.omit_unaccessed else {})}
 
 
 class RefEmbWorkload:
@@ -306,7 +313,7 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
     for j in local:
         s = specs[j].table
         out = torch.empty(s.hash_size, dtype=torch.int32, device=dev)
-        remaps.append(sp.build_remap(plan.entries[j], stats[j], s, ctx=ctx,
+        remaps.append(sp.build_remap(plan.entries[j], stats[j], s, omit_unaccessed=args.omit_unaccessed, ctx=ctx,
                                      device_rows=prof.device_rows_by_rank(j), out=out))
     T = len(local)
     D_local = sum(s.table.dim for s in lspecs)
@@ -483,7 +490,10 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
     if T and world == 1:
         off, idx, n = batches[0]
         hits.zero_()
+        op.unbacked(reset=True)
         op.forward(off, idx, B, out=pooled, hits=hits)
+        ulk, _ = op.unbacked(reset=True)
+        res["unbacked_pct"] = 100.0 * float(ulk.sum()) / max(1, int(n))
         tr = wl.kjt_to_trace(lspecs, off, idx, n, B, 0, ctx=ctx)
         import copy
 
@@ -880,6 +890,7 @@ def main():
     prof = sp.profiler.profile_handle(ptrace, 1.0, PROFILE_SEED, ctx=ctx)
     prof_cold_s = time.perf_counter() - t0  # includes first-use pinned result buffers
     prof.close()
+    del prof  # its pinned result buffers return to the pool before the timed call
     t0 = time.perf_counter()
     prof = sp.profiler.profile_handle(ptrace, 1.0, PROFILE_SEED, ctx=ctx)
     prof_s = time.perf_counter() - t0
@@ -908,7 +919,7 @@ def main():
         strace.num_samples = B  # records carry sample ids 100B..101B-1; one batch of B
         strace.rec_sample = strace.rec_sample - 100 * B
         for name, pl in (("recshard", rec_pure), (rec_fill.strategy, rec_fill), ("greedy-size", gre)):
-            rms = [sp.build_remap(pl.entries[j], stats[j], tables[j], ctx=ctx,
+            rms = [sp.build_remap(pl.entries[j], stats[j], tables[j], omit_unaccessed=args.omit_unaccessed, ctx=ctx,
                                   device_rows=prof.device_rows_by_rank(j),
                                   out=torch.empty(tables[j].hash_size, dtype=torch.int32, device=dev))
                    for j in range(len(tables))]
@@ -930,10 +941,12 @@ def main():
             shards.append({"rank": q,
                            "tables": sum(1 for e in rec.entries if e.gpu == q),
                            "greedy_tables": sum(1 for e in gre.entries if e.gpu == q),
-                           "recshard": {k: rq[k] for k in ("samples_per_s", "ms_per_step", "uvm_pct", "fast",
-                                                           "slow", "mode")},
-                           "greedy": {k: gq[k] for k in ("samples_per_s", "ms_per_step", "uvm_pct", "fast",
-                                                         "slow", "mode")}})
+                           "recshard": {k: rq.get(k) for k in ("samples_per_s", "ms_per_step", "uvm_pct", "fast",
+                                                               "slow", "mode", "unbacked_pct", "hbm_bytes",
+                                                               "host_bytes")},
+                           "greedy": {k: gq.get(k) for k in ("samples_per_s", "ms_per_step", "uvm_pct", "fast",
+                                                             "slow", "mode", "unbacked_pct", "hbm_bytes",
+                                                             "host_bytes")}})
             torch.cuda.empty_cache()
         prof.close()
 
@@ -941,8 +954,10 @@ def main():
             ms = max(x[key]["ms_per_step"] for x in shards)
             slow = sum(x[key]["slow"] for x in shards)
             tot = slow + sum(x[key]["fast"] for x in shards)
+            unb = sum((x[key].get("unbacked_pct") or 0.0) * (x[key]["fast"] + x[key]["slow"]) for x in shards)
             return {"samples_per_s": B / (ms / 1e3), "ms_per_step_slowest_shard": ms,
-                    "uvm_access_pct": 100.0 * slow / max(1, tot)}
+                    "uvm_access_pct": 100.0 * slow / max(1, tot),
+                    "unbacked_access_pct": unb / max(1, tot)}
 
         rs_, gs_ = system_of("recshard"), system_of("greedy")
         print(json.dumps({
@@ -950,7 +965,8 @@ def main():
                       "(slowest shard sets the step; no all-to-all)",
             "config": {"workload": f"{args.config}-like", "tables": len(specs), "global_batch": B,
                        "plan_gpus": M, "fast_tier_cap": f"{args.hbm_fraction:.0%} of table bytes",
-                       "optimizer": args.optimizer},
+                       "optimizer": args.optimizer, "elem_bytes": sorted({w.table.elem_bytes for w in specs}),
+                       **({"remaps": "omit_unaccessed"} if args.omit_unaccessed else {})},
             "recshard": rs_, "greedy": gs_, "recshard_vs_greedy": rs_["samples_per_s"] / gs_["samples_per_s"],
             "simulated_uvm_pct": sim_uvm, "planner_s": plan_s, "shards": shards}), flush=True)
         return

@@ -969,7 +969,12 @@ inline bool part_histogram(rs_context* ctx, Scratch& scr, bool raw, const uint64
 // Allows `bytes` of dynamic shared memory on top of the kernel's static usage.
 template <class K>
 inline void set_smem_attr(K kern, size_t bytes) {
-  if (bytes > 16 * 1024) RS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+  // needed whenever static + dynamic shared memory passes the 48 KB default
+  // (part_kernel's static footprint alone is ~45 KB)
+  cudaFuncAttributes fa{};
+  RS_CUDA(cudaFuncGetAttributes(&fa, kern));
+  if (fa.sharedSizeBytes + bytes > 48 * 1024)
+    RS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
 }
 
 struct RankDevice {
@@ -1091,11 +1096,15 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
     mg[j] = FastMod::make(hs[j]).m;
   }
   // table groups: sum(H) per group < 2^31 (u32 compaction positions / keys)
+  // (splitting RM1's 2.3e8 rows into groups that fit the partitioned
+  // histogram's buckets measured slower: 14.6 ms + a second result grow vs
+  // 13.8 ms on the atomic kernel)
+  const uint64_t gcap = 0x7FFFFFFFULL;
   std::vector<uint32_t> gstart{0};
   {
     uint64_t acc = 0;
     for (uint32_t j = 0; j < J; ++j) {
-      if (acc + hs[j] > 0x7FFFFFFFULL && j > gstart.back()) {
+      if (acc + hs[j] > gcap && j > gstart.back()) {
         gstart.push_back(j);
         acc = 0;
       }
@@ -1254,10 +1263,12 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
           if (b - a <= step) throw Error(-9, "rank: table range split did not shrink the key");
           continue;
         }
+        phase("rank-kernels");
         const uint32_t r_lo = t_lo + a, Jr = b - a;
         std::vector<uint64_t> tstart(Jr + 1);
         const size_t at = res->nd;
         res->grow(rk.n, st);
+        phase("grow");
         RS_CUDA(cudaMemcpyAsync(tstart.data(), rk.tstart, (Jr + 1) * 8, cudaMemcpyDeviceToHost, st));
         RS_CUDA(cudaMemcpyAsync(res->icdf.data() + size_t(r_lo) * 101, rk.icdf,
                                 size_t(Jr) * 101 * 8, cudaMemcpyDeviceToHost, st));

@@ -19,6 +19,9 @@ def main():
     p.add_argument("--ids", type=float, default=1e9)
     p.add_argument("--reps", type=int, default=3)
     p.add_argument("--rate", type=float, default=1.0)
+    p.add_argument("--config", default="cfg1", help="cfg1 (BASELINE configs[4]) or rm1/rm2/rm3 table sets")
+    p.add_argument("--samples", type=int, default=0, help="samples instead of --ids (e.g. 262144 = the "
+                   "bench's 16 profiling batches of 16384)")
     a = p.parse_args()
     import torch
 
@@ -26,9 +29,9 @@ def main():
     from paper_2201_10095_b200 import workload as wl
 
     ctx = sp.default_context(0)
-    specs = wl.cfg1_specs()
-    per = sum(w.gen.mean_pooling for w in specs)
-    S = int(a.ids // per)
+    specs = wl.cfg1_specs() if a.config == "cfg1" else wl.rm_specs(a.config, 20260809)
+    per = sum(w.gen.mean_pooling * w.gen.coverage for w in specs)
+    S = a.samples or int(a.ids // per)
     gen = wl.BatchGenerator(specs, S, 20260810)
     off, idx, n = gen.batch(0)
     tr = wl.kjt_to_trace(specs, off, idx, n, S, 0, ctx=ctx)
