@@ -287,6 +287,29 @@ def run_reference(args, rank, world):
 
 
 # ---------------------------------------------------------------------------- our arm
+def ex_forward(op, ex, off, idx, hits):
+    """K4 + K6 (rs_emb_forward_to_owners): this rank's tables pooled for the
+    global batch, every row stored into its sample owner's block."""
+    import ctypes as C
+
+    from paper_2201_10095_b200 import _lib
+    from paper_2201_10095_b200.runtime import ptr
+
+    f = C.c_void_p()
+    _lib.check(_lib.lib().rs_emb_forward_to_owners(op.h, ex.h, ptr(off), ptr(idx), ptr(hits), C.byref(f)))
+
+
+def ex_backward(op, ex, off, idx, lr):
+    """K6 + K5 (rs_emb_backward_from_owners): the owner block's gradient
+    (in place) back to the table owners, overlapped with K5's sort."""
+    import ctypes as C
+
+    from paper_2201_10095_b200 import _lib
+    from paper_2201_10095_b200.runtime import ptr
+
+    _lib.check(_lib.lib().rs_emb_backward_from_owners(op.h, ex.h, ptr(off), ptr(idx), None, C.c_float(lr)))
+
+
 def h2d_bandwidth(torch, dev):
     a = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
     b = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -359,7 +382,8 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
     if world > 1:
         from paper_2201_10095_b200.sharded import Exchange
 
-        ex = Exchange(plan, [w.table.dim for w in specs], world, rank, B, dev)
+        ex = Exchange(plan, [w.table.dim for w in specs], world, rank, B,
+                      transport=os.environ.get("BENCH_EXCHANGE", "peer"), ctx=ctx)
     # unique slow-tier rows per batch (sizes the HBM staging of the pipelined mode)
     slow_u = 0
     for off, idx, n in batches:
@@ -384,7 +408,10 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
             op.prefetch(nb[0], nb[1], B)
         if ev:
             ev[0].record()
-        if T:
+        fused = ex is not None and T > 0
+        if fused:  # K4 stores straight into the sample owners' blocks (K6)
+            ex_forward(op, ex, off, idx, hits)
+        elif T:
             op.forward(off, idx, B, out=pooled, hits=hits)
         if D == 2 and cache and i + 2 < cache:
             # batch i+2: its claim queues behind this forward, so its host
@@ -394,12 +421,13 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
         if ev:
             ev[1].record()
         g = pooled
-        if ex is not None:  # pooled rows to sample owners, gradients back (NCCL all-to-all)
-            y = ex.to_owners(pooled)  # loss 0.5*||y||^2 on this rank's samples: grad = y
-            g = ex.to_tables(y)
+        if ex is not None and not fused:  # a rank without tables: the unfused primitives
+            g = ex.to_tables(ex.to_owners(pooled))
         if ev:
             ev[2].record()
-        if T:
+        if fused:  # loss 0.5*||y||^2 on this rank's samples: the gradient is the owner block itself
+            ex_backward(op, ex, off, idx, LR)
+        elif T:
             op.backward(off, idx, g, B, LR)
         if ev:
             ev[3].record()
@@ -455,11 +483,9 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
         h = hits.cpu().numpy()
         fast, slow = int(h[0::2][:T].sum()), int(h[1::2][:T].sum())
         if world > 1:
-            t = torch.tensor([tot_ms, fast, slow, all_ms], dtype=torch.float64, device=dev)
-            mx = t.clone()
-            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-            dist.all_reduce(t, op=dist.ReduceOp.SUM)
-            tot_ms, fast, slow, all_ms = float(mx[0]), int(t[1]), int(t[2]), float(mx[3])
+            mx = allreduce(dist, torch, [tot_ms, all_ms], dist.ReduceOp.MAX, dev)
+            sm = allreduce(dist, torch, [fast, slow], dist.ReduceOp.SUM, dev)
+            tot_ms, all_ms, fast, slow = mx[0], mx[1], int(sm[0]), int(sm[1])
         return dict(ms_per_step=tot_ms / steps, samples_per_s=B * steps / (tot_ms / 1e3),
                     ms_per_step_incl_warmup_fill_drain=all_ms / nsteps,
                     uvm_pct=100.0 * slow / max(1, fast + slow), fast=fast, slow=slow,
@@ -702,9 +728,8 @@ def run_profile_sweep_sharded(args, torch, dist, ctx, world, rank):
         t0 = time.perf_counter()
         profile_sharded(tr, 1.0, PROFILE_SEED, profile_fn=prof)
         torch.cuda.synchronize()
-        t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{ctx.device}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        times.append(float(t[0]))
+        times.append(allreduce(dist, torch, [time.perf_counter() - t0], dist.ReduceOp.MAX,
+                               torch.device("cuda", ctx.device))[0])
     secs = float(np.median(times))
     del tr, idx, off
     torch.cuda.empty_cache()
@@ -800,14 +825,17 @@ def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex, cache, 
                 op.prefetch(*view(i + 1), B)
             main.wait_event(ev_in[i % nb])
             d_off, d_idx = view(i)
-            op.forward(d_off, d_idx, B, out=pooled, hits=hits)
+            if ex is not None:
+                ex_forward(op, ex, d_off, d_idx, hits)
+            else:
+                op.forward(d_off, d_idx, B, out=pooled, hits=hits)
             if cache and depth == 2 and i + 2 < total:
                 main.wait_event(ev_in[(i + 2) % nb])  # copied a step ago
                 op.prefetch(*view(i + 2), B)
-            g = pooled
             if ex is not None:
-                g = ex.to_tables(ex.to_owners(pooled))
-            op.backward(d_off, d_idx, g, B, LR)
+                ex_backward(op, ex, d_off, d_idx, LR)
+            else:
+                op.backward(d_off, d_idx, pooled, B, LR)
             h_hits.copy_(hits, non_blocking=True)
             ev_free[i % nb].record(main)
             used[i % nb] = True
@@ -819,12 +847,20 @@ def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex, cache, 
     torch.cuda.synchronize()
     ms = s.elapsed_time(e)
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t[0])
+        ms = allreduce(dist, torch, [ms], dist.ReduceOp.MAX, dev)[0]
     return {"value": B * steps / (ms / 1e3), "unit": "samples/s", "h2d_bytes_per_step": int(bi[0]),
             "d2h_bytes_per_step": int(h_hits.numel() * 8), "ms_per_step": ms / steps,
             "mode": "pipelined" if cache else "zero-copy"}
+
+
+def allreduce(dist, torch, vals, op, dev):
+    """All-reduce a few float64 scalars over the bench's process group (NCCL
+    takes device tensors; the gloo group of a one-GPU multi-rank smoke takes
+    host tensors)."""
+    cpu = dist.get_backend() == "gloo"
+    t = torch.tensor(vals, dtype=torch.float64, device="cpu" if cpu else dev)
+    dist.all_reduce(t, op=op)
+    return [float(x) for x in t.cpu()]
 
 
 def free_port():
@@ -859,8 +895,16 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
+        # one process per GPU over NCCL; BENCH_DIST_BACKEND=gloo lets ranks
+        # share GPUs (a one-GPU smoke of the multi-rank path: the K6 peer
+        # transport maps each rank's owner block with CUDA IPC either way)
+        local_rank %= torch.cuda.device_count()
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
 
     import paper_2201_10095_b200 as sp
     from paper_2201_10095_b200 import planner
@@ -1034,6 +1078,10 @@ def main():
                                   f"one shard (rank {prank}) of a table-wise mp{M} plan, no all-to-all"
                                   if emulate else f"table-wise mp{world}"),
             "uvm_access_pct": r["uvm_pct"],
+            **({"unbacked_access_pct": r.get("unbacked_pct"),
+                "unbacked_note": "lookups of rows the omit_unaccessed remaps left without storage (never "
+                                 "profiled); simulate() and uvm_access_pct count them as slow-tier accesses, "
+                                 "the operator pools them as zero rows"} if args.omit_unaccessed else {}),
             "parity": {
                 "profile_prefix_vs_reference": (sweep or {}).get("cpu_reference", {}).get("bit_exact"),
                 "uvm_counts_vs_simulate": r.get("uvm_matches_simulate"),
