@@ -23,3 +23,8 @@ run racecheck_emb racecheck tests/test_emb_gpu.py -m gpu -k "test_forward_bit_ex
 run racecheck_profile racecheck tests/test_profile_gpu.py -m gpu -k "goldens or many_tables"
 run synccheck_emb synccheck tests/test_emb_gpu.py -m gpu -k "test_backward_matches_oracle and case1 or test_uvm_cache_two_batches_ahead and 4096"
 run synccheck_profile synccheck tests/test_profile_gpu.py -m gpu -k "goldens or many_tables"
+# round 2: fp16 / unbacked rows, the K6 exchange at world size 1, the partitioned histogram
+run memcheck_emb16 memcheck tests/test_emb16_gpu.py -m gpu -k "mixed_dims or rejected"
+run memcheck_exchange memcheck tests/test_exchange_gpu.py -m gpu -k "world1"
+run memcheck_partition memcheck tests/test_profile_gpu.py -m gpu -k "partitioned"
+run racecheck_emb16 racecheck tests/test_emb16_gpu.py -m gpu -k "mixed_dims and False"
