@@ -1292,7 +1292,7 @@ static uint32_t fwd_chunk() {
   return c;
 }
 
-template <int G, int VPL, class E>
+template <int G, int VPL, class E, int UNR_ = (VPL > 1 ? 8 : 2), int MINB_ = (VPL > 1 ? 1 : 8)>
 static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint32_t* off,
                        const uint32_t* idx, const OutMap& out, uint64_t stride, unsigned long long* hits,
                        cudaStream_t st) {
@@ -1304,8 +1304,13 @@ static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint
   const uint32_t chunk = fwd_chunk();
   const uint64_t chunks = (warps + chunk - 1) / chunk;
   if (warps >= (uint64_t(1) << 32)) throw InvalidArgument("emb_forward: batch too large for one launch");
-  constexpr int MINB = VPL > 1 ? 1 : 5;  // B200 RM1: (unroll 4, 5 CTAs/SM) 1.27 ms, 6: 1.33, 4: 1.82
-  auto kern = emb::forward_kernel<G, VPL, (VPL > 1 ? 8 : 4), MINB, E>;
+  // (rows in flight per group, CTAs/SM), B200 RM1 all-HBM (op_bench, one box,
+  // two runs): (2, 8) 1.26-1.31 ms, (2, 6) 1.29-1.30, (3, 6) 1.35, (4, 6)
+  // 1.39-1.40, (4, 5) 1.41-1.42 — with the chunked schedule, occupancy wins
+  // over rows in flight per group (the 32-register cap spills only in the
+  // per-bag cursor code)
+  constexpr int MINB = MINB_;
+  auto kern = emb::forward_kernel<G, VPL, UNR_, MINB, E>;
   static const int per_sm = [&] {
     int n = 0;
     RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, emb::kFwdThreads, 0));
