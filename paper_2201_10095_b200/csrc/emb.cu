@@ -943,8 +943,9 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
     RS_CUDA(cudaMalloc(&e->ppart, max_pieces * e->dmax * 4));
     RS_CUDA(cudaMalloc(&e->pdesc, max_pieces * sizeof(uint4)));
     RS_CUDA(cudaMalloc(&e->gpart, max_groups * e->dmax * 4));
-    e->sort_scratch_bytes = radix_sort_scratch_bytes(L, T) + (4 << 20);
     e->tiles_cap = L / kSortTile + T + 2;
+    e->sort_scratch_bytes =
+        std::max(radix_sort_scratch_bytes(L, T), radix_onesweep_scratch_bytes(L, e->tiles_cap)) + (4 << 20);
     RS_CUDA(cudaMalloc(&e->d_tiles, 3 * e->tiles_cap * 4));
     RS_CUDA(cudaMalloc(&e->sort_scratch, e->sort_scratch_bytes));
     // per-backward metadata: tpos[T+1] | wstart[T+1] | wtab[T] (class-major
@@ -1515,7 +1516,17 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
     tm.cidx = e->d_tiles + tcap;
     tm.cstride = e->d_tiles + 2 * size_t(tcap);
     tm.ntd = e->d_nt;
-    radix_sort_pairs(e->keys, e->vals, Lmax, int(e->key_bits), scr, st, tm, tcap - 1, &skeys, &svals);
+    // one kernel per pass with decoupled look-back (B200 RM1: backward 2.07 ->
+    // 1.99 ms, three A/B runs); RS_SORT_ONESWEEP=0 selects the upsweep /
+    // count-scan / downsweep passes
+    static const bool onesweep = [] {
+      const char* v = getenv("RS_SORT_ONESWEEP");
+      return !(v && v[0] == '0');
+    }();
+    if (onesweep)
+      radix_sort_pairs_onesweep(e->keys, e->vals, Lmax, int(e->key_bits), scr, st, tm, tcap - 1, &skeys, &svals);
+    else
+      radix_sort_pairs(e->keys, e->vals, Lmax, int(e->key_bits), scr, st, tm, tcap - 1, &skeys, &svals);
   }
   emb::BwdArgs a{e->cur_tables, T, d_tpos, skeys, svals, grad, e->total_dim, e->dmax, lr, e->eps, e->opt};
   // segment list: count heads per window, scan, write descriptors

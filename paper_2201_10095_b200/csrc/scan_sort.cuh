@@ -9,7 +9,9 @@
 // tile sums -> tile scan + carry-in).  Radix sort: 8-bit digits, per pass
 // upsweep (per-tile digit counts) -> scan of the digit-major count matrix ->
 // downsweep (stable in-tile ranking with warp ballots, scatter).  No atomics
-// and no inter-CTA spinning, so there is no forward-progress hazard.
+// and no inter-CTA spinning, so there is no forward-progress hazard.  The
+// backward's segmented sort runs the onesweep variant at the end of the file
+// (one kernel per pass, decoupled look-back over tiles claimed in order).
 #pragma once
 
 #include "common.cuh"
@@ -385,6 +387,200 @@ inline void radix_sort_pairs(uint32_t* keys, uint32_t* vals, size_t n, int end_b
     if (vals) RS_CUDA(cudaMemcpyAsync(vals, vi, n * 4, cudaMemcpyDeviceToDevice, st));
   }
   scr.used = mark;
+}
+
+// ----------------------------------------------------------------- onesweep
+// Segmented LSD radix sort with one kernel per pass (decoupled look-back):
+// one histogram kernel counts every pass's digits per segment (table) up
+// front, a small kernel turns them into each (segment, pass, digit) start, and
+// each pass kernel ranks its tile, publishes its digit counts, looks back over
+// the earlier tiles OF ITS SEGMENT for their running totals, and scatters —
+// instead of per pass an upsweep (a second read of the keys), a scan of the
+// [segment][digit][tile] count matrix and a downsweep.  Tiles are claimed in
+// order through an atomic counter, so a tile only ever waits for tiles that
+// were already running (forward progress).  Same stable order as the
+// upsweep/downsweep sort: results are identical.
+constexpr uint32_t kOsAgg = 1u << 30, kOsInc = 2u << 30, kOsCount = (1u << 30) - 1;
+constexpr int kOsMaxPasses = 4;
+
+// First tile of tile b's segment: cidx[b] = kRadix * first + (b - first).
+__device__ __forceinline__ unsigned os_first(const TileMap& tm, unsigned b) {
+  return (tm.cidx[b] - b) / unsigned(kRadix - 1);
+}
+
+static __global__ void __launch_bounds__(kSortThreads)
+radix_os_hist(const uint32_t* __restrict__ keys, size_t n, int end_bit, uint32_t* __restrict__ hist, TileMap tm) {
+  __shared__ uint32_t h[kOsMaxPasses][kRadix];
+  if (tm.idle(blockIdx.x)) return;
+  const int npass = (end_bit + kRadixBits - 1) / kRadixBits;
+  for (int i = threadIdx.x; i < npass * kRadix; i += blockDim.x) h[i / kRadix][i % kRadix] = 0;
+  __syncthreads();
+  const size_t t0 = tm.begin(blockIdx.x), t1 = tm.end(blockIdx.x, n);
+  for (size_t k = t0 + threadIdx.x; k < t1; k += blockDim.x) {
+    const uint32_t key = keys[k];
+    for (int p = 0; p < npass; ++p) {
+      const int nb = min(kRadixBits, end_bit - p * kRadixBits);
+      atomicAdd(&h[p][(key >> (p * kRadixBits)) & ((1u << nb) - 1u)], 1u);
+    }
+  }
+  __syncthreads();
+  const unsigned f = os_first(tm, blockIdx.x);
+  for (int i = threadIdx.x; i < npass * kRadix; i += blockDim.x) {
+    const uint32_t c = h[i / kRadix][i % kRadix];
+    if (c) atomicAdd(&hist[(size_t(f) * npass + i / kRadix) * kRadix + i % kRadix], c);
+  }
+}
+
+// base[(first * npass + p) * 256 + d] = segment start + exclusive digit prefix.
+static __global__ void __launch_bounds__(kSortThreads)
+radix_os_base(const uint32_t* __restrict__ hist, int npass, uint32_t* __restrict__ base, TileMap tm) {
+  if (tm.idle(blockIdx.x) || os_first(tm, blockIdx.x) != blockIdx.x) return;
+  const uint32_t start = uint32_t(tm.begin(blockIdx.x));
+  for (int p = 0; p < npass; ++p) {
+    const size_t o = (size_t(blockIdx.x) * npass + p) * kRadix + threadIdx.x;
+    uint32_t tot;
+    const uint32_t x = block_excl_scan<uint32_t, kSortThreads>(hist[o], tot);
+    base[o] = start + x;
+  }
+}
+
+template <bool HAS_VALUES>
+static __global__ void __launch_bounds__(kSortThreads, RS_SORT_MINB)
+radix_os_pass(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, size_t n, int shift,
+              int nbits, int pass, int npass, const uint32_t* __restrict__ base, uint32_t* __restrict__ status,
+              unsigned* __restrict__ ctr, uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+              TileMap tm) {
+  __shared__ uint32_t wc[kSortWarps][kRadix];
+  __shared__ unsigned s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ctr, 1u);
+  __syncthreads();
+  const unsigned tile = s_tile;
+  if (tm.idle(tile)) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = lane; i < kRadix; i += 32) wc[w][i] = 0;
+  __syncwarp();
+  const unsigned mask = (1u << nbits) - 1u;
+  const size_t tile0 = tm.begin(tile), tend = tm.end(tile, n);
+  const size_t wbase = tile0 + size_t(w) * 32 * kSortItems;
+  uint32_t kk[kSortItems], vv[kSortItems], rank[kSortItems];
+#pragma unroll
+  for (int r = 0; r < kSortItems; ++r) {
+    size_t k = wbase + size_t(r) * 32 + lane;
+    bool valid = k < tend;
+    kk[r] = valid ? keys_in[k] : 0u;
+    if (HAS_VALUES) vv[r] = valid ? vals_in[k] : 0u;
+    unsigned d = (kk[r] >> shift) & mask;
+    unsigned peers = digit_peers<kRadixBits>(d, valid);
+    unsigned leader = peers ? __ffs(peers) - 1 : 0;
+    uint32_t b0 = 0;
+    if (valid && lane == int(leader)) b0 = wc[w][d];
+    uint32_t b2 = __shfl_sync(0xffffffffu, b0, leader);
+    rank[r] = b2 + __popc(peers & lanemask_lt());
+    if (valid && lane == int(leader)) wc[w][d] = b0 + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  __shared__ uint32_t dstart[kRadix], gbase[kRadix];
+  __shared__ uint32_t sk[kSortTile], sv[HAS_VALUES ? kSortTile : 1];
+  const int d0 = threadIdx.x;
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int ww = 0; ww < kSortWarps; ++ww) {
+    const uint32_t c = wc[ww][d0];
+    wc[ww][d0] = cnt;
+    cnt += c;
+  }
+  // publish this tile's count of digit d0, then look back over the earlier
+  // tiles of the segment for their running total
+  const unsigned first = os_first(tm, tile);
+  volatile uint32_t* vs = status;
+  if (tile == first) {
+    vs[size_t(tile) * kRadix + d0] = kOsInc | cnt;
+  } else {
+    vs[size_t(tile) * kRadix + d0] = kOsAgg | cnt;
+  }
+  uint32_t excl = 0;
+  if (tile != first) {
+    unsigned j = tile - 1;
+    while (true) {
+      const uint32_t st = vs[size_t(j) * kRadix + d0];
+      if ((st & ~kOsCount) == 0) continue;  // not published yet
+      excl += st & kOsCount;
+      if (st & kOsInc) break;
+      --j;
+    }
+    vs[size_t(tile) * kRadix + d0] = kOsInc | (excl + cnt);
+  }
+  uint32_t tot_unused;
+  const uint32_t ds = block_excl_scan<uint32_t, kSortThreads>(cnt, tot_unused);
+  dstart[d0] = ds;
+  gbase[d0] = base[(size_t(first) * npass + pass) * kRadix + d0] + excl;
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kSortItems; ++r) {
+    size_t k = wbase + size_t(r) * 32 + lane;
+    if (k < tend) {
+      const unsigned d = (kk[r] >> shift) & mask;
+      const uint32_t tp = dstart[d] + wc[w][d] + rank[r];
+      sk[tp] = kk[r];
+      if (HAS_VALUES) sv[tp] = vv[r];
+    }
+  }
+  __syncthreads();
+  const uint32_t tn = uint32_t(tend - tile0);
+  for (uint32_t i = threadIdx.x; i < tn; i += kSortThreads) {
+    const uint32_t key = sk[i];
+    const unsigned d = (key >> shift) & mask;
+    const uint32_t pos = gbase[d] + (i - dstart[d]);
+    keys_out[pos] = key;
+    if (HAS_VALUES) vals_out[pos] = sv[i];
+  }
+}
+
+inline size_t radix_onesweep_scratch_bytes(size_t n, size_t seg_tiles) {
+  return Scratch::bytes_for(seg_tiles * kOsMaxPasses * kRadix, 4) * 2 + Scratch::bytes_for(seg_tiles * kRadix, 4) +
+         Scratch::bytes_for(n, 4) * 2 + 4096;
+}
+
+// The segmented sort (tm.pos set) through the onesweep kernels; same contract
+// as radix_sort_pairs.
+inline void radix_sort_pairs_onesweep(uint32_t* keys, uint32_t* vals, size_t n, int end_bit, Scratch& scr,
+                                      cudaStream_t st, TileMap tm, unsigned seg_tiles, uint32_t** keys_res,
+                                      uint32_t** vals_res) {
+  *keys_res = keys;
+  if (vals_res) *vals_res = vals;
+  if (n <= 1 || end_bit <= 0) return;
+  const int npass = (end_bit + kRadixBits - 1) / kRadixBits;
+  if (npass > kOsMaxPasses) throw Error(-9, "radix onesweep: more than 32 key bits");
+  uint32_t* hist = scr.take<uint32_t>(size_t(seg_tiles) * npass * kRadix);
+  uint32_t* base = scr.take<uint32_t>(size_t(seg_tiles) * npass * kRadix);
+  uint32_t* status = scr.take<uint32_t>(size_t(seg_tiles) * kRadix);
+  uint32_t* ctr = scr.take<uint32_t>(kOsMaxPasses);
+  uint32_t* k2 = scr.take<uint32_t>(n);
+  uint32_t* v2 = vals ? scr.take<uint32_t>(n) : nullptr;
+  RS_CUDA(cudaMemsetAsync(hist, 0, size_t(seg_tiles) * npass * kRadix * 4, st));
+  RS_CUDA(cudaMemsetAsync(ctr, 0, kOsMaxPasses * 4, st));
+  radix_os_hist<<<seg_tiles, kSortThreads, 0, st>>>(keys, n, end_bit, hist, tm);
+  radix_os_base<<<seg_tiles, kSortThreads, 0, st>>>(hist, npass, base, tm);
+  RS_COUNT(2);
+  uint32_t *ki = keys, *vi = vals, *ko = k2, *vo = v2;
+  for (int p = 0; p < npass; ++p) {
+    const int shift = p * kRadixBits;
+    const int nb = end_bit - shift < kRadixBits ? end_bit - shift : kRadixBits;
+    RS_CUDA(cudaMemsetAsync(status, 0, size_t(seg_tiles) * kRadix * 4, st));
+    if (vals)
+      radix_os_pass<true><<<seg_tiles, kSortThreads, 0, st>>>(ki, vi, n, shift, nb, p, npass, base, status, ctr + p,
+                                                              ko, vo, tm);
+    else
+      radix_os_pass<false><<<seg_tiles, kSortThreads, 0, st>>>(ki, nullptr, n, shift, nb, p, npass, base, status,
+                                                               ctr + p, ko, nullptr, tm);
+    RS_COUNT(1);
+    RS_LAUNCH_CHECK();
+    std::swap(ki, ko);
+    std::swap(vi, vo);
+  }
+  *keys_res = ki;
+  if (vals_res) *vals_res = vi;
 }
 
 }  // namespace rs
