@@ -455,19 +455,37 @@ __device__ __forceinline__ void expand_tile(uint64_t a, uint64_t N, uint64_t R, 
       if (sm.woff[mid] <= q0) lo = mid;
       else hi = mid;
     }
+    // the current record's end, table, hash size and counter base in
+    // registers, refreshed only when an id crosses into the next record
+    // (one shared-memory walk step per record instead of per id)
     uint32_t k = lo;
+    const bool smt = tp.J <= kPSmemTables;
+    uint32_t rend = sm.woff[k + 1];  // woff[nwin] is the end sentinel (>= tend)
+    uint32_t t = sm.winfo[k];
+    uint64_t H = 0, tb = 0;
+    if (t != kSkip) {
+      H = smt ? sm.thash[t] : tp.hsize[t];
+      tb = smt ? sm.tbase[t] : tp.base[t];
+    }
 #pragma unroll
     for (int u = 0; u < kPIds; ++u) {
       const uint64_t q = q0 + u;
       if (q < tend) {
-        while (k + 1 <= nwin && sm.woff[k + 1] <= q) ++k;
-        const uint32_t t = sm.winfo[k];
+        if (q >= rend) {
+          do {
+            ++k;
+            rend = k + 1 <= nwin ? sm.woff[k + 1] : uint32_t(tend);
+          } while (q >= rend && k + 1 <= nwin);
+          t = sm.winfo[k];
+          if (t != kSkip) {
+            H = smt ? sm.thash[t] : tp.hsize[t];
+            tb = smt ? sm.tbase[t] : tp.base[t];
+          }
+        }
         if (t != kSkip) {
-          const bool smt = tp.J <= kPSmemTables;
-          const uint64_t H = smt ? sm.thash[t] : tp.hsize[t];
           const uint64_t row = RAW ? fast_mod(mix64(rawv[u]), H, tp.magic[t]) : uint64_t(idv[u]);
           if (row >= H) atomicOr(err, kErrRowRange);
-          else fn(uint32_t((smt ? sm.tbase[t] : tp.base[t]) + row), u);
+          else fn(uint32_t(tb + row), u);
         }
       }
     }
@@ -534,10 +552,10 @@ part_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restrict__ rinf
   __shared__ uint32_t s_total;
   for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) tcnt[i] = 0;
   for (uint64_t a = a0; a < a1; a += kPTile) {
-    for (int u = 0; u < kPIds; ++u) sa[threadIdx.x * kPIds + u] = kSkip;
+    for (int u = 0; u < kPIds; ++u) sa[u * kPThreads + threadIdx.x] = kSkip;
     expand_tile<RAW>(a, a1, R, roff, rinfo, ids, raw, tp, sm, rcur, err, bad, [&](uint32_t addr, int u) {
-      sa[threadIdx.x * kPIds + u] = addr;
-      sr[threadIdx.x * kPIds + u] = atomicAdd(&tcnt[addr >> kP3Bits], 1u);
+      sa[u * kPThreads + threadIdx.x] = addr;
+      sr[u * kPThreads + threadIdx.x] = atomicAdd(&tcnt[addr >> kP3Bits], 1u);
     });
     // expand_tile ends with a barrier: tile counts complete
     uint32_t part = 0;
@@ -558,8 +576,8 @@ part_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restrict__ rinf
     if (threadIdx.x == 0) s_total = tot;
     __syncthreads();
     for (int u = 0; u < kPIds; ++u) {
-      const uint32_t x = sa[threadIdx.x * kPIds + u];
-      if (x != kSkip) stage[toff[x >> kP3Bits] + sr[threadIdx.x * kPIds + u]] = x;
+      const uint32_t x = sa[u * kPThreads + threadIdx.x];
+      if (x != kSkip) stage[toff[x >> kP3Bits] + sr[u * kPThreads + threadIdx.x]] = x;
     }
     __syncthreads();
     const uint32_t total = s_total;
