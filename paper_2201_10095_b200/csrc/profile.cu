@@ -313,7 +313,7 @@ constexpr int kPThreads = 256;
 constexpr int kPIds = 8;                         // ids per thread per tile
 constexpr int kPTile = kPThreads * kPIds;        // 2048 ids
 constexpr int kPRecWin = kPTile + 1;             // record window (len-1 records)
-constexpr uint32_t kPMaxBuckets = 4096;  // P2 shared bucket cursors + tile counts/offsets (48 KB)
+constexpr uint32_t kPMaxBuckets = 8192;  // P2: cursors + tile counts + offsets in shared memory (3 x 4 B per bucket)
 constexpr int kP3Bits = 15;                      // 32768 counters per bucket (P3 shared histogram)
 
 // P0: contiguity check + per-record info.  bad |= 1 if the records do not
