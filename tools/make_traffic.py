@@ -63,7 +63,7 @@ def main(step_csv, prof_csv=None, config="rm1", out=os.path.join(ROOT, "profiles
         "library_sha256": lib_sha256(),
         "commit": subprocess.run(["git", "-C", ROOT, "rev-parse", "--short", "HEAD"], capture_output=True,
                                  text=True).stdout.strip(),
-        "date": datetime.datetime.utcnow().strftime("%Y-%m-%dT%H:%M:%SZ"),
+        "date": datetime.datetime.now(datetime.timezone.utc).strftime("%Y-%m-%dT%H:%M:%SZ"),
         "script": "tools/make_traffic.py",
         config: {
             "forward_dram_bytes": sum(dram(x) for x in fwd) / max(1, nfwd),
