@@ -232,7 +232,7 @@ __device__ __forceinline__ int32_t fwd_bag_entry(const TableDev* __restrict__ ta
 // contention), 2 1.30, 4 1.44, 16 2.03, 64 4.68; the old grid-stride loop
 // 1.55 ms), and the per-table hit counters are flushed only when the table
 // changes.
-template <int G, int VPL, int UNR, int MINB, class E>
+template <int G, int VPL, int UNR, int MINB, class E, bool FULL>
 __global__ void __launch_bounds__(kFwdThreads, MINB)
 forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__ cls_tables,
                 uint32_t ntab, uint32_t B, const uint32_t* __restrict__ offsets,
@@ -342,7 +342,11 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
           }
         }
       }
-      for (uint32_t j = 0; j < n; j += UNR) {
+      // rows in whole blocks of UNR (no per-row predicate), then the tail;
+      // FULL (every table of the class exactly G*VPL*4 wide) drops the
+      // per-lane width test
+      uint32_t j = 0;
+      for (; j + UNR <= n; j += UNR) {
         float4 v[UNR][VPL];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
@@ -351,21 +355,41 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
 #pragma unroll
           for (int vv = 0; vv < VPL; ++vv) {
             const uint32_t vec = lg + vv * G;
-            v[u][vv] = (j + u < n && vec < V) ? Elem<E>::load_nc(row, vec) : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[u][vv] = (FULL || vec < V) ? Elem<E>::load_nc(row, vec) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
         if (!pf) nidx = fwd_bag_index(indices, lg, ns, ne);  // behind this bag's first rows
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
-          if (j + u < n) {
 #pragma unroll
-            for (int vv = 0; vv < VPL; ++vv) {
-              acc[vv].x = __fadd_rn(acc[vv].x, v[u][vv].x);
-              acc[vv].y = __fadd_rn(acc[vv].y, v[u][vv].y);
-              acc[vv].z = __fadd_rn(acc[vv].z, v[u][vv].z);
-              acc[vv].w = __fadd_rn(acc[vv].w, v[u][vv].w);
-            }
+          for (int vv = 0; vv < VPL; ++vv) {
+            acc[vv].x = __fadd_rn(acc[vv].x, v[u][vv].x);
+            acc[vv].y = __fadd_rn(acc[vv].y, v[u][vv].y);
+            acc[vv].z = __fadd_rn(acc[vv].z, v[u][vv].z);
+            acc[vv].w = __fadd_rn(acc[vv].w, v[u][vv].w);
           }
+        }
+        if (!pf) {
+          nent = fwd_bag_entry(tables, err, lg, nt, ns, ne, nidx);
+          pf = true;
+        }
+      }
+      for (; j < n; ++j) {
+        const int32_t eu = __shfl_sync(gmask, ent, int(j), G);
+        const char* row = row_ptr(td, rbase, eu);
+        float4 v[VPL];
+#pragma unroll
+        for (int vv = 0; vv < VPL; ++vv) {
+          const uint32_t vec = lg + vv * G;
+          v[vv] = (FULL || vec < V) ? Elem<E>::load_nc(row, vec) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        if (!pf) nidx = fwd_bag_index(indices, lg, ns, ne);
+#pragma unroll
+        for (int vv = 0; vv < VPL; ++vv) {
+          acc[vv].x = __fadd_rn(acc[vv].x, v[vv].x);
+          acc[vv].y = __fadd_rn(acc[vv].y, v[vv].y);
+          acc[vv].z = __fadd_rn(acc[vv].z, v[vv].z);
+          acc[vv].w = __fadd_rn(acc[vv].w, v[vv].w);
         }
         if (!pf) {
           nent = fwd_bag_entry(tables, err, lg, nt, ns, ne, nidx);
@@ -382,7 +406,7 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
 #pragma unroll
       for (int vv = 0; vv < VPL; ++vv) {
         const uint32_t vec = lg + vv * G;
-        if (vec < V) o[vec] = acc[vv];
+        if (FULL || vec < V) o[vec] = acc[vv];
       }
     }
     if (!more) break;
@@ -547,6 +571,7 @@ struct rs_emb {
     int G, VPL, EB;
     std::vector<uint32_t> tables;
     uint32_t* d_list = nullptr;
+    bool full = true;  // every table exactly 4*G*VPL wide (no per-lane width test)
   };
   std::vector<Class> classes;
   uint32_t key_bits = 0;  // max over tables of the slot-key width
@@ -891,10 +916,11 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
       auto it = std::find_if(e->classes.begin(), e->classes.end(),
                              [&](const rs_emb::Class& c) { return c.G == G && c.VPL == vp2 && c.EB == EB; });
       if (it == e->classes.end()) {
-        e->classes.push_back({G, vp2, EB, {}, nullptr});
+        e->classes.push_back({G, vp2, EB, {}, nullptr, true});
         it = e->classes.end() - 1;
       }
       it->tables.push_back(t);
+      if (tabs[t].dim != uint32_t(4 * G * vp2)) it->full = false;
     }
     for (auto& c : e->classes) {
       RS_CUDA(cudaMalloc(&c.d_list, 4 * c.tables.size()));
@@ -1311,10 +1337,11 @@ static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint
   // over rows in flight per group (the 32-register cap spills only in the
   // per-bag cursor code)
   constexpr int MINB = MINB_;
-  auto kern = emb::forward_kernel<G, VPL, UNR_, MINB, E>;
+  auto kern = c.full ? emb::forward_kernel<G, VPL, UNR_, MINB, E, true> : emb::forward_kernel<G, VPL, UNR_, MINB, E, false>;
   static const int per_sm = [&] {
     int n = 0;
-    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, emb::kFwdThreads, 0));
+    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, emb::forward_kernel<G, VPL, UNR_, MINB, E, false>,
+                                                          emb::kFwdThreads, 0));
     return std::max(1, n);
   }();
   const unsigned grid = unsigned(std::max<uint64_t>(

@@ -13,7 +13,7 @@ python tools/ncu_summary.py gpurun_out/launches_step.csv > gpurun_out/launches_s
 timeout -s KILL 600 ncu --nvtx --nvtx-include "profile_call/" --metrics $M --clock-control none --csv \
   --log-file gpurun_out/launches_prof.csv python tools/prof_bench.py --ids 1e9 --reps 1 > /dev/null 2>&1
 python tools/ncu_summary.py gpurun_out/launches_prof.csv > gpurun_out/launches_prof_summary.txt 2>&1; head -8 gpurun_out/launches_prof_summary.txt
-for k in "fwd:forward_kernel" "seg:bwd_seg_kernel" "down:radix_downsweep" "scat:part_kernel"; do
+for k in "fwd:forward_kernel" "seg:bwd_seg_kernel" "ospass:radix_os_pass" "scat:part_kernel"; do
   n=${k%%:*}; re=${k#*:}
   if [ $n = scat ]; then cmd="python tools/prof_bench.py --ids 2e8 --reps 1"; rng=profile_call; skip=1;
   else cmd="python tools/op_bench.py --iters 2"; rng=bench_step; skip=0; fi
