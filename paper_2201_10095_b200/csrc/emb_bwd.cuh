@@ -110,6 +110,45 @@ __device__ __forceinline__ void update_row(const BwdArgs& a, const TableDev& td,
   }
 }
 
+// update_row with the row and state pointers already at hand (the
+// short-segment kernel computes them once, before the gradient loads).
+template <int G, int VPL, class E>
+__device__ __forceinline__ void update_row_at(const BwdArgs& a, uint32_t dim, char* wp, float* mp,
+                                              const float4 (&g)[VPL], const float4 (&w)[VPL], float m_old,
+                                              unsigned gmask, int lg) {
+  const uint32_t V = dim >> 2;
+  float mult = a.lr;
+  if (a.opt == RS_OPT_ROWWISE_ADAGRAD) {
+    float q = 0.f;
+#pragma unroll
+    for (int vv = 0; vv < VPL; ++vv) {
+      if (uint32_t(lg + vv * G) < V) {
+        q = __fadd_rn(q, __fmul_rn(g[vv].x, g[vv].x));
+        q = __fadd_rn(q, __fmul_rn(g[vv].y, g[vv].y));
+        q = __fadd_rn(q, __fmul_rn(g[vv].z, g[vv].z));
+        q = __fadd_rn(q, __fmul_rn(g[vv].w, g[vv].w));
+      }
+    }
+#pragma unroll
+    for (int o = G >> 1; o >= 1; o >>= 1) q = __fadd_rn(q, __shfl_xor_sync(gmask, q, o));
+    const float m = __fadd_rn(m_old, __fdiv_rn(q, float(dim)));
+    if (lg == 0) *mp = m;
+    mult = __fdiv_rn(a.lr, __fadd_rn(__fsqrt_rn(m), a.eps));
+  }
+#pragma unroll
+  for (int vv = 0; vv < VPL; ++vv) {
+    const uint32_t vec = lg + vv * G;
+    if (vec < V) {
+      float4 x = w[vv];
+      x.x = __fsub_rn(x.x, __fmul_rn(mult, g[vv].x));
+      x.y = __fsub_rn(x.y, __fmul_rn(mult, g[vv].y));
+      x.z = __fsub_rn(x.z, __fmul_rn(mult, g[vv].z));
+      x.w = __fsub_rn(x.w, __fmul_rn(mult, g[vv].w));
+      Elem<E>::store(wp, vec, x);
+    }
+  }
+}
+
 template <int G, int VPL>
 __device__ __forceinline__ void store_vec(float* base, uint32_t V, int lg, const float4 (&g)[VPL]) {
   float4* p = reinterpret_cast<float4*>(base);
@@ -393,24 +432,41 @@ bwd_seg_kernel(BwdArgs a, const uint4* __restrict__ segs, const uint32_t* __rest
     // the row and its state first: the slot key addresses them directly
     float4 w4[VPL];
     float m_old = 0.f;
-    int32_t e = 0;
+    char* wp = nullptr;
+    float* mp = nullptr;
     // the unbacked sentinel (key nkeys) has no row: summed like any
     // segment (keeps the warp's shuffles converged), never applied
     const bool upd = valid && d.y < td.nkeys;
     if (upd) {
-      e = entry_of_key(td, d.y);
-      const char* wr = row_ptr(td, e);
+      // row and state pointers once (fast-tier keys are the row offset)
+      if (d.y < td.hbm_rows) {
+        wp = td.fast + uint64_t(d.y) * td.rbytes;
+        mp = td.mom_fast + d.y;
+      } else {
+        const int32_t e = entry_of_key(td, d.y);
+        wp = row_ptr(td, e);
+        mp = mom_ptr(td, e);
+      }
 #pragma unroll
       for (int vv = 0; vv < VPL; ++vv) {
         const uint32_t vec = lg + vv * G;
-        w4[vv] = vec < V ? Elem<E>::load(wr, vec) : make_float4(0.f, 0.f, 0.f, 0.f);
+        w4[vv] = vec < V ? Elem<E>::load(wp, vec) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      if (ada) m_old = *mom_ptr(td, e);
+      if (ada) m_old = *mp;
     }
     const float* gcol = a.grad + td.col;
     float4 acc[VPL];
 #pragma unroll
     for (int vv = 0; vv < VPL; ++vv) acc[vv] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (len == 1) {  // most short segments: one gradient row, no unrolled block
+      const uint32_t bu = __shfl_sync(gmask, smp0, 0, G);
+      const float4* gr = reinterpret_cast<const float4*>(gcol + uint64_t(bu) * a.stride);
+#pragma unroll
+      for (int vv = 0; vv < VPL; ++vv) {
+        const uint32_t vec = lg + vv * G;
+        if (vec < V) add4(acc[vv], ld_nc_f4(gr + vec));
+      }
+    } else
     for (uint32_t base = 0; base < len; base += G) {
       const uint32_t nn = min(uint32_t(G), len - base);
       const uint32_t smp = base == 0 ? smp0 : (uint32_t(lg) < nn ? a.vals[d.x + base + lg] : 0u);
@@ -435,7 +491,7 @@ bwd_seg_kernel(BwdArgs a, const uint4* __restrict__ segs, const uint32_t* __rest
       }
     }
     smp0 = d2.z != kNoKey ? a.vals[min(d2.x + uint32_t(lg), npos - 1)] : 0u;
-    if (upd) update_row<G, VPL, E>(a, td, e, acc, w4, m_old, gmask, lg);
+    if (upd) update_row_at<G, VPL, E>(a, td.dim, wp, mp, acc, w4, m_old, gmask, lg);
     d = d2;
   }
 }
