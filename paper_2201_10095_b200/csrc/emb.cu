@@ -670,11 +670,10 @@ struct rs_emb {
   uint4* segs = nullptr;       // [max_lookups] segment descriptors
   size_t long_cap = 0;         // long segments (> 32 positions) <= lookups / 33
   uint4* longs = nullptr;
-  uint32_t* long_np = nullptr;  // [long_cap + 1] pieces per long segment
-  uint32_t* long_ng = nullptr;  // [long_cap + 1] groups per long segment
-  uint32_t* pbase = nullptr;    // [long_cap + 1] exclusive scan of long_np
-  uint32_t* gbase = nullptr;    // [long_cap + 1] exclusive scan of long_ng
-  unsigned* n_long = nullptr;
+  uint32_t* long_np = nullptr;  // [long_cap] first piece of each long segment
+  uint32_t* long_ng = nullptr;  // [long_cap] first group of each long segment
+  uint2* gdesc = nullptr;       // [groups] {long slot, group within it}
+  unsigned* n_long = nullptr;   // {long slots, pieces, groups}
   float* ppart = nullptr;       // [pieces][dmax] piece sums of long segments
   uint4* pdesc = nullptr;       // [pieces] {start, count, table} of each piece
   float* gpart = nullptr;       // [groups][dmax] group sums of long segments
@@ -730,7 +729,7 @@ struct rs_emb {
     if (keys) cudaFree(keys);
     if (vals) cudaFree(vals);
     for (void* p : {(void*)scount, (void*)sbase, (void*)segs, (void*)longs, (void*)long_np, (void*)long_ng,
-                    (void*)pbase, (void*)gbase, (void*)n_long, (void*)ppart, (void*)pdesc, (void*)gpart})
+                    (void*)gdesc, (void*)n_long, (void*)ppart, (void*)pdesc, (void*)gpart})
       if (p) cudaFree(p);
     if (d_meta) cudaFree(d_meta);
     if (h_meta) cudaFreeHost(h_meta);
@@ -959,15 +958,14 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
     RS_CUDA(cudaMalloc(&e->segs, L * sizeof(uint4)));
     e->long_cap = L / (emb::kChunk + 1) + 1;
     RS_CUDA(cudaMalloc(&e->longs, e->long_cap * sizeof(uint4)));
-    RS_CUDA(cudaMalloc(&e->long_np, (e->long_cap + 1) * 4));
-    RS_CUDA(cudaMalloc(&e->long_ng, (e->long_cap + 1) * 4));
-    RS_CUDA(cudaMalloc(&e->pbase, (e->long_cap + 1) * 4));
-    RS_CUDA(cudaMalloc(&e->gbase, (e->long_cap + 1) * 4));
-    RS_CUDA(cudaMalloc(&e->n_long, 4));
+    RS_CUDA(cudaMalloc(&e->long_np, e->long_cap * 4));
+    RS_CUDA(cudaMalloc(&e->long_ng, e->long_cap * 4));
+    RS_CUDA(cudaMalloc(&e->n_long, 16));
     const size_t max_pieces = L / emb::kChunk + e->long_cap + 1;
     const size_t max_groups = L / (emb::kChunk * emb::kGroupPieces) + e->long_cap + 1;
     RS_CUDA(cudaMalloc(&e->ppart, max_pieces * e->dmax * 4));
     RS_CUDA(cudaMalloc(&e->pdesc, max_pieces * sizeof(uint4)));
+    RS_CUDA(cudaMalloc(&e->gdesc, max_groups * sizeof(uint2)));
     RS_CUDA(cudaMalloc(&e->gpart, max_groups * e->dmax * 4));
     e->tiles_cap = L / kSortTile + T + 2;
     e->sort_scratch_bytes =
@@ -1469,11 +1467,12 @@ template <int VPL>
 static void launch_long(rs_emb* e, const emb::BwdArgs& a) {
   const unsigned g = unsigned(sm_count()) * 8;
   cudaStream_t st = e->ctx->stream;
-  emb::bwd_piece_desc_kernel<<<g, emb::kBwdThreads, 0, st>>>(e->longs, e->n_long, e->pbase, e->pdesc);
-  emb::bwd_lpiece_kernel<16, 2 * VPL><<<g, emb::kBwdThreads, 0, st>>>(a, e->pdesc, e->n_long, e->pbase, e->ppart);
-  emb::bwd_group_kernel<VPL><<<g, emb::kBwdThreads, 0, st>>>(a, e->longs, e->n_long, e->pbase, e->gbase,
+  emb::bwd_piece_desc_kernel<<<g, emb::kBwdThreads, 0, st>>>(e->longs, e->n_long, e->long_np, e->long_ng, e->pdesc,
+                                                             e->gdesc);
+  emb::bwd_lpiece_kernel<16, 2 * VPL><<<g, emb::kBwdThreads, 0, st>>>(a, e->pdesc, e->n_long, e->ppart);
+  emb::bwd_group_kernel<VPL><<<g, emb::kBwdThreads, 0, st>>>(a, e->longs, e->n_long, e->long_np, e->gdesc,
                                                              e->ppart, e->gpart);
-  emb::bwd_long_kernel<VPL><<<g, emb::kBwdThreads, 0, st>>>(a, e->longs, e->n_long, e->gbase, e->gpart);
+  emb::bwd_long_kernel<VPL><<<g, emb::kBwdThreads, 0, st>>>(a, e->longs, e->n_long, e->long_ng, e->gpart);
   RS_COUNT(4);
 }
 
@@ -1571,9 +1570,7 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
     e->grad_ready = nullptr;
   }
   // short segments per lane class (long ones are listed)
-  RS_CUDA(cudaMemsetAsync(e->n_long, 0, 4, st));
-  RS_CUDA(cudaMemsetAsync(e->long_np, 0, (e->long_cap + 1) * 4, st));
-  RS_CUDA(cudaMemsetAsync(e->long_ng, 0, (e->long_cap + 1) * 4, st));
+  RS_CUDA(cudaMemsetAsync(e->n_long, 0, 16, st));
   // classes update disjoint rows (the long list is an atomic append): every
   // other class on the forked stream, as in the forward
   const bool fork = e->classes.size() > 1;
@@ -1592,9 +1589,7 @@ void emb_backward(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t* id
     RS_CUDA(cudaEventRecord(e->ev_join, e->fwd_side));
     RS_CUDA(cudaStreamWaitEvent(st, e->ev_join, 0));
   }
-  // long segments: group offsets, group sums, final sums + updates
-  exclusive_scan<uint32_t>(ArrayIn<uint32_t>{e->long_np}, e->long_cap, e->pbase, e->pbase + e->long_cap, scr, st);
-  exclusive_scan<uint32_t>(ArrayIn<uint32_t>{e->long_ng}, e->long_cap, e->gbase, e->gbase + e->long_cap, scr, st);
+  // long segments: piece / group descriptors, piece sums, group sums, final sums + updates
   switch (e->bwd_vpl) {
     case 1: launch_long<1>(e, a); break;
     case 2: launch_long<2>(e, a); break;

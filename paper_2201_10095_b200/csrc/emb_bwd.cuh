@@ -417,11 +417,14 @@ bwd_seg_kernel(BwdArgs a, const uint4* __restrict__ segs, const uint32_t* __rest
     const uint32_t len = valid ? d.w - d.x : 0u;
     if (len > uint32_t(kChunk)) {
       if (lg == 0) {
+        // a slot, and contiguous ranges of pieces and groups (the reduction
+        // tree inside a segment is fixed, so where its range lands does not
+        // change any result)
+        const uint32_t np = (len + kChunk - 1) / kChunk;
         const unsigned slot = atomicAdd(n_long, 1u);
         longs[slot] = make_uint4(d.x, len, d.y, d.z);
-        const uint32_t np = (len + kChunk - 1) / kChunk;
-        long_np[slot] = np;
-        long_ng[slot] = (np + kGroupPieces - 1) / kGroupPieces;
+        long_np[slot] = atomicAdd(n_long + 1, np);                                  // first piece
+        long_ng[slot] = atomicAdd(n_long + 2, (np + kGroupPieces - 1) / kGroupPieces);  // first group
       }
       smp0 = d2.z != kNoKey ? a.vals[min(d2.x + uint32_t(lg), npos - 1)] : 0u;
       d = d2;
@@ -497,25 +500,30 @@ bwd_seg_kernel(BwdArgs a, const uint4* __restrict__ segs, const uint32_t* __rest
 }
 
 // ---------------------------------------------------------------- long segments
-// pbase / gbase = exclusive scans of long_np / long_ng over the long slots
-// (unused slots hold 0 and sort after every used one).
+// Each long slot owns a contiguous range of pieces (first at pfirst[slot])
+// and of groups (gfirst[slot]), reserved with atomics by the short-segment
+// kernel; n_long = {slots, pieces, groups}.
 //
 // Warp per long segment: one {start, count, table} descriptor per 32-position
 // piece at pdesc[pbase[li] + k], so the piece kernel needs no search.
 __global__ void __launch_bounds__(kBwdThreads) bwd_piece_desc_kernel(const uint4* __restrict__ longs,
                                                                     const unsigned* __restrict__ n_long,
-                                                                    const uint32_t* __restrict__ pbase,
-                                                                    uint4* __restrict__ pdesc) {
+                                                                    const uint32_t* __restrict__ pfirst,
+                                                                    const uint32_t* __restrict__ gfirst,
+                                                                    uint4* __restrict__ pdesc,
+                                                                    uint2* __restrict__ gdesc) {
   const int lane = threadIdx.x & 31;
   const uint32_t nl = *n_long;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t li = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; li < nl; li += nwarps) {
     const uint4 L = longs[li];  // {start, len, key, table}
-    const uint32_t base = pbase[li], np = (L.y + kChunk - 1) / kChunk, end = L.x + L.y;
+    const uint32_t base = pfirst[li], np = (L.y + kChunk - 1) / kChunk, end = L.x + L.y;
     for (uint32_t k = lane; k < np; k += 32) {
       const uint32_t pb = L.x + k * kChunk;
       pdesc[base + k] = make_uint4(pb, min(uint32_t(kChunk), end - pb), L.w, 0u);
     }
+    const uint32_t gb = gfirst[li], ng = (np + kGroupPieces - 1) / kGroupPieces;
+    for (uint32_t q = lane; q < ng; q += 32) gdesc[gb + q] = make_uint2(uint32_t(li), q);
   }
 }
 
@@ -526,7 +534,6 @@ __global__ void __launch_bounds__(kBwdThreads) bwd_piece_desc_kernel(const uint4
 template <int G, int VPL>
 __global__ void __launch_bounds__(kBwdThreads, 3) bwd_lpiece_kernel(BwdArgs a, const uint4* __restrict__ pdesc,
                                                                 const unsigned* __restrict__ n_long,
-                                                                const uint32_t* __restrict__ pbase,
                                                                 float* __restrict__ ppart) {
   // G-lane groups (G = 16: two pieces per warp; a dim-128 row is 2 float4
   // per lane, a dim-64 row 1) — the sums are elementwise, so the lane layout
@@ -536,9 +543,9 @@ __global__ void __launch_bounds__(kBwdThreads, 3) bwd_lpiece_kernel(BwdArgs a, c
   const int lane = threadIdx.x & 31;
   const int grp = lane / G, lg = lane % G;
   const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
-  const uint32_t nl = *n_long;
+  const uint32_t nl = n_long[0];
   if (nl == 0) return;
-  const uint32_t npieces = pbase[nl];
+  const uint32_t npieces = n_long[1];
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   uint4 P = make_uint4(0u, 0u, 0u, 0u);
@@ -598,21 +605,20 @@ __global__ void __launch_bounds__(kBwdThreads, 3) bwd_lpiece_kernel(BwdArgs a, c
 template <int VPL>
 __global__ void __launch_bounds__(kBwdThreads) bwd_group_kernel(BwdArgs a, const uint4* __restrict__ longs,
                                                                const unsigned* __restrict__ n_long,
-                                                               const uint32_t* __restrict__ pbase,
-                                                               const uint32_t* __restrict__ gbase,
+                                                               const uint32_t* __restrict__ pfirst,
+                                                               const uint2* __restrict__ gdesc,
                                                                const float* __restrict__ ppart,
                                                                float* __restrict__ gpart) {
   const int lane = threadIdx.x & 31;
-  const uint32_t nl = *n_long;
-  if (nl == 0) return;
-  const uint32_t ngroups = gbase[nl];
+  const uint32_t ngroups = n_long[2];
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t gi = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; gi < ngroups; gi += nwarps) {
-    const uint32_t li = upper_index(gbase, nl, gi);
-    const uint32_t V = a.tables[longs[li].w].dim >> 2;
-    const uint32_t k = uint32_t(gi - gbase[li]);
-    const uint32_t p0 = pbase[li] + k * kGroupPieces;
-    const uint32_t p1 = min(pbase[li + 1], p0 + kGroupPieces);
+    const uint2 gd = gdesc[gi];  // {long slot, group within it}
+    const uint4 L = longs[gd.x];
+    const uint32_t V = a.tables[L.w].dim >> 2;
+    const uint32_t np = (L.y + kChunk - 1) / kChunk;
+    const uint32_t p0 = pfirst[gd.x] + gd.y * kGroupPieces;
+    const uint32_t p1 = min(pfirst[gd.x] + np, p0 + kGroupPieces);
     float4 acc[VPL];
     load_vec<32, VPL>(ppart + uint64_t(p0) * a.dmax, V, lane, acc);
     for (uint32_t p = p0 + 1; p < p1; p += 8) {
@@ -636,7 +642,7 @@ __global__ void __launch_bounds__(kBwdThreads) bwd_group_kernel(BwdArgs a, const
 template <int VPL>
 __global__ void __launch_bounds__(kBwdThreads) bwd_long_kernel(BwdArgs a, const uint4* __restrict__ longs,
                                                               const unsigned* __restrict__ n_long,
-                                                              const uint32_t* __restrict__ gbase,
+                                                              const uint32_t* __restrict__ gfirst,
                                                               const float* __restrict__ gpart) {
   const int lane = threadIdx.x & 31;
   const uint32_t nl = *n_long;
@@ -657,7 +663,8 @@ __global__ void __launch_bounds__(kBwdThreads) bwd_long_kernel(BwdArgs a, const 
       }
     }
     const float m_old = a.opt == RS_OPT_ROWWISE_ADAGRAD ? *mom_ptr(td, e) : 0.f;
-    const uint32_t g0 = gbase[li], g1 = gbase[li + 1];
+    const uint32_t np = (L.y + kChunk - 1) / kChunk;
+    const uint32_t g0 = gfirst[li], g1 = g0 + (np + kGroupPieces - 1) / kGroupPieces;
     load_vec<32, VPL>(gpart + uint64_t(g0) * a.dmax, V, lane, acc);
     for (uint32_t g = g0 + 1; g < g1; ++g) {
       load_vec<32, VPL>(gpart + uint64_t(g) * a.dmax, V, lane, x);
