@@ -252,7 +252,7 @@ int or_emb_forward(uint32_t T, uint64_t B, const uint32_t* D,
 }
 
 /* Lanes per row and the per-lane / xor-butterfly order of the kernel's
- * sum-of-squares (paper_2201_10095_b200/csrc/emb_backward.cu). */
+ * sum-of-squares (paper_2201_10095_b200/csrc/emb_bwd.cuh). */
 static uint32_t lanes_for(uint32_t D) {
   uint32_t v = D / 4, L = 1;
   while (L < v && L < 32) L <<= 1;

@@ -7,19 +7,24 @@
 // encoding include/shardplan/remap.hpp:27-29).  The forward's fast/slow hit
 // counters equal simulate()'s accounting (core/src/simulator.cpp:86).
 //
-// HBM layout: per table a fast-tier block [hbm_rows, dim] fp32 in one device
-// pool, a slow-tier block [slow_rows, dim] fp32 in one pinned, mapped host
-// pool read zero-copy over PCIe, the int32 remap [hash_size] in HBM, and for
-// row-wise Adagrad one fp32 momentum per row in the row's tier.
+// HBM layout: per table a fast-tier block [hbm_rows, dim] (fp32 or fp16
+// rows) in one device pool, the backed slow-tier block [slow_rows, dim] in one
+// pinned, mapped host pool (read zero-copy over PCIe, or staged into HBM slots
+// by uvm_cache.cuh), the int32 remap [hash_size] in HBM, and for row-wise
+// Adagrad one fp32 state per row (both tiers' states in HBM).
 //
-// K4 forward: a G-lane group per bag (G = lanes to cover dim/4 float4s, <=32),
-//   32/G bags per warp, one table per warp.  Lanes load G indices and their
-//   remap entries in parallel, then the group issues 8 row gathers
-//   (128-bit ld.global.nc) before accumulating them in lookup order.
-// K5 backward: keys (row id) / values (sample) -> stable LSD radix sort ->
-//   fixed 64-position chunks: a warp reduces each row-segment piece in its
-//   chunk in sorted order; pieces crossing a chunk edge are combined by the
-//   owning chunk in chunk order.  Fully deterministic, no float atomics.
+// K4 forward (forward_kernel): a G-lane group per bag (G = lanes to cover
+//   dim/4 four-element vectors, <= 32), 32/G bags per warp-iteration; lanes
+//   load G indices and their remap entries in parallel, then each group keeps
+//   2 row gathers (ld.global.nc) in flight and adds them in lookup order.
+//   Warps claim 2 consecutive bag-groups at a time (the GPU sweeps the tables
+//   in a narrow band); the next bag's offsets, first indices and remap
+//   entries are prefetched behind the current bag's rows.
+// K5 backward (emb_bwd.cuh): (slot key, sample) pairs written by the forward
+//   -> per-table onesweep radix sort (scan_sort.cuh) -> segment descriptors ->
+//   short segments (<= 32 lookups) summed in order and updated by G-lane
+//   groups; long ones as 32-position pieces, 64-piece groups, then the row
+//   update.  Fully deterministic, no float atomics.
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
