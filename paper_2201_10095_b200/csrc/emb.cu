@@ -347,10 +347,42 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
           }
         }
       }
-      // rows in whole blocks of UNR (no per-row predicate), then the tail;
-      // FULL (every table of the class exactly G*VPL*4 wide) drops the
-      // per-lane width test
+      // the bag's first block (up to UNR rows, predicated) carries the next
+      // bag's prefetch: its first indices behind these row loads, their remap
+      // entries after the adds; then whole blocks of UNR (no per-row
+      // predicate) and the tail.  FULL (every table of the class exactly
+      // G*VPL*4 wide) drops the per-lane width test.
       uint32_t j = 0;
+      if (!pf) {
+        float4 v[UNR][VPL];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const int32_t eu = __shfl_sync(gmask, ent, u, G);
+          const char* row = row_ptr(td, rbase, eu);
+#pragma unroll
+          for (int vv = 0; vv < VPL; ++vv) {
+            const uint32_t vec = lg + vv * G;
+            v[u][vv] = (uint32_t(u) < n && (FULL || vec < V)) ? Elem<E>::load_nc(row, vec)
+                                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+        nidx = fwd_bag_index(indices, lg, ns, ne);
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          if (uint32_t(u) < n) {
+#pragma unroll
+            for (int vv = 0; vv < VPL; ++vv) {
+              acc[vv].x = __fadd_rn(acc[vv].x, v[u][vv].x);
+              acc[vv].y = __fadd_rn(acc[vv].y, v[u][vv].y);
+              acc[vv].z = __fadd_rn(acc[vv].z, v[u][vv].z);
+              acc[vv].w = __fadd_rn(acc[vv].w, v[u][vv].w);
+            }
+          }
+        }
+        nent = fwd_bag_entry(tables, err, lg, nt, ns, ne, nidx);
+        pf = true;
+        j = min(uint32_t(UNR), n);
+      }
       for (; j + UNR <= n; j += UNR) {
         float4 v[UNR][VPL];
 #pragma unroll
@@ -363,7 +395,6 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
             v[u][vv] = (FULL || vec < V) ? Elem<E>::load_nc(row, vec) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
-        if (!pf) nidx = fwd_bag_index(indices, lg, ns, ne);  // behind this bag's first rows
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
 #pragma unroll
@@ -373,10 +404,6 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
             acc[vv].z = __fadd_rn(acc[vv].z, v[u][vv].z);
             acc[vv].w = __fadd_rn(acc[vv].w, v[u][vv].w);
           }
-        }
-        if (!pf) {
-          nent = fwd_bag_entry(tables, err, lg, nt, ns, ne, nidx);
-          pf = true;
         }
       }
       for (; j < n; ++j) {
@@ -388,17 +415,12 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
           const uint32_t vec = lg + vv * G;
           v[vv] = (FULL || vec < V) ? Elem<E>::load_nc(row, vec) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        if (!pf) nidx = fwd_bag_index(indices, lg, ns, ne);
 #pragma unroll
         for (int vv = 0; vv < VPL; ++vv) {
           acc[vv].x = __fadd_rn(acc[vv].x, v[vv].x);
           acc[vv].y = __fadd_rn(acc[vv].y, v[vv].y);
           acc[vv].z = __fadd_rn(acc[vv].z, v[vv].z);
           acc[vv].w = __fadd_rn(acc[vv].w, v[vv].w);
-        }
-        if (!pf) {
-          nent = fwd_bag_entry(tables, err, lg, nt, ns, ne, nidx);
-          pf = true;
         }
       }
     }
