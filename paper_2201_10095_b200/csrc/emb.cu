@@ -1344,7 +1344,9 @@ static uint32_t fwd_chunk() {
   return c;
 }
 
-template <int G, int VPL, class E, int UNR_ = (VPL > 1 ? 8 : 2), int MINB_ = (VPL > 1 ? 1 : 8)>
+// wide rows (VPL > 1) the same way: B200 RM3-like (dim 256 fp16, G 32, VPL 2):
+// (2 rows, 4 CTAs/SM) 5.96 ms, (2, 6) 5.98, (4, 4) 6.71, (4, 2) 7.27, (8, 1) 10.18
+template <int G, int VPL, class E, int UNR_ = 2, int MINB_ = (VPL == 1 ? 8 : VPL == 2 ? 4 : VPL == 4 ? 3 : 2)>
 static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint32_t* off,
                        const uint32_t* idx, const OutMap& out, uint64_t stride, unsigned long long* hits,
                        cudaStream_t st) {
@@ -1468,7 +1470,9 @@ static void launch_segs_v(rs_emb* e, const emb::BwdArgs& a, uint32_t ci, uint64_
 template <int G, int VPL, class E>
 static void launch_segs(rs_emb* e, const emb::BwdArgs& a, uint32_t ci, uint64_t max_windows, cudaStream_t st) {
   if constexpr (VPL == 1) launch_segs_v<G, 1, 4, RS_SEG_MINB, E>(e, a, ci, max_windows, st);
-  else launch_segs_v<G, VPL, (VPL == 2 ? 2 : 1), 2, E>(e, a, ci, max_windows, st);
+  // wide rows: B200 RM3-like (dim 256 fp16): (2 rows, 4 CTAs/SM) 16.9-17.0 ms
+  // backward, (1, 4) 16.9-17.0, (1, 3) 17.0, (2, 3) 17.3, (2, 2) 18.5
+  else launch_segs_v<G, VPL, 2, (VPL >= 8 ? 2 : 4), E>(e, a, ci, max_windows, st);
 }
 
 template <class E>

@@ -21,6 +21,7 @@ def main():
     p.add_argument("--iters", type=int, default=10)
     p.add_argument("--batch", type=int, default=16384)
     p.add_argument("--optimizer", default="rowwise_adagrad")
+    p.add_argument("--hash-scale", type=float, default=1.0, help="shrink every hash size (rm configs)")
     p.add_argument("--slow-frac", type=float, default=0.0,
                    help="fraction of each table's rows (highest ids) placed in the host tier")
     a = p.parse_args()
@@ -29,7 +30,7 @@ def main():
     import paper_2201_10095_b200 as sp
     from paper_2201_10095_b200 import workload as wl
 
-    specs = wl.rm_specs(a.config) if a.config != "cfg1" else wl.cfg1_specs()
+    specs = wl.rm_specs(a.config, hash_scale=a.hash_scale) if a.config != "cfg1" else wl.cfg1_specs()
     B = a.batch
     dev = torch.device("cuda", 0)
     remaps = []
