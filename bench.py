@@ -535,7 +535,7 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
             and rep.total_accesses == int(hh.sum()))
     if do_e2e and T:
         res["e2e"] = run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex,
-                             res["mode"] == "pipelined", args.prefetch_depth)
+                             res["mode"] == "pipelined", args.prefetch_depth, flush)
     if op:
         op.close()
     del remaps, batches
@@ -765,7 +765,7 @@ def modes(r):
             for m, k in (("zero-copy", "zero_copy"), ("pipelined", "pipelined"))}
 
 
-def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex, cache, depth=2):
+def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex, cache, depth=2, flush=None):
     """Same step through the public API with host inputs: every step's offsets +
     indices are copied from pinned host memory (a copy stream, two batches
     ahead, triple-buffered — the data loader's overlap) and the hit counters
@@ -820,6 +820,8 @@ def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex, cache, 
                 torch.cuda.synchronize()
                 s.record()
             h2d(i + ahead, total)
+            if flush is not None:  # the same L2 flush between steps as the device-resident run
+                flush.zero_()
             if cache and depth == 1 and i + 1 < total:
                 main.wait_event(ev_in[(i + 1) % nb])
                 op.prefetch(*view(i + 1), B)
