@@ -236,15 +236,40 @@ def profile_sharded(trace, sample_rate: float, seed: int, group=None, profile_fn
 
     if profile_fn is None:
         from .profiler import profile as profile_fn
+    import torch
+
+    from .types import FeatureStats
+
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     split = profile_split(trace.tables, world)
     mine = split[rank]
     got = profile_fn(subtrace(trace, mine), sample_rate, seed) if mine else []
+    # the small fields (scalars, 101-step ICDFs, array lengths) as objects;
+    # rows_by_rank (u32) and access_cdf (f64 bits) of all of a rank's tables
+    # as ONE flat int64 tensor per rank — not pickled — all-gathered padded to
+    # the longest rank (device tensors over NCCL, host tensors over gloo)
+    meta = [(int(st.table_id), float(st.coverage), float(st.avg_pooling), int(st.distinct_rows_accessed),
+             int(st.total_accesses), np.asarray(st.icdf_steps, np.uint64)) for st in got]
     parts = [None] * world
-    dist.all_gather_object(parts, (mine, list(got)), group=group)
+    dist.all_gather_object(parts, (mine, meta), group=group)
+    flat = np.concatenate([np.concatenate([np.asarray(st.rows_by_rank, np.uint32).astype(np.int64),
+                                           np.asarray(st.access_cdf, np.float64).view(np.int64)])
+                           for st in got]) if got else np.zeros(0, np.int64)
+    sizes = [sum(2 * m[3] for m in meta_r) for _, meta_r in parts]
+    n = max(1, max(sizes))
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+    buf = torch.zeros(n, dtype=torch.int64, device=dev)
+    buf[:flat.size] = torch.from_numpy(flat).to(dev)
+    bufs = [torch.empty(n, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(bufs, buf, group=group)
     out = [None] * len(trace.tables)
-    for pos, stats in parts:
-        for j, st in zip(pos, stats):
-            out[j] = st
+    for (pos, meta_r), b in zip(parts, bufs):
+        arr = b.cpu().numpy()
+        at = 0
+        for j, (tid, cov, pool, d, tot, icdf) in zip(pos, meta_r):
+            rows = arr[at:at + d].astype(np.uint32)
+            cdf = arr[at + d:at + 2 * d].view(np.float64).copy()
+            at += 2 * d
+            out[j] = FeatureStats(tid, cov, pool, d, tot, icdf, cdf, rows)
     return out

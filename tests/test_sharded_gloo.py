@@ -105,10 +105,12 @@ def _small_trace(seed=3):
 
 
 def _cpu_profile(tr, rate, seed):
+    """The C oracle's profile() as FeatureStats (what profile_sharded gathers)."""
     import oracle
+    from paper_2201_10095_b200.types import FeatureStats
 
-    return oracle.C().profile(tr.tables, tr.num_samples, tr.rec_sample, tr.rec_table, tr.rec_offset,
-                              tr.rec_len, tr.ids, rate, seed)
+    return [FeatureStats(**d) for d in oracle.C().profile(tr.tables, tr.num_samples, tr.rec_sample, tr.rec_table,
+                                                          tr.rec_offset, tr.rec_len, tr.ids, rate, seed)]
 
 
 def _profile_worker(rank, world, port, q):
@@ -122,12 +124,12 @@ def _profile_worker(rank, world, port, q):
         got = profile_sharded(tr, 0.6, 11, profile_fn=_cpu_profile)
         want = _cpu_profile(tr, 0.6, 11)
         ok = len(got) == len(want) and all(
-            g["table_id"] == w["table_id"] and g["total_accesses"] == w["total_accesses"]
-            and g["distinct_rows_accessed"] == w["distinct_rows_accessed"]
-            and float(g["coverage"]) == float(w["coverage"])
-            and np.array_equal(np.asarray(g["rows_by_rank"]), np.asarray(w["rows_by_rank"]))
-            and np.array_equal(np.asarray(g["icdf_steps"]), np.asarray(w["icdf_steps"]))
-            and np.array_equal(np.asarray(g["access_cdf"]).view(np.uint64), np.asarray(w["access_cdf"]).view(np.uint64))
+            g.table_id == w.table_id and g.total_accesses == w.total_accesses
+            and g.distinct_rows_accessed == w.distinct_rows_accessed
+            and float(g.coverage) == float(w.coverage) and float(g.avg_pooling) == float(w.avg_pooling)
+            and np.array_equal(np.asarray(g.rows_by_rank), np.asarray(w.rows_by_rank))
+            and np.array_equal(np.asarray(g.icdf_steps), np.asarray(w.icdf_steps))
+            and np.array_equal(np.asarray(g.access_cdf).view(np.uint64), np.asarray(w.access_cdf).view(np.uint64))
             for g, w in zip(got, want))
         q.put((rank, ok))
     finally:
@@ -155,9 +157,9 @@ def test_subtrace_keeps_each_tables_profile():
         got = _cpu_profile(subtrace(tr, pos), 0.6, 11)
         for j, g in zip(pos, got):
             w = want[j]
-            assert g["table_id"] == w["table_id"]
-            assert np.array_equal(np.asarray(g["rows_by_rank"]), np.asarray(w["rows_by_rank"]))
-            assert float(g["coverage"]) == float(w["coverage"]) and float(g["avg_pooling"]) == float(w["avg_pooling"])
+            assert g.table_id == w.table_id
+            assert np.array_equal(np.asarray(g.rows_by_rank), np.asarray(w.rows_by_rank))
+            assert float(g.coverage) == float(w.coverage) and float(g.avg_pooling) == float(w.avg_pooling)
 
 
 def test_profile_sharded_world2_gloo():
