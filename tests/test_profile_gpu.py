@@ -232,3 +232,26 @@ def test_profile_by_table_shards_equals_whole(cuda_ctx):
             for j, st in zip(pos, sp.profile(subtrace(tr, pos), 0.7, 3, ctx=cuda_ctx)):
                 got[j] = st
         assert_stats_equal(got, [vars(s) for s in whole])
+
+
+def test_profile_partitioned_more_tables_than_shared(cuda_ctx, coracle):
+    """The partitioned histogram with more tables than its shared-memory
+    table-parameter cache holds (kPSmemTables = 512: the expansion reads base
+    and hash size from global memory) and with more than 4096 buckets: 700
+    tables, >= 2^22 ids, bit-exact vs the oracle."""
+    rng = np.random.default_rng(41)
+    J, S = 700, 1500
+    tables = [TableSpec(5000 + j, 1000, int(h), 4, 4) for j, h in enumerate(rng.integers(100, 400_000, J))]
+    assert sum(t.hash_size for t in tables) > 4096 * 32768
+    lens = rng.integers(0, 10, S * J).astype(np.uint32)
+    rec_sample = np.repeat(np.arange(S, dtype=np.uint64), J)
+    rec_table = np.tile(np.array([t.table_id for t in tables], np.uint32), S)
+    rec_offset = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.uint64)
+    N = int(lens.sum())
+    assert N >= (1 << 22)
+    Hs = np.repeat(np.tile(np.array([t.hash_size for t in tables], np.int64), S), lens)
+    ids = (rng.random(N) ** 3 * Hs).astype(np.uint32)  # skewed towards low rows
+    tr = Trace(tables, S, rec_sample, rec_table, rec_offset, lens, ids=ids)
+    got = sp.profile(tr, 1.0, 3, ctx=cuda_ctx)
+    want = coracle.profile(tables, S, rec_sample, rec_table, rec_offset, lens, ids, 1.0, 3)
+    assert_stats_equal(got, want)
