@@ -13,10 +13,12 @@
 // by uvm_cache.cuh), the int32 remap [hash_size] in HBM, and for row-wise
 // Adagrad one fp32 state per row (both tiers' states in HBM).
 //
-// K4 forward (forward_kernel): a G-lane group per bag (G = lanes to cover
-//   dim/4 four-element vectors, <= 32), 32/G bags per warp-iteration; lanes
-//   load G indices and their remap entries in parallel, then each group keeps
-//   2 row gathers (ld.global.nc) in flight and adds them in lookup order.
+// K4 forward: resolve_kernel turns every lookup's index into its storage-slot
+//   key (remap applied; the backward's sort input) at streaming rate, then
+//   forward_kernel runs a G-lane group per bag (G = lanes to cover dim/4
+//   four-element vectors, <= 32), 32/G bags per warp-iteration; lanes load G
+//   slot keys in parallel, then each group keeps 2 row gathers
+//   (ld.global.nc) in flight and adds them in lookup order.
 //   Warps claim 2 consecutive bag-groups at a time (the GPU sweeps the tables
 //   in a narrow band); the next bag's offsets, first indices and remap
 //   entries are prefetched behind the current bag's rows.
@@ -211,9 +213,11 @@ __device__ __forceinline__ uint32_t fwd_bag_index(const uint32_t* __restrict__ i
                                                   uint32_t e) {
   return s < e && uint32_t(lg) < e - s ? ld_stream_u32(indices + s + lg) : 0u;
 }
+template <bool FK = false>
 __device__ __forceinline__ int32_t fwd_bag_entry(const TableDev* __restrict__ tables, unsigned* err, int lg,
                                                  uint32_t t, uint32_t s, uint32_t e, uint32_t idx) {
   if (s >= e || uint32_t(lg) >= e - s) return 0;
+  if (FK) return entry_of_key(tables[t], idx);
   const TableDev& tn = tables[t];
   if (idx >= tn.hash_size) {  // reported by the next backward / rs_emb_check
     atomicOr(err, 1u);
@@ -237,7 +241,9 @@ __device__ __forceinline__ int32_t fwd_bag_entry(const TableDev* __restrict__ ta
 // contention), 2 1.30, 4 1.44, 16 2.03, 64 4.68; the old grid-stride loop
 // 1.55 ms), and the per-table hit counters are flushed only when the table
 // changes.
-template <int G, int VPL, int UNR, int MINB, class E, bool FULL>
+// FK: `indices` are the slot keys resolve_kernel wrote (entry_of_key instead
+// of the remap load; the keys/vals for the backward are already written).
+template <int G, int VPL, int UNR, int MINB, class E, bool FULL, bool FK = false>
 __global__ void __launch_bounds__(kFwdThreads, MINB)
 forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__ cls_tables,
                 uint32_t ntab, uint32_t B, const uint32_t* __restrict__ offsets,
@@ -278,7 +284,7 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
   int32_t nent = 0;
   bag_offsets(ti, k, nt, ns, ne);
   nidx = fwd_bag_index(indices, lg, ns, ne);
-  nent = fwd_bag_entry(tables, err, lg, nt, ns, ne, nidx);
+  nent = fwd_bag_entry<FK>(tables, err, lg, nt, ns, ne, nidx);
   while (true) {
     const uint32_t t = nt, s = ns, e = ne;
     const int32_t ent0 = nent;
@@ -330,15 +336,19 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
           ent = ent0;
         } else {
           uint32_t idx = ld_stream_u32(indices + l);
-          if (idx >= td.hash_size) {
-            atomicOr(err, 1u);
-            idx = 0;
+          if (FK) {
+            ent = entry_of_key(td, idx);
+          } else {
+            if (idx >= td.hash_size) {
+              atomicOr(err, 1u);
+              idx = 0;
+            }
+            ent = td.remap[idx];
           }
-          ent = td.remap[idx];
         }
         fast += ent >= 0;
         unb += ent < 0 && slow_off(ent) >= td.slow_rows;
-        if (keys) {
+        if (!FK && keys) {
           if (l < max_keys) {
             keys[l] = slot_of_entry(td, ent);
             vals[l] = b;
@@ -379,7 +389,7 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
             }
           }
         }
-        nent = fwd_bag_entry(tables, err, lg, nt, ns, ne, nidx);
+        nent = fwd_bag_entry<FK>(tables, err, lg, nt, ns, ne, nidx);
         pf = true;
         j = min(uint32_t(UNR), n);
       }
@@ -426,7 +436,7 @@ forward_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict__
     }
     if (!pf) {  // an empty bag: fetch the next one's head directly
       nidx = fwd_bag_index(indices, lg, ns, ne);
-      nent = fwd_bag_entry(tables, err, lg, nt, ns, ne, nidx);
+      nent = fwd_bag_entry<FK>(tables, err, lg, nt, ns, ne, nidx);
     }
     if (valid) {
       float4* o = reinterpret_cast<float4*>(out_row(om, b, stride) + (om.xcol ? om.xcol[t] : td.col));
@@ -487,6 +497,73 @@ keygen_kernel(const TableDev* __restrict__ tables, uint32_t T, uint64_t B,
         const TableDev& tdk = tables[gk / B];
         keys[l] = slot_of_entry(tdk, tdk.remap[idx < Hk ? idx : 0u]);
         vals[l] = uint32_t(gk % B);
+      }
+    }
+  }
+}
+
+
+// The forward's index resolution as its own streaming pass: for every lookup
+// l of bag (t, b), keys[l] = storage slot of remap[indices[l]] and vals[l] =
+// b (the backward's sort input).  A warp takes 32 consecutive bags, flattens
+// their lookups over its lanes and keeps 4 lookups per lane in flight, so the
+// index -> remap chain runs at streaming rate instead of on the gather's
+// critical path; the gather then reads the slot keys (forward_kernel<FK>).
+__global__ void __launch_bounds__(256)
+resolve_kernel(const TableDev* __restrict__ tables, uint32_t T, uint32_t B, const uint32_t* __restrict__ offsets,
+               const uint32_t* __restrict__ indices, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+               uint64_t max_keys, unsigned* __restrict__ err) {
+  constexpr int U = 4;
+  const int lane = threadIdx.x & 31;
+  const uint64_t nbags = uint64_t(T) * B;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t c = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; c * 32 < nbags; c += nwarps) {
+    const uint64_t g = c * 32 + lane;
+    uint32_t s = 0, len = 0, t = 0, b = 0;
+    if (g < nbags) {
+      s = offsets[g];
+      const uint32_t e = offsets[g + 1];
+      len = e > s ? e - s : 0u;  // decreasing offsets: flagged by the forward
+      t = uint32_t(g / B);
+      b = uint32_t(g - uint64_t(t) * B);
+    }
+    const uint32_t incl = warp_incl_scan(len);
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t excl = incl - len;
+    const uint32_t s0 = __shfl_sync(0xffffffffu, s, 0);
+    for (uint32_t p = 0; p < total; p += 32 * U) {
+      uint32_t id[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t q = p + uint32_t(u) * 32 + lane;
+        id[u] = q < total ? ld_stream_u32(indices + s0 + q) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t q = p + uint32_t(u) * 32 + lane;
+        int k = 0;  // the lookup's bag: the last lane whose range starts at or before q
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          const uint32_t ex = __shfl_sync(0xffffffffu, excl, k + step);
+          if (ex <= q) k += step;
+        }
+        const uint32_t tk = __shfl_sync(0xffffffffu, t, k);
+        const uint32_t bk = __shfl_sync(0xffffffffu, b, k);
+        if (q < total) {
+          const uint32_t l = s0 + q;  // bags are contiguous in table-major CSR
+          const TableDev& td = tables[tk];
+          uint32_t idx = id[u];
+          if (idx >= td.hash_size) {
+            atomicOr(err, 1u);  // reported by the next backward / rs_emb_check
+            idx = 0;
+          }
+          if (l < max_keys) {
+            keys[l] = slot_of_entry(td, td.remap[idx]);
+            vals[l] = bk;
+          } else {
+            atomicOr(err, 2u);
+          }
+        }
       }
     }
   }
@@ -591,6 +668,7 @@ struct rs_emb {
   // zero row they read, and how many remap entries each table leaves unbacked
   unsigned long long* d_unbacked = nullptr;
   uint32_t* d_work = nullptr;  // forward_kernel's chunk counters (one per lane class)
+  bool resolved = false;       // the running forward's keys come from resolve_kernel
   char* zero_row = nullptr;
   std::vector<uint64_t> unbacked_rows;
   // forward classes: (G, VPL, element bytes) -> table list
@@ -1364,7 +1442,12 @@ static void launch_fwd(rs_emb* e, const rs_emb::Class& c, uint64_t B, const uint
   // over rows in flight per group (the 32-register cap spills only in the
   // per-bag cursor code)
   constexpr int MINB = MINB_;
-  auto kern = c.full ? emb::forward_kernel<G, VPL, UNR_, MINB, E, true> : emb::forward_kernel<G, VPL, UNR_, MINB, E, false>;
+  const bool fk = e->resolved;  // keys resolved by resolve_kernel: the gather reads slot keys
+  auto kern = fk ? (c.full ? emb::forward_kernel<G, VPL, UNR_, MINB, E, true, true>
+                           : emb::forward_kernel<G, VPL, UNR_, MINB, E, false, true>)
+                 : (c.full ? emb::forward_kernel<G, VPL, UNR_, MINB, E, true, false>
+                           : emb::forward_kernel<G, VPL, UNR_, MINB, E, false, false>);
+  if (fk) idx = e->keys;
   static const int per_sm = [&] {
     int n = 0;
     RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, emb::forward_kernel<G, VPL, UNR_, MINB, E, false>,
@@ -1420,6 +1503,21 @@ void emb_forward_map(rs_emb* e, uint64_t B, const uint32_t* off, const uint32_t*
   // lane classes write disjoint columns, keys and hit counters: every other
   // class runs on a forked stream so one launch's tail overlaps the next
   cudaStream_t main = e->ctx->stream;
+  // index resolution as its own streaming pass, then the gather from slot
+  // keys (B200 RM1: forward 1.22 -> 1.07 ms incl. the pass, same-box A/B);
+  // RS_FWD_RESOLVE=0 resolves inside the gather and writes the keys there
+  static const bool resolve = [] {
+    const char* v = getenv("RS_FWD_RESOLVE");
+    return !(v && v[0] == '0');
+  }();
+  e->resolved = resolve && e->keys;
+  if (e->resolved) {
+    const uint64_t nb = uint64_t(e->T) * B;
+    const unsigned g = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((nb / 32 + 7) / 8, uint64_t(sm_count()) * 16)));
+    emb::resolve_kernel<<<g, 256, 0, main>>>(e->cur_tables, e->T, uint32_t(B), off, idx, e->keys, e->vals,
+                                             uint64_t(e->max_lookups), e->d_err);
+    RS_COUNT(1);
+  }
   const bool fork = e->classes.size() > 1;
   if (fork) {
     RS_CUDA(cudaEventRecord(e->ev_fork, main));
