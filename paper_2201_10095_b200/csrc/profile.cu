@@ -300,14 +300,18 @@ hash_hist(const uint64_t* __restrict__ rec_sample, const uint32_t* __restrict__ 
 //       bucket (address >> bbits); per-CTA bucket counts -> matrix[b][cta]
 //   scan of the bucket-major matrix (bucket regions, per-CTA sub-regions)
 //   P2  same expansion; each id's address appended to its (bucket, CTA)
-//       sub-region (shared-memory cursors)
+//       sub-region (shared-memory cursors, only the tile's active buckets)
 //   P3  CTA per (bucket, chunk): histogram of the chunk's addresses in shared
 //       memory (the Zipf head contends only within one SM), flushed to the
 //       global counters once
+// With few buckets (<= 1024, e.g. 8 x 1e6 rows) P1 and the scan are skipped:
+// P2 appends each tile's bucket runs to chunks taken from one pool
+// (part_pool_kernel) and P3 reads each bucket's chunk list, so every id is
+// read once.
 // The expansion maps ids to records with a per-tile shared-memory window of
-// record offsets (one binary search per thread, then a forward walk), so ids
-// are read 8 per thread with vector loads.  Counts are exact integers in any
-// order.
+// record offsets (a thread per record marks the threads whose first id it
+// holds, then each thread walks forward), so ids are read 8 per thread with
+// vector loads.  Counts are exact integers in any order.
 constexpr uint32_t kSkip = 0xFFFFFFFFu;
 constexpr int kPThreads = 256;
 constexpr int kPIds = 8;                         // ids per thread per tile
@@ -370,6 +374,7 @@ constexpr uint32_t kPSmemTables = 512;  // per-table (base, H) held in shared me
 struct PSmem {
   uint32_t woff[kPRecWin + 1];  // record offsets of the window (+ end sentinel)
   uint32_t winfo[kPRecWin];
+  uint32_t rec_of[kPThreads];   // window record holding each thread's first id
   uint32_t r0, nrec;
   uint32_t tbase[kPSmemTables];  // group-local counter base of table index t (< 2^31)
   uint32_t thash[kPSmemTables];  // its hash size
@@ -419,6 +424,17 @@ __device__ __forceinline__ void expand_tile(uint64_t a, uint64_t N, uint64_t R, 
   }
   if (threadIdx.x == 0) sm.woff[nwin] = r0 + nwin < R ? roff[r0 + nwin] : uint32_t(N);
   __syncthreads();
+  // owner record of every thread's first id (thread t's ids start at a + t *
+  // kPIds): a thread per window record writes the slots its ids cover, and the
+  // record holding id tend (the next tile's first record) names itself
+  for (uint32_t k = threadIdx.x; k < nwin; k += blockDim.x) {
+    const uint32_t lo = sm.woff[k], hi = sm.woff[k + 1];
+    const uint32_t s0 = lo > a ? (lo - uint32_t(a) + kPIds - 1) / kPIds : 0u;
+    const uint32_t s1 = hi > a ? min(uint32_t(kPThreads), (min(hi, uint32_t(tend)) - uint32_t(a) + kPIds - 1) / kPIds) : 0u;
+    for (uint32_t t = s0; t < s1; ++t) sm.rec_of[t] = k;
+    if (lo <= tend && (k + 1 == nwin || hi > tend)) sm.nrec = r0 + k;
+  }
+  __syncthreads();
   // ids of this thread: q0 .. q0 + kPIds
   const uint64_t q0 = a + uint64_t(threadIdx.x) * kPIds;
   uint32_t idv[kPIds];
@@ -448,17 +464,10 @@ __device__ __forceinline__ void expand_tile(uint64_t a, uint64_t N, uint64_t R, 
     }
   }
   if (q0 < tend) {
-    // record of q0: largest k with woff[k] <= q0
-    uint32_t lo = 0, hi = nwin;
-    while (lo + 1 < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (sm.woff[mid] <= q0) lo = mid;
-      else hi = mid;
-    }
     // the current record's end, table, hash size and counter base in
     // registers, refreshed only when an id crosses into the next record
     // (one shared-memory walk step per record instead of per id)
-    uint32_t k = lo;
+    uint32_t k = min(sm.rec_of[threadIdx.x], nwin - 1);
     const bool smt = tp.J <= kPSmemTables;
     uint32_t rend = sm.woff[k + 1];  // woff[nwin] is the end sentinel (>= tend)
     uint32_t t = sm.winfo[k];
@@ -490,17 +499,7 @@ __device__ __forceinline__ void expand_tile(uint64_t a, uint64_t N, uint64_t R, 
       }
     }
   }
-  // the next tile starts in the record holding id tend
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t lo = 0, hi = nwin;
-    while (lo + 1 < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (sm.woff[mid] <= tend) lo = mid;
-      else hi = mid;
-    }
-    sm.nrec = r0 + lo;
-  }
+  // the next tile starts in the record holding id tend (named above)
   __syncthreads();
   rcur = sm.nrec;
 }
@@ -516,50 +515,166 @@ __device__ __forceinline__ uint32_t find_record(const uint32_t* __restrict__ rof
   return uint32_t(lo);
 }
 
-// P1 (SCATTER = false): bucket counts per CTA -> mat[b * nct + cta].
-// P2 (SCATTER = true): addresses into out[mat_scanned[b * nct + cta] + rank].
-template <bool RAW, bool SCATTER>
+// P1: bucket counts per CTA -> mat[b * nct + cta].
+template <bool RAW>
 __global__ void __launch_bounds__(kPThreads)
-part_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restrict__ rinfo, uint64_t R, uint64_t N,
-            const uint32_t* __restrict__ ids, const uint64_t* __restrict__ raw, Tables tp, uint32_t nb,
-            uint64_t ids_per_cta, uint32_t* __restrict__ mat, uint16_t* __restrict__ out,
-            unsigned* __restrict__ err, unsigned* __restrict__ bad) {
+part_count_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restrict__ rinfo, uint64_t R, uint64_t N,
+                  const uint32_t* __restrict__ ids, const uint64_t* __restrict__ raw, Tables tp, uint32_t nb,
+                  uint64_t ids_per_cta, uint32_t* __restrict__ mat, unsigned* __restrict__ err,
+                  unsigned* __restrict__ bad) {
   __shared__ PSmem sm;
-  extern __shared__ uint32_t cnt[];  // [nb] counts (P1) or cursors (P2) | P2: tile counts, offsets
+  extern __shared__ uint32_t cnt[];  // [nb]
   const uint32_t nct = gridDim.x;
   load_table_params(tp, sm);
-  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x)
-    cnt[i] = SCATTER ? mat[uint64_t(i) * nct + blockIdx.x] : 0u;
+  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) cnt[i] = 0u;
   const uint64_t a0 = uint64_t(blockIdx.x) * ids_per_cta;
   const uint64_t a1 = min(N, a0 + ids_per_cta);
-  uint32_t rcur = 0;
   if (threadIdx.x == 0 && a0 < a1) sm.nrec = find_record(roff, R, a0);
   __syncthreads();
-  rcur = sm.nrec;
-  if (!SCATTER) {
-    for (uint64_t a = a0; a < a1; a += kPTile)
-      expand_tile<RAW>(a, a1, R, roff, rinfo, ids, raw, tp, sm, rcur, err, bad,
-                       [&](uint32_t addr, int) { atomicAdd(&cnt[addr >> kP3Bits], 1u); });
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) mat[uint64_t(i) * nct + blockIdx.x] = cnt[i];
-    return;
+  uint32_t rcur = sm.nrec;
+  for (uint64_t a = a0; a < a1; a += kPTile)
+    expand_tile<RAW>(a, a1, R, roff, rinfo, ids, raw, tp, sm, rcur, err, bad,
+                     [&](uint32_t addr, int) { atomicAdd(&cnt[addr >> kP3Bits], 1u); });
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) mat[uint64_t(i) * nct + blockIdx.x] = cnt[i];
+}
+
+// P2 of the two-pass partition: each tile's addresses are counting-sorted by
+// bucket in shared memory and written as contiguous per-bucket runs at the
+// CTA's cursors (from the scanned P1 matrix).  Only the buckets the tile
+// touches are scanned and advanced (an active list built by the first id of
+// each bucket), so a tile costs O(its ids), not O(nb): with thousands of
+// buckets (RM1: 6927) the per-bucket loops were the whole kernel.  Shared
+// state is 8 B per bucket (cursor u32, tile count u16, active slot u16), so
+// two CTAs fit per SM at 8192 buckets.
+template <bool RAW>
+__global__ void __launch_bounds__(kPThreads, 2)
+part_scatter_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restrict__ rinfo, uint64_t R, uint64_t N,
+                    const uint32_t* __restrict__ ids, const uint64_t* __restrict__ raw, Tables tp, uint32_t nb,
+                    uint64_t ids_per_cta, const uint32_t* __restrict__ mat, uint16_t* __restrict__ out,
+                    unsigned* __restrict__ err, unsigned* __restrict__ bad) {
+  __shared__ PSmem sm;
+  extern __shared__ uint32_t cur[];                               // [nb] output cursors
+  uint32_t* tcs = cur + nb;                                       // [nb] (tile count u16 | active slot << 16)
+  __shared__ uint32_t act[kPTile];                                // active buckets; after the scan: run offsets
+  __shared__ uint32_t abk[kPTile];                                // their bucket ids
+  __shared__ uint32_t stage[kPTile];
+  __shared__ uint32_t s_nact, s_total;
+  const uint32_t nct = gridDim.x;
+  load_table_params(tp, sm);
+  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
+    cur[i] = mat[uint64_t(i) * nct + blockIdx.x];
+    tcs[i] = 0;
   }
-  // P2: each tile's addresses are counting-sorted by bucket in shared memory
-  // and written as contiguous per-bucket runs (coalesced stores)
-  uint32_t* tcnt = cnt + nb;
-  uint32_t* toff = cnt + 2 * nb;
-  __shared__ uint32_t sa[kPTile], sr[kPTile], stage[kPTile];
-  __shared__ uint32_t s_total;
-  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) tcnt[i] = 0;
+  if (threadIdx.x == 0) s_nact = 0;
+  const uint64_t a0 = uint64_t(blockIdx.x) * ids_per_cta;
+  const uint64_t a1 = min(N, a0 + ids_per_cta);
+  if (threadIdx.x == 0 && a0 < a1) sm.nrec = find_record(roff, R, a0);
+  __syncthreads();
+  uint32_t rcur = sm.nrec;
   for (uint64_t a = a0; a < a1; a += kPTile) {
-    for (int u = 0; u < kPIds; ++u) sa[u * kPThreads + threadIdx.x] = kSkip;
+    uint32_t xa[kPIds], xr[kPIds];
+#pragma unroll
+    for (int u = 0; u < kPIds; ++u) xa[u] = kSkip;
     expand_tile<RAW>(a, a1, R, roff, rinfo, ids, raw, tp, sm, rcur, err, bad, [&](uint32_t addr, int u) {
-      sa[u * kPThreads + threadIdx.x] = addr;
-      sr[u * kPThreads + threadIdx.x] = atomicAdd(&tcnt[addr >> kP3Bits], 1u);
+      const uint32_t b = addr >> kP3Bits;
+      const uint32_t r = atomicAdd(&tcs[b], 1u) & 0xFFFFu;
+      if (r == 0) {  // first id of bucket b in this tile: list it
+        const uint32_t slot = atomicAdd(&s_nact, 1u);
+        abk[slot] = b;
+        atomicOr(&tcs[b], slot << 16);
+      }
+      xa[u] = addr;
+      xr[u] = r;
     });
-    // expand_tile ends with a barrier: tile counts complete
+    // expand_tile ends with a barrier: counts and the active list are complete
+    const uint32_t nact = s_nact;
+    const uint32_t per = (nact + blockDim.x - 1) / blockDim.x;
     uint32_t part = 0;
-    const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
+    for (uint32_t j = 0; j < per; ++j) {
+      const uint32_t i = threadIdx.x * per + j;
+      if (i < nact) part += tcs[abk[i]] & 0xFFFFu;
+    }
+    uint32_t tot;
+    uint32_t run = block_excl_scan<uint32_t, kPThreads>(part, tot);
+    for (uint32_t j = 0; j < per; ++j) {
+      const uint32_t i = threadIdx.x * per + j;
+      if (i < nact) {
+        act[i] = run;
+        run += tcs[abk[i]] & 0xFFFFu;
+      }
+    }
+    if (threadIdx.x == 0) s_total = tot;
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kPIds; ++u)
+      if (xa[u] != kSkip) stage[act[tcs[xa[u] >> kP3Bits] >> 16] + xr[u]] = xa[u];
+    __syncthreads();
+    const uint32_t total = s_total;
+    for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
+      const uint32_t x = stage[i];
+      const uint32_t b = x >> kP3Bits;
+      out[cur[b] + (i - act[tcs[b] >> 16])] = uint16_t(x & ((1u << kP3Bits) - 1));  // bucket-local
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nact; i += blockDim.x) {
+      const uint32_t b = abk[i];
+      cur[b] += tcs[b] & 0xFFFFu;
+      tcs[b] = 0;
+    }
+    if (threadIdx.x == 0) s_nact = 0;
+    __syncthreads();
+  }
+}
+
+// Single-pass partition (P2 without P1): the tile's bucket runs are appended
+// to per-(CTA, bucket) chunks of kPTile addresses taken from one pool with a
+// global cursor, so no bucket needs its size in advance and every id is read
+// once.  Every chunk except a CTA's current one per bucket ends full; those
+// are closed with their fill at the end.  Chunk records (bucket, start, fill)
+// go to ch_*; bchunks[b] counts bucket b's chunks.  The pool holds at most
+// N + nct * nb * kPTile addresses (one partial chunk per CTA and bucket).
+constexpr uint32_t kPPoolMaxBuckets = 1024;  // 6 x 4 B of shared state per bucket
+constexpr uint64_t kPoolExtraBytes = uint64_t(640) << 20;  // scratch reserved for partial chunks
+template <bool RAW>
+__global__ void __launch_bounds__(kPThreads, 4)
+part_pool_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restrict__ rinfo, uint64_t R, uint64_t N,
+                 const uint32_t* __restrict__ ids, const uint64_t* __restrict__ raw, Tables tp, uint32_t nb,
+                 uint64_t ids_per_cta, uint16_t* __restrict__ pool, unsigned* __restrict__ pool_top,
+                 uint32_t* __restrict__ ch_b, uint32_t* __restrict__ ch_s, uint32_t* __restrict__ ch_n,
+                 unsigned* __restrict__ n_ch, unsigned* __restrict__ bchunks, unsigned* __restrict__ err,
+                 unsigned* __restrict__ bad) {
+  __shared__ PSmem sm;
+  // per bucket: {cur: next free pool position of the current chunk, rem: free
+  // entries left in it, off: the tile's run offset, nxt: the chunk this
+  // tile's run overflows into} in one 16-byte word (one shared load per id)
+  extern __shared__ uint4 pbs[];
+  uint32_t* tcnt = reinterpret_cast<uint32_t*>(pbs + nb);  // the tile's run lengths
+  uint32_t* chid = tcnt + nb;                              // current chunk record (kSkip: none)
+  __shared__ uint2 stage[kPTile];                          // (pool position, bucket-local address)
+  __shared__ uint32_t s_total;
+  load_table_params(tp, sm);
+  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
+    pbs[i] = make_uint4(0, 0, 0, 0);
+    chid[i] = kSkip;
+    tcnt[i] = 0;
+  }
+  const uint64_t a0 = uint64_t(blockIdx.x) * ids_per_cta;
+  const uint64_t a1 = min(N, a0 + ids_per_cta);
+  if (threadIdx.x == 0 && a0 < a1) sm.nrec = find_record(roff, R, a0);
+  __syncthreads();
+  uint32_t rcur = sm.nrec;
+  const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
+  for (uint64_t a = a0; a < a1; a += kPTile) {
+    // this thread's ids stay in registers: address and rank within its bucket's run
+    uint32_t xa[kPIds], xr[kPIds];
+#pragma unroll
+    for (int u = 0; u < kPIds; ++u) xa[u] = kSkip;
+    expand_tile<RAW>(a, a1, R, roff, rinfo, ids, raw, tp, sm, rcur, err, bad, [&](uint32_t addr, int u) {
+      xa[u] = addr;
+      xr[u] = atomicAdd(&tcnt[addr >> kP3Bits], 1u);
+    });
+    uint32_t part = 0;
     for (uint32_t j = 0; j < per; ++j) {
       const uint32_t b = threadIdx.x * per + j;
       if (b < nb) part += tcnt[b];
@@ -569,31 +684,126 @@ part_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restrict__ rinf
     for (uint32_t j = 0; j < per; ++j) {
       const uint32_t b = threadIdx.x * per + j;
       if (b < nb) {
-        toff[b] = run;
-        run += tcnt[b];
+        const uint32_t c = tcnt[b];
+        uint4 st = pbs[b];
+        st.z = run;
+        run += c;
+        if (c > st.y) {  // the run overflows the current chunk: open the next one
+          const uint32_t base = atomicAdd(pool_top, uint32_t(kPTile));
+          const uint32_t id = atomicAdd(n_ch, 1u);
+          ch_b[id] = b;
+          ch_s[id] = base;
+          ch_n[id] = kPTile;  // full unless it is still current at the end
+          atomicAdd(&bchunks[b], 1u);
+          st.w = base;
+          chid[b] = id;  // the old chunk (if any) ends exactly full
+        }
+        pbs[b] = st;
       }
     }
     if (threadIdx.x == 0) s_total = tot;
     __syncthreads();
+#pragma unroll
     for (int u = 0; u < kPIds; ++u) {
-      const uint32_t x = sa[u * kPThreads + threadIdx.x];
-      if (x != kSkip) stage[toff[x >> kP3Bits] + sr[u * kPThreads + threadIdx.x]] = x;
+      if (xa[u] != kSkip) {
+        const uint4 st = pbs[xa[u] >> kP3Bits];
+        const uint32_t j = xr[u];
+        stage[st.z + j] = make_uint2(j < st.y ? st.x + j : st.w + (j - st.y), xa[u] & ((1u << kP3Bits) - 1));
+      }
     }
     __syncthreads();
     const uint32_t total = s_total;
     for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
-      const uint32_t x = stage[i];
-      const uint32_t b = x >> kP3Bits;
-      out[cnt[b] + (i - toff[b])] = uint16_t(x & ((1u << kP3Bits) - 1));  // bucket-local (the region is the bucket)
+      const uint2 e = stage[i];
+      pool[e.x] = uint16_t(e.y);
     }
-    __syncthreads();
     for (uint32_t j = 0; j < per; ++j) {
       const uint32_t b = threadIdx.x * per + j;
       if (b < nb) {
-        cnt[b] += tcnt[b];
+        const uint32_t c = tcnt[b];
+        uint4 st = pbs[b];
+        if (c > st.y) {
+          st.x = st.w + (c - st.y);
+          st.y = kPTile - (c - st.y);
+        } else {
+          st.x += c;
+          st.y -= c;
+        }
+        pbs[b] = st;
         tcnt[b] = 0;
       }
     }
+    __syncthreads();
+  }
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x)
+    if (chid[b] != kSkip) ch_n[chid[b]] = kPTile - pbs[b].y;
+}
+
+// Chunk lists per bucket: list[bstart[b] + k] = the k-th chunk of bucket b
+// (any order; counts do not depend on it).  cur[] starts as bstart[].
+__global__ void part_pool_list_kernel(const uint32_t* __restrict__ ch_b, const unsigned* __restrict__ n_ch,
+                                      unsigned* __restrict__ cur, uint32_t* __restrict__ list) {
+  const unsigned n = *n_ch;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    list[atomicAdd(&cur[ch_b[i]], 1u)] = i;
+}
+
+// Work items per bucket: ceil(chunks / per_item).
+__global__ void part_pool_items_kernel(const unsigned* __restrict__ bchunks, uint32_t nb, uint32_t per_item,
+                                       uint32_t* __restrict__ nitem) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < nb) nitem[b] = (bchunks[b] + per_item - 1) / per_item;
+}
+
+// P3 over the pool: CTA per (bucket, run of per_item chunks of its list), warp
+// per chunk; histogram in shared memory, flushed once.
+__global__ void __launch_bounds__(1024)
+part_pool_hist_kernel(const uint16_t* __restrict__ pool, const uint32_t* __restrict__ ch_s,
+                      const uint32_t* __restrict__ ch_n, const uint32_t* __restrict__ list,
+                      const uint32_t* __restrict__ lstart, const uint32_t* __restrict__ ibase, uint32_t nb,
+                      uint32_t per_item, uint32_t* __restrict__ counters, uint64_t ncounters) {
+  extern __shared__ uint32_t h[];
+  constexpr uint32_t span = 1u << kP3Bits;
+  const uint32_t total = ibase[nb];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (uint32_t w = blockIdx.x; w < total; w += gridDim.x) {
+    uint32_t lo = 0, hi = nb;  // largest b with ibase[b] <= w (non-empty buckets only)
+    while (lo + 1 < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (ibase[mid] <= w) lo = mid;
+      else hi = mid;
+    }
+    while (lo + 1 < nb && ibase[lo + 1] <= w) ++lo;
+    const uint32_t b = lo, c = w - ibase[lo];
+    for (uint32_t i = threadIdx.x; i < span; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const uint32_t k0 = lstart[b] + c * per_item, k1 = min(lstart[b + 1], k0 + per_item);
+    for (uint32_t k = k0 + warp; k < k1; k += nw) {
+      const uint32_t ch = list[k];
+      const uint32_t s = ch_s[ch], n = ch_n[ch];  // s is a multiple of kPTile: 16-byte aligned
+      const uint4* p = reinterpret_cast<const uint4*>(pool + s);
+      constexpr int V = kPTile / 8 / 32;  // uint4 per lane per full chunk
+      uint4 x[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const uint32_t e = (v * 32 + lane) * 8;
+        x[v] = e < n ? __ldcs(p + v * 32 + lane) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const uint32_t e = (v * 32 + lane) * 8;
+        const uint32_t wv[4] = {x[v].x, x[v].y, x[v].z, x[v].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (e + 2 * q < n) atomicAdd(&h[wv[q] & 0xFFFFu], 1u);
+          if (e + 2 * q + 1 < n) atomicAdd(&h[wv[q] >> 16], 1u);
+        }
+      }
+    }
+    __syncthreads();
+    const uint64_t cb = uint64_t(b) << kP3Bits;
+    for (uint32_t i = threadIdx.x; i < span; i += blockDim.x)
+      if (h[i] && cb + i < ncounters) atomicAdd(&counters[cb + i], h[i]);
     __syncthreads();
   }
 }
@@ -901,7 +1111,7 @@ __global__ void icdf_kernel(const uint64_t* __restrict__ cum_excl, const uint64_
 template <class K>
 inline void set_smem_attr(K kern, size_t bytes);
 
-// K1 partitioned (P0..P3, see part_kernel).  Returns false (nothing counted,
+// K1 partitioned (P0..P3, see part_count_kernel / part_scatter_kernel / part_pool_kernel).  Returns false (nothing counted,
 // record totals already taken by P0 when count_records) when the records do
 // not tile the id pool; the caller then runs the atomic kernel with
 // count_records = false.
@@ -935,17 +1145,66 @@ inline bool part_histogram(rs_context* ctx, Scratch& scr, bool raw, const uint64
   }
   const uint32_t nct = uint32_t(sms) * 4;
   const uint64_t ids_per_cta = ((N + nct - 1) / nct + kPTile - 1) / kPTile * kPTile;
+  // single pass when the pool (N addresses + one partial chunk per CTA and
+  // bucket) fits the addresses' 4 B/id of scratch plus kPoolExtraBytes
+  const bool no_pool = getenv("RS_PROFILE_NO_POOL") != nullptr;  // A/B and tests of the two-pass path
+  const uint64_t pool_cap = N + uint64_t(nct) * nb * kPTile;
+  if (!no_pool && nb <= kPPoolMaxBuckets && pool_cap * 2 <= 4 * N + kPoolExtraBytes &&
+      pool_cap < (uint64_t(1) << 32)) {
+    const uint64_t max_ch = pool_cap / kPTile + 1;
+    uint16_t* pool = reinterpret_cast<uint16_t*>(scr.take<uint32_t>((pool_cap + 1) / 2));
+    uint32_t* ch_b = scr.take<uint32_t>(max_ch);
+    uint32_t* ch_s = scr.take<uint32_t>(max_ch);
+    uint32_t* ch_n = scr.take<uint32_t>(max_ch);
+    uint32_t* list = scr.take<uint32_t>(max_ch);
+    unsigned* ctr = scr.take<unsigned>(2 + nb);  // pool_top, n_ch, bchunks[nb]
+    uint32_t* lstart = scr.take<uint32_t>(nb + 1);
+    unsigned* lcur = scr.take<unsigned>(nb + 1);
+    uint32_t* nitem = scr.take<uint32_t>(nb + 1);
+    uint32_t* ibase = scr.take<uint32_t>(nb + 1);
+    RS_CUDA(cudaMemsetAsync(ctr, 0, (2 + size_t(nb)) * 4, st));
+    const size_t psm = size_t(nb) * 6 * 4;  // 16 B state + run length + chunk id
+    auto launch = [&](auto kern) {
+      set_smem_attr(kern, psm);
+      kern<<<nct, kPThreads, psm, st>>>(roff, rinfo, R, N, d_ids, d_raw, tp, nb, ids_per_cta, pool, ctr, ch_b, ch_s,
+                                        ch_n, ctr + 1, ctr + 2, d_err, d_bad);
+    };
+    if (raw) launch(part_pool_kernel<true>);
+    else launch(part_pool_kernel<false>);
+    RS_COUNT(1);
+    RS_CUDA(cudaMemcpyAsync(hbad, d_bad, 4, cudaMemcpyDeviceToHost, st));
+    ctx->sync();
+    if (*hbad) {  // a tile held more than 2048 empty records: redo with the atomic kernel
+      RS_CUDA(cudaMemsetAsync(d_err, 0, 4, st));
+      scr.used = mark;
+      return false;
+    }
+    exclusive_scan<uint32_t>(ArrayIn<uint32_t>{ctr + 2}, nb, lstart, lstart + nb, scr, st);
+    RS_CUDA(cudaMemcpyAsync(lcur, lstart, (size_t(nb) + 1) * 4, cudaMemcpyDeviceToDevice, st));
+    part_pool_list_kernel<<<unsigned(sms) * 4, 256, 0, st>>>(ch_b, ctr + 1, lcur, list);
+    constexpr uint32_t kItemChunks = (1u << 20) / kPTile;  // ~1M addresses per P3 work item
+    part_pool_items_kernel<<<(nb + 255) / 256, 256, 0, st>>>(ctr + 2, nb, kItemChunks, nitem);
+    exclusive_scan<uint32_t>(ArrayIn<uint32_t>{nitem}, nb, ibase, ibase + nb, scr, st);
+    const size_t hsm = size_t(1) << kP3Bits << 2;
+    set_smem_attr(part_pool_hist_kernel, hsm);
+    part_pool_hist_kernel<<<unsigned(sms), 1024, hsm, st>>>(pool, ch_s, ch_n, list, lstart, ibase, nb, kItemChunks,
+                                                             d_cnt, ncounters);
+    RS_COUNT(3);
+    RS_LAUNCH_CHECK();
+    scr.used = mark;
+    return true;
+  }
   uint32_t* mat = scr.take<uint32_t>(size_t(nb) * nct);
   uint32_t* mscan = scr.take<uint32_t>(size_t(nb) * nct + 1);
   const size_t psm = size_t(nb) * 4;
   if (raw) {
-    set_smem_attr(part_kernel<true, false>, psm);
-    part_kernel<true, false><<<nct, kPThreads, psm, st>>>(roff, rinfo, R, N, d_ids, d_raw, tp, nb, ids_per_cta, mat,
-                                                          nullptr, d_err, d_bad);
+    set_smem_attr(part_count_kernel<true>, psm);
+    part_count_kernel<true><<<nct, kPThreads, psm, st>>>(roff, rinfo, R, N, d_ids, d_raw, tp, nb, ids_per_cta, mat,
+                                                         d_err, d_bad);
   } else {
-    set_smem_attr(part_kernel<false, false>, psm);
-    part_kernel<false, false><<<nct, kPThreads, psm, st>>>(roff, rinfo, R, N, d_ids, d_raw, tp, nb, ids_per_cta, mat,
-                                                           nullptr, d_err, d_bad);
+    set_smem_attr(part_count_kernel<false>, psm);
+    part_count_kernel<false><<<nct, kPThreads, psm, st>>>(roff, rinfo, R, N, d_ids, d_raw, tp, nb, ids_per_cta, mat,
+                                                         d_err, d_bad);
   }
   RS_COUNT(1);
   RS_CUDA(cudaMemcpyAsync(hbad, d_bad, 4, cudaMemcpyDeviceToHost, st));
@@ -960,15 +1219,15 @@ inline bool part_histogram(rs_context* ctx, Scratch& scr, bool raw, const uint64
   uint32_t* bstart = scr.take<uint32_t>(nb + 1);
   part_bstart_kernel<<<(nb + 256) / 256, 256, 0, st>>>(mscan, nb, nct, mscan + size_t(nb) * nct, bstart);
   uint16_t* addrs = reinterpret_cast<uint16_t*>(scr.take<uint32_t>((N + 1) / 2));
-  const size_t psm2 = 3 * psm;  // cursors | tile counts | tile offsets
+  const size_t psm2 = 2 * psm;  // cursors | tile counts + active slots
   if (raw) {
-    set_smem_attr(part_kernel<true, true>, psm2);
-    part_kernel<true, true><<<nct, kPThreads, psm2, st>>>(roff, rinfo, R, N, d_ids, d_raw, tp, nb, ids_per_cta,
-                                                          mscan, addrs, d_err, d_bad);
+    set_smem_attr(part_scatter_kernel<true>, psm2);
+    part_scatter_kernel<true><<<nct, kPThreads, psm2, st>>>(roff, rinfo, R, N, d_ids, d_raw, tp, nb, ids_per_cta,
+                                                             mscan, addrs, d_err, d_bad);
   } else {
-    set_smem_attr(part_kernel<false, true>, psm2);
-    part_kernel<false, true><<<nct, kPThreads, psm2, st>>>(roff, rinfo, R, N, d_ids, d_raw, tp, nb, ids_per_cta,
-                                                           mscan, addrs, d_err, d_bad);
+    set_smem_attr(part_scatter_kernel<false>, psm2);
+    part_scatter_kernel<false><<<nct, kPThreads, psm2, st>>>(roff, rinfo, R, N, d_ids, d_raw, tp, nb, ids_per_cta,
+                                                              mscan, addrs, d_err, d_bad);
   }
   constexpr uint32_t kChunkAddrs = 1u << 20;
   uint32_t* nchk = scr.take<uint32_t>(nb + 1);
@@ -988,7 +1247,7 @@ inline bool part_histogram(rs_context* ctx, Scratch& scr, bool raw, const uint64
 template <class K>
 inline void set_smem_attr(K kern, size_t bytes) {
   // needed whenever static + dynamic shared memory passes the 48 KB default
-  // (part_kernel's static footprint alone is ~45 KB)
+  // (the partition kernels' static footprint alone is ~40 KB)
   cudaFuncAttributes fa{};
   RS_CUDA(cudaFuncGetAttributes(&fa, kern));
   if (fa.sharedSizeBytes + bytes > 48 * 1024)
@@ -1144,7 +1403,10 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
                 // partitioned histogram: record info, bucket matrix, addresses
                 Scratch::bytes_for(R, 4) * 2 + Scratch::bytes_for(size_t(kPMaxBuckets) * sm_count() * 4, 4) * 2 +
                 Scratch::bytes_for(N, 4) + Scratch::bytes_for(kPMaxBuckets + 1, 4) * 3 +
-                scan_scratch_bytes(size_t(kPMaxBuckets) * sm_count() * 4, 4);
+                scan_scratch_bytes(size_t(kPMaxBuckets) * sm_count() * 4, 4) +
+                // single-pass pool: chunk records and lists (the pool itself fits the addresses' N x 4 B)
+                Scratch::bytes_for(N / 1024 + kPoolExtraBytes / 4096 + 2, 4) * 4 +
+                Scratch::bytes_for(kPPoolMaxBuckets + 2, 4) * 5 + (N >= (uint64_t(1) << 22) ? kPoolExtraBytes : 0);
   Scratch scr = ctx->scratch(need);
   phase("scratch");
 

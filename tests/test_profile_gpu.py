@@ -255,3 +255,33 @@ def test_profile_partitioned_more_tables_than_shared(cuda_ctx, coracle):
     got = sp.profile(tr, 1.0, 3, ctx=cuda_ctx)
     want = coracle.profile(tables, S, rec_sample, rec_table, rec_offset, lens, ids, 1.0, 3)
     assert_stats_equal(got, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("two_pass", [False, True])
+def test_profile_partitioned_pool_and_two_pass(cuda_ctx, coracle, monkeypatch, two_pass):
+    """The partitioned histogram's two address layouts on the same trace:
+    the single-pass chunk pool (few buckets: ids read once, runs appended to
+    per-(CTA, bucket) chunks) and, with RS_PROFILE_NO_POOL, the count +
+    scatter passes.  Zipf-hot rows, empty records, a 0.4 sample rate;
+    bit-exact vs the oracle both ways."""
+    if two_pass:
+        monkeypatch.setenv("RS_PROFILE_NO_POOL", "1")
+    rng = np.random.default_rng(57)
+    J, S = 5, 200_000
+    tables = [TableSpec(j + 11, 100_000, int(h), 16, 4)
+              for j, h in enumerate([3_000_000, 65_536, 1_500_001, 32_767, 900_000])]
+    lens = rng.integers(0, 12, S * J).astype(np.uint32)
+    lens[::11] = 0
+    rec_sample = np.repeat(np.arange(S, dtype=np.uint64), J)
+    rec_table = np.tile(np.array([t.table_id for t in tables], np.uint32), S)
+    rec_offset = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.uint64)
+    N = int(lens.sum())
+    assert N >= (1 << 22)
+    Hs = np.repeat(np.tile(np.array([t.hash_size for t in tables], np.int64), S), lens)
+    ids = (rng.random(N) ** 4 * Hs).astype(np.uint32)
+    tr = Trace(tables, S, rec_sample, rec_table, rec_offset, lens, ids=ids)
+    for rate, seed in [(1.0, 2), (0.4, 8)]:
+        got = sp.profile(tr, rate, seed, ctx=cuda_ctx)
+        want = coracle.profile(tables, S, rec_sample, rec_table, rec_offset, lens, ids, rate, seed)
+        assert_stats_equal(got, want)

@@ -13,13 +13,14 @@ python tools/ncu_summary.py gpurun_out/launches_step.csv > gpurun_out/launches_s
 timeout -s KILL 600 ncu --nvtx --nvtx-include "profile_call/" --metrics $M --clock-control none --csv \
   --log-file gpurun_out/launches_prof.csv python tools/prof_bench.py --ids 1e9 --reps 1 > /dev/null 2>&1
 python tools/ncu_summary.py gpurun_out/launches_prof.csv > gpurun_out/launches_prof_summary.txt 2>&1; head -8 gpurun_out/launches_prof_summary.txt
-for k in "fwd:forward_kernel" "seg:bwd_seg_kernel" "ospass:radix_os_pass" "scat:part_kernel"; do
+mkdir -p /tmp; rm -f /tmp/ncu_*.ncu-rep
+for k in "fwd:forward_kernel" "seg:bwd_seg_kernel" "ospass:radix_os_pass" "scat:part_pool_kernel"; do
   n=${k%%:*}; re=${k#*:}
-  if [ $n = scat ]; then cmd="python tools/prof_bench.py --ids 2e8 --reps 1"; rng=profile_call; skip=1;
+  if [ $n = scat ]; then cmd="python tools/prof_bench.py --ids 2e8 --reps 1"; rng=profile_call; skip=0;
   else cmd="python tools/op_bench.py --iters 2"; rng=bench_step; skip=0; fi
   timeout -s KILL 600 ncu --nvtx --nvtx-include "$rng/" --set full --clock-control none --import-source on \
-    -k regex:"$re" -s $skip -c 1 -o gpurun_out/$n $cmd > /dev/null 2>&1
-  python tools/ncu_read.py gpurun_out/$n.ncu-rep > gpurun_out/ncu_${n}_summary.txt 2>&1
+    -k regex:"$re" -s $skip -c 1 -o /tmp/ncu_$n $cmd > /dev/null 2>&1
+  python tools/ncu_read.py /tmp/ncu_$n.ncu-rep > gpurun_out/ncu_${n}_summary.txt 2>&1
 done
 timeout -s KILL 1200 python bench.py > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log > gpurun_out/bench_line.json
 timeout -s KILL 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1; tail -1 gpurun_out/bench_ref.log
