@@ -914,6 +914,11 @@ def main():
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    if os.environ.get("RS_BENCH_PRIO", "1") != "0":
+        # the step's kernels on a high-priority stream: the operator's staging
+        # kernels (claim, stage-in scatter) run on default-priority streams
+        # beside them and yield SMs to the forward/backward
+        torch.cuda.set_stream(torch.cuda.Stream(device=dev, priority=-100))
     ctx = sp.default_context(local_rank)
     specs = specs_for(args.config)
     B = args.batch

@@ -1046,7 +1046,11 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
       RS_CUDA(cudaEventCreateWithFlags(&e->ev_err, cudaEventDisableTiming));
       RS_CUDA(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
       RS_CUDA(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
-      RS_CUDA(cudaStreamCreateWithFlags(&e->fwd_side, cudaStreamNonBlocking));
+      // the second forward lane runs at the caller stream's priority (the
+      // staging streams keep the default, lowest one)
+      int prio = 0;
+      RS_CUDA(cudaStreamGetPriority(e->ctx->stream, &prio));
+      RS_CUDA(cudaStreamCreateWithPriority(&e->fwd_side, cudaStreamNonBlocking, prio));
     }
     {
       int v = 1;

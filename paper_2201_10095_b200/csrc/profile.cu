@@ -1172,8 +1172,15 @@ inline bool part_histogram(rs_context* ctx, Scratch& scr, bool raw, const uint64
     if (raw) launch(part_pool_kernel<true>);
     else launch(part_pool_kernel<false>);
     RS_COUNT(1);
+    hbad = ctx->pinned_buf<unsigned>(3);  // the context's one pinned buffer: {bad, pool_top, n_ch}
+    unsigned* hctr = hbad + 1;
     RS_CUDA(cudaMemcpyAsync(hbad, d_bad, 4, cudaMemcpyDeviceToHost, st));
+    RS_CUDA(cudaMemcpyAsync(hctr, ctr, 8, cudaMemcpyDeviceToHost, st));
     ctx->sync();
+    // the bounds the pool was sized by (N + one partial chunk per CTA and bucket)
+    if (uint64_t(hctr[0]) > pool_cap || uint64_t(hctr[1]) > max_ch)
+      throw Error(-9, "profile: partition pool overflow (" + std::to_string(hctr[0]) + " > " +
+                          std::to_string(pool_cap) + " addresses or " + std::to_string(hctr[1]) + " chunks)");
     if (*hbad) {  // a tile held more than 2048 empty records: redo with the atomic kernel
       RS_CUDA(cudaMemsetAsync(d_err, 0, 4, st));
       scr.used = mark;

@@ -22,6 +22,8 @@ def main():
     p.add_argument("--batch", type=int, default=16384)
     p.add_argument("--optimizer", default="rowwise_adagrad")
     p.add_argument("--hash-scale", type=float, default=1.0, help="shrink every hash size (rm configs)")
+    p.add_argument("--dma-mb", type=float, default=0.0,
+                   help="background H2D + D2H copy-engine traffic (MB per step each way) during the timed steps")
     p.add_argument("--slow-frac", type=float, default=0.0,
                    help="fraction of each table's rows (highest ids) placed in the host tier")
     a = p.parse_args()
@@ -54,6 +56,18 @@ def main():
         op.forward(off, idx, B, out=pooled)
         op.backward(off, idx, pooled, B, 0.01)
     torch.cuda.synchronize()
+    if a.dma_mb > 0:  # copy-engine traffic beside the kernels (staging's PCIe DMA, without the staging)
+        nb = int(a.dma_mb * (1 << 20))
+        hin = torch.empty(nb, dtype=torch.uint8).pin_memory()
+        hout = torch.empty(nb, dtype=torch.uint8).pin_memory()
+        din = torch.empty(nb, dtype=torch.uint8, device=dev)
+        dout = torch.empty(nb, dtype=torch.uint8, device=dev)
+        s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        for _ in range(a.iters + 2):
+            with torch.cuda.stream(s_in):
+                din.copy_(hin, non_blocking=True)
+            with torch.cuda.stream(s_out):
+                hout.copy_(dout, non_blocking=True)
     for i in range(a.iters):
         off, idx, n = batches[i % 2]
         flush.zero_()
