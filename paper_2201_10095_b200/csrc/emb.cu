@@ -713,6 +713,7 @@ struct rs_emb {
   unsigned* h_cnt = nullptr;
   cudaEvent_t ev_claim[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_evict[4] = {nullptr, nullptr, nullptr, nullptr};  // ring: one per eviction in flight
+  std::vector<cudaEvent_t> ev_out_chunk;  // stage-out: one per D2H chunk (grown on demand, out worker only)
   uint64_t n_evicts = 0;
   cudaEvent_t last_claim = nullptr;  // the most recent claim (side stream)
   std::unique_ptr<rs::TaskQueue> worker;      // stage-in tasks (host tier -> slots)
@@ -817,6 +818,7 @@ struct rs_emb {
     for (cudaEvent_t ev : {ev_claim[0], ev_claim[1], ev_claim[2], ev_claim[3], ev_evict[0], ev_evict[1],
                            ev_evict[2], ev_evict[3]})
       if (ev) cudaEventDestroy(ev);
+    for (cudaEvent_t ev : ev_out_chunk) cudaEventDestroy(ev);
     if (d_tables) cudaFree(d_tables);
     if (fast_pool) cudaFree(fast_pool);
     if (host_pool) {
@@ -1271,17 +1273,34 @@ static void stage_out_task(rs_emb* e, cudaEvent_t evicted) {
   const uint64_t stride = e->rmax;
   RS_CUDA(cudaMemcpyAsync(e->h_wtab, e->wb_tab, n * 4, cudaMemcpyDeviceToHost, s));
   RS_CUDA(cudaMemcpyAsync(e->h_wrow, e->wb_row, n * 4, cudaMemcpyDeviceToHost, s));
-  RS_CUDA(cudaMemcpyAsync(e->h_bout, e->d_bout, n * stride, cudaMemcpyDeviceToHost, s));
-  RS_CUDA(cudaStreamSynchronize(s));
+  // rows come back in chunks: the CPU scatters chunk c while chunk c+1 is on
+  // the bus (the stage-out path was D2H then scatter, ~one step end to end)
+  constexpr uint64_t kChunkRows = 16384;
+  const uint64_t nch = (n + kChunkRows - 1) / kChunkRows;
+  while (e->ev_out_chunk.size() < nch) {
+    cudaEvent_t ev;
+    RS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    e->ev_out_chunk.push_back(ev);
+  }
+  for (uint64_t c = 0; c < nch; ++c) {
+    const uint64_t c0 = c * kChunkRows, c1 = std::min(n, c0 + kChunkRows);
+    RS_CUDA(cudaMemcpyAsync(e->h_bout + c0 * stride, e->d_bout + c0 * stride, (c1 - c0) * stride,
+                            cudaMemcpyDeviceToHost, s));
+    RS_CUDA(cudaEventRecord(e->ev_out_chunk[c], s));
+  }
   const double t2 = dbg ? now_us() : 0;
-  e->out_pool->parallel_for(n, [&](size_t b, size_t en) {
-    for (size_t k = b; k < en; ++k) {
-      const uint32_t t = e->h_wtab[k];
-      memcpy(host_slow_row(e, t, e->h_wrow[k]), e->h_bout + k * stride, e->h_tables[t].rbytes);
-    }
-  });
+  for (uint64_t c = 0; c < nch; ++c) {
+    const uint64_t c0 = c * kChunkRows, c1 = std::min(n, c0 + kChunkRows);
+    RS_CUDA(cudaEventSynchronize(e->ev_out_chunk[c]));
+    e->out_pool->parallel_for(c1 - c0, [&](size_t b, size_t en) {
+      for (size_t k = c0 + b; k < c0 + en; ++k) {
+        const uint32_t t = e->h_wtab[k];
+        memcpy(host_slow_row(e, t, e->h_wrow[k]), e->h_bout + k * stride, e->h_tables[t].rbytes);
+      }
+    });
+  }
   if (dbg)
-    fprintf(stderr, "stage_out n=%llu t=%.0f wait_evict=%.0fus d2h=%.0fus scatter=%.0fus\n", (unsigned long long)n,
+    fprintf(stderr, "stage_out n=%llu t=%.0f wait_evict=%.0fus lists+enqueue=%.0fus d2h+scatter=%.0fus\n", (unsigned long long)n,
             t0, t1 - t0, t2 - t1, now_us() - t2);
 }
 
