@@ -64,6 +64,10 @@ struct TableDev {
   uint32_t* slot_of;
   char* staging;
   uint64_t stage_stride;  // bytes per staging slot
+  // bit r: row r is a backed slow row (what the claim stages).  ceil(H/32)
+  // words, L2-resident for a whole table set (RM1: 29 MB), so the claim
+  // reads a row's remap entry only for the ~1% of lookups that are slow
+  const uint32_t* sbits;
 };
 
 __host__ __device__ inline int lanes_for(uint32_t dim) {
@@ -620,6 +624,19 @@ __global__ void read_rows_kernel(TableDev td, const uint32_t* __restrict__ rows,
 // Every remap entry must land inside its tier: fast entries below hbm_rows,
 // slow ones below slow_rows unless unbacked rows are allowed (then anything
 // past slow_rows is an unbacked row and counted).
+// Slow-row bitmap of one table (TableDev::sbits), a warp ballot per 32 rows.
+__global__ void slow_bits_kernel(const int32_t* __restrict__ remap, uint64_t H, uint64_t slow_rows,
+                                 uint32_t* __restrict__ bits) {
+  const uint64_t nw = (H + 31) / 32;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < nw; w += nwarps) {
+    const uint64_t r = w * 32 + (threadIdx.x & 31);
+    const int32_t e = r < H ? remap[r] : 0;
+    const uint32_t b = __ballot_sync(0xffffffffu, e < 0 && slow_off(e) < slow_rows);
+    if ((threadIdx.x & 31) == 0) bits[w] = b;
+  }
+}
+
 __global__ void check_remap_kernel(const int32_t* __restrict__ remap, uint64_t H, uint64_t hbm_rows,
                                    uint64_t slow_rows, int allow_unbacked, unsigned* __restrict__ err,
                                    unsigned long long* __restrict__ n_unbacked) {
@@ -663,6 +680,7 @@ struct rs_emb {
   size_t host_map_bytes = 0;
   size_t host_bytes = 0;
   int32_t* remap_pool = nullptr;
+  uint32_t* sbits_pool = nullptr;  // TableDev::sbits of every table
   size_t remap_bytes = 0;
   // unbacked rows (omit_unaccessed remaps): per-table lookup counters, the
   // zero row they read, and how many remap entries each table leaves unbacked
@@ -830,6 +848,7 @@ struct rs_emb {
       }
     }
     if (remap_pool) cudaFree(remap_pool);
+    if (sbits_pool) cudaFree(sbits_pool);
     for (auto& c : classes)
       if (c.d_list) cudaFree(c.d_list);
     if (d_tiles) cudaFree(d_tiles);
@@ -915,8 +934,8 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
   e->eps = eps;
   try {
     cudaStream_t st = ctx->stream;
-    size_t fb = 0, hb = 0, rb = 0;
-    std::vector<size_t> foff(T), hoff(T), roff(T), mfoff(T), mhoff(T);
+    size_t fb = 0, hb = 0, rb = 0, sb = 0;
+    std::vector<size_t> foff(T), hoff(T), roff(T), soff(T), mfoff(T), mhoff(T);
     std::vector<uint32_t> eb(T);
     for (uint32_t t = 0; t < T; ++t) {
       const rs_emb_table& x = tabs[t];
@@ -937,6 +956,8 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
       hb += align256(x.slow_rows * x.dim * eb[t]);
       roff[t] = rb;
       rb += align256(x.hash_size * 4);
+      soff[t] = sb;
+      sb += align256((x.hash_size + 31) / 32 * 4);
       e->total_dim += x.dim;
       e->dmax = std::max(e->dmax, x.dim);
       e->rmax = std::max(e->rmax, (x.dim * eb[t] + 15) / 16 * 16);
@@ -959,6 +980,7 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
     alloc_host_tier(e);
     RS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->host_pool_dev), e->host_pool, 0));
     RS_CUDA(cudaMalloc(&e->remap_pool, std::max<size_t>(rb, 256)));
+    RS_CUDA(cudaMalloc(&e->sbits_pool, std::max<size_t>(sb, 256)));
     RS_CUDA(cudaMalloc(&e->d_err, 16));
     RS_CUDA(cudaMalloc(&e->d_unbacked, 8 * size_t(T)));
     RS_CUDA(cudaMalloc(&e->d_work, 256));
@@ -976,6 +998,13 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
                               x.remap_location == RS_MEM_DEVICE ? cudaMemcpyDeviceToDevice
                                                                 : cudaMemcpyHostToDevice,
                               st));
+      d.sbits = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(e->sbits_pool) + soff[t]);
+      {
+        const unsigned gb = unsigned(std::max<uint64_t>(
+            1, std::min<uint64_t>(((x.hash_size + 31) / 32 + 7) / 8, uint64_t(sm_count()) * 8)));
+        slow_bits_kernel<<<gb, 256, 0, st>>>(d.remap, x.hash_size, x.slow_rows, const_cast<uint32_t*>(d.sbits));
+        RS_COUNT(1);
+      }
       d.fast = e->fast_pool + foff[t];
       d.slow = e->host_pool_dev + hoff[t];
       d.zero = e->zero_row;

@@ -72,10 +72,10 @@ uvm_claim_kernel(const TableDev* __restrict__ tables, const uint32_t* __restrict
     const uint32_t s1 = offsets[o + nb];
     const TableDev& td = tables[t];
     for (uint32_t l = s0 + lane; l < s1; l += 32) {
-      const int32_t e = td.remap[indices[l]];
-      if (e >= 0) continue;
+      const uint32_t r = indices[l];
+      if (!((td.sbits[r >> 5] >> (r & 31)) & 1u)) continue;  // fast or unbacked: nothing to stage
+      const int32_t e = td.remap[r];
       const uint64_t s = slow_off(e);
-      if (s >= td.slow_rows) continue;  // unbacked: nothing to stage
       uint32_t* p = td.slot_of + s;
       const uint32_t old = atomicCAS(p, kNoSlot, kClaim);
       if (old == kNoSlot) {
