@@ -422,13 +422,19 @@ __device__ __forceinline__ void expand_tile(uint64_t a, uint64_t N, uint64_t R, 
       break;
     }
   }
-  if (threadIdx.x == 0) sm.woff[nwin] = r0 + nwin < R ? roff[r0 + nwin] : uint32_t(N);
-  __syncthreads();
   // owner record of every thread's first id (thread t's ids start at a + t *
   // kPIds): a thread per window record writes the slots its ids cover, and the
-  // record holding id tend (the next tile's first record) names itself
+  // record holding id tend (the next tile's first record) names itself; the
+  // last record's thread also writes the end sentinel woff[nwin]
   for (uint32_t k = threadIdx.x; k < nwin; k += blockDim.x) {
-    const uint32_t lo = sm.woff[k], hi = sm.woff[k + 1];
+    const uint32_t lo = sm.woff[k];
+    uint32_t hi;
+    if (k + 1 < nwin) {
+      hi = sm.woff[k + 1];
+    } else {
+      hi = r0 + nwin < R ? roff[r0 + nwin] : uint32_t(N);
+      sm.woff[nwin] = hi;
+    }
     const uint32_t s0 = lo > a ? (lo - uint32_t(a) + kPIds - 1) / kPIds : 0u;
     const uint32_t s1 = hi > a ? min(uint32_t(kPThreads), (min(hi, uint32_t(tend)) - uint32_t(a) + kPIds - 1) / kPIds) : 0u;
     for (uint32_t t = s0; t < s1; ++t) sm.rec_of[t] = k;
@@ -623,7 +629,8 @@ part_scatter_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restric
       tcs[b] = 0;
     }
     if (threadIdx.x == 0) s_nact = 0;
-    __syncthreads();
+    // no barrier: the next tile writes only its record window before its
+    // window barrier (tcs, abk and s_nact after it; nact is in registers)
   }
 }
 
@@ -733,8 +740,10 @@ part_pool_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restrict__
         tcnt[b] = 0;
       }
     }
-    __syncthreads();
+    // no barrier: the next tile touches pbs / tcnt only after its window
+    // barrier, and writes nothing else this loop reads before it
   }
+  __syncthreads();
   for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x)
     if (chid[b] != kSkip) ch_n[chid[b]] = kPTile - pbs[b].y;
 }
