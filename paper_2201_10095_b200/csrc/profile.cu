@@ -316,7 +316,6 @@ constexpr uint32_t kSkip = 0xFFFFFFFFu;
 constexpr int kPThreads = 256;
 constexpr int kPIds = 8;                         // ids per thread per tile
 constexpr int kPTile = kPThreads * kPIds;        // 2048 ids
-constexpr int kPRecWin = kPTile + 1;             // record window (len-1 records)
 constexpr uint32_t kPMaxBuckets = 8192;  // P2: cursors + tile counts + offsets in shared memory (3 x 4 B per bucket)
 constexpr int kP3Bits = 15;                      // 32768 counters per bucket (P3 shared histogram)
 
@@ -371,18 +370,24 @@ rec_info_kernel(const uint64_t* __restrict__ rec_sample, const uint32_t* __restr
 
 constexpr uint32_t kPSmemTables = 512;  // per-table (base, H) held in shared memory up to this J
 
-struct PSmem {
-  uint32_t woff[kPRecWin + 1];  // record offsets of the window (+ end sentinel)
-  uint32_t winfo[kPRecWin];
+template <int IDS>
+struct alignas(16) PSmemT {
+  static constexpr int kTile = kPThreads * IDS;
+  static constexpr int kWin = kTile + 1;  // record window (len-1 records)
+  uint32_t woff[kWin + 1];  // record offsets of the window (+ end sentinel)
+  uint32_t winfo[kWin];
   uint32_t rec_of[kPThreads];   // window record holding each thread's first id
   uint32_t r0, nrec;
   uint32_t tbase[kPSmemTables];  // group-local counter base of table index t (< 2^31)
   uint32_t thash[kPSmemTables];  // its hash size
 };
+using PSmem = PSmemT<kPIds>;
+
 
 // Loads the per-table (base, H) of the launch's tables into shared memory
 // (the expansion otherwise reads both from global memory for every id).
-__device__ __forceinline__ void load_table_params(const Tables& tp, PSmem& sm) {
+template <class SM>
+__device__ __forceinline__ void load_table_params(const Tables& tp, SM& sm) {
   if (tp.J > kPSmemTables) return;
   for (uint32_t t = threadIdx.x; t < tp.J; t += blockDim.x) {
     sm.tbase[t] = uint32_t(tp.base[t]);
@@ -393,37 +398,37 @@ __device__ __forceinline__ void load_table_params(const Tables& tp, PSmem& sm) {
 // Expands tile [a, a + kPTile) of the id pool: fn(addr) for every selected id
 // of an in-group table.  *rcur: first record of the tile (advanced to the
 // first record of the next tile).
-template <bool RAW, class Fn>
+template <bool RAW, int IDS = kPIds, class Fn>
 __device__ __forceinline__ void expand_tile(uint64_t a, uint64_t N, uint64_t R, const uint32_t* __restrict__ roff,
                                             const uint32_t* __restrict__ rinfo, const uint32_t* __restrict__ ids,
-                                            const uint64_t* __restrict__ raw, const Tables& tp, PSmem& sm,
+                                            const uint64_t* __restrict__ raw, const Tables& tp, PSmemT<IDS>& sm,
                                             uint32_t& rcur, unsigned* __restrict__ err, unsigned* __restrict__ bad,
                                             Fn&& fn) {
-  const uint64_t tend = min(N, a + kPTile);
+  const uint64_t tend = min(N, a + PSmemT<IDS>::kTile);
   // record window: records from rcur covering [a, tend), loaded 256 at a time
   const uint32_t r0 = rcur;
   uint32_t nwin = 0;
   while (true) {
     const uint32_t i = nwin + threadIdx.x;
-    const bool in = i < uint32_t(kPRecWin) && r0 + i < R;
+    const bool in = i < uint32_t(PSmemT<IDS>::kWin) && r0 + i < R;
     uint32_t o = 0;
     if (in) {
       o = roff[r0 + i];
       sm.woff[i] = o;
       sm.winfo[i] = rinfo[r0 + i];
     }
-    const uint32_t got = uint32_t(min(uint64_t(blockDim.x), min(uint64_t(kPRecWin) - nwin, R - r0 - nwin)));
+    const uint32_t got = uint32_t(min(uint64_t(blockDim.x), min(uint64_t(PSmemT<IDS>::kWin) - nwin, R - r0 - nwin)));
     // done once a loaded record starts at or beyond the tile end
     const int covered = __syncthreads_or(in && o >= tend);
     nwin += got;
     if (covered || r0 + nwin >= R) break;
-    if (nwin >= uint32_t(kPRecWin)) {  // > 2048 empty records in one tile: caller falls back
+    if (nwin >= uint32_t(PSmemT<IDS>::kWin)) {  // > 2048 empty records in one tile: caller falls back
       if (threadIdx.x == 0) atomicOr(bad, 2u);
       break;
     }
   }
   // owner record of every thread's first id (thread t's ids start at a + t *
-  // kPIds): a thread per window record writes the slots its ids cover, and the
+  // IDS): a thread per window record writes the slots its ids cover, and the
   // record holding id tend (the next tile's first record) names itself; the
   // last record's thread also writes the end sentinel woff[nwin]
   for (uint32_t k = threadIdx.x; k < nwin; k += blockDim.x) {
@@ -435,24 +440,24 @@ __device__ __forceinline__ void expand_tile(uint64_t a, uint64_t N, uint64_t R, 
       hi = r0 + nwin < R ? roff[r0 + nwin] : uint32_t(N);
       sm.woff[nwin] = hi;
     }
-    const uint32_t s0 = lo > a ? (lo - uint32_t(a) + kPIds - 1) / kPIds : 0u;
-    const uint32_t s1 = hi > a ? min(uint32_t(kPThreads), (min(hi, uint32_t(tend)) - uint32_t(a) + kPIds - 1) / kPIds) : 0u;
+    const uint32_t s0 = lo > a ? (lo - uint32_t(a) + IDS - 1) / IDS : 0u;
+    const uint32_t s1 = hi > a ? min(uint32_t(kPThreads), (min(hi, uint32_t(tend)) - uint32_t(a) + IDS - 1) / IDS) : 0u;
     for (uint32_t t = s0; t < s1; ++t) sm.rec_of[t] = k;
     if (lo <= tend && (k + 1 == nwin || hi > tend)) sm.nrec = r0 + k;
   }
   __syncthreads();
-  // ids of this thread: q0 .. q0 + kPIds
-  const uint64_t q0 = a + uint64_t(threadIdx.x) * kPIds;
-  uint32_t idv[kPIds];
-  uint64_t rawv[RAW ? kPIds : 1];
-  if (q0 + kPIds <= tend) {
+  // ids of this thread: q0 .. q0 + IDS
+  const uint64_t q0 = a + uint64_t(threadIdx.x) * IDS;
+  uint32_t idv[IDS];
+  uint64_t rawv[RAW ? IDS : 1];
+  if (q0 + IDS <= tend) {
     if (RAW) {
 #pragma unroll
-      for (int u = 0; u < kPIds; ++u) rawv[u] = ld_stream_u64(raw + q0 + u);
+      for (int u = 0; u < IDS; ++u) rawv[u] = ld_stream_u64(raw + q0 + u);
     } else {
       const uint4* p = reinterpret_cast<const uint4*>(ids + q0);
 #pragma unroll
-      for (int v = 0; v < kPIds / 4; ++v) {
+      for (int v = 0; v < IDS / 4; ++v) {
         const uint4 x = __ldcs(p + v);
         idv[4 * v] = x.x;
         idv[4 * v + 1] = x.y;
@@ -462,7 +467,7 @@ __device__ __forceinline__ void expand_tile(uint64_t a, uint64_t N, uint64_t R, 
     }
   } else {
 #pragma unroll
-    for (int u = 0; u < kPIds; ++u) {
+    for (int u = 0; u < IDS; ++u) {
       if (q0 + u < tend) {
         if (RAW) rawv[u] = raw[q0 + u];
         else idv[u] = ids[q0 + u];
@@ -483,7 +488,7 @@ __device__ __forceinline__ void expand_tile(uint64_t a, uint64_t N, uint64_t R, 
       tb = smt ? sm.tbase[t] : tp.base[t];
     }
 #pragma unroll
-    for (int u = 0; u < kPIds; ++u) {
+    for (int u = 0; u < IDS; ++u) {
       const uint64_t q = q0 + u;
       if (q < tend) {
         if (q >= rend) {
@@ -643,22 +648,38 @@ part_scatter_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restric
 // N + nct * nb * kPTile addresses (one partial chunk per CTA and bucket).
 constexpr uint32_t kPPoolMaxBuckets = 1024;  // 6 x 4 B of shared state per bucket
 constexpr uint64_t kPoolExtraBytes = uint64_t(640) << 20;  // scratch reserved for partial chunks
+#ifndef RS_POOL_IDS
+#define RS_POOL_IDS 16
+#endif
+#ifndef RS_POOL_CTAS
+#define RS_POOL_CTAS 3
+#endif
+constexpr int kPoolIds = RS_POOL_IDS;                         // ids per thread per tile
+constexpr uint32_t kPoolChunk = kPThreads * kPoolIds;         // 4096: tile = chunk
+constexpr int kPoolCtasPerSm = RS_POOL_CTAS;
 template <bool RAW>
-__global__ void __launch_bounds__(kPThreads, 4)
+__global__ void __launch_bounds__(kPThreads, kPoolCtasPerSm)
 part_pool_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restrict__ rinfo, uint64_t R, uint64_t N,
                  const uint32_t* __restrict__ ids, const uint64_t* __restrict__ raw, Tables tp, uint32_t nb,
                  uint64_t ids_per_cta, uint16_t* __restrict__ pool, unsigned* __restrict__ pool_top,
                  uint32_t* __restrict__ ch_b, uint32_t* __restrict__ ch_s, uint32_t* __restrict__ ch_n,
                  unsigned* __restrict__ n_ch, unsigned* __restrict__ bchunks, unsigned* __restrict__ err,
                  unsigned* __restrict__ bad) {
-  __shared__ PSmem sm;
+  // 4096-id tiles: half the per-tile barriers, window and scan work per id of
+  // the 2048-id tiles (the pass is instruction- and barrier-bound)
+  using SM = PSmemT<kPoolIds>;
+  constexpr uint32_t kTile = SM::kTile;
+  __shared__ SM sm;
   // per bucket: {cur: next free pool position of the current chunk, rem: free
   // entries left in it, off: the tile's run offset, nxt: the chunk this
   // tile's run overflows into} in one 16-byte word (one shared load per id)
   extern __shared__ uint4 pbs[];
   uint32_t* tcnt = reinterpret_cast<uint32_t*>(pbs + nb);  // the tile's run lengths
   uint32_t* chid = tcnt + nb;                              // current chunk record (kSkip: none)
-  __shared__ uint2 stage[kPTile];                          // (pool position, bucket-local address)
+  // (pool position, bucket-local address) of the tile's ids in bucket order:
+  // aliases the record window, dead once the expansion has ended
+  static_assert(sizeof(uint32_t) * (SM::kWin + 1 + SM::kWin) >= sizeof(uint2) * kTile, "stage alias");
+  uint2* stage = reinterpret_cast<uint2*>(sm.woff);
   __shared__ uint32_t s_total;
   load_table_params(tp, sm);
   for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
@@ -672,12 +693,12 @@ part_pool_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restrict__
   __syncthreads();
   uint32_t rcur = sm.nrec;
   const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
-  for (uint64_t a = a0; a < a1; a += kPTile) {
+  for (uint64_t a = a0; a < a1; a += kTile) {
     // this thread's ids stay in registers: address and rank within its bucket's run
-    uint32_t xa[kPIds], xr[kPIds];
+    uint32_t xa[kPoolIds], xr[kPoolIds];
 #pragma unroll
-    for (int u = 0; u < kPIds; ++u) xa[u] = kSkip;
-    expand_tile<RAW>(a, a1, R, roff, rinfo, ids, raw, tp, sm, rcur, err, bad, [&](uint32_t addr, int u) {
+    for (int u = 0; u < kPoolIds; ++u) xa[u] = kSkip;
+    expand_tile<RAW, kPoolIds>(a, a1, R, roff, rinfo, ids, raw, tp, sm, rcur, err, bad, [&](uint32_t addr, int u) {
       xa[u] = addr;
       xr[u] = atomicAdd(&tcnt[addr >> kP3Bits], 1u);
     });
@@ -696,11 +717,11 @@ part_pool_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restrict__
         st.z = run;
         run += c;
         if (c > st.y) {  // the run overflows the current chunk: open the next one
-          const uint32_t base = atomicAdd(pool_top, uint32_t(kPTile));
+          const uint32_t base = atomicAdd(pool_top, kTile);
           const uint32_t id = atomicAdd(n_ch, 1u);
           ch_b[id] = b;
           ch_s[id] = base;
-          ch_n[id] = kPTile;  // full unless it is still current at the end
+          ch_n[id] = kTile;  // full unless it is still current at the end
           atomicAdd(&bchunks[b], 1u);
           st.w = base;
           chid[b] = id;  // the old chunk (if any) ends exactly full
@@ -711,7 +732,7 @@ part_pool_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restrict__
     if (threadIdx.x == 0) s_total = tot;
     __syncthreads();
 #pragma unroll
-    for (int u = 0; u < kPIds; ++u) {
+    for (int u = 0; u < kPoolIds; ++u) {
       if (xa[u] != kSkip) {
         const uint4 st = pbs[xa[u] >> kP3Bits];
         const uint32_t j = xr[u];
@@ -731,7 +752,7 @@ part_pool_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restrict__
         uint4 st = pbs[b];
         if (c > st.y) {
           st.x = st.w + (c - st.y);
-          st.y = kPTile - (c - st.y);
+          st.y = kTile - (c - st.y);
         } else {
           st.x += c;
           st.y -= c;
@@ -740,12 +761,10 @@ part_pool_kernel(const uint32_t* __restrict__ roff, const uint32_t* __restrict__
         tcnt[b] = 0;
       }
     }
-    // no barrier: the next tile touches pbs / tcnt only after its window
-    // barrier, and writes nothing else this loop reads before it
+    __syncthreads();  // the next tile's record window overwrites the stage
   }
-  __syncthreads();
   for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x)
-    if (chid[b] != kSkip) ch_n[chid[b]] = kPTile - pbs[b].y;
+    if (chid[b] != kSkip) ch_n[chid[b]] = kTile - pbs[b].y;
 }
 
 // Chunk lists per bucket: list[bstart[b] + k] = the k-th chunk of bucket b
@@ -789,23 +808,26 @@ part_pool_hist_kernel(const uint16_t* __restrict__ pool, const uint32_t* __restr
     const uint32_t k0 = lstart[b] + c * per_item, k1 = min(lstart[b + 1], k0 + per_item);
     for (uint32_t k = k0 + warp; k < k1; k += nw) {
       const uint32_t ch = list[k];
-      const uint32_t s = ch_s[ch], n = ch_n[ch];  // s is a multiple of kPTile: 16-byte aligned
+      const uint32_t s = ch_s[ch], n = ch_n[ch];  // s is a multiple of kPoolChunk: 16-byte aligned
       const uint4* p = reinterpret_cast<const uint4*>(pool + s);
-      constexpr int V = kPTile / 8 / 32;  // uint4 per lane per full chunk
-      uint4 x[V];
+      constexpr int V = 8;  // uint4 (8 addresses each) per lane in flight
+#pragma unroll 1
+      for (uint32_t h0 = 0; h0 < n; h0 += V * 32 * 8) {
+        uint4 x[V];
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const uint32_t e = (v * 32 + lane) * 8;
-        x[v] = e < n ? __ldcs(p + v * 32 + lane) : make_uint4(0, 0, 0, 0);
-      }
+        for (int v = 0; v < V; ++v) {
+          const uint32_t e = h0 + (v * 32 + lane) * 8;
+          x[v] = e < n ? __ldcs(p + (h0 >> 3) + v * 32 + lane) : make_uint4(0, 0, 0, 0);
+        }
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const uint32_t e = (v * 32 + lane) * 8;
-        const uint32_t wv[4] = {x[v].x, x[v].y, x[v].z, x[v].w};
+        for (int v = 0; v < V; ++v) {
+          const uint32_t e = h0 + (v * 32 + lane) * 8;
+          const uint32_t wv[4] = {x[v].x, x[v].y, x[v].z, x[v].w};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (e + 2 * q < n) atomicAdd(&h[wv[q] & 0xFFFFu], 1u);
-          if (e + 2 * q + 1 < n) atomicAdd(&h[wv[q] >> 16], 1u);
+          for (int q = 0; q < 4; ++q) {
+            if (e + 2 * q < n) atomicAdd(&h[wv[q] & 0xFFFFu], 1u);
+            if (e + 2 * q + 1 < n) atomicAdd(&h[wv[q] >> 16], 1u);
+          }
         }
       }
     }
@@ -1157,10 +1179,12 @@ inline bool part_histogram(rs_context* ctx, Scratch& scr, bool raw, const uint64
   // single pass when the pool (N addresses + one partial chunk per CTA and
   // bucket) fits the addresses' 4 B/id of scratch plus kPoolExtraBytes
   const bool no_pool = getenv("RS_PROFILE_NO_POOL") != nullptr;  // A/B and tests of the two-pass path
-  const uint64_t pool_cap = N + uint64_t(nct) * nb * kPTile;
+  const uint32_t pct = uint32_t(sms) * kPoolCtasPerSm;
+  const uint64_t pool_cap = N + uint64_t(pct) * nb * kPoolChunk;
   if (!no_pool && nb <= kPPoolMaxBuckets && pool_cap * 2 <= 4 * N + kPoolExtraBytes &&
       pool_cap < (uint64_t(1) << 32)) {
-    const uint64_t max_ch = pool_cap / kPTile + 1;
+    const uint64_t max_ch = pool_cap / kPoolChunk + 1;
+    const uint64_t pool_ids_per_cta = ((N + pct - 1) / pct + kPoolChunk - 1) / kPoolChunk * kPoolChunk;
     uint16_t* pool = reinterpret_cast<uint16_t*>(scr.take<uint32_t>((pool_cap + 1) / 2));
     uint32_t* ch_b = scr.take<uint32_t>(max_ch);
     uint32_t* ch_s = scr.take<uint32_t>(max_ch);
@@ -1175,8 +1199,8 @@ inline bool part_histogram(rs_context* ctx, Scratch& scr, bool raw, const uint64
     const size_t psm = size_t(nb) * 6 * 4;  // 16 B state + run length + chunk id
     auto launch = [&](auto kern) {
       set_smem_attr(kern, psm);
-      kern<<<nct, kPThreads, psm, st>>>(roff, rinfo, R, N, d_ids, d_raw, tp, nb, ids_per_cta, pool, ctr, ch_b, ch_s,
-                                        ch_n, ctr + 1, ctr + 2, d_err, d_bad);
+      kern<<<pct, kPThreads, psm, st>>>(roff, rinfo, R, N, d_ids, d_raw, tp, nb, pool_ids_per_cta, pool, ctr, ch_b,
+                                        ch_s, ch_n, ctr + 1, ctr + 2, d_err, d_bad);
     };
     if (raw) launch(part_pool_kernel<true>);
     else launch(part_pool_kernel<false>);
@@ -1198,7 +1222,7 @@ inline bool part_histogram(rs_context* ctx, Scratch& scr, bool raw, const uint64
     exclusive_scan<uint32_t>(ArrayIn<uint32_t>{ctr + 2}, nb, lstart, lstart + nb, scr, st);
     RS_CUDA(cudaMemcpyAsync(lcur, lstart, (size_t(nb) + 1) * 4, cudaMemcpyDeviceToDevice, st));
     part_pool_list_kernel<<<unsigned(sms) * 4, 256, 0, st>>>(ch_b, ctr + 1, lcur, list);
-    constexpr uint32_t kItemChunks = (1u << 20) / kPTile;  // ~1M addresses per P3 work item
+    constexpr uint32_t kItemChunks = (1u << 20) / kPoolChunk;  // ~1M addresses per P3 work item
     part_pool_items_kernel<<<(nb + 255) / 256, 256, 0, st>>>(ctr + 2, nb, kItemChunks, nitem);
     exclusive_scan<uint32_t>(ArrayIn<uint32_t>{nitem}, nb, ibase, ibase + nb, scr, st);
     const size_t hsm = size_t(1) << kP3Bits << 2;
@@ -1421,7 +1445,7 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
                 Scratch::bytes_for(N, 4) + Scratch::bytes_for(kPMaxBuckets + 1, 4) * 3 +
                 scan_scratch_bytes(size_t(kPMaxBuckets) * sm_count() * 4, 4) +
                 // single-pass pool: chunk records and lists (the pool itself fits the addresses' N x 4 B)
-                Scratch::bytes_for(N / 1024 + kPoolExtraBytes / 4096 + 2, 4) * 4 +
+                Scratch::bytes_for(N / 1024 + kPoolExtraBytes / 4096 + 2, 4) * 4 +  // chunk records (>= 2048 addresses each)
                 Scratch::bytes_for(kPPoolMaxBuckets + 2, 4) * 5 + (N >= (uint64_t(1) << 22) ? kPoolExtraBytes : 0);
   Scratch scr = ctx->scratch(need);
   phase("scratch");
