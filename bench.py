@@ -638,7 +638,7 @@ def run_profile_sweep(args, torch, ctx, hbm_peak):
     sp.profile(tr, 1.0, PROFILE_SEED, ctx=ctx)  # warm-up
     torch.cuda.synchronize()
     times = []
-    for _ in range(3):
+    for _ in range(5):
         t0 = time.perf_counter()
         p = sp.profiler.profile_handle(tr, 1.0, PROFILE_SEED, ctx=ctx)
         times.append(time.perf_counter() - t0)
@@ -651,7 +651,7 @@ def run_profile_sweep(args, torch, ctx, hbm_peak):
     H = sum(w.table.hash_size for w in specs)
     alg = 4.0 * n + 24.0 * R + 8.0 * H  # id + record + (zero + read) per row
     out = {"workload": "cfg1 tables, rate 1.0", "ids": int(n), "records": R,
-           "seconds": secs, "ids_per_s": n / secs, "algorithmic_gbs": alg / secs / 1e9,
+           "seconds": secs, "seconds_each": times, "ids_per_s": n / secs, "algorithmic_gbs": alg / secs / 1e9,
            "frac_of_hbm": alg / secs / 1e9 / hbm_peak}
     try:  # DRAM bytes of one such call from the committed ncu launch list
         tb = (traffic_record() or {}).get("cfg1_profile_1e9", {}).get("dram_bytes")

@@ -47,7 +47,7 @@ def main():
         h.close()
         del h  # its pinned result buffers go back to the pool before the next call
     ts.sort()
-    print(json.dumps({"ids": int(n), "records": int(tr.rec_sample.numel()), "s": ts[len(ts) // 2],
+    print(json.dumps({"ids": int(n), "records": int(tr.rec_sample.numel()), "s": ts[len(ts) // 2], "all_s": ts,
                       "ids_per_s": n / ts[len(ts) // 2]}))
 
 
