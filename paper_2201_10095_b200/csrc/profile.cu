@@ -833,8 +833,13 @@ part_pool_hist_kernel(const uint16_t* __restrict__ pool, const uint32_t* __restr
     }
     __syncthreads();
     const uint64_t cb = uint64_t(b) << kP3Bits;
-    for (uint32_t i = threadIdx.x; i < span; i += blockDim.x)
-      if (h[i] && cb + i < ncounters) atomicAdd(&counters[cb + i], h[i]);
+    if (ibase[b + 1] - ibase[b] == 1) {  // the bucket's only work item: plain coalesced stores
+      for (uint32_t i = threadIdx.x; i < span; i += blockDim.x)
+        if (cb + i < ncounters) counters[cb + i] = h[i];
+    } else {
+      for (uint32_t i = threadIdx.x; i < span; i += blockDim.x)
+        if (h[i] && cb + i < ncounters) atomicAdd(&counters[cb + i], h[i]);
+    }
     __syncthreads();
   }
 }
@@ -904,8 +909,13 @@ part_hist_kernel(const uint16_t* __restrict__ addrs, const uint32_t* __restrict_
     if ((p1 & 1) && p1 > q && threadIdx.x == 0) atomicAdd(&h[addrs[p1 - 1]], 1u);  // odd tail
     __syncthreads();
     const uint64_t cb = uint64_t(b) << kP3Bits;
-    for (uint32_t i = threadIdx.x; i < span; i += blockDim.x)
-      if (h[i] && cb + i < ncounters) atomicAdd(&counters[cb + i], h[i]);
+    if (cbase[b + 1] - cbase[b] == 1) {  // the bucket's only work item: plain coalesced stores
+      for (uint32_t i = threadIdx.x; i < span; i += blockDim.x)
+        if (cb + i < ncounters) counters[cb + i] = h[i];
+    } else {
+      for (uint32_t i = threadIdx.x; i < span; i += blockDim.x)
+        if (h[i] && cb + i < ncounters) atomicAdd(&counters[cb + i], h[i]);
+    }
     __syncthreads();
   }
 }
