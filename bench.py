@@ -349,6 +349,11 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
         batches.append((off, idx[:max(1, n)].clone(), n))
         del idx
     cap = max([b[2] for b in batches] + [1])
+    if os.environ.get("BENCH_MEM_DEBUG"):
+        free, tot = torch.cuda.mem_get_info(dev)
+        print(f"mem before operator: free {free / 1e9:.1f} GB of {tot / 1e9:.1f}, torch allocated "
+              f"{torch.cuda.memory_allocated(dev) / 1e9:.1f} reserved {torch.cuda.memory_reserved(dev) / 1e9:.1f}, "
+              f"lookups cap {cap}", file=sys.stderr, flush=True)
     op = sp.TieredEmbeddingBag([w.table for w in lspecs], remaps, B, cap, args.optimizer,
                                ctx=ctx) if T else None
     if op:

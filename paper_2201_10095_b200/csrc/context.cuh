@@ -91,6 +91,17 @@ struct rs_context {
   }
 
   void sync() { RS_CUDA(cudaStreamSynchronize(stream)); }
+
+  // Releases the scratch arena (it holds no data between calls).  A profile
+  // of a huge table set (RM3: ~2^31 counters per group) leaves an arena of
+  // ~150 GB; an operator created on the same context next needs that HBM.
+  void trim_scratch() {
+    if (!arena) return;
+    RS_CUDA(cudaStreamSynchronize(stream));
+    RS_CUDA(cudaFree(arena));
+    arena = nullptr;
+    arena_cap = 0;
+  }
 };
 
 namespace rs {

@@ -927,6 +927,9 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
   if (max_lookups >= (uint64_t(1) << 32)) throw InvalidArgument("emb: max_lookups must be < 2^32");
   auto* e = new rs_emb;
   e->ctx = ctx;
+  // the context's scratch is transient; a large one (left by a profile of a
+  // big table set) would otherwise crowd out the tiers allocated below
+  if (ctx->arena_cap > (size_t(1) << 30)) ctx->trim_scratch();
   e->T = T;
   e->max_batch = max_batch;
   e->max_lookups = max_lookups;
@@ -976,7 +979,13 @@ rs_emb* emb_create(rs_context* ctx, uint32_t T, const rs_emb_table* tabs, uint64
     e->fast_bytes = std::max<size_t>(fb, 256);
     e->host_bytes = std::max<size_t>(hb, 256);
     e->remap_bytes = rb;
-    RS_CUDA(cudaMalloc(&e->fast_pool, e->fast_bytes));
+    if (cudaMalloc(&e->fast_pool, e->fast_bytes) != cudaSuccess) {
+      cudaGetLastError();
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      throw CudaError("emb: fast tier of " + std::to_string(e->fast_bytes >> 20) + " MiB does not fit (" +
+                      std::to_string(fr >> 20) + " MiB free of " + std::to_string(tot >> 20) + ")");
+    }
     alloc_host_tier(e);
     RS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->host_pool_dev), e->host_pool, 0));
     RS_CUDA(cudaMalloc(&e->remap_pool, std::max<size_t>(rb, 256)));

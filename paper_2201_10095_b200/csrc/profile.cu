@@ -1192,6 +1192,7 @@ inline bool part_histogram(rs_context* ctx, Scratch& scr, bool raw, const uint64
   const uint32_t pct = uint32_t(sms) * kPoolCtasPerSm;
   const uint64_t pool_cap = N + uint64_t(pct) * nb * kPoolChunk;
   if (!no_pool && nb <= kPPoolMaxBuckets && pool_cap * 2 <= 4 * N + kPoolExtraBytes &&
+      scr.cap - scr.used >= (pool_cap + 1) / 2 * 4 + (pool_cap / kPoolChunk + 1) * 16 + (size_t(nb) + 2) * 40 + 4096 &&
       pool_cap < (uint64_t(1) << 32)) {
     const uint64_t max_ch = pool_cap / kPoolChunk + 1;
     const uint64_t pool_ids_per_cta = ((N + pct - 1) / pct + kPoolChunk - 1) / kPoolChunk * kPoolChunk;
@@ -1439,12 +1440,18 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
     }
     gstart.push_back(J);
   }
-  uint64_t maxH = 0;
+  uint64_t maxH = 0, minH = ~uint64_t(0);
   for (size_t g = 0; g + 1 < gstart.size(); ++g) {
     uint64_t s = 0;
     for (uint32_t j = gstart[g]; j < gstart[g + 1]; ++j) s += hs[j];
     maxH = std::max(maxH, s);
+    minH = std::min(minH, s);
   }
+  // scratch for the single-pass pool's partial chunks only when some group
+  // can take that path (few buckets, a partitioned-size call): a huge table
+  // set (RM3) keeps its arena as before
+  const bool pool_possible = N >= (uint64_t(1) << 22) &&
+                             ((minH + (uint64_t(1) << kP3Bits) - 1) >> kP3Bits) <= kPPoolMaxBuckets;
 
   size_t need = Scratch::bytes_for(R, 8) * 2 + Scratch::bytes_for(R, 4) * 2 +
                 Scratch::bytes_for(N, raw ? 8 : 4) + Scratch::bytes_for(J, 8) * 8 +
@@ -1456,7 +1463,7 @@ rs_profile* profile_run(rs_context* ctx, const rs_trace* tr, double rate, uint64
                 scan_scratch_bytes(size_t(kPMaxBuckets) * sm_count() * 4, 4) +
                 // single-pass pool: chunk records and lists (the pool itself fits the addresses' N x 4 B)
                 Scratch::bytes_for(N / 1024 + kPoolExtraBytes / 4096 + 2, 4) * 4 +  // chunk records (>= 2048 addresses each)
-                Scratch::bytes_for(kPPoolMaxBuckets + 2, 4) * 5 + (N >= (uint64_t(1) << 22) ? kPoolExtraBytes : 0);
+                Scratch::bytes_for(kPPoolMaxBuckets + 2, 4) * 5 + (pool_possible ? kPoolExtraBytes : 0);
   Scratch scr = ctx->scratch(need);
   phase("scratch");
 
