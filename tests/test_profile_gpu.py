@@ -285,3 +285,41 @@ def test_profile_partitioned_pool_and_two_pass(cuda_ctx, coracle, monkeypatch, t
         got = sp.profile(tr, rate, seed, ctx=cuda_ctx)
         want = coracle.profile(tables, S, rec_sample, rec_table, rec_offset, lens, ids, rate, seed)
         assert_stats_equal(got, want)
+
+
+def test_operator_after_big_profile_releases_scratch(cuda_ctx, coracle):
+    """A profile whose scratch passes 1 GB (2.5e7 counters), then an operator
+    on the same context (its creation releases the context's arena), a
+    forward through it, then the same profile again: both profiles
+    bit-exact vs the oracle, the forward bit-exact vs the oracle."""
+    import torch
+
+    from paper_2201_10095_b200.types import PlanEntry
+
+    rng = np.random.default_rng(71)
+    tables = [TableSpec(90 + j, 100, 12_500_000, 16, 4) for j in range(2)]
+    S = 30_000
+    lens = rng.integers(1, 6, 2 * S).astype(np.uint32)
+    rec_sample = np.repeat(np.arange(S, dtype=np.uint64), 2)
+    rec_table = np.tile(np.array([90, 91], np.uint32), S)
+    rec_offset = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.uint64)
+    N = int(lens.sum())
+    ids = (rng.random(N) ** 3 * 12_500_000).astype(np.uint32)
+    tr = Trace(tables, S, rec_sample, rec_table, rec_offset, lens, ids=ids)
+    want = coracle.profile(tables, S, rec_sample, rec_table, rec_offset, lens, ids, 1.0, 4)
+    got = sp.profile(tr, 1.0, 4, ctx=cuda_ctx)
+    assert_stats_equal(got, want)
+    spec = TableSpec(7, 1000, 5000, 16, 4)
+    st = sp.profile(Trace([spec], 1, np.zeros(1, np.uint64), np.full(1, 7, np.uint32), np.zeros(1, np.uint64),
+                          np.full(1, 3, np.uint32), ids=np.array([1, 2, 3], np.uint32)), 1.0, 0, ctx=cuda_ctx)[0]
+    remap = sp.build_remap(PlanEntry(7, 0, 50, 2), st, spec, ctx=cuda_ctx)
+    B = 32
+    off = np.arange(0, 2 * B + 1, 2, dtype=np.uint32)
+    idx = rng.integers(0, 5000, 2 * B).astype(np.uint32)
+    op = sp.TieredEmbeddingBag([spec], [remap], B, idx.size, "sgd", ctx=cuda_ctx)
+    op.init_weights(3, 0.5)
+    y = op.forward(torch.from_numpy(off.view(np.int32)).cuda(), torch.from_numpy(idx.view(np.int32)).cuda(), B)
+    W = [coracle.init_table(3, 7, 5000, 16, 0.5)]
+    assert np.array_equal(y.cpu().numpy(), coracle.emb_forward(B, [16], off.astype(np.uint64), idx, W))
+    del op
+    assert_stats_equal(sp.profile(tr, 1.0, 4, ctx=cuda_ctx), want)
