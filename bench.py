@@ -80,6 +80,11 @@ def parse():
     return a
 
 
+# where the step queues batch i+2's prefetch (claim + host gather): after the
+# backward (default) or after the forward (BENCH_PREFETCH_AT=fwd)
+PREFETCH_AFTER_BWD = os.environ.get("BENCH_PREFETCH_AT", "bwd") != "fwd"
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -404,6 +409,8 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
 
     D = args.prefetch_depth
 
+    prefetch_after_bwd = PREFETCH_AFTER_BWD
+
     def step(i, cache, ev=None):
         if nvtx:
             torch.cuda.nvtx.range_push("bench_step")
@@ -418,9 +425,9 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
             ex_forward(op, ex, off, idx, hits)
         elif T:
             op.forward(off, idx, B, out=pooled, hits=hits)
-        if D == 2 and cache and i + 2 < cache:
-            # batch i+2: its claim queues behind this forward, so its host
-            # gather has this backward and the whole next step to finish
+        if D == 2 and cache and i + 2 < cache and not prefetch_after_bwd:
+            # batch i+2 (BENCH_PREFETCH_AT=fwd): its claim queues behind this
+            # forward, so its host gather has this backward and the next step
             nb = batches[(i + 2) % len(batches)]
             op.prefetch(nb[0], nb[1], B)
         if ev:
@@ -434,6 +441,13 @@ def run_plan(args, torch, dist, rank, world, dev, ctx, specs, stats, prof, plan,
             ex_backward(op, ex, off, idx, LR)
         elif T:
             op.backward(off, idx, g, B, LR)
+        if D == 2 and cache and i + 2 < cache and prefetch_after_bwd:
+            # batch i+2 (default): its claim queues behind this backward and
+            # runs beside the next forward, not beside this backward (whose
+            # kernels it slowed by ~0.1 ms); the host gather still has a step:
+            # RM1 3.53 -> 3.46 ms/step, three same-box A/B pairs
+            nb = batches[(i + 2) % len(batches)]
+            op.prefetch(nb[0], nb[1], B)
         if ev:
             ev[3].record()
         if nvtx:
@@ -642,8 +656,14 @@ def run_profile_sweep(args, torch, ctx, hbm_peak):
     R = int(tr.rec_sample.numel())
     sp.profile(tr, 1.0, PROFILE_SEED, ctx=ctx)  # warm-up
     torch.cuda.synchronize()
+    # host-side settle: the call is timed end to end on the host, and the
+    # earlier legs free tens of GB of pinned host memory and HBM
+    import gc
+
+    gc.collect()
+    time.sleep(1.0)
     times = []
-    for _ in range(5):
+    for _ in range(9):
         t0 = time.perf_counter()
         p = sp.profiler.profile_handle(tr, 1.0, PROFILE_SEED, ctx=ctx)
         times.append(time.perf_counter() - t0)
@@ -837,13 +857,16 @@ def run_e2e(torch, dist, world, op, batches, pooled, hits, B, steps, ex, cache, 
                 ex_forward(op, ex, d_off, d_idx, hits)
             else:
                 op.forward(d_off, d_idx, B, out=pooled, hits=hits)
-            if cache and depth == 2 and i + 2 < total:
+            if cache and depth == 2 and i + 2 < total and not PREFETCH_AFTER_BWD:
                 main.wait_event(ev_in[(i + 2) % nb])  # copied a step ago
                 op.prefetch(*view(i + 2), B)
             if ex is not None:
                 ex_backward(op, ex, d_off, d_idx, LR)
             else:
                 op.backward(d_off, d_idx, pooled, B, LR)
+            if cache and depth == 2 and i + 2 < total and PREFETCH_AFTER_BWD:
+                main.wait_event(ev_in[(i + 2) % nb])  # copied a step ago
+                op.prefetch(*view(i + 2), B)
             h_hits.copy_(hits, non_blocking=True)
             ev_free[i % nb].record(main)
             used[i % nb] = True
@@ -955,6 +978,16 @@ def main():
     del ptrace, pidx, poff
     torch.cuda.empty_cache()
 
+    # HP1 at scale (the 1e9-id sweep) before any operator exists: its calls
+    # are timed end to end on the host, which the later legs (tens of GB of
+    # pinned host tiers allocated and freed) leave noisy for seconds
+    sweep = None
+    if world == 1 and args.profile_ids > 0:
+        sweep = run_profile_sweep(args, torch, ctx, hbm_peak)
+    elif world > 1 and args.profile_ids > 0:
+        sweep = run_profile_sweep_sharded(args, torch, dist, ctx, world, rank)
+    torch.cuda.empty_cache()
+
     # ---- plans (host): RecShard vs the greedy/size baseline
     t0 = time.perf_counter()
     rec_pure = planner.recshard_plan(tables, stats, system)  # the reference's solve, restated
@@ -1046,11 +1079,6 @@ def main():
         need = sum(w.table.hash_size * (w.table.dim * w.table.elem_bytes + 8) for w in specs)
         if need < 0.8 * torch.cuda.mem_get_info(dev)[0]:
             uniform = run_uniform_control(args, torch, ctx, specs, B, hbm_peak)
-    sweep = None
-    if world == 1 and args.profile_ids > 0:
-        sweep = run_profile_sweep(args, torch, ctx, hbm_peak)
-    elif world > 1 and args.profile_ids > 0:
-        sweep = run_profile_sweep_sharded(args, torch, dist, ctx, world, rank)
     trace_io = None
     if rank == 0 and world == 1 and args.trace_ids > 0:
         import importlib.util
