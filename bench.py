@@ -662,11 +662,16 @@ def run_profile_sweep(args, torch, ctx, hbm_peak):
 
     gc.collect()
     time.sleep(1.0)
-    times = []
-    for _ in range(9):
+    times, dev_times = [], []
+    for _ in range(15):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         t0 = time.perf_counter()
         p = sp.profiler.profile_handle(tr, 1.0, PROFILE_SEED, ctx=ctx)
         times.append(time.perf_counter() - t0)
+        e1.record()  # the call returns with its results on the host: the stream is idle
+        torch.cuda.synchronize()
+        dev_times.append(e0.elapsed_time(e1) / 1e3)
         # release this result before the next call, so its pinned host buffers
         # return to the context's pool (a live result makes the next call pin
         # fresh pages: ~25 ms per 100 MB, which is host allocation, not profiling)
@@ -676,7 +681,9 @@ def run_profile_sweep(args, torch, ctx, hbm_peak):
     H = sum(w.table.hash_size for w in specs)
     alg = 4.0 * n + 24.0 * R + 8.0 * H  # id + record + (zero + read) per row
     out = {"workload": "cfg1 tables, rate 1.0", "ids": int(n), "records": R,
-           "seconds": secs, "seconds_each": times, "ids_per_s": n / secs, "algorithmic_gbs": alg / secs / 1e9,
+           "seconds": secs, "seconds_each": times,
+           "device_seconds": float(np.median(dev_times)),  # the call's span on its stream (host jitter excluded)
+           "ids_per_s": n / secs, "algorithmic_gbs": alg / secs / 1e9,
            "frac_of_hbm": alg / secs / 1e9 / hbm_peak}
     try:  # DRAM bytes of one such call from the committed ncu launch list
         tb = (traffic_record() or {}).get("cfg1_profile_1e9", {}).get("dram_bytes")
